@@ -1,0 +1,199 @@
+/*
+ * contactsim_b200 — C ABI of the B200-native SDF contact generation + contact
+ * reduction path (Factory, arXiv 2205.03532; reference package `contactsim`).
+ *
+ * Plain pointers and sizes only: no torch or CUDA C++ types. `stream` is a
+ * cudaStream_t passed as void* (NULL = legacy default stream). Device pointers
+ * are marked [dev], host pointers [host]. Every function returns a cs_status;
+ * on failure cs_last_error() holds a thread-local message, and the Python shim
+ * (paper_2205_03532_b200/_native.py) raises the reference's exception class:
+ *
+ *   CS_ERR_VALUE     -> ValueError               (e.g. generation.py:64-65)
+ *   CS_ERR_NONFINITE -> NonFiniteStateError       (generation.py:66-68, errors.py:19)
+ *   CS_ERR_MESH      -> MeshValidationError       (grid.py:169,189-192, errors.py:8)
+ *   CS_ERR_HANDLE / CS_ERR_CUDA / CS_ERR_OOM -> RuntimeError
+ *
+ * Numerics: IEEE double arithmetic in the reference's operation order (numba
+ * kernels: no FMA contraction), and the reference's BLAS 3-term dot products
+ * reproduced with explicit FMAs, so outputs are bit-identical to the reference
+ * on the same inputs.
+ */
+#ifndef CONTACTSIM_B200_H
+#define CONTACTSIM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CS_OK = 0,
+    CS_ERR_VALUE = 1,
+    CS_ERR_NONFINITE = 2,
+    CS_ERR_MESH = 3,
+    CS_ERR_HANDLE = 4,
+    CS_ERR_CUDA = 5,
+    CS_ERR_OOM = 6
+} cs_status;
+
+#define CS_ABI_VERSION 1
+
+/* Thread-local message of the last failing call on this thread. */
+const char *cs_last_error(void);
+int cs_abi_version(void);
+/* SM count, L2 bytes and max persisting-L2 bytes of the current device. */
+int cs_device_info(int32_t *sm_count, int64_t *l2_bytes, int64_t *persist_l2_max);
+
+/* ------------------------------------------------------------------------
+ * Device-resident SDF store.
+ * Replaces holding SignedDistanceGrid.values per call (sdf/grid.py:48-68):
+ * the grid is uploaded once and shared by every env that names the handle.
+ * values: float32, x-fastest, index = ix + nx*(iy + ny*iz) (grid.py:1-6).
+ * values_on_device != 0 means `values` is already a device pointer (copied).
+ * ---------------------------------------------------------------------- */
+int cs_sdf_register(const float *values, int values_on_device, int32_t nx, int32_t ny, int32_t nz,
+                    const double origin[3], double voxel, const double aabb_lo[3], const double aabb_hi[3],
+                    int32_t *handle);
+int cs_sdf_free(int32_t handle);
+/* [dev] pointer to the stored values (for the per-pair drop-ins below). */
+int cs_sdf_values(int32_t handle, const float **values);
+/* Pin the grid in L2 for launches on `stream` (cudaAccessPolicyWindow,
+ * hitRatio scaled to the persisting-L2 limit). hit_ratio <= 0 clears it. */
+int cs_sdf_l2_persist(int32_t handle, void *stream, float hit_ratio);
+
+/* Mesh store (geometry/mesh.py:16-47): float64 vertices, int32 triangles. */
+int cs_mesh_register(const double *vertices, int64_t nv, const int32_t *triangles, int64_t nt, int32_t *handle);
+int cs_mesh_free(int32_t handle);
+
+/* ------------------------------------------------------------------------
+ * Per-pair drop-ins for the reference's numba kernels (same argument lists).
+ * ---------------------------------------------------------------------- */
+
+/* contacts/_kernels.py:11-17 face_contacts(values, nx, ny, nz, ox, oy, oz, voxel,
+ * tri_verts, contact_distance, max_iters, tol, out_point, out_phi, out_grad, out_found).
+ * tri_verts [dev] (m,3,3) f64 grid frame; outputs [dev], caller-allocated.
+ * Pruned faces write only out_found = 0, like the reference. */
+int cs_face_contacts(const float *values, int64_t nx, int64_t ny, int64_t nz, double ox, double oy, double oz,
+                     double voxel, const double *tri_verts, int64_t m, double contact_distance, int32_t max_iters,
+                     double tol, double *out_point, double *out_phi, double *out_grad, uint8_t *out_found,
+                     void *stream);
+
+/* sdf/_kernels.py:330-346 sample_batch / gradient_batch: points [dev] (n,3) grid frame. */
+int cs_sdf_sample(const float *values, int64_t nx, int64_t ny, int64_t nz, double ox, double oy, double oz,
+                  double voxel, const double *points, int64_t n, double *out, void *stream);
+int cs_sdf_gradient(const float *values, int64_t nx, int64_t ny, int64_t nz, double ox, double oy, double oz,
+                    double voxel, const double *points, int64_t n, double *out, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Batched collide: the vectorised body of Scene._collect_contacts
+ * (dynamics/scene.py:197-227) over E independent envs, one (SDF, mesh) pair each.
+ * A plan fixes the env -> (sdf, mesh) assignment and ReductionParams, owns all
+ * device buffers, and runs stream-ordered (CUDA-graph capturable).
+ * ---------------------------------------------------------------------- */
+
+/* ReductionParams (contacts/types.py:62-78). */
+typedef struct cs_reduction_params {
+    int32_t max_patches;    /* N, default 128 */
+    int32_t per_patch_cap;  /* K, default 6 */
+    int32_t batch_size;     /* default 1024 */
+    int32_t has_min_depth;  /* 0: min_depth None */
+    double normal_cone_cos; /* default cos(20 deg) */
+    double min_depth;
+} cs_reduction_params;
+
+/* Pose formats for cs_collide. */
+enum { CS_POSE7 = 0 /* (px,py,pz,qw,qx,qy,qz) */, CS_POSE12 = 1 /* (R row-major 9, t 3) */ };
+
+/* What a plan runs. */
+enum { CS_STAGE_GENERATE = 1, CS_STAGE_REDUCE = 2, CS_STAGE_ALL = 3 };
+
+/* Device views of a plan's buffers (all [dev]). Env e owns rows
+ * [cand_base[e], cand_base[e] + capacity_e) of the candidate/member arrays,
+ * where capacity_e = triangle count of its mesh (one candidate per face at most). */
+typedef struct cs_outputs {
+    int64_t n_envs;
+    int32_t max_patches, per_patch_cap;
+    int64_t total_capacity;
+    const int64_t *cand_base;   /* [E] */
+    int32_t *env_status;        /* [E] 0 ok, 1 non-finite pose, 2 cd < 0 */
+    int32_t *n_cand;            /* [E] candidates (ContactSet length) */
+    int32_t *n_patch;           /* [E] */
+    int32_t *n_kept;            /* [E] sum of kept contacts over patches */
+    float *stats;               /* [E,4] n_cand, n_patch, n_kept, max kept depth (all-gather payload) */
+    double *cand_point;         /* [cap,3] world frame (ContactSet.points) */
+    double *cand_normal;        /* [cap,3] */
+    double *cand_depth;         /* [cap] */
+    int32_t *cand_face;         /* [cap] ascending per env */
+    double *patch_normal;       /* [E,N,3] representative normal */
+    int32_t *patch_nkept;       /* [E,N] */
+    int32_t *kept_cand;         /* [E,N,K] candidate index (within env), -1 pad */
+    double *kept_point;         /* [E,N,K,3] */
+    double *kept_normal;        /* [E,N,K,3] */
+    double *kept_depth;         /* [E,N,K] */
+    int32_t *kept_face;         /* [E,N,K] mesh face index, -1 pad */
+    double *w_sum;              /* [E,N] */
+    double *wp_sum;             /* [E,N,3] */
+    double *wn_sum;             /* [E,N,3] */
+    double *wt_sum;             /* [E,N,3] */
+    double *area;               /* [E,N] */
+    double *max_depth;          /* [E,N] */
+    int32_t *member_offsets;    /* [E,N+1] CSR into members (relative to cand_base[e]) */
+    int32_t *members;           /* [cap] candidate indices, patch-major, ascending within a patch */
+} cs_outputs;
+
+typedef struct cs_plan cs_plan;
+
+/* Generate (+ reduce) plan. sdf_handles / mesh_handles [host] (E).
+ * With the reduce stage and has_min_depth == 0 the cull is min_depth = -cd per
+ * env, as Scene._collect_contacts builds ReductionParams (scene.py:215-225). */
+int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *mesh_handles,
+                   const cs_reduction_params *params, int32_t stages, cs_plan **plan);
+/* Reduce-only plan over caller-supplied candidate sets with per-env capacity [host] (E). */
+int cs_plan_create_reduce(int64_t n_envs, const int64_t *capacity, const cs_reduction_params *params,
+                          cs_plan **plan);
+int cs_plan_destroy(cs_plan *plan);
+int cs_plan_outputs(cs_plan *plan, cs_outputs *out);
+
+/* One collide step: sdf_pose/mesh_pose [dev] (E,7) or (E,12) per pose_format,
+ * contact_distance [dev] (E). Stream-ordered; no host synchronisation. */
+int cs_collide(cs_plan *plan, const double *sdf_pose, const double *mesh_pose, int32_t pose_format,
+               const double *contact_distance, void *stream);
+
+/* Phase timing: with slots > 0 every cs_collide records CUDA events on its
+ * stream around its phases into a ring of `slots` steps (0 disables).
+ * cs_plan_timing_read writes, per recorded step (oldest first, at most
+ * max_steps), CS_TIMING_PHASES floats in ms:
+ *   [env_xf, faces, compact, reduce, finalize(+stats), total]. */
+#define CS_TIMING_EVENTS 6
+#define CS_TIMING_PHASES 6
+int cs_plan_timing(cs_plan *plan, int32_t slots);
+int cs_plan_timing_read(cs_plan *plan, float *ms, int32_t max_steps, int32_t *n_steps);
+
+/* Roofline accounting: enable != 0 zeroes a device counter and switches the
+ * plan's face kernel to a build that tallies every trilinear SDF sample;
+ * enable == 0 synchronises, returns the tally in *count and switches back. */
+int cs_plan_count_samples(cs_plan *plan, int32_t enable, uint64_t *count);
+
+/* Reduce step of a reduce-only plan: the caller has written n_cand and the
+ * cand_point/cand_normal/cand_depth/cand_face rows of cs_outputs. */
+int cs_reduce(cs_plan *plan, void *stream);
+
+/* Host-buffer end-to-end call (the e2e path): copies poses/cd from host,
+ * runs cs_collide, copies stats [E,4] back. Host buffers should be pinned. */
+int cs_collide_host(cs_plan *plan, const double *sdf_pose_host, const double *mesh_pose_host, int32_t pose_format,
+                    const double *contact_distance_host, float *stats_host, void *stream);
+
+/* ------------------------------------------------------------------------
+ * SDF generation (sdf/grid.py:163-239): exact unsigned distance to the mesh
+ * and ray-parity sign voting on the GPU, bit-identical to the reference.
+ * vertices/triangles [host]; values_out [host] (nx*ny*nz).
+ * ---------------------------------------------------------------------- */
+int cs_sdf_generate(const double *vertices, int64_t nv, const int32_t *triangles, int64_t nt, int32_t nx, int32_t ny,
+                    int32_t nz, const double origin[3], double voxel, float *values_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CONTACTSIM_B200_H */

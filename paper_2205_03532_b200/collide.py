@@ -1,0 +1,270 @@
+"""Batched collide: SDF contact generation + contact reduction for E envs per call.
+
+This is the vectorised body of contactsim's per-pair loop in
+Scene._collect_contacts (/root/reference/pkg/src/contactsim/dynamics/scene.py:188-227):
+for every env e, generate_contacts(sdf_e, mesh_e, poses_e, cd_e) followed by
+reduce_contacts(candidates, ReductionParams(min_depth=-cd_e)). Results stay on
+the device in a padded layout (ReducedContacts); `patches(e)` rebuilds the
+reference's list[ContactPatch] for one env.
+
+    register_sdf(grid) -> int          device SDF store handle (uploaded once)
+    register_mesh(mesh) -> int         device mesh store handle
+    collide(sdf_handles, mesh_handles, sdf_pose, mesh_pose, contact_distance, params)
+        -> ReducedContacts
+"""
+
+from __future__ import annotations
+
+import ctypes
+import weakref
+
+import numpy as np
+
+from . import _native
+from .contacts.types import ContactPatch, ContactSet, ReductionParams
+from .errors import NonFiniteStateError
+from .geometry.mesh import TriMesh
+from .sdf.grid import SignedDistanceGrid
+
+_mesh_handles: "weakref.WeakKeyDictionary[TriMesh, int]" = weakref.WeakKeyDictionary()
+
+
+def _free_mesh(h: int) -> None:
+    try:
+        _native.lib().cs_mesh_free(h)
+    except Exception:
+        pass
+
+
+def register_sdf(grid: SignedDistanceGrid) -> int:
+    """SDF asset registration: upload the grid once; every env naming it shares it."""
+    return grid.device_handle()
+
+
+def register_mesh(mesh: TriMesh) -> int:
+    h = _mesh_handles.get(mesh)
+    if h is None:
+        out = ctypes.c_int32(-1)
+        _native.call("cs_mesh_register", mesh.vertices.ctypes.data, len(mesh.vertices), mesh.triangles.ctypes.data,
+                     len(mesh.triangles), ctypes.byref(out))
+        h = int(out.value)
+        _mesh_handles[mesh] = h
+        weakref.finalize(mesh, _free_mesh, h)
+    return h
+
+
+def pin_sdf_in_l2(grid: SignedDistanceGrid, hit_ratio: float = 1.0, stream=None) -> None:
+    """Persist the grid in L2 for launches on `stream` (cudaAccessPolicyWindow)."""
+    _native.call("cs_sdf_l2_persist", grid.device_handle(), _native.stream_handle(stream), float(hit_ratio))
+
+
+def _destroy_plan(ptr: int) -> None:
+    try:
+        _native.lib().cs_plan_destroy(ptr)
+    except Exception:
+        pass
+
+
+class Plan:
+    """Owns the device buffers of one env configuration (cs_plan_create)."""
+
+    def __init__(self, sdf_handles, mesh_handles, params: ReductionParams | None, stages: int = _native.CS_STAGE_ALL,
+                 capacity=None):
+        lib = _native.lib()
+        ptr = ctypes.c_void_p()
+        self.params = params or ReductionParams()
+        cparams = self.params.to_c()
+        if stages == _native.CS_STAGE_REDUCE:
+            cap = np.ascontiguousarray(capacity, dtype=np.int64)
+            self.n_envs = len(cap)
+            _native.check(lib.cs_plan_create_reduce(self.n_envs, cap.ctypes.data, ctypes.byref(cparams), ctypes.byref(ptr)))
+        else:
+            s = np.ascontiguousarray(sdf_handles, dtype=np.int32)
+            m = np.ascontiguousarray(mesh_handles, dtype=np.int32)
+            if s.shape != m.shape or s.ndim != 1:
+                raise ValueError("sdf_handles and mesh_handles must be 1-D of equal length")
+            self.n_envs = len(s)
+            _native.check(lib.cs_plan_create(self.n_envs, s.ctypes.data, m.ctypes.data, ctypes.byref(cparams),
+                                             stages, ctypes.byref(ptr)))
+        self.ptr = int(ptr.value)
+        self.stages = stages
+        weakref.finalize(self, _destroy_plan, self.ptr)
+        o = _native.OutputsC()
+        _native.check(lib.cs_plan_outputs(self.ptr, ctypes.byref(o)))
+        self.c = o
+        E, N, K, cap = o.n_envs, o.max_patches, o.per_patch_cap, o.total_capacity
+        v = lambda name, shape, dt: _native.device_view(getattr(o, name), shape, dt, self)  # noqa: E731
+        self.cand_base = v("cand_base", (E,), "i8")
+        self.env_status = v("env_status", (E,), "i4")
+        self.n_cand = v("n_cand", (E,), "i4")
+        self.cand_point = v("cand_point", (cap, 3), "f8")
+        self.cand_normal = v("cand_normal", (cap, 3), "f8")
+        self.cand_depth = v("cand_depth", (cap,), "f8")
+        self.cand_face = v("cand_face", (cap,), "i4")
+        if stages & _native.CS_STAGE_REDUCE:
+            self.n_patch = v("n_patch", (E,), "i4")
+            self.n_kept = v("n_kept", (E,), "i4")
+            self.stats = v("stats", (E, 4), "f4")
+            self.patch_normal = v("patch_normal", (E, N, 3), "f8")
+            self.patch_nkept = v("patch_nkept", (E, N), "i4")
+            self.kept_cand = v("kept_cand", (E, N, K), "i4")
+            self.kept_point = v("kept_point", (E, N, K, 3), "f8")
+            self.kept_normal = v("kept_normal", (E, N, K, 3), "f8")
+            self.kept_depth = v("kept_depth", (E, N, K), "f8")
+            self.kept_face = v("kept_face", (E, N, K), "i4")
+            self.w_sum = v("w_sum", (E, N), "f8")
+            self.wp_sum = v("wp_sum", (E, N, 3), "f8")
+            self.wn_sum = v("wn_sum", (E, N, 3), "f8")
+            self.wt_sum = v("wt_sum", (E, N, 3), "f8")
+            self.area = v("area", (E, N), "f8")
+            self.max_depth = v("max_depth", (E, N), "f8")
+            self.member_offsets = v("member_offsets", (E, N + 1), "i4")
+            self.members = v("members", (cap,), "i4")
+
+    def collide(self, sdf_pose, mesh_pose, contact_distance, pose_format: int = _native.CS_POSE7, stream=None):
+        """One step on device tensors (float64, contiguous). Stream-ordered, no sync."""
+        for t in (sdf_pose, mesh_pose, contact_distance):
+            if not (t.is_cuda and t.dtype.is_floating_point and t.element_size() == 8 and t.is_contiguous()):
+                raise ValueError("poses and contact_distance must be contiguous float64 CUDA tensors")
+        _native.call("cs_collide", self.ptr, sdf_pose.data_ptr(), mesh_pose.data_ptr(), pose_format,
+                     contact_distance.data_ptr(), _native.stream_handle(stream))
+
+    def collide_host(self, sdf_pose: np.ndarray, mesh_pose: np.ndarray, contact_distance: np.ndarray,
+                     pose_format: int = _native.CS_POSE7, stats_out: np.ndarray | None = None, stream=None):
+        """End-to-end call with host buffers: H2D poses, collide, D2H stats [E,4], synchronise."""
+        st = stats_out if stats_out is not None else np.empty((self.n_envs, 4), np.float32)
+        _native.call("cs_collide_host", self.ptr, sdf_pose.ctypes.data, mesh_pose.ctypes.data, pose_format,
+                     contact_distance.ctypes.data, st.ctypes.data, _native.stream_handle(stream))
+        return st
+
+    def reduce(self, stream=None):
+        _native.call("cs_reduce", self.ptr, _native.stream_handle(stream))
+
+    PHASES = ("env_xf", "faces", "compact", "reduce", "finalize", "total")
+
+    def enable_timing(self, slots: int) -> None:
+        """Record CUDA events around each phase of the next `slots` collide calls (0 disables)."""
+        _native.call("cs_plan_timing", self.ptr, int(slots))
+
+    def read_timing(self, max_steps: int) -> np.ndarray:
+        """(steps, 6) ms per phase [env_xf, faces, compact, reduce, finalize, total], oldest first."""
+        out = np.zeros((max_steps, len(self.PHASES)), np.float32)
+        n = ctypes.c_int32(0)
+        _native.call("cs_plan_timing_read", self.ptr, out.ctypes.data, int(max_steps), ctypes.byref(n))
+        return out[: n.value]
+
+    def count_samples(self, sdf_pose, mesh_pose, contact_distance, pose_format: int = _native.CS_POSE7) -> int:
+        """Exact number of trilinear SDF samples one collide step performs (counting build)."""
+        _native.call("cs_plan_count_samples", self.ptr, 1, None)
+        self.collide(sdf_pose, mesh_pose, contact_distance, pose_format)
+        c = ctypes.c_uint64(0)
+        _native.call("cs_plan_count_samples", self.ptr, 0, ctypes.byref(c))
+        return int(c.value)
+
+
+class ReducedContacts:
+    """Device-resident result of one collide step (views into the plan's buffers;
+    valid until the plan runs again)."""
+
+    def __init__(self, plan: Plan, body_ids=None):
+        self.plan = plan
+        self.body_ids = body_ids
+
+    def __getattr__(self, name):
+        return getattr(self.plan, name)
+
+    @property
+    def n_envs(self) -> int:
+        return self.plan.n_envs
+
+    def check(self) -> None:
+        """Raise the reference's errors for envs flagged on device (syncs)."""
+        st = self.plan.env_status.cpu().numpy()
+        if (st == 1).any():
+            raise NonFiniteStateError(f"non-finite pose in contact generation (envs {np.nonzero(st == 1)[0][:8].tolist()})")
+        if (st == 2).any():
+            raise ValueError("contact_distance must be non-negative")
+
+    def contact_set(self, e: int, body_a: int = -1, body_b: int = -1) -> ContactSet:
+        p = self.plan
+        base = int(p.cand_base[e].item())
+        n = int(p.n_cand[e].item())
+        sl = slice(base, base + n)
+        return ContactSet(p.cand_point[sl].cpu().numpy(), p.cand_normal[sl].cpu().numpy(),
+                          p.cand_depth[sl].cpu().numpy(), p.cand_face[sl].cpu().numpy().astype(np.int64), body_a, body_b)
+
+    def patches(self, e: int, face_indices: np.ndarray | None = None) -> list[ContactPatch]:
+        """list[ContactPatch] of env e in slot order (reduction.py:75)."""
+        p = self.plan
+        P = int(p.n_patch[e].item())
+        if P == 0:
+            return []
+        base = int(p.cand_base[e].item())
+        moff = p.member_offsets[e, : P + 1].cpu().numpy().astype(np.int64)
+        members = p.members[base: base + int(moff[-1])].cpu().numpy().astype(np.int64)
+        host = {k: getattr(p, k)[e, :P].cpu().numpy() for k in (
+            "patch_normal", "patch_nkept", "kept_cand", "kept_point", "kept_normal", "kept_depth", "kept_face",
+            "w_sum", "wp_sum", "wn_sum", "wt_sum", "area", "max_depth")}
+        out = []
+        for q in range(P):
+            k = int(host["patch_nkept"][q])
+            if face_indices is not None:
+                faces = np.asarray(face_indices, dtype=np.int64)[host["kept_cand"][q, :k].astype(np.int64)]
+            else:
+                faces = host["kept_face"][q, :k].astype(np.int64)
+            out.append(ContactPatch(
+                representative_normal=host["patch_normal"][q].copy(),
+                points=host["kept_point"][q, :k].copy(),
+                normals=host["kept_normal"][q, :k].copy(),
+                depths=host["kept_depth"][q, :k].copy(),
+                face_indices=faces,
+                member_indices=members[moff[q]: moff[q + 1]].copy(),
+                weight_sum=float(host["w_sum"][q]),
+                weighted_point_sum=host["wp_sum"][q].copy(),
+                weighted_normal_sum=host["wn_sum"][q].copy(),
+                weighted_torque_sum=host["wt_sum"][q].copy(),
+                area_metric=float(host["area"][q]),
+                max_depth=float(host["max_depth"][q]),
+            ))
+        return out
+
+
+_plan_cache: dict = {}
+
+
+def get_plan(sdf_handles, mesh_handles, params: ReductionParams | None) -> Plan:
+    params = params or ReductionParams()
+    key = (tuple(np.asarray(sdf_handles).tolist()), tuple(np.asarray(mesh_handles).tolist()),
+           params.max_patches, params.per_patch_cap, params.normal_cone_cos, params.min_depth, params.batch_size)
+    plan = _plan_cache.get(key)
+    if plan is None:
+        plan = _plan_cache[key] = Plan(sdf_handles, mesh_handles, params)
+    return plan
+
+
+def collide(sdf_handles, mesh_handles, sdf_pose, mesh_pose, contact_distance, params: ReductionParams | None = None,
+            check: bool = True, stream=None) -> ReducedContacts:
+    """Generate + reduce contacts for E envs.
+
+    sdf_handles / mesh_handles: (E,) ints from register_sdf / register_mesh.
+    sdf_pose / mesh_pose: (E, 7) float64 (px, py, pz, qw, qx, qy, qz), host or CUDA.
+    contact_distance: (E,) or scalar float64.
+    params: ReductionParams shared by every env. As in Scene._collect_contacts
+    (scene.py:215-225), min_depth=None means "-contact_distance per env"; pass
+    params with min_depth set to override.
+    """
+    import torch
+
+    E = len(sdf_handles)
+    plan = get_plan(sdf_handles, mesh_handles, params if params is not None else ReductionParams())
+    dev = lambda x: torch.as_tensor(np.asarray(x, dtype=np.float64) if not torch.is_tensor(x) else x,  # noqa: E731
+                                    dtype=torch.float64).cuda().contiguous()
+    sp, mp = dev(sdf_pose).reshape(E, 7), dev(mesh_pose).reshape(E, 7)
+    cd = dev(contact_distance).reshape(-1)
+    if cd.numel() == 1:
+        cd = cd.expand(E).contiguous()
+    plan.collide(sp, mp, cd, _native.CS_POSE7, stream)
+    res = ReducedContacts(plan)
+    if check:
+        res.check()
+    return res

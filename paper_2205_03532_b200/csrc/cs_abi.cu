@@ -1,0 +1,641 @@
+// extern "C" boundary of libcontactsim_b200.so (include/contactsim_b200.h).
+// Host-side state: SDF / mesh handle tables (fixed-capacity device descriptor
+// arrays, so captured CUDA graphs stay valid across registrations), plans, and
+// the thread-local error string the Python shim turns into the reference's
+// exception classes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "cs_reduce.cuh"
+#include "cs_sdfgen.cuh"
+
+using namespace cs;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CS_CUDA(call)                                                                                    \
+    do {                                                                                                 \
+        cudaError_t _e = (call);                                                                         \
+        if (_e != cudaSuccess)                                                                           \
+            return fail(_e == cudaErrorMemoryAllocation ? CS_ERR_OOM : CS_ERR_CUDA, "%s: %s (%s:%d)", #call, \
+                        cudaGetErrorString(_e), __FILE__, __LINE__);                                     \
+    } while (0)
+
+#define CS_LAUNCHED()                                                                                      \
+    do {                                                                                                   \
+        cudaError_t _e = cudaGetLastError();                                                               \
+        if (_e != cudaSuccess) return fail(CS_ERR_CUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(_e), \
+                                           __FILE__, __LINE__);                                            \
+    } while (0)
+
+constexpr int MAX_HANDLES = 4096;
+
+struct SdfEntry {
+    bool live = false;
+    float *values = nullptr;
+    size_t bytes = 0;
+    SdfDesc desc{};
+};
+struct MeshEntry {
+    bool live = false;
+    double4 *verts = nullptr;
+    int4 *tris = nullptr;
+    MeshDesc desc{};
+};
+
+std::mutex g_mu;
+std::vector<SdfEntry> g_sdf;
+std::vector<MeshEntry> g_mesh;
+SdfDesc *d_sdfs = nullptr;
+MeshDesc *d_meshes = nullptr;
+int g_sms = 0;
+
+int ensure_tables() {
+    if (d_sdfs) return CS_OK;
+    CS_CUDA(cudaMalloc(&d_sdfs, sizeof(SdfDesc) * MAX_HANDLES));
+    CS_CUDA(cudaMalloc(&d_meshes, sizeof(MeshDesc) * MAX_HANDLES));
+    CS_CUDA(cudaMemset(d_sdfs, 0, sizeof(SdfDesc) * MAX_HANDLES));
+    CS_CUDA(cudaMemset(d_meshes, 0, sizeof(MeshDesc) * MAX_HANDLES));
+    int dev = 0;
+    CS_CUDA(cudaGetDevice(&dev));
+    CS_CUDA(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
+    g_sdf.resize(MAX_HANDLES);
+    g_mesh.resize(MAX_HANDLES);
+    return CS_OK;
+}
+
+bool finite3(const double *v) { return std::isfinite(v[0]) && std::isfinite(v[1]) && std::isfinite(v[2]); }
+
+template <class T>
+int dalloc(T **p, size_t n) {
+    *p = nullptr;
+    if (n == 0) n = 1;
+    CS_CUDA(cudaMalloc(reinterpret_cast<void **>(p), n * sizeof(T)));
+    return CS_OK;
+}
+
+}  // namespace
+
+struct cs_plan {
+    int64_t E = 0;
+    int32_t stages = 0;
+    ReduceParams rp{};
+    int64_t max_batch = 1;
+    int64_t total_cap = 0;
+    int64_t nblocks = 0;
+    std::vector<void *> allocs;
+    // inputs / tables
+    int32_t *env_sdf = nullptr, *env_mesh = nullptr;
+    int64_t *cand_base = nullptr;
+    int2 *block_map = nullptr;
+    EnvXf *xf = nullptr;
+    Staging st{};
+    Candidates cands{};
+    ReduceIO io{};
+    cs_outputs out{};
+    // host e2e staging
+    double *in_sdf = nullptr, *in_mesh = nullptr, *in_cd = nullptr;
+    int32_t *status = nullptr;
+    double *env_min_depth = nullptr;  // scene semantics: min_depth None -> -cd per env
+    unsigned long long *sample_counter = nullptr;  // non-null: counting build of k_faces
+    unsigned long long *counter_buf = nullptr;
+    // phase timing: ring of `timing_slots` steps x CS_TIMING_EVENTS events
+    std::vector<cudaEvent_t> events;
+    int64_t timing_step = 0;
+    int32_t timing_slots = 0;
+
+    template <class T>
+    int alloc(T **p, size_t n) {
+        int r = dalloc(p, n);
+        if (r == CS_OK) allocs.push_back(*p);
+        return r;
+    }
+    ~cs_plan() {
+        for (cudaEvent_t e : events) cudaEventDestroy(e);
+        for (void *p : allocs) cudaFree(p);
+    }
+};
+
+extern "C" {
+
+const char *cs_last_error(void) { return g_err.c_str(); }
+
+int cs_abi_version(void) { return CS_ABI_VERSION; }
+
+int cs_device_info(int32_t *sm_count, int64_t *l2_bytes, int64_t *persist_l2_max) {
+    int dev = 0, v = 0;
+    CS_CUDA(cudaGetDevice(&dev));
+    CS_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+    if (sm_count) *sm_count = v;
+    CS_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev));
+    if (l2_bytes) *l2_bytes = v;
+    CS_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, dev));
+    if (persist_l2_max) *persist_l2_max = v;
+    return CS_OK;
+}
+
+// ---------------------------------------------------------------- SDF store
+
+int cs_sdf_register(const float *values, int values_on_device, int32_t nx, int32_t ny, int32_t nz,
+                    const double origin[3], double voxel, const double aabb_lo[3], const double aabb_hi[3],
+                    int32_t *handle) {
+    if (nx < 2 || ny < 2 || nz < 2) return fail(CS_ERR_VALUE, "grid dims must be at least 2 per axis");
+    if (!(voxel > 0.0)) return fail(CS_ERR_VALUE, "voxel_size must be positive");
+    const int64_t n = (int64_t)nx * ny * nz;
+    if (n >= (int64_t)1 << 31) return fail(CS_ERR_VALUE, "grid of %lld voxels exceeds the 2^31 device index range", (long long)n);
+    if (!values || !handle || !origin || !aabb_lo || !aabb_hi) return fail(CS_ERR_VALUE, "null argument");
+    std::lock_guard<std::mutex> lk(g_mu);
+    int r = ensure_tables();
+    if (r) return r;
+    int h = -1;
+    for (int i = 0; i < MAX_HANDLES; ++i)
+        if (!g_sdf[i].live) { h = i; break; }
+    if (h < 0) return fail(CS_ERR_HANDLE, "SDF handle table full (%d)", MAX_HANDLES);
+    SdfEntry &s = g_sdf[h];
+    s.bytes = (size_t)n * sizeof(float);
+    CS_CUDA(cudaMalloc(&s.values, s.bytes));
+    CS_CUDA(cudaMemcpy(s.values, values, s.bytes, values_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+    SdfDesc &d = s.desc;
+    d.values = s.values;
+    d.nx = nx; d.ny = ny; d.nz = nz; d.pad = 0;
+    d.ox = origin[0]; d.oy = origin[1]; d.oz = origin[2];
+    d.voxel = voxel;
+    for (int k = 0; k < 3; ++k) { d.lo[k] = aabb_lo[k]; d.hi[k] = aabb_hi[k]; }
+    CS_CUDA(cudaMemcpy(d_sdfs + h, &d, sizeof(SdfDesc), cudaMemcpyHostToDevice));
+    s.live = true;
+    *handle = h;
+    return CS_OK;
+}
+
+int cs_sdf_free(int32_t handle) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (handle < 0 || handle >= (int)g_sdf.size() || !g_sdf[handle].live) return fail(CS_ERR_HANDLE, "bad SDF handle %d", handle);
+    SdfEntry &s = g_sdf[handle];
+    CS_CUDA(cudaFree(s.values));
+    s = SdfEntry{};
+    return CS_OK;
+}
+
+int cs_sdf_values(int32_t handle, const float **values) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (handle < 0 || handle >= (int)g_sdf.size() || !g_sdf[handle].live) return fail(CS_ERR_HANDLE, "bad SDF handle %d", handle);
+    *values = g_sdf[handle].values;
+    return CS_OK;
+}
+
+int cs_sdf_l2_persist(int32_t handle, void *stream, float hit_ratio) {
+    float *base;
+    size_t bytes;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (handle < 0 || handle >= (int)g_sdf.size() || !g_sdf[handle].live) return fail(CS_ERR_HANDLE, "bad SDF handle %d", handle);
+        base = g_sdf[handle].values;
+        bytes = g_sdf[handle].bytes;
+    }
+    int dev = 0, max_win = 0, max_persist = 0;
+    CS_CUDA(cudaGetDevice(&dev));
+    CS_CUDA(cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+    CS_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
+    cudaStreamAttrValue attr;
+    memset(&attr, 0, sizeof(attr));
+    if (hit_ratio > 0.0f && max_win > 0 && max_persist > 0) {
+        size_t win = std::min(bytes, (size_t)max_win);
+        size_t persist = std::min(win, (size_t)max_persist);
+        CS_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
+        attr.accessPolicyWindow.base_ptr = base;
+        attr.accessPolicyWindow.num_bytes = win;
+        attr.accessPolicyWindow.hitRatio = std::min(1.0f, hit_ratio * (float)persist / (float)win);
+        attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    } else {
+        attr.accessPolicyWindow.num_bytes = 0;
+    }
+    CS_CUDA(cudaStreamSetAttribute((cudaStream_t)stream, cudaStreamAttributeAccessPolicyWindow, &attr));
+    return CS_OK;
+}
+
+// ---------------------------------------------------------------- mesh store
+
+int cs_mesh_register(const double *vertices, int64_t nv, const int32_t *triangles, int64_t nt, int32_t *handle) {
+    if (!vertices || !triangles || !handle) return fail(CS_ERR_VALUE, "null argument");
+    if (nv < 3 || nt < 1) return fail(CS_ERR_MESH, "mesh needs at least 3 vertices and 1 triangle");
+    if (nt >= ((int64_t)1 << 31)) return fail(CS_ERR_MESH, "too many triangles");
+    std::vector<double4> v4((size_t)nv);
+    for (int64_t i = 0; i < nv; ++i) {
+        const double *p = vertices + 3 * i;
+        if (!finite3(p)) return fail(CS_ERR_MESH, "non-finite vertex coordinate");
+        v4[(size_t)i] = make_double4(p[0], p[1], p[2], 0.0);
+    }
+    std::vector<int4> t4((size_t)nt);
+    for (int64_t i = 0; i < nt; ++i) {
+        const int32_t *t = triangles + 3 * i;
+        for (int k = 0; k < 3; ++k)
+            if (t[k] < 0 || t[k] >= nv) return fail(CS_ERR_MESH, "triangle index out of range (have %lld vertices)", (long long)nv);
+        t4[(size_t)i] = make_int4(t[0], t[1], t[2], 0);
+    }
+    std::lock_guard<std::mutex> lk(g_mu);
+    int r = ensure_tables();
+    if (r) return r;
+    int h = -1;
+    for (int i = 0; i < MAX_HANDLES; ++i)
+        if (!g_mesh[i].live) { h = i; break; }
+    if (h < 0) return fail(CS_ERR_HANDLE, "mesh handle table full (%d)", MAX_HANDLES);
+    MeshEntry &m = g_mesh[h];
+    CS_CUDA(cudaMalloc(&m.verts, sizeof(double4) * (size_t)nv));
+    CS_CUDA(cudaMalloc(&m.tris, sizeof(int4) * (size_t)nt));
+    CS_CUDA(cudaMemcpy(m.verts, v4.data(), sizeof(double4) * (size_t)nv, cudaMemcpyHostToDevice));
+    CS_CUDA(cudaMemcpy(m.tris, t4.data(), sizeof(int4) * (size_t)nt, cudaMemcpyHostToDevice));
+    m.desc.verts = m.verts;
+    m.desc.tris = m.tris;
+    m.desc.nv = nv;
+    m.desc.nt = nt;
+    CS_CUDA(cudaMemcpy(d_meshes + h, &m.desc, sizeof(MeshDesc), cudaMemcpyHostToDevice));
+    m.live = true;
+    *handle = h;
+    return CS_OK;
+}
+
+int cs_mesh_free(int32_t handle) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (handle < 0 || handle >= (int)g_mesh.size() || !g_mesh[handle].live) return fail(CS_ERR_HANDLE, "bad mesh handle %d", handle);
+    MeshEntry &m = g_mesh[handle];
+    CS_CUDA(cudaFree(m.verts));
+    CS_CUDA(cudaFree(m.tris));
+    m = MeshEntry{};
+    return CS_OK;
+}
+
+// ---------------------------------------------------------------- per-pair drop-ins
+
+static int make_grid(const float *values, int64_t nx, int64_t ny, int64_t nz, double ox, double oy, double oz,
+                     double voxel, GridView *g) {
+    if (nx < 2 || ny < 2 || nz < 2) return fail(CS_ERR_VALUE, "grid dims must be at least 2 per axis");
+    if (nx * ny * nz >= ((int64_t)1 << 31)) return fail(CS_ERR_VALUE, "grid exceeds the 2^31 device index range");
+    if (!(voxel > 0.0)) return fail(CS_ERR_VALUE, "voxel_size must be positive");
+    g->v = values;
+    g->nx = (int)nx; g->ny = (int)ny; g->nz = (int)nz;
+    g->ox = ox; g->oy = oy; g->oz = oz; g->voxel = voxel;
+    return CS_OK;
+}
+
+int cs_face_contacts(const float *values, int64_t nx, int64_t ny, int64_t nz, double ox, double oy, double oz,
+                     double voxel, const double *tri_verts, int64_t m, double contact_distance, int32_t max_iters,
+                     double tol, double *out_point, double *out_phi, double *out_grad, uint8_t *out_found,
+                     void *stream) {
+    GridView g;
+    int r = make_grid(values, nx, ny, nz, ox, oy, oz, voxel, &g);
+    if (r) return r;
+    if (m < 0) return fail(CS_ERR_VALUE, "negative face count");
+    launch_face_contacts(g, tri_verts, m, contact_distance, max_iters, tol, out_point, out_phi, out_grad, out_found,
+                         (cudaStream_t)stream);
+    CS_LAUNCHED();
+    return CS_OK;
+}
+
+int cs_sdf_sample(const float *values, int64_t nx, int64_t ny, int64_t nz, double ox, double oy, double oz,
+                  double voxel, const double *points, int64_t n, double *out, void *stream) {
+    GridView g;
+    int r = make_grid(values, nx, ny, nz, ox, oy, oz, voxel, &g);
+    if (r) return r;
+    launch_sdf_sample(g, points, n, out, (cudaStream_t)stream);
+    CS_LAUNCHED();
+    return CS_OK;
+}
+
+int cs_sdf_gradient(const float *values, int64_t nx, int64_t ny, int64_t nz, double ox, double oy, double oz,
+                    double voxel, const double *points, int64_t n, double *out, void *stream) {
+    GridView g;
+    int r = make_grid(values, nx, ny, nz, ox, oy, oz, voxel, &g);
+    if (r) return r;
+    launch_sdf_gradient(g, points, n, out, (cudaStream_t)stream);
+    CS_LAUNCHED();
+    return CS_OK;
+}
+
+// ---------------------------------------------------------------- plans
+
+static int check_params(const cs_reduction_params *p) {
+    if (!p) return fail(CS_ERR_VALUE, "null ReductionParams");
+    // contacts/types.py:70-78
+    if (p->max_patches < 1) return fail(CS_ERR_VALUE, "max_patches must be positive");
+    if (p->per_patch_cap < 1) return fail(CS_ERR_VALUE, "per_patch_cap must be at least 1");
+    if (!(p->normal_cone_cos >= -1.0 && p->normal_cone_cos <= 1.0)) return fail(CS_ERR_VALUE, "normal_cone_cos must be a cosine");
+    if (p->batch_size < 1) return fail(CS_ERR_VALUE, "batch_size must be positive");
+    if (p->per_patch_cap > MAX_KEPT) return fail(CS_ERR_VALUE, "per_patch_cap above the GPU limit of %d", MAX_KEPT);
+    if (p->max_patches > 4096) return fail(CS_ERR_VALUE, "max_patches above the GPU limit of 4096");
+    return CS_OK;
+}
+
+static int plan_buffers(cs_plan *P, const std::vector<int64_t> &cap) {
+    const int64_t E = P->E;
+    std::vector<int64_t> base((size_t)E);
+    int64_t tot = 0, maxcap = 1;
+    for (int64_t e = 0; e < E; ++e) {
+        base[(size_t)e] = tot;
+        tot += cap[(size_t)e];
+        maxcap = std::max(maxcap, cap[(size_t)e]);
+    }
+    P->total_cap = tot;
+    const int N = P->rp.N, K = P->rp.K;
+    int r;
+#define A(ptr, n) if ((r = P->alloc(&(ptr), (size_t)(n)))) return r
+    A(P->cand_base, E);
+    CS_CUDA(cudaMemcpy(P->cand_base, base.data(), sizeof(int64_t) * (size_t)E, cudaMemcpyHostToDevice));
+    A(P->status, E);
+    A(P->io.n_cand, E);
+    A(P->cands.point, 3 * tot); A(P->cands.normal, 3 * tot); A(P->cands.depth, tot); A(P->cands.face, tot);
+    CS_CUDA(cudaMemset(P->status, 0, sizeof(int32_t) * (size_t)E));
+    CS_CUDA(cudaMemset(P->io.n_cand, 0, sizeof(int32_t) * (size_t)E));
+    ReduceIO &io = P->io;
+    io.E = E;
+    io.cand_base = P->cand_base;
+    io.point = P->cands.point; io.normal = P->cands.normal; io.depth = P->cands.depth; io.face = P->cands.face;
+    if (P->stages & CS_STAGE_REDUCE) {
+        A(io.order, tot); A(io.label, tot); A(io.su, tot); A(io.sv, tot); A(io.sp, tot);
+        A(io.sh, 2 * tot + E * (4 * (int64_t)N + 4));
+        A(io.gP, 3 * tot); A(io.gN, 3 * tot); A(io.gD, tot);
+        A(io.patch_off, E + 1);
+        A(io.n_patch, E); A(io.n_kept, E);
+        A(io.patch_normal, 3 * E * N); A(io.builder_maxd, E * N);
+        A(io.member_offsets, E * (N + 1)); A(io.members, tot);
+        A(io.patch_nkept, E * N); A(io.kept_cand, E * N * K); A(io.kept_face, E * N * K);
+        A(io.kept_point, 3 * E * N * K); A(io.kept_normal, 3 * E * N * K); A(io.kept_depth, E * N * K);
+        A(io.w_sum, E * N); A(io.wp_sum, 3 * E * N); A(io.wn_sum, 3 * E * N); A(io.wt_sum, 3 * E * N);
+        A(io.area, E * N); A(io.max_depth, E * N);
+        A(io.stats, 4 * E);
+        CS_CUDA(cudaMemset(io.n_patch, 0, sizeof(int32_t) * (size_t)E));
+        CS_CUDA(cudaMemset(io.stats, 0, sizeof(float) * 4 * (size_t)E));
+    }
+#undef A
+    P->max_batch = std::min<int64_t>(P->rp.batch_size, maxcap);
+    cs_outputs &o = P->out;
+    o.n_envs = E;
+    o.max_patches = N;
+    o.per_patch_cap = K;
+    o.total_capacity = tot;
+    o.cand_base = P->cand_base;
+    o.env_status = P->status;
+    o.n_cand = io.n_cand;
+    o.n_patch = io.n_patch; o.n_kept = io.n_kept; o.stats = io.stats;
+    o.cand_point = P->cands.point; o.cand_normal = P->cands.normal; o.cand_depth = P->cands.depth;
+    o.cand_face = P->cands.face;
+    o.patch_normal = io.patch_normal; o.patch_nkept = io.patch_nkept; o.kept_cand = io.kept_cand;
+    o.kept_point = io.kept_point; o.kept_normal = io.kept_normal; o.kept_depth = io.kept_depth;
+    o.kept_face = io.kept_face;
+    o.w_sum = io.w_sum; o.wp_sum = io.wp_sum; o.wn_sum = io.wn_sum; o.wt_sum = io.wt_sum;
+    o.area = io.area; o.max_depth = io.max_depth;
+    o.member_offsets = io.member_offsets; o.members = io.members;
+    return CS_OK;
+}
+
+int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *mesh_handles,
+                   const cs_reduction_params *params, int32_t stages, cs_plan **plan) {
+    if (!plan) return fail(CS_ERR_VALUE, "null plan pointer");
+    *plan = nullptr;
+    if (n_envs < 1) return fail(CS_ERR_VALUE, "n_envs must be positive");
+    if (!(stages & CS_STAGE_GENERATE)) return fail(CS_ERR_VALUE, "cs_plan_create needs the generate stage");
+    if (stages & CS_STAGE_REDUCE) {
+        int r = check_params(params);
+        if (r) return r;
+    }
+    std::vector<int64_t> cap((size_t)n_envs);
+    std::vector<int2> bmap;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        int r = ensure_tables();
+        if (r) return r;
+        for (int64_t e = 0; e < n_envs; ++e) {
+            int s = sdf_handles[e], m = mesh_handles[e];
+            if (s < 0 || s >= MAX_HANDLES || !g_sdf[s].live) return fail(CS_ERR_HANDLE, "env %lld: bad SDF handle %d", (long long)e, s);
+            if (m < 0 || m >= MAX_HANDLES || !g_mesh[m].live) return fail(CS_ERR_HANDLE, "env %lld: bad mesh handle %d", (long long)e, m);
+            int64_t nt = g_mesh[m].desc.nt;
+            cap[(size_t)e] = nt;
+            for (int64_t f = 0; f < nt; f += FACE_BLOCK) bmap.push_back(make_int2((int)e, (int)f));
+        }
+    }
+    cs_plan *P = new cs_plan();
+    P->E = n_envs;
+    P->stages = stages;
+    if (stages & CS_STAGE_REDUCE) {
+        P->rp.N = params->max_patches; P->rp.K = params->per_patch_cap; P->rp.batch_size = params->batch_size;
+        P->rp.has_min_depth = params->has_min_depth; P->rp.cone = params->normal_cone_cos; P->rp.min_depth = params->min_depth;
+    } else {
+        P->rp.N = 1; P->rp.K = 1; P->rp.batch_size = 1;
+    }
+    int r = plan_buffers(P, cap);
+    if (!r) r = P->alloc(&P->env_sdf, (size_t)n_envs);
+    if (!r) r = P->alloc(&P->env_mesh, (size_t)n_envs);
+    if (!r) r = P->alloc(&P->block_map, bmap.size());
+    if (!r) r = P->alloc(&P->xf, (size_t)n_envs);
+    if (!r) r = P->alloc(&P->st.found, (size_t)P->total_cap);
+    if (!r) r = P->alloc(&P->st.point, 3 * (size_t)P->total_cap);
+    if (!r) r = P->alloc(&P->st.phi, (size_t)P->total_cap);
+    if (!r) r = P->alloc(&P->st.grad, 3 * (size_t)P->total_cap);
+    if (!r && (stages & CS_STAGE_REDUCE) && !params->has_min_depth) {
+        r = P->alloc(&P->env_min_depth, (size_t)n_envs);
+        P->io.env_min_depth = P->env_min_depth;
+    }
+    if (r) { delete P; return r; }
+    P->nblocks = (int64_t)bmap.size();
+    cudaError_t ce = cudaMemcpy(P->env_sdf, sdf_handles, sizeof(int32_t) * (size_t)n_envs, cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess) ce = cudaMemcpy(P->env_mesh, mesh_handles, sizeof(int32_t) * (size_t)n_envs, cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess) ce = cudaMemcpy(P->block_map, bmap.data(), sizeof(int2) * bmap.size(), cudaMemcpyHostToDevice);
+    if (ce != cudaSuccess) { delete P; return fail(CS_ERR_CUDA, "plan upload: %s", cudaGetErrorString(ce)); }
+    *plan = P;
+    return CS_OK;
+}
+
+int cs_plan_create_reduce(int64_t n_envs, const int64_t *capacity, const cs_reduction_params *params, cs_plan **plan) {
+    if (!plan) return fail(CS_ERR_VALUE, "null plan pointer");
+    *plan = nullptr;
+    if (n_envs < 1) return fail(CS_ERR_VALUE, "n_envs must be positive");
+    int r = check_params(params);
+    if (r) return r;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        r = ensure_tables();
+        if (r) return r;
+    }
+    std::vector<int64_t> cap((size_t)n_envs);
+    for (int64_t e = 0; e < n_envs; ++e) {
+        if (capacity[e] < 0 || capacity[e] >= ((int64_t)1 << 31)) return fail(CS_ERR_VALUE, "bad capacity");
+        cap[(size_t)e] = capacity[e];
+    }
+    cs_plan *P = new cs_plan();
+    P->E = n_envs;
+    P->stages = CS_STAGE_REDUCE;
+    P->rp.N = params->max_patches; P->rp.K = params->per_patch_cap; P->rp.batch_size = params->batch_size;
+    P->rp.has_min_depth = params->has_min_depth; P->rp.cone = params->normal_cone_cos; P->rp.min_depth = params->min_depth;
+    r = plan_buffers(P, cap);
+    if (r) { delete P; return r; }
+    *plan = P;
+    return CS_OK;
+}
+
+int cs_plan_destroy(cs_plan *plan) {
+    delete plan;
+    return CS_OK;
+}
+
+int cs_plan_outputs(cs_plan *plan, cs_outputs *out) {
+    if (!plan || !out) return fail(CS_ERR_VALUE, "null argument");
+    *out = plan->out;
+    return CS_OK;
+}
+
+static int run_reduce(cs_plan *P, cudaStream_t s) {
+    launch_reduce(P->io, P->rp, P->max_batch, s);
+    CS_LAUNCHED();
+    launch_finalize(P->io, P->rp, g_sms > 0 ? g_sms : 148, s);
+    CS_LAUNCHED();
+    return CS_OK;
+}
+
+int cs_collide(cs_plan *P, const double *sdf_pose, const double *mesh_pose, int32_t pose_format,
+               const double *contact_distance, void *stream) {
+    if (!P || !(P->stages & CS_STAGE_GENERATE)) return fail(CS_ERR_VALUE, "plan has no generate stage");
+    if (pose_format != CS_POSE7 && pose_format != CS_POSE12) return fail(CS_ERR_VALUE, "bad pose format");
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaEvent_t *ev = nullptr;
+    if (!P->events.empty()) {
+        ev = &P->events[(size_t)(P->timing_step % P->timing_slots) * CS_TIMING_EVENTS];
+        ++P->timing_step;
+    }
+    auto mark = [&](int i) { if (ev) cudaEventRecord(ev[i], s); };
+    mark(0);
+    launch_env_xf(P->E, P->env_sdf, P->env_mesh, d_sdfs, sdf_pose, mesh_pose, pose_format, contact_distance, P->xf,
+                  P->status, P->env_min_depth, s);
+    CS_LAUNCHED();
+    mark(1);
+    launch_faces(P->nblocks, P->block_map, P->xf, d_sdfs, d_meshes, P->cand_base, P->st, P->sample_counter, s);
+    CS_LAUNCHED();
+    mark(2);
+    launch_compact(P->E, P->xf, d_meshes, P->cand_base, P->st, P->cands, P->io.n_cand, s);
+    CS_LAUNCHED();
+    mark(3);
+    if (P->stages & CS_STAGE_REDUCE) {
+        launch_reduce(P->io, P->rp, P->max_batch, s);
+        CS_LAUNCHED();
+        mark(4);
+        launch_finalize(P->io, P->rp, g_sms > 0 ? g_sms : 148, s);
+        CS_LAUNCHED();
+    } else {
+        mark(4);
+    }
+    mark(5);
+    return CS_OK;
+}
+
+int cs_plan_timing(cs_plan *P, int32_t slots) {
+    if (!P) return fail(CS_ERR_VALUE, "null plan");
+    for (cudaEvent_t e : P->events) cudaEventDestroy(e);
+    P->events.clear();
+    P->timing_step = 0;
+    P->timing_slots = slots > 0 ? slots : 0;
+    for (int64_t i = 0; i < (int64_t)P->timing_slots * CS_TIMING_EVENTS; ++i) {
+        cudaEvent_t e;
+        CS_CUDA(cudaEventCreate(&e));
+        P->events.push_back(e);
+    }
+    return CS_OK;
+}
+
+int cs_plan_timing_read(cs_plan *P, float *ms, int32_t max_steps, int32_t *n_steps) {
+    if (!P || P->events.empty()) return fail(CS_ERR_VALUE, "plan timing is not enabled");
+    int64_t n = std::min<int64_t>(P->timing_step, P->timing_slots);
+    n = std::min<int64_t>(n, max_steps);
+    const int64_t first = P->timing_step - n;
+    for (int64_t k = 0; k < n; ++k) {
+        cudaEvent_t *ev = &P->events[(size_t)((first + k) % P->timing_slots) * CS_TIMING_EVENTS];
+        CS_CUDA(cudaEventSynchronize(ev[CS_TIMING_EVENTS - 1]));
+        for (int p = 0; p < CS_TIMING_EVENTS - 1; ++p)
+            CS_CUDA(cudaEventElapsedTime(ms + k * CS_TIMING_PHASES + p, ev[p], ev[p + 1]));
+        CS_CUDA(cudaEventElapsedTime(ms + k * CS_TIMING_PHASES + CS_TIMING_EVENTS - 1, ev[0], ev[CS_TIMING_EVENTS - 1]));
+    }
+    *n_steps = (int32_t)n;
+    return CS_OK;
+}
+
+int cs_plan_count_samples(cs_plan *P, int32_t enable, uint64_t *count) {
+    if (!P) return fail(CS_ERR_VALUE, "null plan");
+    if (enable) {
+        if (!P->counter_buf) {
+            int r = P->alloc(&P->counter_buf, 1);
+            if (r) return r;
+        }
+        CS_CUDA(cudaMemset(P->counter_buf, 0, sizeof(unsigned long long)));
+        P->sample_counter = P->counter_buf;
+        return CS_OK;
+    }
+    if (count) {
+        if (!P->counter_buf) return fail(CS_ERR_VALUE, "sample counting was never enabled");
+        CS_CUDA(cudaDeviceSynchronize());
+        CS_CUDA(cudaMemcpy(count, P->counter_buf, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    }
+    P->sample_counter = nullptr;
+    return CS_OK;
+}
+
+int cs_reduce(cs_plan *P, void *stream) {
+    if (!P || !(P->stages & CS_STAGE_REDUCE)) return fail(CS_ERR_VALUE, "plan has no reduce stage");
+    return run_reduce(P, (cudaStream_t)stream);
+}
+
+int cs_collide_host(cs_plan *P, const double *sdf_pose_host, const double *mesh_pose_host, int32_t pose_format,
+                    const double *contact_distance_host, float *stats_host, void *stream) {
+    if (!P || !(P->stages & CS_STAGE_GENERATE)) return fail(CS_ERR_VALUE, "plan has no generate stage");
+    const size_t w = pose_format == CS_POSE12 ? 12 : 7;
+    if (!P->in_sdf) {
+        int r;
+        if ((r = P->alloc(&P->in_sdf, 12 * (size_t)P->E))) return r;
+        if ((r = P->alloc(&P->in_mesh, 12 * (size_t)P->E))) return r;
+        if ((r = P->alloc(&P->in_cd, (size_t)P->E))) return r;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    CS_CUDA(cudaMemcpyAsync(P->in_sdf, sdf_pose_host, sizeof(double) * w * (size_t)P->E, cudaMemcpyHostToDevice, s));
+    CS_CUDA(cudaMemcpyAsync(P->in_mesh, mesh_pose_host, sizeof(double) * w * (size_t)P->E, cudaMemcpyHostToDevice, s));
+    CS_CUDA(cudaMemcpyAsync(P->in_cd, contact_distance_host, sizeof(double) * (size_t)P->E, cudaMemcpyHostToDevice, s));
+    int r = cs_collide(P, P->in_sdf, P->in_mesh, pose_format, P->in_cd, stream);
+    if (r) return r;
+    if (stats_host && (P->stages & CS_STAGE_REDUCE))
+        CS_CUDA(cudaMemcpyAsync(stats_host, P->io.stats, sizeof(float) * 4 * (size_t)P->E, cudaMemcpyDeviceToHost, s));
+    CS_CUDA(cudaStreamSynchronize(s));
+    return CS_OK;
+}
+
+// ---------------------------------------------------------------- SDF generation
+
+int cs_sdf_generate(const double *vertices, int64_t nv, const int32_t *triangles, int64_t nt, int32_t nx, int32_t ny,
+                    int32_t nz, const double origin[3], double voxel, float *values_out) {
+    if (!vertices || !triangles || !values_out || !origin) return fail(CS_ERR_VALUE, "null argument");
+    if (nx < 2 || ny < 2 || nz < 2) return fail(CS_ERR_VALUE, "grid dims must be at least 2 per axis");
+    if (!(voxel > 0.0)) return fail(CS_ERR_VALUE, "voxel must be positive");
+    if (nt < 1) return fail(CS_ERR_MESH, "empty mesh");
+    for (int64_t i = 0; i < 3 * nt; ++i)
+        if (triangles[i] < 0 || triangles[i] >= nv) return fail(CS_ERR_MESH, "triangle index out of range");
+    std::string err;
+    int code = sdf_generate(vertices, nv, triangles, nt, nx, ny, nz, origin, voxel, values_out, &err);
+    if (code) return fail(code, "%s", err.c_str());
+    return CS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,44 @@
+#pragma once
+#include "cs_generate.cuh"
+
+namespace cs {
+
+constexpr int REDUCE_BLOCK = 256;
+constexpr int FINALIZE_BLOCK = 128;
+constexpr int FINALIZE_SMEM_POINTS = 512;  // patches up to this many members are staged in shared memory
+constexpr int MAX_KEPT = 64;               // per_patch_cap limit of the GPU path
+constexpr double MERGE_COS = 0.9961946980917455;  // float(np.cos(np.radians(5.0))) (reduction.py:25)
+
+struct ReduceParams {
+    int N, K, batch_size, has_min_depth;
+    double cone, min_depth;
+};
+
+struct ReduceIO {
+    int64_t E;
+    const int64_t *cand_base;
+    int32_t *n_cand;
+    const double *env_min_depth;  // [E] or null: per-env cull (Scene passes -cd, scene.py:219-223)
+    const double *point, *normal, *depth;
+    const int32_t *face;
+    // workspace (rows indexed like candidates)
+    int32_t *order, *label;
+    double *su, *sv;   // sort keys
+    int32_t *sp;       // sort payload
+    int32_t *sh;       // hull/stack scratch: env e uses [2 cand_base(e) + e (4N + 4), + 2 cap_e + 4N + 4)
+    double *gP, *gN, *gD;  // large-patch member staging (rows like candidates)
+    int32_t *patch_off;  // [E+1]
+    // outputs
+    int32_t *n_patch, *n_kept;
+    double *patch_normal, *builder_maxd;
+    int32_t *member_offsets, *members;
+    int32_t *patch_nkept, *kept_cand, *kept_face;
+    double *kept_point, *kept_normal, *kept_depth;
+    double *w_sum, *wp_sum, *wn_sum, *wt_sum, *area, *max_depth;
+    float *stats;
+};
+
+void launch_reduce(const ReduceIO &io, const ReduceParams &p, int64_t max_batch, cudaStream_t s);
+void launch_finalize(const ReduceIO &io, const ReduceParams &p, int sm_count, cudaStream_t s);
+
+}  // namespace cs

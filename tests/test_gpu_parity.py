@@ -1,0 +1,243 @@
+"""GPU parity: the sm_100a path (through libcontactsim_b200.so) against the
+reference's golden outputs and the pinned oracle. Bit-exact, no exclusions:
+the kernels reproduce the reference's IEEE operation order and its BLAS FMA
+patterns."""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import CS_KEYS, GOLDEN, PATCH_KEYS, assert_same, pack_patch_list
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2205_03532_b200 as P
+    from paper_2205_03532_b200 import _native
+
+    _native.lib()  # fails loudly without the library / a GPU
+    return P
+
+
+@pytest.fixture(scope="module")
+def grid64(P, grid64_npz):
+    d = grid64_npz
+    return P.SignedDistanceGrid(d["origin"], float(d["voxel"]), d["dims"], d["values"], (d["aabb_lo"], d["aabb_hi"]))
+
+
+@pytest.fixture(scope="module")
+def nut(P, meshes):
+    return P.TriMesh(meshes["nut_v"], meshes["nut_t"])
+
+
+@pytest.fixture(scope="module")
+def bolt(P, meshes):
+    return P.TriMesh(meshes["bolt_v"], meshes["bolt_t"])
+
+
+def _tf(P, pose7):
+    return P.Transform.from_pose(pose7[:3], pose7[3:])
+
+
+def test_library_loaded(P):
+    from paper_2205_03532_b200 import _native
+
+    assert _native.lib().cs_abi_version() == 1
+
+
+def test_sdf_sample_gradient(P, grid64, sdf_query):
+    q = sdf_query
+    assert np.array_equal(grid64.sample(q["points"]), q["sample"])
+    assert np.array_equal(grid64.gradient(q["points"], normalize=False), q["gradient"])
+    assert np.array_equal(grid64.gradient(q["points"]), q["gradient_n"])
+    pose = _tf(P, q["pose7"])
+    np.testing.assert_array_equal(grid64.sample(q["points"], pose), q["sample_posed"])
+    np.testing.assert_array_equal(grid64.gradient(q["points"], pose), q["gradient_posed"])
+
+
+def test_face_contacts_dropin_bitexact(P, grid64, grid64_npz, meshes, gen64):
+    """Stage 1a: cs_face_contacts fed the reference's tri_verts == numba kernel output."""
+    from oracle import oracle as O
+
+    g = O.Grid.from_npz(grid64_npz)
+    for e in gen64["envs"]:
+        tv = O.tri_verts(gen64[f"e{e}_sdf_pose"], gen64[f"e{e}_mesh_pose"], meshes["nut_v"], meshes["nut_t"])
+        assert hashlib.sha256(tv.tobytes()).hexdigest() == str(gen64[f"e{e}_tri_verts_sha"])
+        cd = float(gen64["cd"])
+        op, ophi, ogr, ofd = O.face_contacts(g, tv, cd)
+        m = len(tv)
+        d_tv = torch.from_numpy(tv).cuda()
+        outs = [torch.zeros((m, 3), dtype=torch.float64, device="cuda"), torch.zeros(m, dtype=torch.float64, device="cuda"),
+                torch.zeros((m, 3), dtype=torch.float64, device="cuda"), torch.full((m,), 7, dtype=torch.uint8, device="cuda")]
+        vals = torch.from_numpy(grid64_npz["values"]).cuda()
+        nx, ny, nz = g.dims
+        P.contacts.face_contacts(vals, nx, ny, nz, *g.origin, g.voxel, d_tv, cd, 12, 0.1 * g.voxel, *outs)
+        gp, gphi, ggr, gfd = (t.cpu().numpy() for t in outs)
+        assert np.array_equal(gfd, ofd), f"env {e}: found flags differ"
+        # both sides zero-initialise, and pruned faces leave point/phi/grad untouched
+        assert np.array_equal(gp, op) and np.array_equal(gphi, ophi) and np.array_equal(ggr, ogr)
+
+
+@pytest.mark.parametrize("e", range(6))
+def test_generate_contacts_r64(P, grid64, nut, gen64, e):
+    pairing = P.CollisionPairing(0, 1)
+    cs = P.generate_contacts(pairing, grid64, nut, _tf(P, gen64[f"e{e}_sdf_pose"]), _tf(P, gen64[f"e{e}_mesh_pose"]),
+                             float(gen64["cd"]))
+    got = {"points": cs.points, "normals": cs.normals, "depths": cs.depths, "faces": cs.face_indices}
+    assert_same(got, gen64, f"e{e}_cs_", CS_KEYS, f"env {e} ")
+
+
+@pytest.mark.parametrize("e", range(6))
+def test_reduce_contacts_r64(P, gen64, e):
+    pre = f"e{e}_"
+    cs = P.ContactSet(gen64[pre + "cs_points"], gen64[pre + "cs_normals"], gen64[pre + "cs_depths"],
+                      gen64[pre + "cs_faces"], 0, 1)
+    patches = P.reduce_contacts(cs, P.ReductionParams(min_depth=-float(gen64["cd"])))
+    assert_same(pack_patch_list(patches, 6), gen64, pre + "pt_", PATCH_KEYS, f"env {e} ")
+
+
+def test_reduce_contacts_synthetic(P, synth):
+    """Eviction + fold, batch sizes 1 / 7 / 512, caps 1..9, cones, min_depth."""
+    for c in synth["cases"]:
+        pre = f"c{c}_"
+        N, K, cone, md, bs = synth[pre + "params"]
+        cs = P.ContactSet(synth[pre + "cs_points"], synth[pre + "cs_normals"], synth[pre + "cs_depths"],
+                          synth[pre + "cs_faces"], 0, 1)
+        rp = P.ReductionParams(int(N), int(K), float(cone), None if np.isnan(md) else float(md), int(bs))
+        patches = P.reduce_contacts(cs, rp)
+        assert_same(pack_patch_list(patches, int(K)), synth, pre + "pt_", PATCH_KEYS, f"case {c} ")
+
+
+def test_batched_collide_r64(P, grid64, nut, gen64):
+    """All six golden envs (two with a moved SDF pose) in one collide call."""
+    envs = list(gen64["envs"])
+    E = len(envs)
+    h_sdf = [P.register_sdf(grid64)] * E
+    h_mesh = [P.register_mesh(nut)] * E
+    sp = np.stack([gen64[f"e{e}_sdf_pose"] for e in envs])
+    mp = np.stack([gen64[f"e{e}_mesh_pose"] for e in envs])
+    res = P.collide(h_sdf, h_mesh, sp, mp, np.full(E, float(gen64["cd"])))
+    for i, e in enumerate(envs):
+        cs = res.contact_set(i)
+        got = {"points": cs.points, "normals": cs.normals, "depths": cs.depths, "faces": cs.face_indices}
+        assert_same(got, gen64, f"e{e}_cs_", CS_KEYS, f"env {e} ")
+        assert_same(pack_patch_list(res.patches(i), 6), gen64, f"e{e}_pt_", PATCH_KEYS, f"env {e} ")
+
+
+def test_sphere_plane_known_answers(P, kat):
+    g = P.SignedDistanceGrid(kat["sphere_origin"], float(kat["sphere_voxel"]), kat["sphere_dims"], kat["sphere_values"],
+                             (kat["sphere_aabb_lo"], kat["sphere_aabb_hi"]))
+    plane = P.TriMesh(kat["plane_v"], kat["plane_t"])
+    for j in range(4):
+        cd = float(kat[f"sp{j}_cd"])
+        cs = P.generate_contacts(P.CollisionPairing(0, 1), g, plane, P.Transform(), _tf(P, kat[f"sp{j}_mesh_pose"]), cd)
+        got = {"points": cs.points, "normals": cs.normals, "depths": cs.depths, "faces": cs.face_indices}
+        assert_same(got, kat, f"sp{j}_cs_", CS_KEYS, f"sphere-plane {j} ")
+        patches = P.reduce_contacts(cs, P.ReductionParams(min_depth=-cd))
+        assert_same(pack_patch_list(patches, 6), kat, f"sp{j}_pt_", PATCH_KEYS, f"sphere-plane {j} ")
+
+
+def test_gpu_sdf_generation_matches_reference(P, bolt, meshes):
+    """cs_sdf_generate reproduces the reference's generate_sdf grids bit for bit."""
+    meta = json.load(open(os.path.join(GOLDEN, "grids.json")))
+    for res in (64, 128, 256):
+        g = P.generate_sdf(bolt, P.SdfResolutionSpec(res, 4))
+        m = meta[f"bolt_r{res}"]
+        assert list(g.dims) == m["dims"]
+        assert g.voxel_size == m["voxel"] and list(g.origin) == m["origin"]
+        assert hashlib.sha256(g.values.tobytes()).hexdigest() == m["sha256"], f"res {res} grid differs"
+    peg = P.TriMesh(meshes["peg_v"], meshes["peg_t"])
+    gp = P.generate_sdf(peg, P.SdfResolutionSpec(64, 4))
+    assert hashlib.sha256(gp.values.tobytes()).hexdigest() == meta["peg_r64"]["sha256"]
+
+
+def test_batched_collide_r256_vs_golden(P, bolt, nut, gen256):
+    g = P.generate_sdf(bolt, P.SdfResolutionSpec(256, 4))
+    envs = list(gen256["envs"])
+    E = len(envs)
+    sp = np.stack([gen256[f"e{e}_sdf_pose"] for e in envs])
+    mp = np.stack([gen256[f"e{e}_mesh_pose"] for e in envs])
+    res = P.collide([P.register_sdf(g)] * E, [P.register_mesh(nut)] * E, sp, mp, np.full(E, float(gen256["cd"])))
+    for i, e in enumerate(envs):
+        cs = res.contact_set(i)
+        got = {"points": cs.points, "normals": cs.normals, "depths": cs.depths, "faces": cs.face_indices}
+        assert_same(got, gen256, f"e{e}_cs_", CS_KEYS, f"env {e} ")
+        assert_same(pack_patch_list(res.patches(i), 6), gen256, f"e{e}_pt_", PATCH_KEYS, f"env {e} ")
+
+
+def test_full_size_1024_envs_vs_oracle(P):
+    """Config 2 at full size: every env's stats against the oracle, a sample of
+    envs field by field, determinism across runs, and Algorithm-1 invariants."""
+    from oracle import oracle as O
+    from paper_2205_03532_b200.scenes import m16_workload
+
+    E = 1024
+    w = m16_workload(E, seed=0)
+    grid, nut = w["grid"], w["nut"]
+    res = P.collide([P.register_sdf(grid)] * E, [P.register_mesh(nut)] * E, w["sdf_pose"], w["mesh_pose"], w["cd"])
+    stats = res.stats.cpu().numpy()
+    n_cand = res.n_cand.cpu().numpy()
+    n_patch = res.n_patch.cpu().numpy()
+    og = O.Grid(grid.values, grid.dims, grid.origin, grid.voxel_size, *grid.mesh_aabb)
+    ost = O.collide_batched(og, nut.vertices, nut.triangles, w["sdf_pose"], w["mesh_pose"], w["cd"])
+    assert np.array_equal(n_cand, ost[:, 0].astype(np.int64))
+    assert np.array_equal(n_patch, ost[:, 1].astype(np.int64))
+    assert np.array_equal(stats[:, 2], ost[:, 2].astype(np.float32))
+    assert np.array_equal(stats[:, 3], ost[:, 3].astype(np.float32))
+    rng = np.random.default_rng(7)
+    for e in rng.choice(E, size=12, replace=False):
+        cs = res.contact_set(int(e))
+        ref = O.generate_contacts(og, nut.vertices, nut.triangles, w["sdf_pose"][e], w["mesh_pose"][e], float(w["cd"][e]))
+        assert np.array_equal(cs.points, ref["points"]) and np.array_equal(cs.normals, ref["normals"])
+        assert np.array_equal(cs.depths, ref["depths"]) and np.array_equal(cs.face_indices, ref["faces"])
+        r = O.reduce_contacts(ref["points"], ref["normals"], ref["depths"], ref["faces"], min_depth=-float(w["cd"][e]))
+        got = pack_patch_list(res.patches(int(e)), 6)
+        for k in ("rep", "nkept", "members", "kept_faces", "wsum", "wp", "wn", "wt", "area", "maxd"):
+            assert np.array_equal(np.asarray(got[k]), np.asarray(r[k])), (int(e), k)
+        # invariants: patches <= N, kept <= K, members partition the candidates,
+        # the deepest candidate of every patch is kept
+        assert len(got["nkept"]) <= 128 and (got["nkept"] <= 6).all()
+        assert np.array_equal(np.sort(got["members"]), np.arange(len(cs)))
+    # bitwise determinism across launches
+    snap = {k: getattr(res, k).clone() for k in ("cand_point", "patch_normal", "kept_point", "w_sum", "area")}
+    res2 = P.collide([P.register_sdf(grid)] * E, [P.register_mesh(nut)] * E, w["sdf_pose"], w["mesh_pose"], w["cd"])
+    for k, v in snap.items():
+        assert torch.equal(getattr(res2, k), v), k
+
+
+def test_errors_map_to_reference_classes(P, grid64, nut):
+    from paper_2205_03532_b200.errors import NonFiniteStateError
+
+    pairing = P.CollisionPairing(0, 1)
+    ok = P.Transform()
+    with pytest.raises(ValueError):
+        P.generate_contacts(pairing, grid64, nut, ok, ok, -1.0)
+    bad = P.Transform(translation=[np.nan, 0.0, 0.0])
+    with pytest.raises(NonFiniteStateError):
+        P.generate_contacts(pairing, grid64, nut, ok, bad, 1e-3)
+    sp = np.tile([0, 0, 0, 1.0, 0, 0, 0], (2, 1))
+    mp = sp.copy()
+    mp[1, 0] = np.inf
+    with pytest.raises(NonFiniteStateError):
+        P.collide([P.register_sdf(grid64)] * 2, [P.register_mesh(nut)] * 2, sp, mp, np.full(2, 1e-3))
+    with pytest.raises(ValueError):
+        P.ReductionParams(max_patches=0)
+    with pytest.raises(ValueError):
+        P.collide([P.register_sdf(grid64)] * 2, [P.register_mesh(nut)] * 2, sp, sp, np.array([1e-3, -1.0]))
+
+
+def test_empty_and_separated(P, grid64, nut):
+    assert P.reduce_contacts(P.ContactSet.empty()) == []
+    far = P.Transform(translation=[1.0, 0.0, 0.0])
+    cs = P.generate_contacts(P.CollisionPairing(0, 1), grid64, nut, P.Transform(), far, 1e-3)
+    assert len(cs) == 0
+    res = P.collide([P.register_sdf(grid64)], [P.register_mesh(nut)], [[0, 0, 0, 1.0, 0, 0, 0]],
+                    [[1.0, 0, 0, 1.0, 0, 0, 0]], [1e-3])
+    assert int(res.n_cand[0]) == 0 and int(res.n_patch[0]) == 0 and res.patches(0) == []
