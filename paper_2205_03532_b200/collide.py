@@ -26,7 +26,6 @@ from .errors import NonFiniteStateError
 from .geometry.mesh import TriMesh
 from .sdf.grid import SignedDistanceGrid
 
-_mesh_handles: "weakref.WeakKeyDictionary[TriMesh, int]" = weakref.WeakKeyDictionary()
 
 
 def _free_mesh(h: int) -> None:
@@ -42,13 +41,13 @@ def register_sdf(grid: SignedDistanceGrid) -> int:
 
 
 def register_mesh(mesh: TriMesh) -> int:
-    h = _mesh_handles.get(mesh)
+    """Upload the mesh to the device mesh store once; freed with the TriMesh."""
+    h = mesh._device_handle
     if h is None:
         out = ctypes.c_int32(-1)
         _native.call("cs_mesh_register", mesh.vertices.ctypes.data, len(mesh.vertices), mesh.triangles.ctypes.data,
                      len(mesh.triangles), ctypes.byref(out))
-        h = int(out.value)
-        _mesh_handles[mesh] = h
+        h = mesh._device_handle = int(out.value)
         weakref.finalize(mesh, _free_mesh, h)
     return h
 

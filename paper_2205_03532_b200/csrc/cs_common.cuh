@@ -230,7 +230,9 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
 }
 
 // Exclusive scan over the block; returns this thread's exclusive prefix and
-// writes the block total to *total. `ws` needs blockDim.x/32 ints of smem.
+// writes the block total to *total. `ws` needs WS_INTS ints of shared memory
+// (one per warp plus the total, so 1024-thread blocks are safe).
+constexpr int WS_INTS = 33;
 __device__ __forceinline__ int block_excl_scan(int v, int *ws, int *total) {
     int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
     int inc = warp_incl_scan(v);
@@ -240,11 +242,11 @@ __device__ __forceinline__ int block_excl_scan(int v, int *ws, int *total) {
         int x = lane < nw ? ws[lane] : 0;
         int xi = warp_incl_scan(x);
         if (lane < nw) ws[lane] = xi - x;
-        if (lane == nw - 1) ws[31] = xi;
+        if (lane == nw - 1) ws[32] = xi;
     }
     __syncthreads();
     int r = ws[wid] + inc - v;
-    *total = ws[31];
+    *total = ws[32];
     __syncthreads();
     return r;
 }

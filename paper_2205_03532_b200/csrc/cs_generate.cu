@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(COMPACT_BLOCK) k_compact(const EnvXf *__restri
                                                            const MeshDesc *__restrict__ meshes,
                                                            const int64_t *__restrict__ cand_base, Staging st,
                                                            Candidates cs, int32_t *__restrict__ n_cand) {
-    __shared__ int ws[32];
+    __shared__ int ws[WS_INTS];
     __shared__ EnvXf sx;
     int e = blockIdx.x;
     if (threadIdx.x < sizeof(EnvXf) / 8)

@@ -205,7 +205,7 @@ __device__ double pairwise(F a, int off, int n) {
 
 struct RedShared {
     ArgMax am[32];
-    int ws[32];
+    int ws[WS_INTS];
     int P;         // number of builders
     int decision;  // 0 append, 1 merge, 2 evict
     int target;
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(REDUCE_BLOCK) k_reduce(ReduceIO io, ReducePara
 // ------------------------------------------------------------------ finalize
 
 __global__ void k_patch_off(int64_t E, const int32_t *__restrict__ n_patch, int32_t *__restrict__ off) {
-    __shared__ int ws[32];
+    __shared__ int ws[WS_INTS];
     int running = 0;
     for (int64_t e0 = 0; e0 < E; e0 += blockDim.x) {
         int64_t e = e0 + threadIdx.x;
@@ -556,7 +556,7 @@ __global__ void k_patch_off(int64_t E, const int32_t *__restrict__ n_patch, int3
 
 struct FinShared {
     ArgMax am[32];
-    int ws[32];
+    int ws[WS_INTS];
     double t1[3], t2[3];
     int H, nkept;
     double area;

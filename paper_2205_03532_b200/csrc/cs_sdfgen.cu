@@ -125,7 +125,7 @@ __global__ void k_cross(const double *__restrict__ tv, int64_t nt, AxisSetup a, 
 
 __global__ void k_scan_serial(const int *__restrict__ counts, int64_t n, int *__restrict__ starts) {
     // single block: chunked block scan
-    __shared__ int ws[32];
+    __shared__ int ws[WS_INTS];
     int running = 0;
     for (int64_t i0 = 0; i0 < n; i0 += blockDim.x) {
         int64_t i = i0 + threadIdx.x;

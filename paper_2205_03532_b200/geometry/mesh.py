@@ -17,7 +17,7 @@ from ..errors import MeshValidationError
 
 
 class TriMesh:
-    __slots__ = ("vertices", "triangles", "face_normals", "_watertight", "_aabb")
+    __slots__ = ("vertices", "triangles", "face_normals", "_watertight", "_aabb", "_device_handle", "__weakref__")
 
     def __init__(self, vertices, triangles):
         v = np.ascontiguousarray(np.asarray(vertices, dtype=np.float64).reshape(-1, 3))
@@ -41,6 +41,7 @@ class TriMesh:
             a.flags.writeable = False
         self._watertight = None
         self._aabb = None
+        self._device_handle = None  # set by collide.register_mesh
 
     def __len__(self) -> int:
         return len(self.triangles)
