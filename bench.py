@@ -183,7 +183,7 @@ def run_reference(args):
 def _reference_grid(bolt, res):
     """Bolt grid for the CPU arm: cached next to the repo by the GPU arm when it ran
     on this box; otherwise generated by the GPU generator if a GPU is present."""
-    cache = os.path.join(ROOT, "gpurun_out", f"bolt_r{res}.npz")
+    cache = os.path.join(ROOT, ".bench_cache", f"bolt_r{res}.npz")
     if os.path.exists(cache):
         d = np.load(cache)
         return {k: d[k] for k in d.files}
@@ -227,8 +227,8 @@ def main():
     grid, nut = w["grid"], w["nut"]
     F = len(nut.triangles)
     if rank == 0:
-        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-        np.savez(os.path.join(ROOT, "gpurun_out", f"bolt_r{args.res}.npz"), values=grid.values, dims=np.array(grid.dims),
+        os.makedirs(os.path.join(ROOT, ".bench_cache"), exist_ok=True)
+        np.savez(os.path.join(ROOT, ".bench_cache", f"bolt_r{args.res}.npz"), values=grid.values, dims=np.array(grid.dims),
                  origin=grid.origin, voxel=grid.voxel_size, lo=grid.mesh_aabb[0], hi=grid.mesh_aabb[1])
     h_sdf, h_mesh = P.register_sdf(grid), P.register_mesh(nut)
     plan = P.Plan([h_sdf] * E, [h_mesh] * E, P.ReductionParams())

@@ -52,6 +52,7 @@ constexpr int MAX_HANDLES = 4096;
 struct SdfEntry {
     bool live = false;
     float *values = nullptr;
+    double *values64 = nullptr;
     size_t bytes = 0;
     SdfDesc desc{};
 };
@@ -102,11 +103,14 @@ struct cs_plan {
     int64_t max_batch = 1;
     int64_t total_cap = 0;
     int64_t nblocks = 0;
+    bool uniform_sdf = false;      // every env samples the same grid
+    GridT<double> uniform_grid{};  // ...whose view then travels as a kernel parameter
     std::vector<void *> allocs;
     // inputs / tables
     int32_t *env_sdf = nullptr, *env_mesh = nullptr;
     int64_t *cand_base = nullptr;
-    int2 *block_map = nullptr;
+    int2 *block_map = nullptr;   // k_faces block -> (env, first face)
+    int32_t *chunk_first = nullptr;  // [E+1] first k_faces block of each env
     EnvXf *xf = nullptr;
     Staging st{};
     Candidates cands{};
@@ -174,12 +178,21 @@ int cs_sdf_register(const float *values, int values_on_device, int32_t nx, int32
     s.bytes = (size_t)n * sizeof(float);
     CS_CUDA(cudaMalloc(&s.values, s.bytes));
     CS_CUDA(cudaMemcpy(s.values, values, s.bytes, values_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+    {   // exact float64 promotion for the plan kernels (no F2F on the hot path)
+        std::vector<float> h32((size_t)n);
+        CS_CUDA(cudaMemcpy(h32.data(), s.values, s.bytes, cudaMemcpyDeviceToHost));
+        std::vector<double> h64(h32.begin(), h32.end());
+        CS_CUDA(cudaMalloc(&s.values64, (size_t)n * sizeof(double)));
+        CS_CUDA(cudaMemcpy(s.values64, h64.data(), (size_t)n * sizeof(double), cudaMemcpyHostToDevice));
+    }
     SdfDesc &d = s.desc;
     d.values = s.values;
+    d.values64 = s.values64;
     d.nx = nx; d.ny = ny; d.nz = nz; d.pad = 0;
     d.ox = origin[0]; d.oy = origin[1]; d.oz = origin[2];
     d.voxel = voxel;
     for (int k = 0; k < 3; ++k) { d.lo[k] = aabb_lo[k]; d.hi[k] = aabb_hi[k]; }
+    d.g64 = cs::make_grid<double>(s.values64, nx, ny, nz, origin[0], origin[1], origin[2], voxel);
     CS_CUDA(cudaMemcpy(d_sdfs + h, &d, sizeof(SdfDesc), cudaMemcpyHostToDevice));
     s.live = true;
     *handle = h;
@@ -191,6 +204,7 @@ int cs_sdf_free(int32_t handle) {
     if (handle < 0 || handle >= (int)g_sdf.size() || !g_sdf[handle].live) return fail(CS_ERR_HANDLE, "bad SDF handle %d", handle);
     SdfEntry &s = g_sdf[handle];
     CS_CUDA(cudaFree(s.values));
+    CS_CUDA(cudaFree(s.values64));
     s = SdfEntry{};
     return CS_OK;
 }
@@ -203,13 +217,13 @@ int cs_sdf_values(int32_t handle, const float **values) {
 }
 
 int cs_sdf_l2_persist(int32_t handle, void *stream, float hit_ratio) {
-    float *base;
+    void *base;
     size_t bytes;
-    {
+    {   // the plan kernels read the float64 copy: that is the array to keep resident
         std::lock_guard<std::mutex> lk(g_mu);
         if (handle < 0 || handle >= (int)g_sdf.size() || !g_sdf[handle].live) return fail(CS_ERR_HANDLE, "bad SDF handle %d", handle);
-        base = g_sdf[handle].values;
-        bytes = g_sdf[handle].bytes;
+        base = g_sdf[handle].values64;
+        bytes = 2 * g_sdf[handle].bytes;
     }
     int dev = 0, max_win = 0, max_persist = 0;
     CS_CUDA(cudaGetDevice(&dev));
@@ -291,9 +305,7 @@ static int make_grid(const float *values, int64_t nx, int64_t ny, int64_t nz, do
     if (nx < 2 || ny < 2 || nz < 2) return fail(CS_ERR_VALUE, "grid dims must be at least 2 per axis");
     if (nx * ny * nz >= ((int64_t)1 << 31)) return fail(CS_ERR_VALUE, "grid exceeds the 2^31 device index range");
     if (!(voxel > 0.0)) return fail(CS_ERR_VALUE, "voxel_size must be positive");
-    g->v = values;
-    g->nx = (int)nx; g->ny = (int)ny; g->nz = (int)nz;
-    g->ox = ox; g->oy = oy; g->oz = oz; g->voxel = voxel;
+    *g = cs::make_grid<float>(values, (int)nx, (int)ny, (int)nz, ox, oy, oz, voxel);
     return CS_OK;
 }
 
@@ -374,6 +386,7 @@ static int plan_buffers(cs_plan *P, const std::vector<int64_t> &cap) {
         A(io.sh, 2 * tot + E * (4 * (int64_t)N + 4));
         A(io.gP, 3 * tot); A(io.gN, 3 * tot); A(io.gD, tot);
         A(io.patch_off, E + 1);
+        A(io.large_list, E * N); A(io.large_count, 1);
         A(io.n_patch, E); A(io.n_kept, E);
         A(io.patch_normal, 3 * E * N); A(io.builder_maxd, E * N);
         A(io.member_offsets, E * (N + 1)); A(io.members, tot);
@@ -419,22 +432,31 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
     }
     std::vector<int64_t> cap((size_t)n_envs);
     std::vector<int2> bmap;
+    std::vector<int32_t> chunk_first;
+    bool uniform = true;
+    GridT<double> ugrid{};
     {
         std::lock_guard<std::mutex> lk(g_mu);
         int r = ensure_tables();
         if (r) return r;
         for (int64_t e = 0; e < n_envs; ++e) {
+            uniform &= sdf_handles[e] == sdf_handles[0];
             int s = sdf_handles[e], m = mesh_handles[e];
             if (s < 0 || s >= MAX_HANDLES || !g_sdf[s].live) return fail(CS_ERR_HANDLE, "env %lld: bad SDF handle %d", (long long)e, s);
             if (m < 0 || m >= MAX_HANDLES || !g_mesh[m].live) return fail(CS_ERR_HANDLE, "env %lld: bad mesh handle %d", (long long)e, m);
             int64_t nt = g_mesh[m].desc.nt;
             cap[(size_t)e] = nt;
+            chunk_first.push_back((int32_t)bmap.size());
             for (int64_t f = 0; f < nt; f += FACE_BLOCK) bmap.push_back(make_int2((int)e, (int)f));
         }
+        if (uniform) ugrid = g_sdf[sdf_handles[0]].desc.g64;
+        chunk_first.push_back((int32_t)bmap.size());
     }
     cs_plan *P = new cs_plan();
     P->E = n_envs;
     P->stages = stages;
+    P->uniform_sdf = uniform;
+    P->uniform_grid = ugrid;
     if (stages & CS_STAGE_REDUCE) {
         P->rp.N = params->max_patches; P->rp.K = params->per_patch_cap; P->rp.batch_size = params->batch_size;
         P->rp.has_min_depth = params->has_min_depth; P->rp.cone = params->normal_cone_cos; P->rp.min_depth = params->min_depth;
@@ -446,7 +468,10 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
     if (!r) r = P->alloc(&P->env_mesh, (size_t)n_envs);
     if (!r) r = P->alloc(&P->block_map, bmap.size());
     if (!r) r = P->alloc(&P->xf, (size_t)n_envs);
-    if (!r) r = P->alloc(&P->st.found, (size_t)P->total_cap);
+    if (!r) r = P->alloc(&P->st.face, (size_t)P->total_cap);
+    if (!r) r = P->alloc(&P->st.chunk_count, bmap.size());
+    if (!r) r = P->alloc(&P->st.chunk_off, bmap.size());
+    if (!r) r = P->alloc(&P->chunk_first, chunk_first.size());
     if (!r) r = P->alloc(&P->st.point, 3 * (size_t)P->total_cap);
     if (!r) r = P->alloc(&P->st.phi, (size_t)P->total_cap);
     if (!r) r = P->alloc(&P->st.grad, 3 * (size_t)P->total_cap);
@@ -459,6 +484,8 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
     cudaError_t ce = cudaMemcpy(P->env_sdf, sdf_handles, sizeof(int32_t) * (size_t)n_envs, cudaMemcpyHostToDevice);
     if (ce == cudaSuccess) ce = cudaMemcpy(P->env_mesh, mesh_handles, sizeof(int32_t) * (size_t)n_envs, cudaMemcpyHostToDevice);
     if (ce == cudaSuccess) ce = cudaMemcpy(P->block_map, bmap.data(), sizeof(int2) * bmap.size(), cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess)
+        ce = cudaMemcpy(P->chunk_first, chunk_first.data(), sizeof(int32_t) * chunk_first.size(), cudaMemcpyHostToDevice);
     if (ce != cudaSuccess) { delete P; return fail(CS_ERR_CUDA, "plan upload: %s", cudaGetErrorString(ce)); }
     *plan = P;
     return CS_OK;
@@ -526,10 +553,11 @@ int cs_collide(cs_plan *P, const double *sdf_pose, const double *mesh_pose, int3
                   P->status, P->env_min_depth, s);
     CS_LAUNCHED();
     mark(1);
-    launch_faces(P->nblocks, P->block_map, P->xf, d_sdfs, d_meshes, P->cand_base, P->st, P->sample_counter, s);
+    launch_faces(P->nblocks, P->block_map, P->xf, d_sdfs, d_meshes, P->cand_base, P->st, P->sample_counter,
+                 P->uniform_sdf ? &P->uniform_grid : nullptr, s);
     CS_LAUNCHED();
     mark(2);
-    launch_compact(P->E, P->xf, d_meshes, P->cand_base, P->st, P->cands, P->io.n_cand, s);
+    launch_compact(P->E, P->xf, P->cand_base, P->block_map, P->chunk_first, P->st, P->cands, P->io.n_cand, s);
     CS_LAUNCHED();
     mark(3);
     if (P->stages & CS_STAGE_REDUCE) {

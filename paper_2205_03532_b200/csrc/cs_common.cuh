@@ -2,6 +2,20 @@
 // double arithmetic is never contracted, so every expression rounds exactly like
 // the reference's numba kernels; the reference's BLAS dot products are
 // reproduced with explicit fma (G3 / V3 below).
+//
+// The SDF sampler is written for the B200 pipes rather than transliterated: it
+// produces the reference's bits (sdf/_kernels.py:253-327) but
+//   * reads a float64 copy of the float32 grid (the promotion is exact), so no
+//     F2F conversions on the XU pipe;
+//   * divides by the voxel size with a reciprocal + two FMA corrections and an
+//     exact remainder check (IEEE division only when the check cannot prove
+//     correct rounding), instead of the MUFU + Newton IEEE division;
+//   * clamps and floors grid coordinates with integer operations on the bit
+//     pattern (no F2I / I2F on the XU pipe); the results are exact;
+//   * skips the outside-distance term for samples inside the grid, where the
+//     reference adds sqrt(0) * voxel == +0.0;
+//   * reuses the per-axis work of the centre point across the six
+//     central-difference samples.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -20,13 +34,6 @@ __device__ __forceinline__ double G3(double a0, double a1, double a2, double b0,
 __device__ __forceinline__ double V3(double a0, double a1, double a2, double b0, double b1, double b2) {
     return __fma_rn(a2, b2, __fma_rn(a0, b0, __dmul_rn(a1, b1)));
 }
-
-struct SdfDesc {
-    const float *values;
-    int32_t nx, ny, nz, pad;
-    double ox, oy, oz, voxel;
-    double lo[3], hi[3];  // mesh AABB (grid.mesh_aabb)
-};
 
 struct MeshDesc {
     const double4 *verts;  // (x, y, z, 0)
@@ -47,66 +54,167 @@ struct EnvXf {
     int32_t pad;
 };
 
-struct GridView {
-    const float *__restrict__ v;
+// Grid + everything the sampler derives from its scalars once.
+template <class T>
+struct GridT {
+    const T *__restrict__ v;
     int nx, ny, nz;
-    double ox, oy, oz, voxel;
+    int sy, sz;
+    double o[3];
+    double voxel, rv;   // voxel, RN(1 / voxel)
+    double h2, rh2;     // 2 voxel, RN(1 / (2 voxel))  (gradient denominator)
+    double nm1[3];      // n - 1 (clamp bound, sdf/_kernels.py:302-304)
+    double nm2[3];      // n - 2 (cell clamp, sdf/_kernels.py:261-270)
+    int n2[3];
 };
 
-__device__ __forceinline__ GridView make_view(const SdfDesc &d) {
-    GridView g;
-    g.v = d.values;
-    g.nx = d.nx; g.ny = d.ny; g.nz = d.nz;
-    g.ox = d.ox; g.oy = d.oy; g.oz = d.oz; g.voxel = d.voxel;
+template <class T>
+__host__ __device__ inline GridT<T> make_grid(const T *v, int nx, int ny, int nz, double ox, double oy, double oz,
+                                               double voxel) {
+    GridT<T> g;
+    g.v = v;
+    g.nx = nx; g.ny = ny; g.nz = nz;
+    g.sy = nx; g.sz = nx * ny;
+    g.o[0] = ox; g.o[1] = oy; g.o[2] = oz;
+    g.voxel = voxel;
+    g.rv = 1.0 / voxel;
+    g.h2 = 2.0 * voxel;
+    g.rh2 = 1.0 / g.h2;
+    g.nm1[0] = nx - 1.0; g.nm1[1] = ny - 1.0; g.nm1[2] = nz - 1.0;
+    g.nm2[0] = nx - 2.0; g.nm2[1] = ny - 2.0; g.nm2[2] = nz - 2.0;
+    g.n2[0] = nx - 2; g.n2[1] = ny - 2; g.n2[2] = nz - 2;
     return g;
 }
+
+using GridView = GridT<float>;  // per-pair drop-ins sample the caller's float32 grid
+
+// Device SDF store entry.
+struct SdfDesc {
+    const float *values;     // the grid as registered (float32, x-fastest)
+    const double *values64;  // exact float64 promotion read by the plan kernels
+    int32_t nx, ny, nz, pad;
+    double ox, oy, oz, voxel;
+    double lo[3], hi[3];  // mesh AABB (grid.mesh_aabb)
+    GridT<double> g64;    // sampler view of values64
+};
 
 __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
 __device__ __forceinline__ double dmax(double a, double b) { return b > a ? b : a; }
 
-// sdf/_kernels.py:253-292
-__device__ __forceinline__ double trilinear(const GridView &g, double gx, double gy, double gz) {
-    int x0 = (int)floor(gx), y0 = (int)floor(gy), z0 = (int)floor(gz);
-    x0 = x0 < 0 ? 0 : x0; x0 = x0 > g.nx - 2 ? g.nx - 2 : x0;
-    y0 = y0 < 0 ? 0 : y0; y0 = y0 > g.ny - 2 ? g.ny - 2 : y0;
-    z0 = z0 < 0 ? 0 : z0; z0 = z0 > g.nz - 2 ? g.nz - 2 : z0;
-    double fx = gx - (double)x0, fy = gy - (double)y0, fz = gz - (double)z0;
-    int sy = g.nx, sz = g.nx * g.ny;
-    const float *p = g.v + (x0 + g.nx * (y0 + g.ny * z0));
-    double c000 = __ldg(p), c100 = __ldg(p + 1), c010 = __ldg(p + sy), c110 = __ldg(p + 1 + sy);
-    double c001 = __ldg(p + sz), c101 = __ldg(p + 1 + sz), c011 = __ldg(p + sy + sz), c111 = __ldg(p + 1 + sy + sz);
-    double ox = 1.0 - fx, oy = 1.0 - fy, oz = 1.0 - fz;
-    double c00 = c000 * ox + c100 * fx;
-    double c10 = c010 * ox + c110 * fx;
-    double c01 = c001 * ox + c101 * fx;
-    double c11 = c011 * ox + c111 * fx;
-    double c0 = c00 * oy + c10 * fy;
-    double c1 = c01 * oy + c11 * fy;
-    return c0 * oz + c1 * fz;
+// RN(a / b) for b > 0 normal, given rb = RN(1 / b): one reciprocal multiply and
+// a Markstein correction, then the exact remainder r2 = a - q b proves q is the
+// correctly rounded quotient (|r2| below b times half the spacing of q); if the
+// proof fails the IEEE division is used. Bit-identical to a / b. The threshold is
+// assembled on the high word only (32-bit integer ops).
+__device__ __forceinline__ double div_rn(double a, double b, double rb) {
+    double q = a * rb;
+    double r = __fma_rn(-q, b, a);
+    q = __fma_rn(r, rb, q);
+    double r2 = __fma_rn(-q, b, a);
+    const int qh = __double2hiint(q);
+    const int E = (qh >> 20) & 0x7ff;
+    // b * 2^(E - 1023 - 53), halved when q is a power of two and the quotient lies below it
+    int sh = E - 1076;
+    if (((qh & 0xfffff) | __double2loint(q)) == 0 && ((r2 < 0.0) != (q < 0.0))) sh -= 1;
+    const double thr = __hiloint2double(__double2hiint(b) + (sh << 20), __double2loint(b));
+    if (E >= 120 && E <= 2000 && fabs(r2) < thr) return q;
+    return a / b;  // zero, tiny/huge quotients, and unproven roundings (never seen in practice)
 }
 
-// sdf/_kernels.py:295-309
-__device__ __forceinline__ double sample(const GridView &g, double px, double py, double pz) {
-    double gx = (px - g.ox) / g.voxel;
-    double gy = (py - g.oy) / g.voxel;
-    double gz = (pz - g.oz) / g.voxel;
-    double cx = dmin(dmax(gx, 0.0), (double)g.nx - 1.0);
-    double cy = dmin(dmax(gy, 0.0), (double)g.ny - 1.0);
-    double cz = dmin(dmax(gz, 0.0), (double)g.nz - 1.0);
-    double dx = gx - cx, dy = gy - cy, dz = gz - cz;
-    double out = dx * dx + dy * dy + dz * dz;
-    double t = trilinear(g, cx, cy, cz);
-    // sqrt(0) * voxel == 0 exactly: skip the sqrt for the (98.6%) inside samples.
-    return out == 0.0 ? t + 0.0 * g.voxel : t + sqrt(out) * g.voxel;
+// One axis of a sample (sdf/_kernels.py:299-308, 256-273): c = min(max(g, 0.0), n - 1.0)
+// (numba's max/min keep -0.0), d = g - c (the outside-distance component),
+// i = min(floor(c), n - 2), f = c - i.
+struct Axis {
+    double f, d;
+    int i;
+};
+
+__device__ __forceinline__ Axis make_axis(double g, double nm1, double nm2, int n2) {
+    Axis a;
+    const bool lo = g < 0.0;
+    double c = lo ? 0.0 : g;
+    const bool hi = nm1 < c;
+    c = hi ? nm1 : c;
+    a.d = (lo || hi) ? g - c : 0.0;  // g - c is exactly 0 when not clamped
+    int ip = __double2int_rd(c);      // floor (c >= 0)
+    double fl = __int2double_rn(ip);
+    if (ip > n2) { ip = n2; fl = nm2; }
+    a.i = ip;
+    a.f = c - fl;
+    return a;
 }
 
-// sdf/_kernels.py:312-327
-__device__ __forceinline__ void gradient(const GridView &g, double px, double py, double pz, double &gx, double &gy,
+template <class T>
+__device__ __forceinline__ double ld(const T *p) { return (double)__ldg(p); }
+
+// sample_point with the per-axis work precomputed (sdf/_kernels.py:253-309)
+template <class T>
+__device__ __forceinline__ double sample_axes(const GridT<T> &g, const Axis &ax, const Axis &ay, const Axis &az) {
+    const T *p = g.v + (ax.i + g.nx * (ay.i + g.ny * az.i));
+    const int sy = g.sy, sz = g.sz;
+    double c000 = ld(p), c100 = ld(p + 1), c010 = ld(p + sy), c110 = ld(p + 1 + sy);
+    double c001 = ld(p + sz), c101 = ld(p + 1 + sz), c011 = ld(p + sy + sz), c111 = ld(p + 1 + sy + sz);
+    double ox = 1.0 - ax.f, oy = 1.0 - ay.f, oz = 1.0 - az.f;
+    double c00 = c000 * ox + c100 * ax.f;
+    double c10 = c010 * ox + c110 * ax.f;
+    double c01 = c001 * ox + c101 * ax.f;
+    double c11 = c011 * ox + c111 * ax.f;
+    double c0 = c00 * oy + c10 * ay.f;
+    double c1 = c01 * oy + c11 * ay.f;
+    double t = c0 * oz + c1 * az.f;
+    // inside the grid the reference adds sqrt(0) * voxel == +0.0
+    if ((__double_as_longlong(ax.d) | __double_as_longlong(ay.d) | __double_as_longlong(az.d)) == 0) return t + 0.0;
+    return t + sqrt(ax.d * ax.d + ay.d * ay.d + az.d * az.d) * g.voxel;
+}
+
+template <class T>
+__device__ __forceinline__ Axis axis_at(const GridT<T> &g, int k, double p) {
+    return make_axis(div_rn(p - g.o[k], g.voxel, g.rv), g.nm1[k], g.nm2[k], g.n2[k]);
+}
+
+// A point with its three axes (so the gradient can reuse them).
+struct GPoint {
+    double x, y, z;
+    Axis ax, ay, az;
+};
+
+template <class T>
+__device__ __forceinline__ GPoint gpoint(const GridT<T> &g, double x, double y, double z) {
+    GPoint q;
+    q.x = x; q.y = y; q.z = z;
+    q.ax = axis_at(g, 0, x);
+    q.ay = axis_at(g, 1, y);
+    q.az = axis_at(g, 2, z);
+    return q;
+}
+
+template <class T>
+__device__ __forceinline__ double sample(const GridT<T> &g, double px, double py, double pz) {
+    return sample_axes(g, axis_at(g, 0, px), axis_at(g, 1, py), axis_at(g, 2, pz));
+}
+
+template <class T>
+__device__ __forceinline__ double sample(const GridT<T> &g, const GPoint &q) {
+    return sample_axes(g, q.ax, q.ay, q.az);
+}
+
+// gradient_point (sdf/_kernels.py:312-327): offsets added in metres before the
+// grid conversion, so only the shifted axis is recomputed per sample.
+template <class T>
+__device__ __forceinline__ void gradient(const GridT<T> &g, const GPoint &p, double &gx, double &gy, double &gz) {
+    const double h = g.voxel;
+    gx = div_rn(sample_axes(g, axis_at(g, 0, p.x + h), p.ay, p.az) - sample_axes(g, axis_at(g, 0, p.x - h), p.ay, p.az),
+                g.h2, g.rh2);
+    gy = div_rn(sample_axes(g, p.ax, axis_at(g, 1, p.y + h), p.az) - sample_axes(g, p.ax, axis_at(g, 1, p.y - h), p.az),
+                g.h2, g.rh2);
+    gz = div_rn(sample_axes(g, p.ax, p.ay, axis_at(g, 2, p.z + h)) - sample_axes(g, p.ax, p.ay, axis_at(g, 2, p.z - h)),
+                g.h2, g.rh2);
+}
+
+template <class T>
+__device__ __forceinline__ void gradient(const GridT<T> &g, double px, double py, double pz, double &gx, double &gy,
                                          double &gz) {
-    double h = g.voxel, h2 = 2.0 * g.voxel;
-    gx = (sample(g, px + h, py, pz) - sample(g, px - h, py, pz)) / h2;
-    gy = (sample(g, px, py + h, pz) - sample(g, px, py - h, pz)) / h2;
-    gz = (sample(g, px, py, pz + h) - sample(g, px, py, pz - h)) / h2;
+    gradient(g, gpoint(g, px, py, pz), gx, gy, gz);
 }
 
 // sdf/_kernels.py:20-61
@@ -159,32 +267,30 @@ struct FaceResult {
 // The final gradient equals the last in-loop gradient whenever the point did not
 // move after it (same input -> same value), so it is reused in that case.
 // COUNT: tally trilinear samples in r.nsamp (roofline accounting).
-template <bool COUNT = false>
-__device__ __forceinline__ bool face_body(const GridView &g, double ax, double ay, double az, double bx, double by,
+template <bool COUNT = false, class T>
+__device__ __forceinline__ bool face_body(const GridT<T> &g, double ax, double ay, double az, double bx, double by,
                                           double bz, double cx, double cy, double cz, double cd, int max_iters,
                                           double tol, FaceResult &r) {
     if (COUNT) r.nsamp = 3;
-    double phi_a = sample(g, ax, ay, az);
-    double phi_b = sample(g, bx, by, bz);
-    double phi_c = sample(g, cx, cy, cz);
+    double phi_a = sample(g, ax, ay, az), phi_b = sample(g, bx, by, bz), phi_c = sample(g, cx, cy, cz);
     double e0 = sqrt((bx - ax) * (bx - ax) + (by - ay) * (by - ay) + (bz - az) * (bz - az));
     double e1 = sqrt((cx - bx) * (cx - bx) + (cy - by) * (cy - by) + (cz - bz) * (cz - bz));
     double e2 = sqrt((ax - cx) * (ax - cx) + (ay - cy) * (ay - cy) + (az - cz) * (az - cz));
     double diam = dmax(e0, dmax(e1, e2));
     double phi_min = dmin(phi_a, dmin(phi_b, phi_c));
     if (phi_min - diam > cd) return false;
-    double gxc = (ax + bx + cx) / 3.0, gyc = (ay + by + cy) / 3.0, gzc = (az + bz + cz) / 3.0;
-    double phi = sample(g, gxc, gyc, gzc);
+    double sx = (ax + bx + cx) / 3.0, sy = (ay + by + cy) / 3.0, sz = (az + bz + cz) / 3.0;
+    double phi = sample(g, sx, sy, sz);
     if (COUNT) r.nsamp += 1;
-    double px = gxc, py = gyc, pz = gzc;
-    if (phi_a < phi) { px = ax; py = ay; pz = az; phi = phi_a; }
-    if (phi_b < phi) { px = bx; py = by; pz = bz; phi = phi_b; }
-    if (phi_c < phi) { px = cx; py = cy; pz = cz; phi = phi_c; }
+    if (phi_a < phi) { sx = ax; sy = ay; sz = az; phi = phi_a; }
+    if (phi_b < phi) { sx = bx; sy = by; sz = bz; phi = phi_b; }
+    if (phi_c < phi) { sx = cx; sy = cy; sz = cz; phi = phi_c; }
+    GPoint p = gpoint(g, sx, sy, sz);  // axes recomputed (same inputs, same bits)
     double alpha = g.voxel, amax = 4.0 * g.voxel;
     double grx = 0.0, gry = 0.0, grz = 0.0;
-    bool have_grad = false;  // gradient at the current (px,py,pz) is in gr*
+    bool have_grad = false;  // gradient at the current p is in gr*
     for (int it = 0; it < max_iters; ++it) {
-        gradient(g, px, py, pz, grx, gry, grz);
+        gradient(g, p, grx, gry, grz);
         if (COUNT) r.nsamp += 6;
         have_grad = true;
         double gnorm = sqrt(grx * grx + gry * gry + grz * grz);
@@ -193,13 +299,15 @@ __device__ __forceinline__ bool face_body(const GridView &g, double ax, double a
         double moved = 0.0;
         for (int bt = 0; bt < 4; ++bt) {
             double qx, qy, qz;
-            closest_point(ax, ay, az, bx, by, bz, cx, cy, cz, px - alpha * ux, py - alpha * uy, pz - alpha * uz, qx,
-                          qy, qz);
-            double phi_new = sample(g, qx, qy, qz);
+            closest_point(ax, ay, az, bx, by, bz, cx, cy, cz, p.x - alpha * ux, p.y - alpha * uy, p.z - alpha * uz,
+                          qx, qy, qz);
+            GPoint q = gpoint(g, qx, qy, qz);
+            double phi_new = sample(g, q);
             if (COUNT) r.nsamp += 1;
             if (phi_new < phi) {
-                moved = sqrt((qx - px) * (qx - px) + (qy - py) * (qy - py) + (qz - pz) * (qz - pz));
-                px = qx; py = qy; pz = qz; phi = phi_new;
+                moved = sqrt((qx - p.x) * (qx - p.x) + (qy - p.y) * (qy - p.y) + (qz - p.z) * (qz - p.z));
+                p = q;
+                phi = phi_new;
                 have_grad = false;
                 alpha = dmin(alpha * 1.5, amax);
                 break;
@@ -209,10 +317,10 @@ __device__ __forceinline__ bool face_body(const GridView &g, double ax, double a
         if (moved < tol) break;
     }
     if (!have_grad) {
-        gradient(g, px, py, pz, grx, gry, grz);
+        gradient(g, p, grx, gry, grz);
         if (COUNT) r.nsamp += 6;
     }
-    r.px = px; r.py = py; r.pz = pz; r.phi = phi;
+    r.px = p.x; r.py = p.y; r.pz = p.z; r.phi = phi;
     r.gx = grx; r.gy = gry; r.gz = grz;
     return true;
 }

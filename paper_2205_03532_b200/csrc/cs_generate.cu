@@ -87,100 +87,119 @@ __device__ __forceinline__ double3 to_grid(const EnvXf &X, double4 v) {
     return r;
 }
 
-template <bool COUNT>
+// UNIFORM: every env of the plan samples the same SDF, passed by value so its
+// scalars are constant-bank operands; otherwise the env's SDF view is staged in
+// shared memory per block.
+template <bool COUNT, bool UNIFORM>
 __global__ void __launch_bounds__(FACE_BLOCK) k_faces(const int2 *__restrict__ block_map, const EnvXf *__restrict__ xf,
                                                       const SdfDesc *__restrict__ sdfs,
                                                       const MeshDesc *__restrict__ meshes,
                                                       const int64_t *__restrict__ cand_base, Staging st,
-                                                      unsigned long long *__restrict__ counter) {
+                                                      unsigned long long *__restrict__ counter,
+                                                      const GridT<double> gu) {
     __shared__ EnvXf sx;
+    __shared__ GridT<double> sg;
     int2 bm = block_map[blockIdx.x];
     int e = bm.x;
     if (threadIdx.x < sizeof(EnvXf) / 8)
         reinterpret_cast<double *>(&sx)[threadIdx.x] = reinterpret_cast<const double *>(xf + e)[threadIdx.x];
     __syncthreads();
+    if (!UNIFORM) {
+        static_assert(sizeof(GridT<double>) % 8 == 0 && sizeof(GridT<double>) / 8 <= FACE_BLOCK, "GridT copy");
+        if (threadIdx.x < sizeof(GridT<double>) / 8)
+            reinterpret_cast<double *>(&sg)[threadIdx.x] = reinterpret_cast<const double *>(&sdfs[sx.sdf].g64)[threadIdx.x];
+        __syncthreads();
+    }
+    const GridT<double> &grid = UNIFORM ? gu : sg;
     const MeshDesc M = meshes[sx.mesh];
-    int64_t f = (int64_t)bm.y + threadIdx.x;
-    if (f >= M.nt) return;
-    int64_t slot = cand_base[e] + f;
-    if (sx.status != 0) { st.found[slot] = 0; return; }
-    int4 tri = __ldg(M.tris + f);
-    double3 a = to_grid(sx, ld_vert(M.verts + tri.x));
-    double3 b = to_grid(sx, ld_vert(M.verts + tri.y));
-    double3 c = to_grid(sx, ld_vert(M.verts + tri.z));
-    // AABB cull (generation.py:74-83)
-    bool near = dmin(dmin(a.x, b.x), c.x) <= sx.cull_hi[0] && dmax(dmax(a.x, b.x), c.x) >= sx.cull_lo[0] &&
-                dmin(dmin(a.y, b.y), c.y) <= sx.cull_hi[1] && dmax(dmax(a.y, b.y), c.y) >= sx.cull_lo[1] &&
-                dmin(dmin(a.z, b.z), c.z) <= sx.cull_hi[2] && dmax(dmax(a.z, b.z), c.z) >= sx.cull_lo[2];
-    uint8_t found = 0;
-    if (near) {
-        GridView g = make_view(sdfs[sx.sdf]);
-        FaceResult r;
-        bool computed = face_body<COUNT>(g, a.x, a.y, a.z, b.x, b.y, b.z, c.x, c.y, c.z, sx.cd, MAX_MINIMIZE_ITERS,
-                                         sx.tol, r);
-        if (COUNT) atomicAdd(counter, (unsigned long long)r.nsamp);
-        if (computed && r.phi <= sx.cd) {
-            found = 1;
-            st.point[3 * slot + 0] = r.px;
-            st.point[3 * slot + 1] = r.py;
-            st.point[3 * slot + 2] = r.pz;
-            st.phi[slot] = r.phi;
-            st.grad[3 * slot + 0] = r.gx;
-            st.grad[3 * slot + 1] = r.gy;
-            st.grad[3 * slot + 2] = r.gz;
+    const int64_t f = (int64_t)bm.y + threadIdx.x;
+    bool found = false;
+    FaceResult r;
+    if (f < M.nt && sx.status == 0) {
+        int4 tri = __ldg(M.tris + f);
+        double3 a = to_grid(sx, ld_vert(M.verts + tri.x));
+        double3 b = to_grid(sx, ld_vert(M.verts + tri.y));
+        double3 c = to_grid(sx, ld_vert(M.verts + tri.z));
+        // AABB cull (generation.py:74-83)
+        bool near = dmin(dmin(a.x, b.x), c.x) <= sx.cull_hi[0] && dmax(dmax(a.x, b.x), c.x) >= sx.cull_lo[0] &&
+                    dmin(dmin(a.y, b.y), c.y) <= sx.cull_hi[1] && dmax(dmax(a.y, b.y), c.y) >= sx.cull_lo[1] &&
+                    dmin(dmin(a.z, b.z), c.z) <= sx.cull_hi[2] && dmax(dmax(a.z, b.z), c.z) >= sx.cull_lo[2];
+        if (near) {
+            bool computed = face_body<COUNT>(grid, a.x, a.y, a.z, b.x, b.y, b.z, c.x, c.y, c.z, sx.cd,
+                                             MAX_MINIMIZE_ITERS, sx.tol, r);
+            if (COUNT) atomicAdd(counter, (unsigned long long)r.nsamp);
+            found = computed && r.phi <= sx.cd;
         }
     }
-    st.found[slot] = found;
+    // chunk-local ordered compaction: this block's found faces land at the start of
+    // its staging rows in ascending face order; k_compact stitches the chunks.
+    __shared__ int ws[WS_INTS];
+    int total;
+    const int pos = block_excl_scan(found ? 1 : 0, ws, &total);
+    if (found) {
+        const int64_t s = cand_base[e] + bm.y + pos;
+        st.point[3 * s + 0] = r.px;
+        st.point[3 * s + 1] = r.py;
+        st.point[3 * s + 2] = r.pz;
+        st.phi[s] = r.phi;
+        st.grad[3 * s + 0] = r.gx;
+        st.grad[3 * s + 1] = r.gy;
+        st.grad[3 * s + 2] = r.gz;
+        st.face[s] = (int32_t)f;
+    }
+    if (threadIdx.x == 0) st.chunk_count[blockIdx.x] = total;
 }
 
-// Ordered compaction of found faces + world-frame epilogue (generation.py:98-114).
+// Stitch the per-chunk compacted rows into the env's candidate list (ascending
+// face order) and apply the world-frame epilogue (generation.py:98-114).
+// One CTA per env: chunk offsets by a block scan, then one warp per chunk.
 __global__ void __launch_bounds__(COMPACT_BLOCK) k_compact(const EnvXf *__restrict__ xf,
-                                                           const MeshDesc *__restrict__ meshes,
-                                                           const int64_t *__restrict__ cand_base, Staging st,
+                                                           const int64_t *__restrict__ cand_base,
+                                                           const int2 *__restrict__ block_map,
+                                                           const int32_t *__restrict__ chunk_first, Staging st,
                                                            Candidates cs, int32_t *__restrict__ n_cand) {
     __shared__ int ws[WS_INTS];
     __shared__ EnvXf sx;
-    int e = blockIdx.x;
+    const int e = blockIdx.x;
     if (threadIdx.x < sizeof(EnvXf) / 8)
         reinterpret_cast<double *>(&sx)[threadIdx.x] = reinterpret_cast<const double *>(xf + e)[threadIdx.x];
-    __syncthreads();
-    const int64_t nt = meshes[sx.mesh].nt;
+    const int c0 = chunk_first[e], nch = chunk_first[e + 1] - c0;
     const int64_t base = cand_base[e];
-    const uint8_t *fd = st.found + base;
-    // pass 1: count (the world transform's BLAS path depends on the total, C >= 2 -> G3)
-    int cnt = 0;
-    for (int64_t f = threadIdx.x; f < nt; f += blockDim.x) cnt += fd[f];
-    int total;
-    block_excl_scan(cnt, ws, &total);
-    const bool gemm = total >= 2;
-    // pass 2: ordered write
     int running = 0;
-    for (int64_t f0 = 0; f0 < nt; f0 += blockDim.x) {
-        int64_t f = f0 + threadIdx.x;
-        int flag = (f < nt) ? fd[f] : 0;
-        int chunk;
-        int pos = running + block_excl_scan(flag, ws, &chunk);
-        if (flag) {
-            int64_t s = base + f, d = base + pos;
+    for (int j0 = 0; j0 < nch; j0 += blockDim.x) {
+        const int j = j0 + threadIdx.x;
+        const int v = j < nch ? st.chunk_count[c0 + j] : 0;
+        int tot;
+        const int x = block_excl_scan(v, ws, &tot);
+        if (j < nch) st.chunk_off[c0 + j] = running + x;
+        running += tot;
+    }
+    __syncthreads();
+    const int C = running;
+    const bool gemm = C >= 2;  // the world transform's BLAS path (C >= 2 -> G3)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int j = wid; j < nch; j += nw) {
+        const int cnt = st.chunk_count[c0 + j];
+        const int64_t src0 = base + block_map[c0 + j].y;
+        const int64_t dst0 = base + st.chunk_off[c0 + j];
+        for (int i = lane; i < cnt; i += 32) {
+            const int64_t s = src0 + i, d = dst0 + i;
             double px = st.point[3 * s], py = st.point[3 * s + 1], pz = st.point[3 * s + 2];
             double gx = st.grad[3 * s], gy = st.grad[3 * s + 1], gz = st.grad[3 * s + 2];
             double nrm = sqrt(gx * gx + gy * gy + gz * gz);  // np.linalg.norm(axis=1): ((x2+y2)+z2)
             if (nrm < 1e-12) { gx = 0.0; gy = 0.0; gz = 1.0; nrm = 1.0; }
-            double nx = gx / nrm, ny = gy / nrm, nz = gz / nrm;
-            const double *R = sx.Rs;
-            for (int j = 0; j < 3; ++j) {
-                const double *r = R + 3 * j;
-                double nw = gemm ? G3(nx, ny, nz, r[0], r[1], r[2]) : V3(nx, ny, nz, r[0], r[1], r[2]);
-                double pw = (gemm ? G3(px, py, pz, r[0], r[1], r[2]) : V3(px, py, pz, r[0], r[1], r[2])) + sx.ts[j];
-                cs.normal[3 * d + j] = nw;
-                cs.point[3 * d + j] = pw;
+            const double nx = gx / nrm, ny = gy / nrm, nz = gz / nrm;
+            for (int k = 0; k < 3; ++k) {
+                const double *rr = sx.Rs + 3 * k;
+                cs.normal[3 * d + k] = gemm ? G3(nx, ny, nz, rr[0], rr[1], rr[2]) : V3(nx, ny, nz, rr[0], rr[1], rr[2]);
+                cs.point[3 * d + k] =
+                    (gemm ? G3(px, py, pz, rr[0], rr[1], rr[2]) : V3(px, py, pz, rr[0], rr[1], rr[2])) + sx.ts[k];
             }
             cs.depth[d] = -st.phi[s];
-            cs.face[d] = (int32_t)f;
+            cs.face[d] = st.face[s];
         }
-        running += chunk;
     }
-    if (threadIdx.x == 0) n_cand[e] = running;
+    if (threadIdx.x == 0) n_cand[e] = C;
 }
 
 // ---------------------------------------------------------------- per-pair drop-ins
@@ -224,17 +243,24 @@ void launch_env_xf(int64_t E, const int32_t *env_sdf, const int32_t *env_mesh, c
 
 void launch_faces(int64_t nblocks, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs,
                   const MeshDesc *meshes, const int64_t *cand_base, const Staging &st, unsigned long long *counter,
-                  cudaStream_t s) {
+                  const GridT<double> *uniform, cudaStream_t s) {
     if (nblocks <= 0) return;
-    if (counter)
-        k_faces<true><<<(unsigned)nblocks, FACE_BLOCK, 0, s>>>(block_map, xf, sdfs, meshes, cand_base, st, counter);
-    else
-        k_faces<false><<<(unsigned)nblocks, FACE_BLOCK, 0, s>>>(block_map, xf, sdfs, meshes, cand_base, st, nullptr);
+    const GridT<double> gu = uniform ? *uniform : GridT<double>{};
+    const unsigned nb = (unsigned)nblocks;
+    if (uniform) {
+        if (counter) k_faces<true, true><<<nb, FACE_BLOCK, 0, s>>>(block_map, xf, sdfs, meshes, cand_base, st, counter, gu);
+        else k_faces<false, true><<<nb, FACE_BLOCK, 0, s>>>(block_map, xf, sdfs, meshes, cand_base, st, nullptr, gu);
+    } else {
+        if (counter) k_faces<true, false><<<nb, FACE_BLOCK, 0, s>>>(block_map, xf, sdfs, meshes, cand_base, st, counter, gu);
+        else k_faces<false, false><<<nb, FACE_BLOCK, 0, s>>>(block_map, xf, sdfs, meshes, cand_base, st, nullptr, gu);
+    }
 }
 
-void launch_compact(int64_t E, const EnvXf *xf, const MeshDesc *meshes, const int64_t *cand_base,
-                    const Staging &st, const Candidates &cs, int32_t *n_cand, cudaStream_t s) {
-    if (E > 0) k_compact<<<(unsigned)E, COMPACT_BLOCK, 0, s>>>(xf, meshes, cand_base, st, cs, n_cand);
+void launch_compact(int64_t E, const EnvXf *xf, const int64_t *cand_base, const int2 *block_map,
+                    const int32_t *chunk_first, const Staging &st, const Candidates &cs, int32_t *n_cand,
+                    cudaStream_t s) {
+    if (E > 0)
+        k_compact<<<(unsigned)E, COMPACT_BLOCK, 0, s>>>(xf, cand_base, block_map, chunk_first, st, cs, n_cand);
 }
 
 void launch_face_contacts(const GridView &g, const double *tv, int64_t m, double cd, int max_iters, double tol,

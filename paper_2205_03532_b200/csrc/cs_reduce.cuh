@@ -28,6 +28,7 @@ struct ReduceIO {
     int32_t *sh;       // hull/stack scratch: env e uses [2 cand_base(e) + e (4N + 4), + 2 cap_e + 4N + 4)
     double *gP, *gN, *gD;  // large-patch member staging (rows like candidates)
     int32_t *patch_off;  // [E+1]
+    int32_t *large_list, *large_count;  // finalize work list of patches above FIN_SMALL members
     // outputs
     int32_t *n_patch, *n_kept;
     double *patch_normal, *builder_maxd;
