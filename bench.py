@@ -34,7 +34,7 @@ sys.path.insert(0, ROOT)
 METRIC = "SDF contact queries/s & collide-step ms, 1024 nut-bolt envs, 1/2/4/8 B200"
 UNIT = "queries/s"
 PAPER_QPS = 1024 * 17798 / 11e-3  # PAPER.md:227,584 (A5000, whole contact-handling step), derived
-LAUNCHES_PER_STEP = 7  # k_env_xf, k_faces, k_compact, k_reduce, k_patch_off, k_finalize, k_stats
+LAUNCHES_PER_STEP = 8  # k_env_xf, k_face_prep, k_face_pgd, k_compact, k_reduce, k_patch_off, k_finalize, k_stats
 
 
 def parse():
@@ -109,9 +109,9 @@ def measured_peaks() -> dict:
 
 
 def ncu_traffic():
-    """dram bytes per k_faces launch from the committed ncu capture, if present."""
+    """dram bytes per k_face_pgd launch from the committed ncu capture, if present."""
     try:
-        with open(os.path.join(ROOT, "profiles", "k_faces_ncu.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "k_face_pgd_ncu.json")) as fh:
             return json.load(fh).get("dram_bytes_per_launch")
     except (OSError, ValueError):
         return None
@@ -241,7 +241,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     # exact sample count of one step (counting build, outside the timed region)
-    samples = plan.count_samples(sp, mp, cd)
+    samples_prep, samples_pgd = plan.count_samples(sp, mp, cd)
     for _ in range(max(3, args.warmup)):
         plan.collide(sp, mp, cd)
     torch.cuda.synchronize()
@@ -260,7 +260,7 @@ def main():
         dist.barrier()
     clk = clocks.stop()
     phases = plan.read_timing(args.steps)
-    total_ms = float(phases[:, 5].sum())
+    total_ms = float(phases[:, plan.PHASES.index("total")].sum())
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -272,11 +272,13 @@ def main():
     stats = gather_env_stats(plan.stats.clone(), E * world)
     plan.enable_timing(0)
 
-    # roofline of the dominant kernel (k_faces): SURVEY §8(d) bytes / live event time
-    faces_ms = float(phases[:, 1].mean())
-    alg_bytes = 48.0 * E * F + 32.0 * samples
+    # roofline of the dominant kernel (k_face_pgd): SURVEY §8(d) bytes / live event time
+    pgd_ms = float(phases[:, plan.PHASES.index("face_pgd")].mean())
+    alg_bytes = 32.0 * samples_pgd
     peaks = measured_peaks()
-    achieved = alg_bytes / (faces_ms * 1e-3) / 1e9
+    achieved = alg_bytes / (pgd_ms * 1e-3) / 1e9
+    faces_ms = pgd_ms + float(phases[:, plan.PHASES.index("face_prep")].mean())
+    faces_bytes = 48.0 * E * F + 32.0 * (samples_prep + samples_pgd)
     mean_phase = {n: float(phases[:, i].mean()) for i, n in enumerate(plan.PHASES)}
 
     # end-to-end through the public API with host buffers (H2D poses, D2H stats)
@@ -316,12 +318,16 @@ def main():
             "e2e": e2e,
             "gpu_launches": LAUNCHES_PER_STEP * args.steps,
             "phase_ms": mean_phase,
-            "roofline": {"kernel": "k_faces", "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
+            "roofline": {"kernel": "k_face_pgd", "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                          "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic(),
                          "peak_source": peaks["source"],
-                         "alg_bytes_per_launch": alg_bytes, "samples_per_launch": samples,
-                         "basis": "48 B per face query + 32 B per trilinear sample (SURVEY §8(d)); "
-                                  "samples counted exactly by the counting build of k_faces"},
+                         "alg_bytes_per_launch": alg_bytes, "samples_per_launch": samples_pgd,
+                         "basis": "32 B per trilinear sample (8 float32 corners, SURVEY §8(d)); samples counted "
+                                  "exactly by the counting build of k_face_pgd",
+                         "faces_phase": {"kernels": "k_face_prep + k_face_pgd", "ms": faces_ms,
+                                         "alg_bytes": faces_bytes, "samples": samples_prep + samples_pgd,
+                                         "achieved_gbs": faces_bytes / (faces_ms * 1e-3) / 1e9,
+                                         "basis": "48 B per face query + 32 B per trilinear sample"}},
             "clocks": clk,
             "stats": {"candidates_per_env": float(stats[:, 0].double().mean()),
                       "patches_per_env": float(stats[:, 1].double().mean()),

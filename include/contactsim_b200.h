@@ -164,15 +164,18 @@ int cs_collide(cs_plan *plan, const double *sdf_pose, const double *mesh_pose, i
  * stream around its phases into a ring of `slots` steps (0 disables).
  * cs_plan_timing_read writes, per recorded step (oldest first, at most
  * max_steps), CS_TIMING_PHASES floats in ms:
- *   [env_xf, faces, compact, reduce, finalize(+stats), total]. */
-#define CS_TIMING_EVENTS 6
-#define CS_TIMING_PHASES 6
+ *   [env_xf, face_prep, face_pgd, compact, reduce, finalize(+stats), total]. */
+#define CS_TIMING_EVENTS 7
+#define CS_TIMING_PHASES 7
 int cs_plan_timing(cs_plan *plan, int32_t slots);
 int cs_plan_timing_read(cs_plan *plan, float *ms, int32_t max_steps, int32_t *n_steps);
 
-/* Roofline accounting: enable != 0 zeroes a device counter and switches the
- * plan's face kernel to a build that tallies every trilinear SDF sample;
- * enable == 0 synchronises, returns the tally in *count and switches back. */
+/* Roofline accounting: enable != 0 zeroes the device counters and switches the
+ * plan's face kernels to builds that tally every trilinear SDF sample;
+ * enable == 0 synchronises, writes CS_SAMPLE_COUNTERS tallies to count
+ * ([0] k_face_prep: vertex + centroid samples, [1] k_face_pgd: descent
+ * samples) and switches back. */
+#define CS_SAMPLE_COUNTERS 2
 int cs_plan_count_samples(cs_plan *plan, int32_t enable, uint64_t *count);
 
 /* Reduce step of a reduce-only plan: the caller has written n_cand and the

@@ -139,26 +139,27 @@ class Plan:
     def reduce(self, stream=None):
         _native.call("cs_reduce", self.ptr, _native.stream_handle(stream))
 
-    PHASES = ("env_xf", "faces", "compact", "reduce", "finalize", "total")
+    PHASES = ("env_xf", "face_prep", "face_pgd", "compact", "reduce", "finalize", "total")
 
     def enable_timing(self, slots: int) -> None:
         """Record CUDA events around each phase of the next `slots` collide calls (0 disables)."""
         _native.call("cs_plan_timing", self.ptr, int(slots))
 
     def read_timing(self, max_steps: int) -> np.ndarray:
-        """(steps, 6) ms per phase [env_xf, faces, compact, reduce, finalize, total], oldest first."""
+        """(steps, 7) ms per phase (Plan.PHASES), oldest first."""
         out = np.zeros((max_steps, len(self.PHASES)), np.float32)
         n = ctypes.c_int32(0)
         _native.call("cs_plan_timing_read", self.ptr, out.ctypes.data, int(max_steps), ctypes.byref(n))
         return out[: n.value]
 
-    def count_samples(self, sdf_pose, mesh_pose, contact_distance, pose_format: int = _native.CS_POSE7) -> int:
-        """Exact number of trilinear SDF samples one collide step performs (counting build)."""
+    def count_samples(self, sdf_pose, mesh_pose, contact_distance, pose_format: int = _native.CS_POSE7):
+        """Exact trilinear SDF samples of one collide step (counting builds):
+        (k_face_prep samples, k_face_pgd samples)."""
         _native.call("cs_plan_count_samples", self.ptr, 1, None)
         self.collide(sdf_pose, mesh_pose, contact_distance, pose_format)
-        c = ctypes.c_uint64(0)
-        _native.call("cs_plan_count_samples", self.ptr, 0, ctypes.byref(c))
-        return int(c.value)
+        c = (ctypes.c_uint64 * 2)()
+        _native.call("cs_plan_count_samples", self.ptr, 0, c)
+        return int(c[0]), int(c[1])
 
 
 class ReducedContacts:

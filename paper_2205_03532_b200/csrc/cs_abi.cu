@@ -60,6 +60,8 @@ struct MeshEntry {
     bool live = false;
     double4 *verts = nullptr;
     int4 *tris = nullptr;
+    int32_t *chunk_voff = nullptr, *chunk_verts = nullptr;
+    uint2 *face_loc = nullptr;
     MeshDesc desc{};
 };
 
@@ -109,8 +111,10 @@ struct cs_plan {
     // inputs / tables
     int32_t *env_sdf = nullptr, *env_mesh = nullptr;
     int64_t *cand_base = nullptr;
-    int2 *block_map = nullptr;   // k_faces block -> (env, first face)
-    int32_t *chunk_first = nullptr;  // [E+1] first k_faces block of each env
+    int2 *block_map = nullptr;       // k_face_prep block -> (env, first face of the chunk)
+    int32_t *chunk_first = nullptr;  // [E+1] first k_face_prep block of each env
+    int32_t max_chunk_verts = 1;     // largest chunk vertex list over the plan's meshes
+    int pgd_grid = 0;                // persistent k_face_pgd CTAs
     EnvXf *xf = nullptr;
     Staging st{};
     Candidates cands{};
@@ -120,7 +124,7 @@ struct cs_plan {
     double *in_sdf = nullptr, *in_mesh = nullptr, *in_cd = nullptr;
     int32_t *status = nullptr;
     double *env_min_depth = nullptr;  // scene semantics: min_depth None -> -cd per env
-    unsigned long long *sample_counter = nullptr;  // non-null: counting build of k_faces
+    unsigned long long *sample_counter = nullptr;  // non-null: counting builds ([0] prep, [1] pgd)
     unsigned long long *counter_buf = nullptr;
     // phase timing: ring of `timing_slots` steps x CS_TIMING_EVENTS events
     std::vector<cudaEvent_t> events;
@@ -252,7 +256,7 @@ int cs_sdf_l2_persist(int32_t handle, void *stream, float hit_ratio) {
 int cs_mesh_register(const double *vertices, int64_t nv, const int32_t *triangles, int64_t nt, int32_t *handle) {
     if (!vertices || !triangles || !handle) return fail(CS_ERR_VALUE, "null argument");
     if (nv < 3 || nt < 1) return fail(CS_ERR_MESH, "mesh needs at least 3 vertices and 1 triangle");
-    if (nt >= ((int64_t)1 << 31)) return fail(CS_ERR_MESH, "too many triangles");
+    if (nt >= ((int64_t)1 << 29)) return fail(CS_ERR_MESH, "too many triangles (limit 2^29)");
     std::vector<double4> v4((size_t)nv);
     for (int64_t i = 0; i < nv; ++i) {
         const double *p = vertices + 3 * i;
@@ -266,6 +270,30 @@ int cs_mesh_register(const double *vertices, int64_t nv, const int32_t *triangle
             if (t[k] < 0 || t[k] >= nv) return fail(CS_ERR_MESH, "triangle index out of range (have %lld vertices)", (long long)nv);
         t4[(size_t)i] = make_int4(t[0], t[1], t[2], 0);
     }
+    // chunk-local vertex lists (k_face_prep samples each distinct vertex of a chunk once)
+    const int64_t nchunks = (nt + FACE_CHUNK - 1) / FACE_CHUNK;
+    std::vector<int32_t> voff((size_t)nchunks + 1), cverts;
+    std::vector<uint2> floc((size_t)nt);
+    int32_t maxcv = 0;
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int64_t f0 = c * FACE_CHUNK, f1 = std::min<int64_t>(nt, f0 + FACE_CHUNK);
+        std::vector<int32_t> ids;
+        ids.reserve((size_t)(3 * (f1 - f0)));
+        for (int64_t f = f0; f < f1; ++f)
+            for (int k = 0; k < 3; ++k) ids.push_back(triangles[3 * f + k]);
+        std::sort(ids.begin(), ids.end());
+        ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+        voff[(size_t)c] = (int32_t)cverts.size();
+        for (int64_t f = f0; f < f1; ++f) {
+            uint32_t loc[3];
+            for (int k = 0; k < 3; ++k)
+                loc[k] = (uint32_t)(std::lower_bound(ids.begin(), ids.end(), triangles[3 * f + k]) - ids.begin());
+            floc[(size_t)f] = make_uint2(loc[0] | (loc[1] << 16), loc[2]);
+        }
+        cverts.insert(cverts.end(), ids.begin(), ids.end());
+        maxcv = std::max<int32_t>(maxcv, (int32_t)ids.size());
+    }
+    voff[(size_t)nchunks] = (int32_t)cverts.size();
     std::lock_guard<std::mutex> lk(g_mu);
     int r = ensure_tables();
     if (r) return r;
@@ -278,10 +306,21 @@ int cs_mesh_register(const double *vertices, int64_t nv, const int32_t *triangle
     CS_CUDA(cudaMalloc(&m.tris, sizeof(int4) * (size_t)nt));
     CS_CUDA(cudaMemcpy(m.verts, v4.data(), sizeof(double4) * (size_t)nv, cudaMemcpyHostToDevice));
     CS_CUDA(cudaMemcpy(m.tris, t4.data(), sizeof(int4) * (size_t)nt, cudaMemcpyHostToDevice));
+    CS_CUDA(cudaMalloc(&m.chunk_voff, sizeof(int32_t) * voff.size()));
+    CS_CUDA(cudaMalloc(&m.chunk_verts, sizeof(int32_t) * std::max<size_t>(1, cverts.size())));
+    CS_CUDA(cudaMalloc(&m.face_loc, sizeof(uint2) * floc.size()));
+    CS_CUDA(cudaMemcpy(m.chunk_voff, voff.data(), sizeof(int32_t) * voff.size(), cudaMemcpyHostToDevice));
+    CS_CUDA(cudaMemcpy(m.chunk_verts, cverts.data(), sizeof(int32_t) * cverts.size(), cudaMemcpyHostToDevice));
+    CS_CUDA(cudaMemcpy(m.face_loc, floc.data(), sizeof(uint2) * floc.size(), cudaMemcpyHostToDevice));
     m.desc.verts = m.verts;
     m.desc.tris = m.tris;
+    m.desc.chunk_voff = m.chunk_voff;
+    m.desc.chunk_verts = m.chunk_verts;
+    m.desc.face_loc = m.face_loc;
     m.desc.nv = nv;
     m.desc.nt = nt;
+    m.desc.nchunks = (int32_t)nchunks;
+    m.desc.max_chunk_verts = maxcv;
     CS_CUDA(cudaMemcpy(d_meshes + h, &m.desc, sizeof(MeshDesc), cudaMemcpyHostToDevice));
     m.live = true;
     *handle = h;
@@ -294,6 +333,9 @@ int cs_mesh_free(int32_t handle) {
     MeshEntry &m = g_mesh[handle];
     CS_CUDA(cudaFree(m.verts));
     CS_CUDA(cudaFree(m.tris));
+    CS_CUDA(cudaFree(m.chunk_voff));
+    CS_CUDA(cudaFree(m.chunk_verts));
+    CS_CUDA(cudaFree(m.face_loc));
     m = MeshEntry{};
     return CS_OK;
 }
@@ -435,6 +477,7 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
     std::vector<int32_t> chunk_first;
     bool uniform = true;
     GridT<double> ugrid{};
+    int32_t maxcv = 1;
     {
         std::lock_guard<std::mutex> lk(g_mu);
         int r = ensure_tables();
@@ -446,8 +489,9 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
             if (m < 0 || m >= MAX_HANDLES || !g_mesh[m].live) return fail(CS_ERR_HANDLE, "env %lld: bad mesh handle %d", (long long)e, m);
             int64_t nt = g_mesh[m].desc.nt;
             cap[(size_t)e] = nt;
+            maxcv = std::max(maxcv, g_mesh[m].desc.max_chunk_verts);
             chunk_first.push_back((int32_t)bmap.size());
-            for (int64_t f = 0; f < nt; f += FACE_BLOCK) bmap.push_back(make_int2((int)e, (int)f));
+            for (int64_t f = 0; f < nt; f += FACE_CHUNK) bmap.push_back(make_int2((int)e, (int)f));
         }
         if (uniform) ugrid = g_sdf[sdf_handles[0]].desc.g64;
         chunk_first.push_back((int32_t)bmap.size());
@@ -457,6 +501,8 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
     P->stages = stages;
     P->uniform_sdf = uniform;
     P->uniform_grid = ugrid;
+    P->max_chunk_verts = maxcv;
+    P->pgd_grid = face_pgd_grid(g_sms > 0 ? g_sms : 148);
     if (stages & CS_STAGE_REDUCE) {
         P->rp.N = params->max_patches; P->rp.K = params->per_patch_cap; P->rp.batch_size = params->batch_size;
         P->rp.has_min_depth = params->has_min_depth; P->rp.cone = params->normal_cone_cos; P->rp.min_depth = params->min_depth;
@@ -471,6 +517,9 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
     if (!r) r = P->alloc(&P->st.face, (size_t)P->total_cap);
     if (!r) r = P->alloc(&P->st.chunk_count, bmap.size());
     if (!r) r = P->alloc(&P->st.chunk_off, bmap.size());
+    if (!r) r = P->alloc(&P->st.chunk_found, bmap.size());
+    if (!r) r = P->alloc(&P->st.work, (size_t)P->total_cap);
+    if (!r) r = P->alloc(&P->st.work_count, 2);
     if (!r) r = P->alloc(&P->chunk_first, chunk_first.size());
     if (!r) r = P->alloc(&P->st.point, 3 * (size_t)P->total_cap);
     if (!r) r = P->alloc(&P->st.phi, (size_t)P->total_cap);
@@ -550,26 +599,31 @@ int cs_collide(cs_plan *P, const double *sdf_pose, const double *mesh_pose, int3
     auto mark = [&](int i) { if (ev) cudaEventRecord(ev[i], s); };
     mark(0);
     launch_env_xf(P->E, P->env_sdf, P->env_mesh, d_sdfs, sdf_pose, mesh_pose, pose_format, contact_distance, P->xf,
-                  P->status, P->env_min_depth, s);
+                  P->status, P->env_min_depth, P->st.work_count, s);
     CS_LAUNCHED();
     mark(1);
-    launch_faces(P->nblocks, P->block_map, P->xf, d_sdfs, d_meshes, P->cand_base, P->st, P->sample_counter,
-                 P->uniform_sdf ? &P->uniform_grid : nullptr, s);
+    const GridT<double> *ug = P->uniform_sdf ? &P->uniform_grid : nullptr;
+    launch_face_prep(P->nblocks, P->block_map, P->xf, d_sdfs, d_meshes, P->cand_base, P->st, P->max_chunk_verts,
+                     P->sample_counter, ug, s);
     CS_LAUNCHED();
     mark(2);
-    launch_compact(P->E, P->xf, P->cand_base, P->block_map, P->chunk_first, P->st, P->cands, P->io.n_cand, s);
+    launch_face_pgd(P->pgd_grid, P->block_map, P->xf, d_sdfs, d_meshes, P->st,
+                    P->sample_counter ? P->sample_counter + 1 : nullptr, ug, s);
     CS_LAUNCHED();
     mark(3);
+    launch_compact(P->E, P->xf, P->cand_base, P->block_map, P->chunk_first, P->st, P->cands, P->io.n_cand, s);
+    CS_LAUNCHED();
+    mark(4);
     if (P->stages & CS_STAGE_REDUCE) {
         launch_reduce(P->io, P->rp, P->max_batch, s);
         CS_LAUNCHED();
-        mark(4);
+        mark(5);
         launch_finalize(P->io, P->rp, g_sms > 0 ? g_sms : 148, s);
         CS_LAUNCHED();
     } else {
-        mark(4);
+        mark(5);
     }
-    mark(5);
+    mark(6);
     return CS_OK;
 }
 
@@ -607,17 +661,17 @@ int cs_plan_count_samples(cs_plan *P, int32_t enable, uint64_t *count) {
     if (!P) return fail(CS_ERR_VALUE, "null plan");
     if (enable) {
         if (!P->counter_buf) {
-            int r = P->alloc(&P->counter_buf, 1);
+            int r = P->alloc(&P->counter_buf, CS_SAMPLE_COUNTERS);
             if (r) return r;
         }
-        CS_CUDA(cudaMemset(P->counter_buf, 0, sizeof(unsigned long long)));
+        CS_CUDA(cudaMemset(P->counter_buf, 0, sizeof(unsigned long long) * CS_SAMPLE_COUNTERS));
         P->sample_counter = P->counter_buf;
         return CS_OK;
     }
     if (count) {
         if (!P->counter_buf) return fail(CS_ERR_VALUE, "sample counting was never enabled");
         CS_CUDA(cudaDeviceSynchronize());
-        CS_CUDA(cudaMemcpy(count, P->counter_buf, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        CS_CUDA(cudaMemcpy(count, P->counter_buf, sizeof(uint64_t) * CS_SAMPLE_COUNTERS, cudaMemcpyDeviceToHost));
     }
     P->sample_counter = nullptr;
     return CS_OK;

@@ -35,10 +35,19 @@ __device__ __forceinline__ double V3(double a0, double a1, double a2, double b0,
     return __fma_rn(a2, b2, __fma_rn(a0, b0, __dmul_rn(a1, b1)));
 }
 
+// Faces are processed in chunks of FACE_CHUNK consecutive triangles; each chunk
+// carries the sorted list of the distinct vertices it references and, per face,
+// the three corners as indices into that list (so a chunk samples every vertex once).
+constexpr int FACE_CHUNK = 256;
+
 struct MeshDesc {
-    const double4 *verts;  // (x, y, z, 0)
-    const int4 *tris;      // (a, b, c, 0)
+    const double4 *verts;        // (x, y, z, 0)
+    const int4 *tris;            // (a, b, c, 0)
+    const int32_t *chunk_voff;   // [nchunks + 1] offsets into chunk_verts
+    const int32_t *chunk_verts;  // distinct vertex ids per chunk, ascending
+    const uint2 *face_loc;       // per face: (a_loc | b_loc << 16, c_loc) chunk-local corners
     int64_t nv, nt;
+    int32_t nchunks, max_chunk_verts;
 };
 
 // Per-env transform state, computed on device from the poses.
@@ -257,6 +266,11 @@ __device__ __forceinline__ void closest_point(double ax, double ay, double az, d
     qz = az + abz * v + acz * w;
 }
 
+__device__ __forceinline__ bool same3(double x, double y, double z, double a, double b, double c) {
+    return __double_as_longlong(x) == __double_as_longlong(a) && __double_as_longlong(y) == __double_as_longlong(b) &&
+           __double_as_longlong(z) == __double_as_longlong(c);
+}
+
 struct FaceResult {
     double px, py, pz, phi, gx, gy, gz;
     int nsamp;
@@ -301,12 +315,24 @@ __device__ __forceinline__ bool face_body(const GridT<T> &g, double ax, double a
             double qx, qy, qz;
             closest_point(ax, ay, az, bx, by, bz, cx, cy, cz, p.x - alpha * ux, p.y - alpha * uy, p.z - alpha * uz,
                           qx, qy, qz);
-            GPoint q = gpoint(g, qx, qy, qz);
-            double phi_new = sample(g, q);
-            if (COUNT) r.nsamp += 1;
+            // The projection often lands exactly on the current point or on a vertex
+            // (Ericson's vertex regions return the corner itself): identical inputs,
+            // so the sample's value is already known.
+            double phi_new;
+            int known = same3(qx, qy, qz, p.x, p.y, p.z) ? 0
+                        : same3(qx, qy, qz, ax, ay, az)  ? 1
+                        : same3(qx, qy, qz, bx, by, bz)  ? 2
+                        : same3(qx, qy, qz, cx, cy, cz)  ? 3
+                                                         : -1;
+            if (known >= 0) {
+                phi_new = known == 0 ? phi : known == 1 ? phi_a : known == 2 ? phi_b : phi_c;
+            } else {
+                phi_new = sample(g, qx, qy, qz);
+                if (COUNT) r.nsamp += 1;
+            }
             if (phi_new < phi) {
                 moved = sqrt((qx - p.x) * (qx - p.x) + (qy - p.y) * (qy - p.y) + (qz - p.z) * (qz - p.z));
-                p = q;
+                p = gpoint(g, qx, qy, qz);
                 phi = phi_new;
                 have_grad = false;
                 alpha = dmin(alpha * 1.5, amax);

@@ -161,21 +161,22 @@ struct BlockTeam {
 // All-ascending bitonic sort of m (u, v, pos) keys by a team (virtual +inf padding).
 template <class Team, class Idx>
 __device__ void team_sort(const Team &t, double *su, double *sv, Idx *sp, int m) {
-    int P2 = 1;
-    while (P2 < m) P2 <<= 1;
+    int P2 = 1, lg = 0;
+    while (P2 < m) { P2 <<= 1; ++lg; }
     const int half = P2 >> 1;
-    for (int k = 2; k <= P2; k <<= 1) {
-        const int hk = k >> 1;
-        for (int jj = hk; jj >= 1; jj >>= 1) {
+    for (int lk = 1; lk <= lg; ++lk) {  // k = 2^lk
+        const int k = 1 << lk, hk = k >> 1;
+        for (int lj = lk - 1; lj >= 0; --lj) {  // jj = 2^lj
+            const int jj = 1 << lj;
             for (int idx = t.rank(); idx < half; idx += t.size()) {
                 int i, j;
-                if (jj == hk) {
-                    int blk = idx / hk, off = idx % hk;
-                    i = blk * k + off;
-                    j = blk * k + k - 1 - off;
+                if (jj == hk) {  // first step of a merge: mirrored partner
+                    const int blk = idx >> lj, off = idx & (jj - 1);
+                    i = (blk << lk) + off;
+                    j = (blk << lk) + k - 1 - off;
                 } else {
-                    int blk = idx / jj, off = idx % jj;
-                    i = blk * 2 * jj + off;
+                    const int blk = idx >> lj, off = idx & (jj - 1);
+                    i = (blk << (lj + 1)) + off;
                     j = i + jj;
                 }
                 if (j < m) {
@@ -369,11 +370,11 @@ __device__ void finalize_patch(const Team &t, const ReduceIO &io, const ReducePa
     // of members through a shared tile (su is free now) so the folds read shared
     // memory, and keeps the weights for the pairwise sum in wbuf.
     t.sync();
-    const int r = t.rank(), CH = t.size();
+    const int r = t.rank(), CH = min(t.size(), 64);  // tile: 9 x CH doubles in su
     double s = 0.0;
     for (int c0 = 0; c0 < m; c0 += CH) {
         const int k = c0 + r;
-        if (k < m) {
+        if (r < CH && k < m) {
             const double wk = weight_of(wbuf[k]);
             const double px = pt(k, 0), py = pt(k, 1), pz = pt(k, 2);
             const double nx = nr(k, 0), ny = nr(k, 1), nz = nr(k, 2);

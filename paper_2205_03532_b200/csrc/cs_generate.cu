@@ -2,8 +2,10 @@
 //
 //   k_env_xf       per env: poses -> to_grid transform, cull box, status
 //                  (generation.py:64-83, math3d.py:45-53,168-179)
-//   k_faces        per (env, face): grid-frame corners, AABB cull, face_contacts
-//                  (generation.py:70-96, contacts/_kernels.py:11-87)
+//   k_face_prep    per (env, chunk): grid-frame vertices, AABB cull, Lipschitz
+//                  prune, descent start (generation.py:70-96, contacts/_kernels.py:20-43)
+//   k_face_pgd     persistent warps: projected-gradient descent per surviving face
+//                  (contacts/_kernels.py:44-87)
 //   k_compact      per env: ordered compaction of found faces + world-frame
 //                  epilogue (generation.py:98-114)
 //   k_face_contacts / k_sdf_sample / k_sdf_gradient: per-pair drop-ins for the
@@ -30,8 +32,9 @@ __global__ void k_env_xf(int64_t E, const int32_t *__restrict__ env_sdf, const i
                          const SdfDesc *__restrict__ sdfs, const double *__restrict__ sdf_pose,
                          const double *__restrict__ mesh_pose, int pose_format, const double *__restrict__ cdv,
                          EnvXf *__restrict__ xf, int32_t *__restrict__ env_status,
-                         double *__restrict__ env_min_depth) {
+                         double *__restrict__ env_min_depth, unsigned *__restrict__ work_count) {
     int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e == 0 && work_count) { work_count[0] = 0; work_count[1] = 0; }
     if (e >= E) return;
     double Rs[9], Rm[9], ts[3], tm[3];
     int ok = 1;
@@ -87,72 +90,283 @@ __device__ __forceinline__ double3 to_grid(const EnvXf &X, double4 v) {
     return r;
 }
 
+// k_face_prep: one CTA per (env, chunk of FACE_CHUNK faces). The chunk's distinct
+// vertices are transformed and (where a face needs them) sampled once into shared
+// memory; each thread then culls one face (generation.py:74-83), applies the
+// Lipschitz prune and picks the descent start (contacts/_kernels.py:28-43). The
+// survivors are appended, in face order within the chunk, to a dense work list.
 // UNIFORM: every env of the plan samples the same SDF, passed by value so its
-// scalars are constant-bank operands; otherwise the env's SDF view is staged in
-// shared memory per block.
+// scalars are constant-bank operands; otherwise the env's grid view is staged in
+// shared memory.
 template <bool COUNT, bool UNIFORM>
-__global__ void __launch_bounds__(FACE_BLOCK) k_faces(const int2 *__restrict__ block_map, const EnvXf *__restrict__ xf,
-                                                      const SdfDesc *__restrict__ sdfs,
-                                                      const MeshDesc *__restrict__ meshes,
-                                                      const int64_t *__restrict__ cand_base, Staging st,
-                                                      unsigned long long *__restrict__ counter,
-                                                      const GridT<double> gu) {
+__global__ void __launch_bounds__(FACE_CHUNK) k_face_prep(const int2 *__restrict__ block_map,
+                                                          const EnvXf *__restrict__ xf,
+                                                          const SdfDesc *__restrict__ sdfs,
+                                                          const MeshDesc *__restrict__ meshes,
+                                                          const int64_t *__restrict__ cand_base, Staging st, int maxcv,
+                                                          unsigned long long *__restrict__ counter,
+                                                          const GridT<double> gu) {
+    extern __shared__ double dsm[];
     __shared__ EnvXf sx;
     __shared__ GridT<double> sg;
-    int2 bm = block_map[blockIdx.x];
-    int e = bm.x;
+    __shared__ int ws[WS_INTS];
+    __shared__ unsigned sbase;
+    const int2 bm = block_map[blockIdx.x];
+    const int e = bm.x, f0 = bm.y;
     if (threadIdx.x < sizeof(EnvXf) / 8)
         reinterpret_cast<double *>(&sx)[threadIdx.x] = reinterpret_cast<const double *>(xf + e)[threadIdx.x];
     __syncthreads();
+    if (sx.status != 0) {  // non-finite pose or cd < 0: nothing is generated
+        if (threadIdx.x == 0) { st.chunk_count[blockIdx.x] = 0; st.chunk_found[blockIdx.x] = 0; }
+        return;
+    }
     if (!UNIFORM) {
-        static_assert(sizeof(GridT<double>) % 8 == 0 && sizeof(GridT<double>) / 8 <= FACE_BLOCK, "GridT copy");
+        static_assert(sizeof(GridT<double>) % 8 == 0 && sizeof(GridT<double>) / 8 <= FACE_CHUNK, "GridT copy");
         if (threadIdx.x < sizeof(GridT<double>) / 8)
             reinterpret_cast<double *>(&sg)[threadIdx.x] = reinterpret_cast<const double *>(&sdfs[sx.sdf].g64)[threadIdx.x];
-        __syncthreads();
     }
     const GridT<double> &grid = UNIFORM ? gu : sg;
-    const MeshDesc M = meshes[sx.mesh];
-    const int64_t f = (int64_t)bm.y + threadIdx.x;
-    bool found = false;
-    FaceResult r;
-    if (f < M.nt && sx.status == 0) {
-        int4 tri = __ldg(M.tris + f);
-        double3 a = to_grid(sx, ld_vert(M.verts + tri.x));
-        double3 b = to_grid(sx, ld_vert(M.verts + tri.y));
-        double3 c = to_grid(sx, ld_vert(M.verts + tri.z));
-        // AABB cull (generation.py:74-83)
-        bool near = dmin(dmin(a.x, b.x), c.x) <= sx.cull_hi[0] && dmax(dmax(a.x, b.x), c.x) >= sx.cull_lo[0] &&
-                    dmin(dmin(a.y, b.y), c.y) <= sx.cull_hi[1] && dmax(dmax(a.y, b.y), c.y) >= sx.cull_lo[1] &&
-                    dmin(dmin(a.z, b.z), c.z) <= sx.cull_hi[2] && dmax(dmax(a.z, b.z), c.z) >= sx.cull_lo[2];
-        if (near) {
-            bool computed = face_body<COUNT>(grid, a.x, a.y, a.z, b.x, b.y, b.z, c.x, c.y, c.z, sx.cd,
-                                             MAX_MINIMIZE_ITERS, sx.tol, r);
-            if (COUNT) atomicAdd(counter, (unsigned long long)r.nsamp);
-            found = computed && r.phi <= sx.cd;
+    const double4 *verts = meshes[sx.mesh].verts;
+    const int32_t *cverts = meshes[sx.mesh].chunk_verts;
+    const int64_t nt = meshes[sx.mesh].nt;
+    const int chunk = f0 / FACE_CHUNK;
+    const int v0 = __ldg(meshes[sx.mesh].chunk_voff + chunk);
+    const int ncv = __ldg(meshes[sx.mesh].chunk_voff + chunk + 1) - v0;
+    double *vx = dsm, *vy = dsm + maxcv, *vz = dsm + 2 * maxcv, *vphi = dsm + 3 * maxcv;
+    unsigned char *need = reinterpret_cast<unsigned char *>(dsm + 4 * maxcv);
+    // verts_grid = to_grid.apply(vertices) (generation.py:70), per distinct vertex
+    for (int j = threadIdx.x; j < ncv; j += FACE_CHUNK) {
+        const double3 p = to_grid(sx, ld_vert(verts + __ldg(cverts + v0 + j)));
+        vx[j] = p.x; vy[j] = p.y; vz[j] = p.z;
+        need[j] = 0;
+    }
+    __syncthreads();
+    const int64_t f = (int64_t)f0 + threadIdx.x;
+    int la = 0, lb = 0, lc = 0;
+    bool near = false;
+    if (f < nt) {
+        const uint2 loc = __ldg(meshes[sx.mesh].face_loc + f);
+        la = (int)(loc.x & 0xffffu); lb = (int)(loc.x >> 16); lc = (int)loc.y;
+        const double ax = vx[la], bx = vx[lb], cx = vx[lc];
+        const double ay = vy[la], by = vy[lb], cy = vy[lc];
+        const double az = vz[la], bz = vz[lb], cz = vz[lc];
+        near = dmin(dmin(ax, bx), cx) <= sx.cull_hi[0] && dmax(dmax(ax, bx), cx) >= sx.cull_lo[0] &&
+               dmin(dmin(ay, by), cy) <= sx.cull_hi[1] && dmax(dmax(ay, by), cy) >= sx.cull_lo[1] &&
+               dmin(dmin(az, bz), cz) <= sx.cull_hi[2] && dmax(dmax(az, bz), cz) >= sx.cull_lo[2];
+        if (near) { need[la] = 1; need[lb] = 1; need[lc] = 1; }
+    }
+    __syncthreads();
+    int ns = 0;
+    for (int j = threadIdx.x; j < ncv; j += FACE_CHUNK)
+        if (need[j]) {
+            vphi[j] = sample(grid, vx[j], vy[j], vz[j]);
+            ++ns;
+        }
+    __syncthreads();
+    bool survive = false;
+    int which = 0;
+    double pa = 0.0, pb = 0.0, pc = 0.0, ps = 0.0;
+    if (near) {
+        const double ax = vx[la], ay = vy[la], az = vz[la];
+        const double bx = vx[lb], by = vy[lb], bz = vz[lb];
+        const double cx = vx[lc], cy = vy[lc], cz = vz[lc];
+        pa = vphi[la]; pb = vphi[lb]; pc = vphi[lc];
+        const double e0 = sqrt((bx - ax) * (bx - ax) + (by - ay) * (by - ay) + (bz - az) * (bz - az));
+        const double e1 = sqrt((cx - bx) * (cx - bx) + (cy - by) * (cy - by) + (cz - bz) * (cz - bz));
+        const double e2 = sqrt((ax - cx) * (ax - cx) + (ay - cy) * (ay - cy) + (az - cz) * (az - cz));
+        const double diam = dmax(e0, dmax(e1, e2));
+        const double phi_min = dmin(pa, dmin(pb, pc));
+        if (!(phi_min - diam > sx.cd)) {
+            ps = sample(grid, (ax + bx + cx) / 3.0, (ay + by + cy) / 3.0, (az + bz + cz) / 3.0);
+            ++ns;
+            if (pa < ps) { ps = pa; which = 1; }
+            if (pb < ps) { ps = pb; which = 2; }
+            if (pc < ps) { ps = pc; which = 3; }
+            survive = true;
         }
     }
-    // chunk-local ordered compaction: this block's found faces land at the start of
-    // its staging rows in ascending face order; k_compact stitches the chunks.
-    __shared__ int ws[WS_INTS];
-    int total;
-    const int pos = block_excl_scan(found ? 1 : 0, ws, &total);
-    if (found) {
-        const int64_t s = cand_base[e] + bm.y + pos;
-        st.point[3 * s + 0] = r.px;
-        st.point[3 * s + 1] = r.py;
-        st.point[3 * s + 2] = r.pz;
-        st.phi[s] = r.phi;
-        st.grad[3 * s + 0] = r.gx;
-        st.grad[3 * s + 1] = r.gy;
-        st.grad[3 * s + 2] = r.gz;
-        st.face[s] = (int32_t)f;
+    if (COUNT) {
+        for (int o = 16; o; o >>= 1) ns += __shfl_xor_sync(0xffffffffu, ns, o);
+        if ((threadIdx.x & 31) == 0 && ns) atomicAdd(counter, (unsigned long long)ns);
     }
-    if (threadIdx.x == 0) st.chunk_count[blockIdx.x] = total;
+    int total;
+    const int pos = block_excl_scan(survive ? 1 : 0, ws, &total);
+    if (threadIdx.x == 0) {
+        sbase = total ? atomicAdd(st.work_count, (unsigned)total) : 0u;
+        st.chunk_count[blockIdx.x] = total;
+        st.chunk_found[blockIdx.x] = 0;
+    }
+    __syncthreads();
+    if (survive) {
+        FaceWork *w = st.work + sbase + pos;
+        w->row = cand_base[e] + f0 + pos;
+        w->blk = (int32_t)blockIdx.x;
+        w->face = (int32_t)f | (which << 30);
+        w->phi[0] = pa; w->phi[1] = pb; w->phi[2] = pc; w->phi[3] = ps;
+    }
 }
 
-// Stitch the per-chunk compacted rows into the env's candidate list (ascending
-// face order) and apply the world-frame epilogue (generation.py:98-114).
-// One CTA per env: chunk offsets by a block scan, then one warp per chunk.
+// k_face_pgd: the projected-gradient descent of every surviving face
+// (contacts/_kernels.py:44-87), one face per lane. Warps are persistent: a lane
+// that finishes its face takes the next one from the warp's claimed block of the
+// work list, so the warp's lanes stay busy whatever the per-face iteration count.
+// A step is one descent iteration; the final gradient (contacts/_kernels.py:84)
+// is the next step's gradient, so it also runs in lockstep.
+template <bool COUNT, bool UNIFORM>
+__global__ void __launch_bounds__(PGD_BLOCK) k_face_pgd(const int2 *__restrict__ block_map,
+                                                        const EnvXf *__restrict__ xf,
+                                                        const SdfDesc *__restrict__ sdfs,
+                                                        const MeshDesc *__restrict__ meshes, Staging st,
+                                                        unsigned long long *__restrict__ counter,
+                                                        const GridT<double> gu) {
+    __shared__ double sc[12][PGD_BLOCK];  // per lane: corners a, b, c (grid frame), phi at a, b, c
+    const int t = threadIdx.x, lane = t & 31;
+    const unsigned FULL = 0xffffffffu;
+    const unsigned n = st.work_count[0];
+    bool active = false, exhausted = false, final_step = false, have_grad = false;
+    unsigned qb = 0, qe = 0;
+    double px = 0.0, py = 0.0, pz = 0.0, phi = 0.0, alpha = 0.0, cd = 0.0, tol = 0.0;
+    int it = 0, face = 0, blk = 0, sdf = 0;
+    int64_t row = 0;
+    unsigned long long ns = 0;
+
+    auto start = [&](unsigned idx, const GridT<double> &g) {
+        const FaceWork *w = st.work + idx;
+        row = w->row;
+        blk = w->blk;
+        const int fw = w->face;
+        face = fw & 0x3fffffff;
+        const int which = (int)((unsigned)fw >> 30);
+        const EnvXf &X = xf[__ldg(&block_map[blk].x)];
+        cd = X.cd;
+        tol = X.tol;
+        const MeshDesc &M = meshes[X.mesh];
+        const int4 tri = __ldg(M.tris + face);
+        const double3 a = to_grid(X, ld_vert(M.verts + tri.x));
+        const double3 b = to_grid(X, ld_vert(M.verts + tri.y));
+        const double3 c = to_grid(X, ld_vert(M.verts + tri.z));
+        sc[0][t] = a.x; sc[1][t] = a.y; sc[2][t] = a.z;
+        sc[3][t] = b.x; sc[4][t] = b.y; sc[5][t] = b.z;
+        sc[6][t] = c.x; sc[7][t] = c.y; sc[8][t] = c.z;
+        sc[9][t] = w->phi[0]; sc[10][t] = w->phi[1]; sc[11][t] = w->phi[2];
+        phi = w->phi[3];
+        if (which == 0) {
+            px = (a.x + b.x + c.x) / 3.0; py = (a.y + b.y + c.y) / 3.0; pz = (a.z + b.z + c.z) / 3.0;
+        } else {
+            const double3 s = which == 1 ? a : which == 2 ? b : c;
+            px = s.x; py = s.y; pz = s.z;
+        }
+        alpha = g.voxel;
+        it = 0;
+        final_step = false;
+        have_grad = false;
+    };
+
+    auto step = [&](const GridT<double> &g) {
+        const GPoint p = gpoint(g, px, py, pz);
+        double grx, gry, grz;
+        gradient(g, p, grx, gry, grz);
+        if (COUNT) ns += 6;
+        bool done = final_step;
+        if (!done) {
+            have_grad = true;
+            const double gnorm = sqrt(grx * grx + gry * gry + grz * grz);
+            if (gnorm < 1e-12) {
+                done = true;
+            } else {
+                const double ux = grx / gnorm, uy = gry / gnorm, uz = grz / gnorm;
+                const double ax = sc[0][t], ay = sc[1][t], az = sc[2][t];
+                const double bx = sc[3][t], by = sc[4][t], bz = sc[5][t];
+                const double cx = sc[6][t], cy = sc[7][t], cz = sc[8][t];
+                double moved = 0.0;
+                for (int bt = 0; bt < 4; ++bt) {
+                    double qx, qy, qz;
+                    closest_point(ax, ay, az, bx, by, bz, cx, cy, cz, px - alpha * ux, py - alpha * uy,
+                                  pz - alpha * uz, qx, qy, qz);
+                    // the projection often is the current point or a corner itself:
+                    // identical inputs, so the sample's value is already known
+                    double phi_new;
+                    if (same3(qx, qy, qz, px, py, pz)) phi_new = phi;
+                    else if (same3(qx, qy, qz, ax, ay, az)) phi_new = sc[9][t];
+                    else if (same3(qx, qy, qz, bx, by, bz)) phi_new = sc[10][t];
+                    else if (same3(qx, qy, qz, cx, cy, cz)) phi_new = sc[11][t];
+                    else {
+                        phi_new = sample(g, qx, qy, qz);
+                        if (COUNT) ns += 1;
+                    }
+                    if (phi_new < phi) {
+                        moved = sqrt((qx - px) * (qx - px) + (qy - py) * (qy - py) + (qz - pz) * (qz - pz));
+                        px = qx; py = qy; pz = qz;
+                        phi = phi_new;
+                        have_grad = false;
+                        alpha = dmin(alpha * 1.5, 4.0 * g.voxel);
+                        break;
+                    }
+                    alpha *= 0.5;
+                }
+                if (moved < tol || ++it >= MAX_MINIMIZE_ITERS) {
+                    if (have_grad) done = true;
+                    else final_step = true;  // the next step's gradient is the final one
+                }
+            }
+        }
+        if (done) {
+            const bool found = phi <= cd;
+            if (found) {
+                st.point[3 * row + 0] = px; st.point[3 * row + 1] = py; st.point[3 * row + 2] = pz;
+                st.phi[row] = phi;
+                st.grad[3 * row + 0] = grx; st.grad[3 * row + 1] = gry; st.grad[3 * row + 2] = grz;
+                atomicAdd(st.chunk_found + blk, 1);
+            }
+            st.face[row] = found ? face : -1;
+            active = false;
+        }
+    };
+
+    while (true) {
+        unsigned need = __ballot_sync(FULL, !active && !exhausted);
+        while (need) {
+            if (qb >= qe) {
+                unsigned b = 0;
+                if (lane == 0) b = atomicAdd(st.work_count + 1, (unsigned)PGD_GRAB);
+                b = __shfl_sync(FULL, b, 0);
+                if (b >= n) {
+                    if (!active) exhausted = true;
+                    break;
+                }
+                qb = b;
+                qe = min(b + (unsigned)PGD_GRAB, n);
+            }
+            const unsigned avail = qe - qb;
+            const unsigned rank = __popc(need & ((1u << lane) - 1u));
+            if (((need >> lane) & 1u) && rank < avail) {
+                if (UNIFORM) {
+                    start(qb + rank, gu);
+                } else {
+                    sdf = xf[__ldg(&block_map[st.work[qb + rank].blk].x)].sdf;
+                    start(qb + rank, sdfs[sdf].g64);
+                }
+                active = true;
+            }
+            qb += min((unsigned)__popc(need), avail);
+            need = __ballot_sync(FULL, !active && !exhausted);
+        }
+        if (!__any_sync(FULL, active)) break;
+        if (active) {
+            if (UNIFORM) step(gu);
+            else step(sdfs[sdf].g64);
+        }
+    }
+    if (COUNT) {
+        for (int o = 16; o; o >>= 1) ns += __shfl_xor_sync(FULL, ns, o);
+        if (lane == 0 && ns) atomicAdd(counter, ns);
+    }
+}
+
+// Stitch the per-chunk survivor rows into the env's candidate list (found faces
+// in ascending face order) and apply the world-frame epilogue (generation.py:98-114).
+// One CTA per env: chunk offsets by a block scan of the found counts, then one
+// warp per chunk compacts its rows with a ballot.
 __global__ void __launch_bounds__(COMPACT_BLOCK) k_compact(const EnvXf *__restrict__ xf,
                                                            const int64_t *__restrict__ cand_base,
                                                            const int2 *__restrict__ block_map,
@@ -168,7 +382,7 @@ __global__ void __launch_bounds__(COMPACT_BLOCK) k_compact(const EnvXf *__restri
     int running = 0;
     for (int j0 = 0; j0 < nch; j0 += blockDim.x) {
         const int j = j0 + threadIdx.x;
-        const int v = j < nch ? st.chunk_count[c0 + j] : 0;
+        const int v = j < nch ? st.chunk_found[c0 + j] : 0;
         int tot;
         const int x = block_excl_scan(v, ws, &tot);
         if (j < nch) st.chunk_off[c0 + j] = running + x;
@@ -179,24 +393,33 @@ __global__ void __launch_bounds__(COMPACT_BLOCK) k_compact(const EnvXf *__restri
     const bool gemm = C >= 2;  // the world transform's BLAS path (C >= 2 -> G3)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int j = wid; j < nch; j += nw) {
+        if (st.chunk_found[c0 + j] == 0) continue;
         const int cnt = st.chunk_count[c0 + j];
         const int64_t src0 = base + block_map[c0 + j].y;
-        const int64_t dst0 = base + st.chunk_off[c0 + j];
-        for (int i = lane; i < cnt; i += 32) {
-            const int64_t s = src0 + i, d = dst0 + i;
-            double px = st.point[3 * s], py = st.point[3 * s + 1], pz = st.point[3 * s + 2];
-            double gx = st.grad[3 * s], gy = st.grad[3 * s + 1], gz = st.grad[3 * s + 2];
-            double nrm = sqrt(gx * gx + gy * gy + gz * gz);  // np.linalg.norm(axis=1): ((x2+y2)+z2)
-            if (nrm < 1e-12) { gx = 0.0; gy = 0.0; gz = 1.0; nrm = 1.0; }
-            const double nx = gx / nrm, ny = gy / nrm, nz = gz / nrm;
-            for (int k = 0; k < 3; ++k) {
-                const double *rr = sx.Rs + 3 * k;
-                cs.normal[3 * d + k] = gemm ? G3(nx, ny, nz, rr[0], rr[1], rr[2]) : V3(nx, ny, nz, rr[0], rr[1], rr[2]);
-                cs.point[3 * d + k] =
-                    (gemm ? G3(px, py, pz, rr[0], rr[1], rr[2]) : V3(px, py, pz, rr[0], rr[1], rr[2])) + sx.ts[k];
+        int64_t dst = base + st.chunk_off[c0 + j];
+        for (int i0 = 0; i0 < cnt; i0 += 32) {
+            const int i = i0 + lane;
+            const int64_t s = src0 + i;
+            const int fidx = i < cnt ? st.face[s] : -1;
+            const unsigned bal = __ballot_sync(0xffffffffu, fidx >= 0);
+            if (fidx >= 0) {
+                const int64_t d = dst + __popc(bal & ((1u << lane) - 1u));
+                double px = st.point[3 * s], py = st.point[3 * s + 1], pz = st.point[3 * s + 2];
+                double gx = st.grad[3 * s], gy = st.grad[3 * s + 1], gz = st.grad[3 * s + 2];
+                double nrm = sqrt(gx * gx + gy * gy + gz * gz);  // np.linalg.norm(axis=1): ((x2+y2)+z2)
+                if (nrm < 1e-12) { gx = 0.0; gy = 0.0; gz = 1.0; nrm = 1.0; }
+                const double nx = gx / nrm, ny = gy / nrm, nz = gz / nrm;
+                for (int k = 0; k < 3; ++k) {
+                    const double *rr = sx.Rs + 3 * k;
+                    cs.normal[3 * d + k] =
+                        gemm ? G3(nx, ny, nz, rr[0], rr[1], rr[2]) : V3(nx, ny, nz, rr[0], rr[1], rr[2]);
+                    cs.point[3 * d + k] =
+                        (gemm ? G3(px, py, pz, rr[0], rr[1], rr[2]) : V3(px, py, pz, rr[0], rr[1], rr[2])) + sx.ts[k];
+                }
+                cs.depth[d] = -st.phi[s];
+                cs.face[d] = fidx;
             }
-            cs.depth[d] = -st.phi[s];
-            cs.face[d] = st.face[s];
+            dst += __popc(bal);
         }
     }
     if (threadIdx.x == 0) n_cand[e] = C;
@@ -235,24 +458,48 @@ __global__ void k_sdf_gradient(GridView g, const double *__restrict__ p, int64_t
 
 void launch_env_xf(int64_t E, const int32_t *env_sdf, const int32_t *env_mesh, const SdfDesc *sdfs,
                    const double *sdf_pose, const double *mesh_pose, int pose_format, const double *cd, EnvXf *xf,
-                   int32_t *env_status, double *env_min_depth, cudaStream_t s) {
+                   int32_t *env_status, double *env_min_depth, unsigned *work_count, cudaStream_t s) {
     int bs = 128;
     k_env_xf<<<(unsigned)((E + bs - 1) / bs), bs, 0, s>>>(E, env_sdf, env_mesh, sdfs, sdf_pose, mesh_pose,
-                                                          pose_format, cd, xf, env_status, env_min_depth);
+                                                          pose_format, cd, xf, env_status, env_min_depth, work_count);
 }
 
-void launch_faces(int64_t nblocks, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs,
-                  const MeshDesc *meshes, const int64_t *cand_base, const Staging &st, unsigned long long *counter,
-                  const GridT<double> *uniform, cudaStream_t s) {
+size_t face_prep_smem(int maxcv) { return (size_t)maxcv * (4 * sizeof(double) + 1); }
+
+void launch_face_prep(int64_t nblocks, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs,
+                      const MeshDesc *meshes, const int64_t *cand_base, const Staging &st, int maxcv,
+                      unsigned long long *counter, const GridT<double> *uniform, cudaStream_t s) {
     if (nblocks <= 0) return;
     const GridT<double> gu = uniform ? *uniform : GridT<double>{};
     const unsigned nb = (unsigned)nblocks;
+    const size_t sm = face_prep_smem(maxcv);
     if (uniform) {
-        if (counter) k_faces<true, true><<<nb, FACE_BLOCK, 0, s>>>(block_map, xf, sdfs, meshes, cand_base, st, counter, gu);
-        else k_faces<false, true><<<nb, FACE_BLOCK, 0, s>>>(block_map, xf, sdfs, meshes, cand_base, st, nullptr, gu);
+        if (counter) k_face_prep<true, true><<<nb, FACE_CHUNK, sm, s>>>(block_map, xf, sdfs, meshes, cand_base, st, maxcv, counter, gu);
+        else k_face_prep<false, true><<<nb, FACE_CHUNK, sm, s>>>(block_map, xf, sdfs, meshes, cand_base, st, maxcv, nullptr, gu);
     } else {
-        if (counter) k_faces<true, false><<<nb, FACE_BLOCK, 0, s>>>(block_map, xf, sdfs, meshes, cand_base, st, counter, gu);
-        else k_faces<false, false><<<nb, FACE_BLOCK, 0, s>>>(block_map, xf, sdfs, meshes, cand_base, st, nullptr, gu);
+        if (counter) k_face_prep<true, false><<<nb, FACE_CHUNK, sm, s>>>(block_map, xf, sdfs, meshes, cand_base, st, maxcv, counter, gu);
+        else k_face_prep<false, false><<<nb, FACE_CHUNK, sm, s>>>(block_map, xf, sdfs, meshes, cand_base, st, maxcv, nullptr, gu);
+    }
+}
+
+int face_pgd_grid(int sm_count) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_face_pgd<false, true>, PGD_BLOCK, 0) != cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    return per_sm * sm_count;
+}
+
+void launch_face_pgd(int grid, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs, const MeshDesc *meshes,
+                     const Staging &st, unsigned long long *counter, const GridT<double> *uniform, cudaStream_t s) {
+    if (grid <= 0) return;
+    const GridT<double> gu = uniform ? *uniform : GridT<double>{};
+    if (uniform) {
+        if (counter) k_face_pgd<true, true><<<grid, PGD_BLOCK, 0, s>>>(block_map, xf, sdfs, meshes, st, counter, gu);
+        else k_face_pgd<false, true><<<grid, PGD_BLOCK, 0, s>>>(block_map, xf, sdfs, meshes, st, nullptr, gu);
+    } else {
+        if (counter) k_face_pgd<true, false><<<grid, PGD_BLOCK, 0, s>>>(block_map, xf, sdfs, meshes, st, counter, gu);
+        else k_face_pgd<false, false><<<grid, PGD_BLOCK, 0, s>>>(block_map, xf, sdfs, meshes, st, nullptr, gu);
     }
 }
 

@@ -3,19 +3,32 @@
 
 namespace cs {
 
-constexpr int FACE_BLOCK = 128;
+constexpr int PGD_BLOCK = 128;
+constexpr int PGD_GRAB = 64;  // work items a warp claims per atomic
 constexpr int COMPACT_BLOCK = 256;
 constexpr int MAX_MINIMIZE_ITERS = 12;  // generation.py:19
 
-// Per-face staging. k_faces block b covers faces [f0, f0 + FACE_BLOCK) of one env
-// and writes its found faces, compacted, to rows cand_base[e] + f0 + [0, count).
+// One face that survived the cull and the Lipschitz prune (k_face_prep), waiting
+// for its projected-gradient descent (k_face_pgd).
+struct FaceWork {
+    int64_t row;        // staging row: cand_base[e] + f0 + rank among the chunk's survivors
+    int32_t blk;        // k_face_prep block (env, chunk)
+    int32_t face;       // face index | start corner << 30 (0 centroid, 1..3 = a, b, c)
+    double phi[4];      // phi at a, b, c and at the start point
+};
+
+// Per-face staging. k_face_prep block b covers faces [f0, f0 + FACE_CHUNK) of one
+// env; its survivors own rows cand_base[e] + f0 + [0, chunk_count[b]) in face order.
 struct Staging {
     double *point;         // [row,3] grid frame
     double *phi;
     double *grad;          // [row,3] unnormalised
-    int32_t *face;         // [row]
-    int32_t *chunk_count;  // [nblocks] found faces per k_faces block
+    int32_t *face;         // [row] face index if found, else -1
+    int32_t *chunk_count;  // [nblocks] survivors per block
+    int32_t *chunk_found;  // [nblocks] found faces per block
     int32_t *chunk_off;    // [nblocks] candidate offset of the block's first found face
+    FaceWork *work;        // [capacity] survivors, dense
+    unsigned *work_count;  // [0] survivors listed, [1] survivors claimed by k_face_pgd
 };
 
 // Candidate arrays (row = cand_base[e] + candidate index).
@@ -28,10 +41,14 @@ struct Candidates {
 
 void launch_env_xf(int64_t E, const int32_t *env_sdf, const int32_t *env_mesh, const SdfDesc *sdfs,
                    const double *sdf_pose, const double *mesh_pose, int pose_format, const double *cd, EnvXf *xf,
-                   int32_t *env_status, double *env_min_depth, cudaStream_t s);
-void launch_faces(int64_t nblocks, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs,
-                  const MeshDesc *meshes, const int64_t *cand_base, const Staging &st, unsigned long long *counter,
-                  const GridT<double> *uniform, cudaStream_t s);
+                   int32_t *env_status, double *env_min_depth, unsigned *work_count, cudaStream_t s);
+void launch_face_prep(int64_t nblocks, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs,
+                      const MeshDesc *meshes, const int64_t *cand_base, const Staging &st, int max_chunk_verts,
+                      unsigned long long *counter, const GridT<double> *uniform, cudaStream_t s);
+void launch_face_pgd(int grid, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs, const MeshDesc *meshes,
+                     const Staging &st, unsigned long long *counter, const GridT<double> *uniform, cudaStream_t s);
+int face_pgd_grid(int sm_count);  // resident CTAs of k_face_pgd over the device
+size_t face_prep_smem(int max_chunk_verts);
 void launch_compact(int64_t E, const EnvXf *xf, const int64_t *cand_base, const int2 *block_map,
                     const int32_t *chunk_first, const Staging &st, const Candidates &cs, int32_t *n_cand,
                     cudaStream_t s);

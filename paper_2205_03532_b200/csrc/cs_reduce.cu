@@ -95,19 +95,27 @@ __global__ void __launch_bounds__(RED_T) k_reduce(ReduceIO io, ReduceParams p, i
     // order = candidates passing min_depth (reduction.py:50-53), ascending
     const bool has_md = io.env_min_depth ? true : (p.has_min_depth != 0);
     const double md = io.env_min_depth ? io.env_min_depth[e] : p.min_depth;
-    int n_order = 0;
-    if (wid == 0) n_order = warp_compact(C, [&](int i) { return !has_md || __ldg(dep + i) >= md; }, ord);
-    if (tid == 0) s_P = n_order;
-    __syncthreads();
-    n_order = s_P;
-    __syncthreads();
+    // Generated candidates always pass (phi <= cd  =>  depth >= -cd), so check that
+    // in parallel first and keep the identity order; compact only when some fail.
+    bool any_fail = false;
+    if (has_md)
+        for (int i = tid; i < C; i += RED_T) any_fail |= !(__ldg(dep + i) >= md);
+    const bool identity = !__syncthreads_or(any_fail);
+    int n_order = C;
+    if (!identity) {
+        if (wid == 0) n_order = warp_compact(C, [&](int i) { return !has_md || __ldg(dep + i) >= md; }, ord);
+        if (tid == 0) s_P = n_order;
+        __syncthreads();
+        n_order = s_P;
+        __syncthreads();
+    }
 
     int P = 0;  // builders; uniform across the CTA at every barrier
     for (int start = 0; start < n_order; start += p.batch_size) {
         const int bsz = min(p.batch_size, n_order - start);
         // stage the batch: candidate index, normal and depth per position (read many times below)
         for (int k = tid; k < bsz; k += RED_T) {
-            const int i = ord[start + k];
+            const int i = identity ? start + k : ord[start + k];
             sbo[k] = i;
             bnrm[3 * k] = __ldg(nrm + 3 * (int64_t)i);
             bnrm[3 * k + 1] = __ldg(nrm + 3 * (int64_t)i + 1);
@@ -343,15 +351,25 @@ __global__ void __launch_bounds__(RED_T) k_reduce(ReduceIO io, ReduceParams p, i
     }
     __syncwarp();
     int32_t *mem = io.members + base;
-    for (int c0 = 0; c0 < C; c0 += 32) {
-        const int i = c0 + lane;
-        const int l = (i < C) ? lab[i] : -1;
-        const unsigned peers = __match_any_sync(FULL, l);
-        const int rank = __popc(peers & lt);
-        if (l >= 0) mem[hcnt[l] + rank] = i;
-        __syncwarp();
-        if (l >= 0 && rank == 0) hcnt[l] += __popc(peers);
-        __syncwarp();
+    constexpr int PF = 8;  // labels prefetched per lane: keeps 8 loads in flight per round
+    for (int c0 = 0; c0 < C; c0 += 32 * PF) {
+        int lb[PF];
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+            const int i = c0 + 32 * u + lane;
+            lb[u] = (i < C) ? lab[i] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+            const int i = c0 + 32 * u + lane;
+            const int l = lb[u];
+            const unsigned peers = __match_any_sync(FULL, l);
+            const int rank = __popc(peers & lt);
+            if (l >= 0) mem[hcnt[l] + rank] = i;
+            __syncwarp();
+            if (l >= 0 && rank == 0) hcnt[l] += __popc(peers);
+            __syncwarp();
+        }
     }
 }
 
