@@ -1,32 +1,45 @@
-// Per-patch finalisation on sm_100a (reduction.py:146-236).
+// Per-patch finalisation on sm_100a (reduction.py:146-236), split by the kind of
+// parallelism each part has:
 //
-//   k_patch_off     exclusive scan of patch counts -> work list [E+1].
-//   k_finalize<W>   ONE WARP PER PATCH for patches of <= FIN_SMALL members
-//                   (~95% of patches): the (u, v, pos) sort keys and the chain
-//                   stack live in this warp's slice of shared memory; member rows
-//                   are read through the read-only path. Warps never block each
-//                   other, so an SM keeps ~20 patches in flight and the inherently
-//                   sequential parts (monotone chain, axis-0 folds) overlap.
-//   k_finalize<B>   ONE CTA PER PATCH for larger patches (shared memory up to
-//                   FIN_LARGE members, global scratch beyond).
-//   k_stats         per env stats (the multi-GPU all-gather payload).
-// Both paths run the same templated per-patch code (finalize_patch) over a
-// "team" (warp or block) abstraction, so they produce identical bits.
+//   k_patch_off       exclusive scan of patch counts -> work list [E+1].
+//   k_fin_sort_warp   ONE WARP PER PATCH (<= FW_SMEM members), in shared memory:
+//                     deepest member (first argmax), max depth, touching count, the
+//                     weighted sums (reduction.py:162-165), the (u, v) projections
+//                     (reduction.py:202-204) and a merge-path sort by (u, v, member)
+//                     -- lexsort's order (reduction.py:211) -- written to the
+//                     patch's scratch rows; queues the patch's chain jobs.
+//   k_fin_sort_block  the same, ONE CTA per larger patch.
+//   k_fin_chain       ONE WARP PER PATCH, an 8-lane group per half chain of Andrew's
+//                     monotone chain (reduction.py:214-223), lower and upper, over all
+//                     members (the area hull) and, when the kept selection uses them,
+//                     over the touching members (reduction.py:183-185); the pops of a
+//                     key are tested in parallel. A persistent queue, long patches first.
+//   k_fin_kept        one warp per patch: hull assembly, kept selection
+//                     (reduction.py:172-199), hull area (reduction.py:227-236), rows.
+//   k_stats           per env stats (the multi-GPU all-gather payload).
+//
+// The chains are sequential by definition (each step depends on the stack the
+// previous steps left), so their parallelism is across patches, not within one.
+// One sort serves both hulls: lexsort of the touching subset breaks (u, v) ties by
+// position in that subset, which is monotone in the member position, so its order
+// is the all-members order (u, v, member) filtered to the touching members; the
+// projections are the same V3 gemv dot products either way.
+#include <cuda_pipeline.h>
 #include <stdint.h>
 
 #include "cs_reduce_util.cuh"
 
 namespace cs {
 
-constexpr int FIN_SMALL = 512;        // members per warp-path patch
-constexpr int FIN_WARPS = 2;          // warp teams per CTA (small path)
-constexpr int FIN_LARGE = 1024;       // members per CTA-path patch held in shared memory
-constexpr int FIN_LARGE_THREADS = 256;
+constexpr int FW_WARPS = 4;      // warp teams per k_fin_sort_warp CTA
+constexpr int FW_SMEM = 256;     // members per warp-path patch (all in shared memory)
+constexpr int FB_THREADS = 128;  // k_fin_sort_block
 
 __global__ void k_patch_off(int64_t E, const int32_t *__restrict__ n_patch, int32_t *__restrict__ off,
-                            int32_t *__restrict__ large_count) {
+                            int32_t *__restrict__ large_count, int32_t *__restrict__ njob) {
     __shared__ int ws[WS_INTS];
     if (threadIdx.x == 0) *large_count = 0;
+    if (threadIdx.x < 4) njob[threadIdx.x] = 0;
     int running = 0;
     for (int64_t e0 = 0; e0 < E; e0 += blockDim.x) {
         int64_t e = e0 + threadIdx.x;
@@ -64,9 +77,12 @@ struct WarpTeam {
         for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
         return x;
     }
+    __device__ int isum(int x) const {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        return x;
+    }
     __device__ bool any(bool b) const { return __any_sync(0xffffffffu, b); }
-    __device__ int bcast(int v) const { return __shfl_sync(0xffffffffu, v, 0); }
-    __device__ double bcast(double v) const { return __shfl_sync(0xffffffffu, v, 0); }
     // best (bk, bd) under depth_before over the team
     __device__ void best_depth(int &bk, double &bd) const {
 #pragma unroll
@@ -76,28 +92,12 @@ struct WarpTeam {
             if (ok >= 0 && (bk < 0 || depth_before(od, ok, bd, bk))) { bk = ok; bd = od; }
         }
     }
-    template <class Idx, class Pred>
-    __device__ int compact(int m, Pred pred, Idx *out) const {
-        const unsigned lt = (1u << rank()) - 1u;
-        int running = 0;
-        for (int c0 = 0; c0 < m; c0 += 32) {
-            int k = c0 + rank();
-            bool f = k < m && pred(k);
-            unsigned b = __ballot_sync(0xffffffffu, f);
-            if (f) out[running + __popc(b & lt)] = (Idx)k;
-            running += __popc(b);
-        }
-        __syncwarp();
-        return running;
-    }
 };
 
 struct BlockTeam {
-    int *misc;        // >= 4 ints
-    ArgMax *am;       // 32 entries
-    int *ws;          // WS_INTS
-    double *dred;     // 32 doubles
-    int *ired;        // 32 ints
+    ArgMax *am;    // 32 entries
+    double *dred;  // 32 doubles
+    int *ired;     // 32 ints
     __device__ int rank() const { return threadIdx.x; }
     __device__ int size() const { return blockDim.x; }
     __device__ void sync() const { __syncthreads(); }
@@ -113,21 +113,18 @@ struct BlockTeam {
         __syncthreads();
         return r;
     }
+    __device__ int isum(int x) const {
+        int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) ired[wid] = x;
+        __syncthreads();
+        int r = 0;
+        for (int i = 0; i < nw; ++i) r += ired[i];
+        __syncthreads();
+        return r;
+    }
     __device__ bool any(bool b) const { return __syncthreads_or(b) != 0; }
-    __device__ int bcast(int v) const {
-        if (threadIdx.x == 0) misc[3] = v;
-        __syncthreads();
-        int r = misc[3];
-        __syncthreads();
-        return r;
-    }
-    __device__ double bcast(double v) const {
-        if (threadIdx.x == 0) dred[31] = v;
-        __syncthreads();
-        double r = dred[31];
-        __syncthreads();
-        return r;
-    }
     __device__ void best_depth(int &bk, double &bd) const {
         int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
 #pragma unroll
@@ -143,191 +140,438 @@ struct BlockTeam {
             if (ired[i] >= 0 && (bk < 0 || depth_before(dred[i], ired[i], bd, bk))) { bk = ired[i]; bd = dred[i]; }
         __syncthreads();
     }
-    template <class Idx, class Pred>
-    __device__ int compact(int m, Pred pred, Idx *out) const {
-        int running = 0;
-        for (int c0 = 0; c0 < m; c0 += blockDim.x) {
-            int k = c0 + threadIdx.x;
-            int f = (k < m && pred(k)) ? 1 : 0;
-            int tot;
-            int pos = running + block_excl_scan(f, ws, &tot);
-            if (f) out[pos] = (Idx)k;
-            running += tot;
-        }
-        return running;
-    }
 };
 
-// All-ascending bitonic sort of m (u, v, pos) keys by a team (virtual +inf padding).
-template <class Team, class Idx>
-__device__ void team_sort(const Team &t, double *su, double *sv, Idx *sp, int m) {
-    int P2 = 1, lg = 0;
-    while (P2 < m) { P2 <<= 1; ++lg; }
-    const int half = P2 >> 1;
-    for (int lk = 1; lk <= lg; ++lk) {  // k = 2^lk
-        const int k = 1 << lk, hk = k >> 1;
-        for (int lj = lk - 1; lj >= 0; --lj) {  // jj = 2^lj
-            const int jj = 1 << lj;
-            for (int idx = t.rank(); idx < half; idx += t.size()) {
-                int i, j;
-                if (jj == hk) {  // first step of a merge: mirrored partner
-                    const int blk = idx >> lj, off = idx & (jj - 1);
-                    i = (blk << lk) + off;
-                    j = (blk << lk) + k - 1 - off;
+// ------------------------------------------------------------------ sort
+
+struct Keys {
+    double *u, *v;
+    int32_t *k;
+};
+
+// Merge-path merge sort of m (u, v, k) keys (k distinct, so the order is total).
+// Each rank owns c = ceil(m / T) consecutive output slots: it insertion-sorts its
+// segment, then in every round binary-searches its split of the merge path of the
+// two runs it falls in and merges c outputs into the other buffer. log2(T) rounds.
+// Returns the buffer holding the result (0: a, 1: b).
+template <class Team>
+__device__ int team_merge_sort(const Team &t, Keys a, Keys b, int m) {
+    const int T = t.size(), r = t.rank();
+    const int c = (m + T - 1) / T;
+    const int s0 = r * c, s1 = min(s0 + c, m);
+    for (int i = s0 + 1; i < s1; ++i) {
+        const double u = a.u[i], v = a.v[i];
+        const int k = a.k[i];
+        int j = i - 1;
+        while (j >= s0) {
+            const double uj = a.u[j], vj = a.v[j];
+            const int kj = a.k[j];
+            if (!key_less(u, v, k, uj, vj, kj)) break;
+            a.u[j + 1] = uj; a.v[j + 1] = vj; a.k[j + 1] = kj;
+            --j;
+        }
+        a.u[j + 1] = u; a.v[j + 1] = v; a.k[j + 1] = k;
+    }
+    t.sync();
+    int src = 0;
+    for (int run = c; run < m; run <<= 1) {
+        const Keys S = src ? b : a, D = src ? a : b;
+        if (s0 < m) {
+            const int ps = (s0 / (2 * run)) * (2 * run);
+            const int a0 = ps, a1 = min(ps + run, m), b1 = min(ps + 2 * run, m);
+            const int d = s0 - ps;
+            int lo = max(0, d - (b1 - a1)), hi = min(d, a1 - a0);
+            while (lo < hi) {  // first A element that is not among the first d outputs
+                const int mid = (lo + hi) >> 1, bj = a1 + d - 1 - mid;
+                if (key_less(S.u[a0 + mid], S.v[a0 + mid], S.k[a0 + mid], S.u[bj], S.v[bj], S.k[bj])) lo = mid + 1;
+                else hi = mid;
+            }
+            int i = a0 + lo, j = a1 + (d - lo);
+            double ua = 0.0, va = 0.0, ub = 0.0, vb = 0.0;
+            int ka = 0, kb = 0;
+            if (i < a1) { ua = S.u[i]; va = S.v[i]; ka = S.k[i]; }
+            if (j < b1) { ub = S.u[j]; vb = S.v[j]; kb = S.k[j]; }
+            for (int o = s0; o < s1; ++o) {
+                if (j >= b1 || (i < a1 && key_less(ua, va, ka, ub, vb, kb))) {
+                    D.u[o] = ua; D.v[o] = va; D.k[o] = ka;
+                    if (++i < a1) { ua = S.u[i]; va = S.v[i]; ka = S.k[i]; }
                 } else {
-                    const int blk = idx >> lj, off = idx & (jj - 1);
-                    i = (blk << (lj + 1)) + off;
-                    j = i + jj;
-                }
-                if (j < m) {
-                    double ui = su[i], uj = su[j], vi = sv[i], vj = sv[j];
-                    int pi = sp[i], pj = sp[j];
-                    if (key_less(uj, vj, pj, ui, vi, pi)) {
-                        su[i] = uj; su[j] = ui; sv[i] = vj; sv[j] = vi; sp[i] = (Idx)pj; sp[j] = (Idx)pi;
-                    }
+                    D.u[o] = ub; D.v[o] = vb; D.k[o] = kb;
+                    if (++j < b1) { ub = S.u[j]; vb = S.v[j]; kb = S.k[j]; }
                 }
             }
-            t.sync();
-        }
-    }
-}
-
-// One half of Andrew's monotone chain (reduction.py:214-223) over the sorted keys:
-// dir > 0 is the lower chain (ascending), dir < 0 the upper one (descending).
-// The two stack-top points are cached in registers, so a step costs one cross
-// product; the stack itself (indices) is only reloaded on a pop. Returns length.
-template <class Idx>
-__device__ int half_chain(const double *su, const double *sv, int m, int dir, Idx *h) {
-    int top = 0;
-    double ua = 0.0, va = 0.0, ub = 0.0, vb = 0.0;  // h[top-2], h[top-1]
-    for (int t = 0; t < m; ++t) {
-        const int s = dir > 0 ? t : m - 1 - t;
-        const double us = su[s], vs = sv[s];
-        while (top >= 2) {
-            // cross(o, a, b) = (a.u - o.u)(b.v - o.v) - (a.v - o.v)(b.u - o.u), o = h[top-2], a = h[top-1]
-            const double cr = (ub - ua) * (vs - va) - (vb - va) * (us - ua);
-            if (cr > 0.0) break;
-            --top;
-            ub = ua; vb = va;
-            if (top >= 2) { const int o = h[top - 2]; ua = su[o]; va = sv[o]; }
-        }
-        h[top] = (Idx)s;
-        ua = ub; va = vb;
-        ub = us; vb = vs;
-        ++top;
-    }
-    return top;
-}
-
-// _monotone_hull: lower and upper chains run concurrently in ranks 0 and 1, then
-// hull = lower[:-1] + upper[:-1] is assembled in h[0..H). h needs 2m + 4 entries.
-template <class Team, class Idx>
-__device__ int team_chain(const Team &t, const double *su, const double *sv, int m, Idx *h) {
-    const int r = t.rank();
-    int len = 0;
-    if (r < 2) len = half_chain(su, sv, m, r == 0 ? 1 : -1, h + (r == 0 ? 0 : m + 1));
-    if (r == 0) t.misc[1] = len;
-    if (r == 1) t.misc[2] = len;
-    t.sync();
-    const int L = t.misc[1], U = t.misc[2];
-    t.sync();
-    if (r == 0)  // upper[:-1] after lower[:-1] (ascending copy: the ranges overlap downwards only)
-        for (int j = 0; j < U - 1; ++j) h[L - 1 + j] = h[m + 1 + j];
-    t.sync();
-    return (L - 1) + (U - 1);
-}
-
-template <class Idx>
-__device__ double chain_area(const double *su, const double *sv, const Idx *h, int H) {
-    double d1 = ddot_x2(H, [&](int k) { return su[h[k]]; }, [&](int k) { return sv[h[(k + 1) % H]]; });
-    double d2 = ddot_x2(H, [&](int k) { return sv[h[k]]; }, [&](int k) { return su[h[(k + 1) % H]]; });
-    return 0.5 * fabs(d1 - d2);
-}
-
-// the member weights, for numpy's pairwise summation
-struct WeightBuf {
-    const double *d;  // staged member depths; the weight is max(depth, 0)
-    __device__ double operator()(int k) const { return weight_of(d[k]); }
-};
-
-// One patch (reduction.py:146-199). su/sv/sp/sh/wbuf: team-private scratch of >= m
-// (wbuf holds the member depths once gathered)
-// entries (sh: >= 2m + 4; su: >= 9 x team size); chosen: MAX_KEPT ints.
-template <class Team, class Idx>
-__device__ void finalize_patch(const Team &t, const ReduceIO &io, const ReduceParams &p, int64_t e, int q,
-                               double *su, double *sv, Idx *sp, Idx *sh, double *wbuf, int *chosen) {
-    const int N = p.N, K = p.K;
-    const int64_t base = io.cand_base[e];
-    const int32_t *moffp = io.member_offsets + e * (N + 1);
-    const int moff = moffp[q];
-    const int m = moffp[q + 1] - moff;
-    const int32_t *mem = io.members + base + moff;
-    const int64_t pq = e * N + q;
-    const double *P = io.point + 3 * base, *Nn = io.normal + 3 * base, *D = io.depth + base;
-    auto dep = [&](int k) { return __ldg(D + mem[k]); };
-    auto pt = [&](int k, int c) { return __ldg(P + 3 * (int64_t)mem[k] + c); };
-    auto nr = [&](int k, int c) { return __ldg(Nn + 3 * (int64_t)mem[k] + c); };
-
-    // deepest (first argmax), NaN-propagating max
-    ArgMax am = {0.0, -1, 0};
-    double mx = -INFINITY;
-    bool anynan = false;
-    for (int k = t.rank(); k < m; k += t.size()) {
-        const double d = dep(k);
-        wbuf[k] = d;
-        am = argmax_combine(am, ArgMax{d, k, 1});
-        anynan |= isnan(d);
-        if (d > mx) mx = d;
-    }
-    am = t.argmax(am);
-    const int deepest = am.i;
-    mx = t.max(mx);
-    anynan = t.any(anynan);
-
-    double t1[3], t2[3];
-    tangent_basis(io.patch_normal + 3 * pq, t1, t2);
-    // base = touching members (depth >= 0) if >= 3 else all (reduction.py:183-184)
-    t.sync();
-    const int nt = t.compact(m, [&](int k) { return wbuf[k] >= 0.0; }, sp);
-    const bool all_base = nt < 3 || nt == m;
-    const int nb = nt < 3 ? m : nt;
-    const bool need_sel = m > K;
-    bool have_hull = false;
-    int H = 0;
-    if (need_sel || (m >= 3 && all_base)) {
-        for (int j = t.rank(); j < nb; j += t.size()) {
-            int k = (nt < 3) ? j : (int)sp[j];
-            double x = pt(k, 0), y = pt(k, 1), z = pt(k, 2);
-            su[j] = V3(x, y, z, t1[0], t1[1], t1[2]);  // _project_2d, n >= 2
-            sv[j] = V3(x, y, z, t2[0], t2[1], t2[2]);
-            sp[j] = (Idx)k;  // payload: member position (monotone in base order)
         }
         t.sync();
-        team_sort(t, su, sv, sp, nb);
-        H = team_chain(t, su, sv, nb, sh);
-        have_hull = true;
+        src ^= 1;
     }
+    return src;
+}
+
+// Which hulls a patch needs (reduction.py:152,174-185,227-231).
+__device__ __forceinline__ bool needs_all_hull(int m, int K) { return m >= 3 || m > K; }
+__device__ __forceinline__ bool needs_touch_hull(int m, int nt, int K) { return m > K && nt >= 3 && nt < m; }
+
+// ------------------------------------------------------------------ stage 1: per patch
+
+__device__ __forceinline__ int64_t env_of(const int32_t *patch_off, int64_t E, int w) {
+    int64_t lo = 0, hi = E - 1;  // last e with patch_off[e] <= w
+    while (lo < hi) {
+        int64_t mid = (lo + hi + 1) >> 1;
+        if (patch_off[mid] <= w) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// Patch w = (e, q), by a team (warp or CTA). A/B: the team's sort buffers (shared
+// memory, or the patch's global rows when it is very large); B holds the member
+// weights until the sort. tile: 9 x T doubles of shared memory.
+//   * one pass over the members: deepest (first argmax), max depth, touching count,
+//     weights, the nine weighted products (np.cross(pts, norms) * w etc.) through
+//     the tile, folded by ranks 0..8 in member order (numpy's axis-0 sums add row
+//     after row, reduction.py:163-165), and the (u, v) projections
+//     (reduction.py:202-204);
+//   * the pairwise weight sum (reduction.py:162);
+//   * a merge-path sort by (u, v, member) (lexsort, reduction.py:211), written to
+//     the patch's rows of suv/sp (non-touching members as ~k), and the patch's
+//     chain jobs queued (long patches and short patches in separate lists).
+template <class Team>
+__device__ void sort_patch(const Team &t, const ReduceIO &io, const ReduceParams &p, int w, int64_t e, int q, Keys A,
+                           Keys B, double *tile) {
+    const int N = p.N, K = p.K;
+    const int64_t base = io.cand_base[e];
+    const int32_t *mo = io.member_offsets + e * (N + 1);
+    const int moff = mo[q], m = mo[q + 1] - moff;
+    const int32_t *mem = io.members + base + moff;
+    const int64_t pq = e * N + q, row0 = base + moff;
+    const double *P = io.point + 3 * base, *Nn = io.normal + 3 * base, *D = io.depth + base;
+    const bool hull = needs_all_hull(m, K);
+    double t1[3] = {0.0, 0.0, 0.0}, t2[3] = {0.0, 0.0, 0.0};
+    if (hull) tangent_basis(io.patch_normal + 3 * pq, t1, t2);
+    double *wb = B.u;
+    const int r = t.rank(), T = t.size();
+    ArgMax am = {0.0, -1, 0};
+    double mx = -INFINITY, s = 0.0;
+    bool anynan = false;
+    int nt = 0;
+    for (int c0 = 0; c0 < m; c0 += T) {
+        const int k = c0 + r;
+        if (k < m) {
+            const int64_t i = mem[k];
+            const double d = __ldg(D + i);
+            const double px = __ldg(P + 3 * i), py = __ldg(P + 3 * i + 1), pz = __ldg(P + 3 * i + 2);
+            const double nx = __ldg(Nn + 3 * i), ny = __ldg(Nn + 3 * i + 1), nz = __ldg(Nn + 3 * i + 2);
+            const double wk = weight_of(d);
+            wb[k] = wk;
+            am = argmax_combine(am, ArgMax{d, k, 1});
+            anynan |= isnan(d);
+            if (d > mx) mx = d;
+            nt += d >= 0.0 ? 1 : 0;
+            tile[0 * T + r] = px * wk; tile[1 * T + r] = py * wk; tile[2 * T + r] = pz * wk;
+            tile[3 * T + r] = nx * wk; tile[4 * T + r] = ny * wk; tile[5 * T + r] = nz * wk;
+            tile[6 * T + r] = (py * nz - pz * ny) * wk;
+            tile[7 * T + r] = (pz * nx - px * nz) * wk;
+            tile[8 * T + r] = (px * ny - py * nx) * wk;
+            if (hull) {
+                A.u[k] = V3(px, py, pz, t1[0], t1[1], t1[2]);  // _project_2d: (n,3) @ (3,), n >= 2
+                A.v[k] = V3(px, py, pz, t2[0], t2[1], t2[2]);
+                A.k[k] = k;
+            }
+        }
+        t.sync();
+        if (r < 9) {
+            const int cnt = min(T, m - c0);
+            const double *row = tile + r * T;
+            for (int j = 0; j < cnt; ++j) s = (c0 + j == 0) ? row[j] : s + row[j];
+        }
+        t.sync();
+    }
+    am = t.argmax(am);
+    mx = t.max(mx);
+    anynan = t.any(anynan);
+    nt = t.isum(nt);
+    if (r < 9) {
+        const int kind = r / 3, c = r % 3;
+        double *o = (kind == 0 ? io.wp_sum : kind == 1 ? io.wn_sum : io.wt_sum) + 3 * pq;
+        o[c] = s;
+    } else if (r == 9) {
+        io.w_sum[pq] = 0.0 + pairwise([&](int k) { return wb[k]; }, 0, m);
+    } else if (r == 10) {
+        io.max_depth[pq] = anynan ? (double)NAN : mx;  // deps.max() propagates NaN
+        io.pdeep[w] = am.i;
+        io.pnt[w] = nt;
+        io.wenv[w] = (int32_t)e;
+        if (hull) {  // chain job; long patches first (their chains are the critical path)
+            const int list = m > FW_SMEM ? 0 : 1;
+            io.jobs[(int64_t)list * io.E * N + atomicAdd(io.njob + list, 1)] = w;
+        }
+    }
+    t.sync();
+    if (!hull) return;
+    const Keys R = team_merge_sort(t, A, B, m) ? B : A;
+    for (int j = r; j < m; j += T) {
+        const int k = R.k[j];
+        io.suv[row0 + j] = make_double2(R.u[j], R.v[j]);
+        io.sp[row0 + j] = __ldg(D + mem[k]) >= 0.0 ? k : ~k;
+    }
+    t.sync();
+}
+
+// shared-memory sort buffers of `cap` keys, A then B, from `p`
+__device__ __forceinline__ void carve(unsigned char *p, int cap, Keys &A, Keys &B) {
+    double *d = reinterpret_cast<double *>(p);
+    int32_t *k = reinterpret_cast<int32_t *>(d + 4 * cap);
+    A = Keys{d, d + cap, k};
+    B = Keys{d + 2 * cap, d + 3 * cap, k + cap};
+}
+
+constexpr size_t FW_BYTES_PER_WARP = (size_t)FW_SMEM * 2 * (8 + 8 + 4) + 9 * 32 * 8;
+constexpr int FB_SMEM = 1024;  // members a k_fin_sort_block CTA sorts in shared memory
+constexpr size_t FB_BYTES = (size_t)FB_SMEM * 2 * (8 + 8 + 4);
+
+// Patches of <= FW_SMEM members: one warp each.
+__global__ void __launch_bounds__(FW_WARPS * 32) k_fin_sort_warp(ReduceIO io, ReduceParams p) {
+    extern __shared__ __align__(16) unsigned char dyn[];
+    const int wib = threadIdx.x >> 5;
+    unsigned char *mine = dyn + wib * FW_BYTES_PER_WARP;
+    Keys A, B;
+    carve(mine, FW_SMEM, A, B);
+    double *tile = reinterpret_cast<double *>(mine + (size_t)FW_SMEM * 40);
+    WarpTeam t{nullptr};
+    const int64_t E = io.E;
+    const int total = io.patch_off[E];
+    for (int w = blockIdx.x * FW_WARPS + wib; w < total; w += gridDim.x * FW_WARPS) {
+        const int64_t e = env_of(io.patch_off, E, w);
+        const int q = w - io.patch_off[e];
+        const int32_t *mo = io.member_offsets + e * (p.N + 1);
+        if (mo[q + 1] - mo[q] > FW_SMEM) {  // handed to the CTA path (order-free: patches are independent)
+            if ((threadIdx.x & 31) == 0) io.large_list[atomicAdd(io.large_count, 1)] = w;
+            continue;
+        }
+        sort_patch(t, io, p, w, e, q, A, B, tile);
+    }
+}
+
+// Larger patches: one CTA each; shared memory up to FB_SMEM members, global scratch rows beyond.
+__global__ void __launch_bounds__(FB_THREADS) k_fin_sort_block(ReduceIO io, ReduceParams p) {
+    extern __shared__ __align__(16) unsigned char dyn[];
+    __shared__ double tile[9 * FB_THREADS];
+    __shared__ ArgMax s_am[32];
+    __shared__ double s_dred[32];
+    __shared__ int s_ired[32];
+    BlockTeam t{s_am, s_dred, s_ired};
+    const int64_t E = io.E;
+    const int total = *io.large_count;
+    for (int li = blockIdx.x; li < total; li += gridDim.x) {
+        const int w = io.large_list[li];
+        const int64_t e = env_of(io.patch_off, E, w);
+        const int q = w - io.patch_off[e];
+        const int32_t *mo = io.member_offsets + e * (p.N + 1);
+        Keys A, B;
+        if (mo[q + 1] - mo[q] <= FB_SMEM) {
+            carve(dyn, FB_SMEM, A, B);
+        } else {
+            const int64_t row0 = io.cand_base[e] + mo[q];
+            A = Keys{io.su + row0, io.sv + row0, io.sp + row0};
+            B = Keys{io.tu + row0, io.tv + row0, io.tk + row0};
+        }
+        sort_patch(t, io, p, w, e, q, A, B, tile);
+    }
+}
+
+// ------------------------------------------------------------------ stage 2: chains
+
+constexpr int CH_WARPS = 4;  // warps per k_fin_chain CTA
+constexpr int CG = 8;        // lanes per half chain: the stack-top window
+constexpr int CR = 64;       // stack entries per half chain kept in shared memory
+
+// ONE WARP PER PATCH, one 8-lane group per half chain of _monotone_hull
+// (reduction.py:214-223): group 0/1 the lower/upper chain over all sorted members
+// (the hull area), 2/3 over the touching members (the kept selection). Patches are
+// claimed from the job queue (long patches first).
+//
+// The chain is sequential in its keys, but the pops of one key are not: the
+// sequential loop tests cross(h[top-2-i], h[top-1-i], b) for i = 0, 1, ... on the
+// unchanged stack below the pops, stopping at the first positive one. Lane i of a
+// group holds stack entry top-1-i, takes entry top-2-i from lane i+1, evaluates
+// that same test, and a ballot gives the number of pops; so one key costs one
+// cross product whatever it pops. The window shifts by shuffles; entries below it
+// come from a shared-memory ring of the top CR entries (older ones spilled to
+// hu/hv/hj when a new high-water mark reuses their slot). Keys stream from the
+// sorted rows, each lane prefetching every 8th key one round ahead.
+__global__ void __launch_bounds__(CH_WARPS * 32) k_fin_chain(ReduceIO io, ReduceParams p) {
+    __shared__ double2 s_ruv[CH_WARPS][4][CR];
+    __shared__ int32_t s_rpos[CH_WARPS][4][CR];
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int g = lane >> 3, li = lane & 7, gb = g * CG;
+    double2 *ruv = s_ruv[wib][g];
+    int32_t *rpos = s_rpos[wib][g];
+    const int nl = io.njob[0], ntot = nl + io.njob[1];
+    const int64_t lcap = io.E * (int64_t)p.N;
+    while (true) {
+        int idx = 0;
+        if (lane == 0) idx = atomicAdd(io.njob + 2, 1);
+        idx = __shfl_sync(FULL, idx, 0);
+        if (idx >= ntot) break;
+        const int w = idx < nl ? io.jobs[idx] : io.jobs[lcap + idx - nl];
+        const int64_t e = io.wenv[w];
+        const int q = w - io.patch_off[e];
+        const int32_t *mo = io.member_offsets + e * (p.N + 1);
+        const int m = mo[q + 1] - mo[q];
+        const int64_t row0 = io.cand_base[e] + mo[q];
+        const bool run = g < 2 ? needs_all_hull(m, p.K) : needs_touch_hull(m, io.pnt[w], p.K);
+        const int dir = (g & 1) ? -1 : 1;
+        const bool touching = g >= 2;
+        const double2 *suv = io.suv + row0;
+        const int32_t *sk = io.sp + row0;
+        const int64_t h0 = 4 * row0 + (int64_t)g * m;
+        int32_t *hj = io.hj + h0;
+        double *hu = io.hu + h0, *hv = io.hv + h0;
+        auto load_key = [&](int x, double2 &uv, int &k) {
+            if (run && x < m) {
+                const int s = dir > 0 ? x : m - 1 - x;
+                uv = __ldg(suv + s);
+                k = __ldg(sk + s);
+            } else {
+                uv = make_double2(0.0, 0.0);
+                k = -1;
+            }
+        };
+        int hw = 0;  // high-water mark of the stack (ring invariant below)
+        auto entry = [&](int j, double &u, double &v) {  // stack entry j (j < top)
+            if (j < 0) { u = 0.0; v = 0.0; return; }
+            if (j >= hw - CR) { const double2 x = ruv[j % CR]; u = x.x; v = x.y; }
+            else { u = hu[j]; v = hv[j]; }
+        };
+        double2 cur_uv, nxt_uv;
+        int cur_k, nxt_k;
+        load_key(li, cur_uv, cur_k);
+        load_key(CG + li, nxt_uv, nxt_k);
+        double wu = 0.0, wv = 0.0, bu = 0.0, bv = 0.0;  // entry top-1-li; lane 7 also entry top-9
+        int top = 0;
+        for (int t = 0; t < m; ++t) {
+            const int c = t & (CG - 1);
+            if (c == 0 && t > 0) {
+                cur_uv = nxt_uv; cur_k = nxt_k;
+                load_key(t + CG + li, nxt_uv, nxt_k);
+            }
+            const double ub = __shfl_sync(FULL, cur_uv.x, gb + c), vb = __shfl_sync(FULL, cur_uv.y, gb + c);
+            const int kb = __shfl_sync(FULL, cur_k, gb + c);
+            const bool act = run && (!touching || kb >= 0);
+            // pops: lane i tests cross(o = entry top-2-i, a = entry top-1-i, b)
+            bool more = act;
+            while (__any_sync(FULL, more)) {
+                double ou = __shfl_down_sync(FULL, wu, 1), ov = __shfl_down_sync(FULL, wv, 1);
+                if (li == CG - 1) { ou = bu; ov = bv; }
+                const bool popi = more && top - li >= 2 && !((wu - ou) * (vb - ov) - (wv - ov) * (ub - ou) > 0.0);
+                const unsigned stop = (__ballot_sync(FULL, !popi) >> gb) & 0xffu;
+                const int np = more ? (stop ? __ffs(stop) - 1 : CG) : 0;
+                top -= np;
+                double nu = __shfl_sync(FULL, wu, (lane + np) & 31), nv = __shfl_sync(FULL, wv, (lane + np) & 31);
+                if (li + np >= CG) entry(top - 1 - li, nu, nv);
+                if (li == CG - 1 && np > 0) entry(top - 1 - CG, bu, bv);
+                wu = nu; wv = nv;
+                more = more && np == CG;
+            }
+            // push b
+            const double pu = __shfl_up_sync(FULL, wu, 1), pv = __shfl_up_sync(FULL, wv, 1);
+            if (act) {
+                if (li == CG - 1) { bu = wu; bv = wv; }
+                if (li == 0) {
+                    const int slot = top % CR;
+                    // Ring invariant: live entry j is in slot j % CR iff j >= hw - CR, else in
+                    // hu/hv/hj. A push at a new high-water mark moves entry top - CR out.
+                    if (top == hw && top >= CR) {
+                        const double2 old = ruv[slot];
+                        hu[top - CR] = old.x; hv[top - CR] = old.y; hj[top - CR] = rpos[slot];
+                    }
+                    ruv[slot] = make_double2(ub, vb);
+                    rpos[slot] = dir > 0 ? t : m - 1 - t;
+                    wu = ub; wv = vb;
+                } else {
+                    wu = pu; wv = pv;
+                }
+                ++top;
+                hw = max(hw, top);
+            }
+            __syncwarp();
+        }
+        // the stack is the half hull: ring entries -> hj (spilled ones are there already)
+        if (run) {
+            for (int j = max(0, hw - CR) + li; j < top; j += CG) hj[j] = rpos[j % CR];
+            if (li == 0) io.hlen[4 * (int64_t)w + g] = top;
+        }
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------ stage 4: kept selection
+
+__device__ __forceinline__ int dec_k(int k) { return k < 0 ? ~k : k; }
+
+// hull = lower[:-1] + upper[:-1] as sorted positions
+struct HullView {
+    const int32_t *lo, *up;
+    int L, H;
+    __device__ int at(int h) const { return h < L - 1 ? __ldg(lo + h) : __ldg(up + h - (L - 1)); }
+};
+
+// One patch per warp: hull assembly, kept selection (reduction.py:172-199), hull
+// area (reduction.py:227-236), the kept rows.
+__device__ void kept_patch(const WarpTeam &t, const ReduceIO &io, const ReduceParams &p, int w, int *chosen) {
+    const int N = p.N, K = p.K;
+    const int64_t e = io.wenv[w];
+    const int q = w - io.patch_off[e];
+    const int64_t base = io.cand_base[e];
+    const int32_t *mo = io.member_offsets + e * (N + 1);
+    const int moff = mo[q], m = mo[q + 1] - moff;
+    const int32_t *mem = io.members + base + moff;
+    const int64_t pq = e * N + q, row0 = base + moff;
+    const double *P = io.point + 3 * base, *Nn = io.normal + 3 * base, *D = io.depth + base;
+    const double2 *suv = io.suv + row0;
+    const int32_t *sk = io.sp + row0, *hj = io.hj + 4 * row0;
+    const int nt = io.pnt[w], deepest = io.pdeep[w];
+    const int4 len = *reinterpret_cast<const int4 *>(io.hlen + 4 * (int64_t)w);
+    const int lane = t.rank();
     double area = 0.0;
-    if (t.rank() == 0 && m >= 3 && have_hull && all_base) area = H < 3 ? 0.0 : chain_area(su, sv, sh, H);
-    // kept selection (reduction.py:172-199)
-    int nc = 0;
-    if (!need_sel) {
-        for (int k = t.rank(); k < m; k += t.size()) chosen[k] = k;
+    if (lane == 0 && m >= 3) {
+        const HullView h{hj, hj + m, len.x, (len.x - 1) + (len.y - 1)};
+        if (h.H >= 3) {
+            const int H = h.H;
+            const double d1 = ddot_x2(H, [&](int k) { return suv[h.at(k)].x; }, [&](int k) { return suv[h.at((k + 1) % H)].y; });
+            const double d2 = ddot_x2(H, [&](int k) { return suv[h.at(k)].y; }, [&](int k) { return suv[h.at((k + 1) % H)].x; });
+            area = 0.5 * fabs(d1 - d2);
+        }
+    }
+    int nc;
+    if (m <= K) {
+        for (int k = lane; k < m; k += 32) chosen[k] = k;
         nc = m;
     } else {
-        if (t.rank() == 0) {
-            int nh = 0;  // hull -> member positions with the deepest excluded (in place)
-            for (int h = 0; h < H; ++h) {
-                int k = sp[sh[h]];
-                if (k != deepest) sh[nh++] = (Idx)k;
-            }
+        if (lane == 0) {
+            const HullView h = needs_touch_hull(m, nt, K)  // base = touching members, else all
+                                   ? HullView{hj + 2 * m, hj + 3 * m, len.z, (len.z - 1) + (len.w - 1)}
+                                   : HullView{hj, hj + m, len.x, (len.x - 1) + (len.y - 1)};
+            int nh = 0;  // hull members other than the deepest
+            for (int j = 0; j < h.H; ++j) nh += dec_k(sk[h.at(j)]) != deepest;
             chosen[0] = deepest;
             int c = 1;
             if (nh <= K - 1) {
-                for (int h = 0; h < nh; ++h) chosen[c++] = sh[h];
-            } else {  // picks = linspace(0, len(hull), K-1, endpoint=False).astype(int)
-                double step = (double)nh / (double)(K - 1);
-                for (int j = 0; j < K - 1; ++j) chosen[c++] = sh[(int)((double)j * step + 0.0)];
+                for (int j = 0; j < h.H; ++j) {
+                    const int k = dec_k(sk[h.at(j)]);
+                    if (k != deepest) chosen[c++] = k;
+                }
+            } else {  // picks = linspace(0, len(hull), K-1, endpoint=False).astype(int), strictly increasing
+                const double step = (double)nh / (double)(K - 1);
+                int f = -1, j = -1, k = -1;  // f: position among the non-deepest hull members
+                for (int pk = 0; pk < K - 1; ++pk) {
+                    const int target = (int)((double)pk * step + 0.0);
+                    while (f < target) {
+                        k = dec_k(sk[h.at(++j)]);
+                        if (k != deepest) ++f;
+                    }
+                    chosen[c++] = k;
+                }
             }
             t.misc[0] = c;
         }
@@ -337,84 +581,37 @@ __device__ void finalize_patch(const Team &t, const ReduceIO &io, const ReducePa
         while (nc < K) {  // fill by np.argsort(-depths, kind="stable"), skipping chosen
             int bk = -1;
             double bd = 0.0;
-            for (int k = t.rank(); k < m; k += t.size()) {
+            for (int k = lane; k < m; k += 32) {
                 bool in = false;
                 for (int j = 0; j < nc; ++j) in |= (chosen[j] == k);
                 if (in) continue;
-                const double d = wbuf[k];
+                const double d = __ldg(D + mem[k]);
                 if (bk < 0 || depth_before(d, k, bd, bk)) { bk = k; bd = d; }
             }
             t.best_depth(bk, bd);
             if (bk < 0) break;
-            if (t.rank() == 0) chosen[nc] = bk;
+            if (lane == 0) chosen[nc] = bk;
             t.sync();
             ++nc;
         }
     }
     t.sync();
     const int nk = nc < K ? nc : K;
-    if (m >= 3 && !(have_hull && all_base)) {  // area hull over all members
-        for (int j = t.rank(); j < m; j += t.size()) {
-            double x = pt(j, 0), y = pt(j, 1), z = pt(j, 2);
-            su[j] = V3(x, y, z, t1[0], t1[1], t1[2]);
-            sv[j] = V3(x, y, z, t2[0], t2[1], t2[2]);
-            sp[j] = (Idx)j;
-        }
-        t.sync();
-        team_sort(t, su, sv, sp, m);
-        const int h2 = team_chain(t, su, sv, m, sh);
-        if (t.rank() == 0) area = h2 < 3 ? 0.0 : chain_area(su, sv, sh, h2);
-    }
-    // aggregates (reduction.py:153-168). The axis-0 sums are sequential folds (one
-    // thread per component); the team streams the weighted products of each chunk
-    // of members through a shared tile (su is free now) so the folds read shared
-    // memory, and keeps the weights for the pairwise sum in wbuf.
-    t.sync();
-    const int r = t.rank(), CH = min(t.size(), 64);  // tile: 9 x CH doubles in su
-    double s = 0.0;
-    for (int c0 = 0; c0 < m; c0 += CH) {
-        const int k = c0 + r;
-        if (r < CH && k < m) {
-            const double wk = weight_of(wbuf[k]);
-            const double px = pt(k, 0), py = pt(k, 1), pz = pt(k, 2);
-            const double nx = nr(k, 0), ny = nr(k, 1), nz = nr(k, 2);
-            su[0 * CH + r] = px * wk; su[1 * CH + r] = py * wk; su[2 * CH + r] = pz * wk;
-            su[3 * CH + r] = nx * wk; su[4 * CH + r] = ny * wk; su[5 * CH + r] = nz * wk;
-            su[6 * CH + r] = (py * nz - pz * ny) * wk;  // np.cross(pts, norms) * w
-            su[7 * CH + r] = (pz * nx - px * nz) * wk;
-            su[8 * CH + r] = (px * ny - py * nx) * wk;
-        }
-        t.sync();
-        if (r < 9) {
-            const int cnt = min(CH, m - c0);
-            const double *row = su + r * CH;
-            for (int j = 0; j < cnt; ++j) s = (c0 + j == 0) ? row[j] : s + row[j];
-        }
-        t.sync();
-    }
-    if (r < 9) {
-        const int kind = r / 3, c = r % 3;
-        double *o = (kind == 0 ? io.wp_sum : kind == 1 ? io.wn_sum : io.wt_sum) + 3 * pq;
-        o[c] = s;
-    } else if (r == 9) {
-        io.w_sum[pq] = 0.0 + pairwise(WeightBuf{wbuf}, 0, m);
-    }
-    if (r == 0) {
-        io.max_depth[pq] = anynan ? (double)NAN : mx;
+    if (lane == 0) {
         io.area[pq] = area;
         io.patch_nkept[pq] = nk;
     }
-    for (int j = r; j < K; j += t.size()) {
+    for (int j = lane; j < K; j += 32) {
         const int64_t o = pq * K + j;
         if (j < nk) {
             const int k = chosen[j];
             const int i = mem[k];
             io.kept_cand[o] = i;
             io.kept_face[o] = io.face ? io.face[base + i] : -1;
-            io.kept_depth[o] = wbuf[k];
+            io.kept_depth[o] = __ldg(D + i);
             for (int c = 0; c < 3; ++c) {
-                io.kept_point[3 * o + c] = pt(k, c);
-                io.kept_normal[3 * o + c] = nr(k, c);
+                io.kept_point[3 * o + c] = __ldg(P + 3 * (int64_t)i + c);
+                io.kept_normal[3 * o + c] = __ldg(Nn + 3 * (int64_t)i + c);
             }
         } else {
             io.kept_cand[o] = -1;
@@ -426,74 +623,16 @@ __device__ void finalize_patch(const Team &t, const ReduceIO &io, const ReducePa
     t.sync();
 }
 
-__device__ __forceinline__ int64_t env_of(const int32_t *patch_off, int64_t E, int w) {
-    int64_t lo = 0, hi = E - 1;  // last e with patch_off[e] <= w
-    while (lo < hi) {
-        int64_t mid = (lo + hi + 1) >> 1;
-        if (patch_off[mid] <= w) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-}
+constexpr int FK_WARPS = 4;
 
-__device__ __forceinline__ int patch_size(const ReduceIO &io, int N, int64_t e, int q) {
-    const int32_t *m = io.member_offsets + e * (N + 1);
-    return m[q + 1] - m[q];
-}
-
-// Small patches: one warp each.
-__global__ void __launch_bounds__(FIN_WARPS * 32, 10) k_finalize_warp(ReduceIO io, ReduceParams p) {
-    __shared__ double s_u[FIN_WARPS][FIN_SMALL], s_v[FIN_WARPS][FIN_SMALL];
-    __shared__ uint16_t s_p[FIN_WARPS][FIN_SMALL], s_h[FIN_WARPS][2 * FIN_SMALL + 4];
-    __shared__ double s_w[FIN_WARPS][FIN_SMALL];
-    __shared__ int s_chosen[FIN_WARPS][MAX_KEPT];
-    __shared__ int s_misc[FIN_WARPS][4];
+__global__ void __launch_bounds__(FK_WARPS * 32) k_fin_kept(ReduceIO io, ReduceParams p) {
+    __shared__ int s_chosen[FK_WARPS][MAX_KEPT];
+    __shared__ int s_misc[FK_WARPS][4];
     const int wib = threadIdx.x >> 5;
     WarpTeam t{s_misc[wib]};
-    const int64_t E = io.E;
-    const int total = io.patch_off[E];
-    for (int w = blockIdx.x * FIN_WARPS + wib; w < total; w += gridDim.x * FIN_WARPS) {
-        const int64_t e = env_of(io.patch_off, E, w);
-        const int q = w - io.patch_off[e];
-        if (patch_size(io, p.N, e, q) > FIN_SMALL) {  // handed to the CTA path (order-free: patches are independent)
-            if ((threadIdx.x & 31) == 0) io.large_list[atomicAdd(io.large_count, 1)] = w;
-            continue;
-        }
-        finalize_patch(t, io, p, e, q, s_u[wib], s_v[wib], s_p[wib], s_h[wib], s_w[wib], s_chosen[wib]);
-    }
-}
-
-// Large patches: one CTA each; shared memory up to FIN_LARGE members, global scratch beyond.
-__global__ void __launch_bounds__(FIN_LARGE_THREADS) k_finalize_block(ReduceIO io, ReduceParams p) {
-    extern __shared__ __align__(16) unsigned char dyn[];
-    double *su = reinterpret_cast<double *>(dyn);
-    double *sv = su + FIN_LARGE;
-    double *sw = sv + FIN_LARGE;
-    int *sp = reinterpret_cast<int *>(sw + FIN_LARGE);
-    int *sh = sp + FIN_LARGE;  // 2 FIN_LARGE + 4
-    __shared__ ArgMax s_am[32];
-    __shared__ int s_ws[WS_INTS];
-    __shared__ double s_dred[32];
-    __shared__ int s_ired[32];
-    __shared__ int s_misc[4];
-    __shared__ int s_chosen[MAX_KEPT];
-    BlockTeam t{s_misc, s_am, s_ws, s_dred, s_ired};
-    const int64_t E = io.E;
-    const int total = *io.large_count;
-    for (int li = blockIdx.x; li < total; li += gridDim.x) {
-        const int w = io.large_list[li];
-        const int64_t e = env_of(io.patch_off, E, w);
-        const int q = w - io.patch_off[e];
-        const int m = patch_size(io, p.N, e, q);
-        if (m <= FIN_LARGE) {
-            finalize_patch(t, io, p, e, q, su, sv, sp, sh, sw, s_chosen);
-        } else {
-            const int64_t base = io.cand_base[e];
-            const int moff = io.member_offsets[e * (p.N + 1) + q];
-            finalize_patch(t, io, p, e, q, io.su + base + moff, io.sv + base + moff, io.sp + base + moff,
-                           io.sh + 2 * base + e * (4 * (int64_t)p.N + 4) + 2 * (int64_t)moff + 4 * q,
-                           io.gD + base + moff, s_chosen);
-        }
-    }
+    const int total = io.patch_off[io.E];
+    for (int w = blockIdx.x * FK_WARPS + wib; w < total; w += gridDim.x * FK_WARPS)
+        kept_patch(t, io, p, w, s_chosen[wib]);
 }
 
 __global__ void k_stats(ReduceIO io, ReduceParams p) {
@@ -519,19 +658,20 @@ __global__ void k_stats(ReduceIO io, ReduceParams p) {
 
 void launch_finalize(const ReduceIO &io, const ReduceParams &p, int sm_count, cudaStream_t s) {
     if (io.E <= 0) return;
-    k_patch_off<<<1, 1024, 0, s>>>(io.E, io.n_patch, io.patch_off, io.large_count);
+    k_patch_off<<<1, 1024, 0, s>>>(io.E, io.n_patch, io.patch_off, io.large_count, io.njob);
     const int64_t maxw = io.E * (int64_t)p.N;
-    int64_t grid = (int64_t)sm_count * 12;
-    int64_t need = (maxw + FIN_WARPS - 1) / FIN_WARPS;
-    k_finalize_warp<<<(unsigned)(grid < need ? grid : need), FIN_WARPS * 32, 0, s>>>(io, p);
-    const size_t smem = (size_t)FIN_LARGE * (8 + 8 + 8 + 4 + 8) + 16;
+    const size_t wsm = FW_BYTES_PER_WARP * FW_WARPS;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(k_finalize_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_fin_sort_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
+        cudaFuncSetAttribute(k_fin_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FB_BYTES);
         configured = true;
     }
-    int64_t lgrid = (int64_t)sm_count * 4;
-    k_finalize_block<<<(unsigned)(lgrid < maxw ? lgrid : maxw), FIN_LARGE_THREADS, smem, s>>>(io, p);
+    auto cap = [&](int64_t want, int64_t limit) { return (unsigned)(want < limit ? want : limit); };
+    k_fin_sort_warp<<<cap((int64_t)sm_count * 8, (maxw + FW_WARPS - 1) / FW_WARPS), FW_WARPS * 32, wsm, s>>>(io, p);
+    k_fin_sort_block<<<cap((int64_t)sm_count * 4, maxw), FB_THREADS, FB_BYTES, s>>>(io, p);
+    k_fin_chain<<<cap((int64_t)sm_count * 8, (maxw + CH_WARPS - 1) / CH_WARPS), CH_WARPS * 32, 0, s>>>(io, p);
+    k_fin_kept<<<cap((int64_t)sm_count * 8, (maxw + FK_WARPS - 1) / FK_WARPS), FK_WARPS * 32, 0, s>>>(io, p);
     k_stats<<<(unsigned)((io.E + 127) / 128), 128, 0, s>>>(io, p);
 }
 

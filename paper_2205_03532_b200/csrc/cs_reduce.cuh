@@ -26,9 +26,20 @@ struct ReduceIO {
     double *su, *sv;   // sort keys
     int32_t *sp;       // sort payload
     int32_t *sh;       // hull/stack scratch: env e uses [2 cand_base(e) + e (4N + 4), + 2 cap_e + 4N + 4)
-    double *gP, *gN, *gD;  // large-patch member staging (rows like candidates)
+    // finalisation scratch (cs_finalize.cu); rows like candidates unless stated
+    double2 *suv;        // sorted (u, v) of every patch's members (rows), with sp the member (~k: not touching)
+    double *tu, *tv;     // second sort buffer of patches too large for shared memory
+    int32_t *tk;
+    int32_t *hj;         // [4 rows] chain stacks: sorted positions (the hull output) ...
+    double *hu, *hv;     // ... and their (u, v) (backing store of the shared-memory window)
+    int32_t *hlen;       // [E N 4] chain lengths per patch and job
+    int32_t *pdeep;      // [E N] per patch (work index): deepest member position
+    int32_t *pnt;        // [E N] touching members (depth >= 0)
+    int32_t *wenv;       // [E N] env of each work index
+    int32_t *jobs;       // [2][E N] chain jobs (patch work index): long patches, short patches
+    int32_t *njob;       // [4] long count, short count, claimed
     int32_t *patch_off;  // [E+1]
-    int32_t *large_list, *large_count;  // finalize work list of patches above FIN_SMALL members
+    int32_t *large_list, *large_count;  // patches above the warp path's size limit
     // outputs
     int32_t *n_patch, *n_kept;
     double *patch_normal, *builder_maxd;

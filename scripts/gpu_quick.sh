@@ -1,6 +1,13 @@
+# quick iteration: gpu tests + a short bench (+ optional launch list / ncu of $PROFK kernels)
 cd $GRAFT_REPO_ROOT
 export PATH=/usr/local/cuda/bin:$PATH
-timeout 1200 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
-timeout 600 python bench.py --steps 30 --warmup 5 --quick > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+timeout 900 python -m pytest tests -m gpu -q -x --timeout 600 -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
+timeout 600 python bench.py --steps 20 --warmup 5 --quick > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+if [ -n "$LAUNCHES" ]; then
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --quick --steps 3 --warmup 1 > gpurun_out/launches_bench.log 2>&1
+fi
+for k in ${PROFK:-}; do
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 \
+    -o gpurun_out/prof_$k python bench.py --quick --steps 3 --warmup 1 > gpurun_out/prof_$k.log 2>&1
+done
