@@ -73,7 +73,9 @@ def main():
         i = args.index("--launches")
         launches = args[i + 1]
         args = args[:i] + args[i + 2:]
-    prof = os.path.join(ROOT, "profiles")
+    # tag "tmp": scratch summaries outside the repo (iteration), else tracked under profiles/
+    prof = "/tmp/prof" if tag == "tmp" else os.path.join(ROOT, "profiles")
+    os.makedirs(prof, exist_ok=True)
     for rep in args:
         kern = os.path.basename(rep).replace(".ncu-rep", "").replace("prof_", "")
         out = [f"# ncu --set full --clock-control none capture of {kern} ({tag})", f"# source: {rep}", ""]
