@@ -14,7 +14,8 @@ import threading
 from .errors import MeshValidationError, NonFiniteStateError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libcontactsim_b200.so")
+# CS_LIB_PATH: developer override (build variants for A/B timing); the default is the in-tree build
+LIB_PATH = os.environ.get("CS_LIB_PATH") or os.path.join(_HERE, "_lib", "libcontactsim_b200.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 CS_OK, CS_ERR_VALUE, CS_ERR_NONFINITE, CS_ERR_MESH, CS_ERR_HANDLE, CS_ERR_CUDA, CS_ERR_OOM = range(7)

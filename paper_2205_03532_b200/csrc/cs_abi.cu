@@ -52,7 +52,7 @@ constexpr int MAX_HANDLES = 4096;
 struct SdfEntry {
     bool live = false;
     float *values = nullptr;
-    double *values64 = nullptr;
+    float *bmin = nullptr;  // brick minima (GridT::bmin)
     size_t bytes = 0;
     SdfDesc desc{};
 };
@@ -106,7 +106,7 @@ struct cs_plan {
     int64_t total_cap = 0;
     int64_t nblocks = 0;
     bool uniform_sdf = false;      // every env samples the same grid
-    GridT<double> uniform_grid{};  // ...whose view then travels as a kernel parameter
+    PlanGrid uniform_grid{};  // ...whose view then travels as a kernel parameter
     std::vector<void *> allocs;
     // inputs / tables
     int32_t *env_sdf = nullptr, *env_mesh = nullptr;
@@ -182,21 +182,38 @@ int cs_sdf_register(const float *values, int values_on_device, int32_t nx, int32
     s.bytes = (size_t)n * sizeof(float);
     CS_CUDA(cudaMalloc(&s.values, s.bytes));
     CS_CUDA(cudaMemcpy(s.values, values, s.bytes, values_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
-    {   // exact float64 promotion for the plan kernels (no F2F on the hot path)
+    GridT<float> probe = cs::make_grid<float>(nullptr, nx, ny, nz, origin[0], origin[1], origin[2], voxel);
+    {   // brick minima of the face lower bound (cs_common.cuh: sample_lower_bound)
         std::vector<float> h32((size_t)n);
         CS_CUDA(cudaMemcpy(h32.data(), s.values, s.bytes, cudaMemcpyDeviceToHost));
-        std::vector<double> h64(h32.begin(), h32.end());
-        CS_CUDA(cudaMalloc(&s.values64, (size_t)n * sizeof(double)));
-        CS_CUDA(cudaMemcpy(s.values64, h64.data(), (size_t)n * sizeof(double), cudaMemcpyHostToDevice));
+        const int bx = probe.bnx, by = probe.bny, bz = probe.bnz;
+        std::vector<float> bm((size_t)bx * by * bz, INFINITY);
+        for (int z = 0; z < nz; ++z)
+            for (int y = 0; y < ny; ++y)
+                for (int x = 0; x < nx; ++x) {
+                    const float v = h32[(size_t)x + (size_t)nx * ((size_t)y + (size_t)ny * z)];
+                    // node x belongs to bricks (x - 1) / BRICK .. x / BRICK (a brick's node range is closed)
+                    for (int kz = std::max(0, (z - 1) / BRICK); kz <= std::min(bz - 1, z / BRICK); ++kz)
+                        for (int ky = std::max(0, (y - 1) / BRICK); ky <= std::min(by - 1, y / BRICK); ++ky)
+                            for (int kx = std::max(0, (x - 1) / BRICK); kx <= std::min(bx - 1, x / BRICK); ++kx) {
+                                if (kx * BRICK > x || kx * BRICK + BRICK < x || ky * BRICK > y || ky * BRICK + BRICK < y ||
+                                    kz * BRICK > z || kz * BRICK + BRICK < z)
+                                    continue;
+                                float &o = bm[(size_t)kx + (size_t)bx * ((size_t)ky + (size_t)by * kz)];
+                                o = std::fmin(o, v);
+                            }
+                }
+        CS_CUDA(cudaMalloc(&s.bmin, bm.size() * sizeof(float)));
+        CS_CUDA(cudaMemcpy(s.bmin, bm.data(), bm.size() * sizeof(float), cudaMemcpyHostToDevice));
     }
     SdfDesc &d = s.desc;
     d.values = s.values;
-    d.values64 = s.values64;
     d.nx = nx; d.ny = ny; d.nz = nz; d.pad = 0;
     d.ox = origin[0]; d.oy = origin[1]; d.oz = origin[2];
     d.voxel = voxel;
     for (int k = 0; k < 3; ++k) { d.lo[k] = aabb_lo[k]; d.hi[k] = aabb_hi[k]; }
-    d.g64 = cs::make_grid<double>(s.values64, nx, ny, nz, origin[0], origin[1], origin[2], voxel);
+    d.gp = cs::make_grid<float>(s.values, nx, ny, nz, origin[0], origin[1], origin[2], voxel);
+    d.gp.bmin = s.bmin;
     CS_CUDA(cudaMemcpy(d_sdfs + h, &d, sizeof(SdfDesc), cudaMemcpyHostToDevice));
     s.live = true;
     *handle = h;
@@ -208,7 +225,7 @@ int cs_sdf_free(int32_t handle) {
     if (handle < 0 || handle >= (int)g_sdf.size() || !g_sdf[handle].live) return fail(CS_ERR_HANDLE, "bad SDF handle %d", handle);
     SdfEntry &s = g_sdf[handle];
     CS_CUDA(cudaFree(s.values));
-    CS_CUDA(cudaFree(s.values64));
+    CS_CUDA(cudaFree(s.bmin));
     s = SdfEntry{};
     return CS_OK;
 }
@@ -223,11 +240,11 @@ int cs_sdf_values(int32_t handle, const float **values) {
 int cs_sdf_l2_persist(int32_t handle, void *stream, float hit_ratio) {
     void *base;
     size_t bytes;
-    {   // the plan kernels read the float64 copy: that is the array to keep resident
+    {   // the plan kernels gather from the float32 values: that is the array to keep resident
         std::lock_guard<std::mutex> lk(g_mu);
         if (handle < 0 || handle >= (int)g_sdf.size() || !g_sdf[handle].live) return fail(CS_ERR_HANDLE, "bad SDF handle %d", handle);
-        base = g_sdf[handle].values64;
-        bytes = 2 * g_sdf[handle].bytes;
+        base = g_sdf[handle].values;
+        bytes = g_sdf[handle].bytes;
     }
     int dev = 0, max_win = 0, max_persist = 0;
     CS_CUDA(cudaGetDevice(&dev));
@@ -479,7 +496,7 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
     std::vector<int2> bmap;
     std::vector<int32_t> chunk_first;
     bool uniform = true;
-    GridT<double> ugrid{};
+    PlanGrid ugrid{};
     int32_t maxcv = 1;
     {
         std::lock_guard<std::mutex> lk(g_mu);
@@ -496,7 +513,7 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
             chunk_first.push_back((int32_t)bmap.size());
             for (int64_t f = 0; f < nt; f += FACE_CHUNK) bmap.push_back(make_int2((int)e, (int)f));
         }
-        if (uniform) ugrid = g_sdf[sdf_handles[0]].desc.g64;
+        if (uniform) ugrid = g_sdf[sdf_handles[0]].desc.gp;
         chunk_first.push_back((int32_t)bmap.size());
     }
     cs_plan *P = new cs_plan();
@@ -605,7 +622,7 @@ int cs_collide(cs_plan *P, const double *sdf_pose, const double *mesh_pose, int3
                   P->status, P->env_min_depth, P->st.work_count, s);
     CS_LAUNCHED();
     mark(1);
-    const GridT<double> *ug = P->uniform_sdf ? &P->uniform_grid : nullptr;
+    const PlanGrid *ug = P->uniform_sdf ? &P->uniform_grid : nullptr;
     launch_face_prep(P->nblocks, P->block_map, P->xf, d_sdfs, d_meshes, P->cand_base, P->st, P->max_chunk_verts,
                      P->sample_counter, ug, s);
     CS_LAUNCHED();

@@ -5,8 +5,6 @@
 //
 // The SDF sampler is written for the B200 pipes rather than transliterated: it
 // produces the reference's bits (sdf/_kernels.py:253-327) but
-//   * reads a float64 copy of the float32 grid (the promotion is exact), so no
-//     F2F conversions on the XU pipe;
 //   * divides by the voxel size with a reciprocal + two FMA corrections and an
 //     exact remainder check (IEEE division only when the check cannot prove
 //     correct rounding), instead of the MUFU + Newton IEEE division;
@@ -75,7 +73,15 @@ struct GridT {
     double nm1[3];      // n - 1 (clamp bound, sdf/_kernels.py:302-304)
     double nm2[3];      // n - 2 (cell clamp, sdf/_kernels.py:261-270)
     int n2[3];
+    // Brick minima (optional): bmin[bx + bnx (by + bny bz)] = min of the grid values at
+    // nodes [BRICK b, BRICK b + BRICK] per axis, i.e. of every corner of the cells
+    // [BRICK b, BRICK b + BRICK) -- a lower bound of any sample in those cells.
+    const float *__restrict__ bmin;
+    int bnx, bny, bnz;
 };
+
+constexpr int BRICK = 2;                // cells per brick edge
+constexpr int BRICK_MAX_LOOKUPS = 64;   // larger face boxes skip the bound
 
 template <class T>
 __host__ __device__ inline GridT<T> make_grid(const T *v, int nx, int ny, int nz, double ox, double oy, double oz,
@@ -92,19 +98,25 @@ __host__ __device__ inline GridT<T> make_grid(const T *v, int nx, int ny, int nz
     g.nm1[0] = nx - 1.0; g.nm1[1] = ny - 1.0; g.nm1[2] = nz - 1.0;
     g.nm2[0] = nx - 2.0; g.nm2[1] = ny - 2.0; g.nm2[2] = nz - 2.0;
     g.n2[0] = nx - 2; g.n2[1] = ny - 2; g.n2[2] = nz - 2;
+    g.bmin = nullptr;
+    g.bnx = (nx - 2) / BRICK + 1; g.bny = (ny - 2) / BRICK + 1; g.bnz = (nz - 2) / BRICK + 1;
     return g;
 }
 
 using GridView = GridT<float>;  // per-pair drop-ins sample the caller's float32 grid
 
+// The plan kernels sample the registered float32 values (the promotion to float64
+// is exact). Measured against a float64 copy of the grid: half the gather bytes and
+// L2 footprint, and faster despite the conversions (profiles/r1_*).
+using PlanGrid = GridT<float>;
+
 // Device SDF store entry.
 struct SdfDesc {
     const float *values;     // the grid as registered (float32, x-fastest)
-    const double *values64;  // exact float64 promotion read by the plan kernels
     int32_t nx, ny, nz, pad;
     double ox, oy, oz, voxel;
     double lo[3], hi[3];  // mesh AABB (grid.mesh_aabb)
-    GridT<double> g64;    // sampler view of values64
+    PlanGrid gp;          // the plan kernels' sampler view (values + brick minima)
 };
 
 __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
@@ -224,6 +236,41 @@ template <class T>
 __device__ __forceinline__ void gradient(const GridT<T> &g, double px, double py, double pz, double &gx, double &gy,
                                          double &gz) {
     gradient(g, gpoint(g, px, py, pz), gx, gy, gz);
+}
+
+// A lower bound of every trilinear sample (sdf/_kernels.py:253-309) at points of
+// the box [lo, hi] (grid frame, metres), from the brick minima; -inf (no bound)
+// when the box spans more than BRICK_MAX_LOOKUPS bricks. A sample is a convex
+// combination of its cell's corners (weights f and 1 - f, evaluated in float64)
+// plus a non-negative outside term, and points outside the grid sample a clamped
+// boundary cell, so no sample in the box's cells is below the minimum corner
+// minus the lerps' rounding (a few ulps; margin 2^-40 relative). The box is
+// widened by 1e-6 voxel so roundings of the points themselves stay inside.
+template <class T>
+__device__ __forceinline__ double sample_lower_bound(const GridT<T> &g, const double lo[3], const double hi[3]) {
+    int b0[3], b1[3], n = 1;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double a = (lo[k] - g.o[k]) * g.rv - 1e-6, b = (hi[k] - g.o[k]) * g.rv + 1e-6;
+        const int c0 = a < 0.0 ? 0 : (a > g.nm2[k] ? g.n2[k] : (int)a);
+        const int c1 = b < 0.0 ? 0 : (b > g.nm2[k] ? g.n2[k] : (int)b);
+        b0[k] = c0 / BRICK;
+        b1[k] = c1 / BRICK;
+        n *= b1[k] - b0[k] + 1;
+    }
+    if (n > BRICK_MAX_LOOKUPS) return -INFINITY;
+    const int sx = b1[0] - b0[0] + 1;
+    float m = INFINITY;
+    for (int z = b0[2]; z <= b1[2]; ++z)
+        for (int y = b0[1]; y <= b1[1]; ++y) {
+            const float *row = g.bmin + b0[0] + g.bnx * (y + g.bny * z);
+#pragma unroll
+            for (int x = 0; x < 4; ++x)  // a row's loads are independent: four in flight
+                if (x < sx) m = fminf(m, __ldg(row + x));
+            for (int x = 4; x < sx; ++x) m = fminf(m, __ldg(row + x));
+        }
+    const double md = (double)m;
+    return md - fabs(md) * 0x1p-40 - 1e-300;
 }
 
 // sdf/_kernels.py:20-61

@@ -99,16 +99,16 @@ __device__ __forceinline__ double3 to_grid(const EnvXf &X, double4 v) {
 // scalars are constant-bank operands; otherwise the env's grid view is staged in
 // shared memory.
 template <bool COUNT, bool UNIFORM>
-__global__ void __launch_bounds__(FACE_CHUNK) k_face_prep(const int2 *__restrict__ block_map,
+__global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int2 *__restrict__ block_map,
                                                           const EnvXf *__restrict__ xf,
                                                           const SdfDesc *__restrict__ sdfs,
                                                           const MeshDesc *__restrict__ meshes,
                                                           const int64_t *__restrict__ cand_base, Staging st, int maxcv,
                                                           unsigned long long *__restrict__ counter,
-                                                          const GridT<double> gu) {
+                                                          const PlanGrid gu) {
     extern __shared__ double dsm[];
     __shared__ EnvXf sx;
-    __shared__ GridT<double> sg;
+    __shared__ PlanGrid sg;
     __shared__ int ws[WS_INTS];
     __shared__ unsigned sbase;
     const int2 bm = block_map[blockIdx.x];
@@ -121,11 +121,11 @@ __global__ void __launch_bounds__(FACE_CHUNK) k_face_prep(const int2 *__restrict
         return;
     }
     if (!UNIFORM) {
-        static_assert(sizeof(GridT<double>) % 8 == 0 && sizeof(GridT<double>) / 8 <= FACE_CHUNK, "GridT copy");
-        if (threadIdx.x < sizeof(GridT<double>) / 8)
-            reinterpret_cast<double *>(&sg)[threadIdx.x] = reinterpret_cast<const double *>(&sdfs[sx.sdf].g64)[threadIdx.x];
+        static_assert(sizeof(PlanGrid) % 8 == 0 && sizeof(PlanGrid) / 8 <= FACE_CHUNK, "grid view copy");
+        if (threadIdx.x < sizeof(PlanGrid) / 8)
+            reinterpret_cast<double *>(&sg)[threadIdx.x] = reinterpret_cast<const double *>(&sdfs[sx.sdf].gp)[threadIdx.x];
     }
-    const GridT<double> &grid = UNIFORM ? gu : sg;
+    const PlanGrid &grid = UNIFORM ? gu : sg;
     const double4 *verts = meshes[sx.mesh].verts;
     const int32_t *cverts = meshes[sx.mesh].chunk_verts;
     const int64_t nt = meshes[sx.mesh].nt;
@@ -150,9 +150,14 @@ __global__ void __launch_bounds__(FACE_CHUNK) k_face_prep(const int2 *__restrict
         const double ax = vx[la], bx = vx[lb], cx = vx[lc];
         const double ay = vy[la], by = vy[lb], cy = vy[lc];
         const double az = vz[la], bz = vz[lb], cz = vz[lc];
-        near = dmin(dmin(ax, bx), cx) <= sx.cull_hi[0] && dmax(dmax(ax, bx), cx) >= sx.cull_lo[0] &&
-               dmin(dmin(ay, by), cy) <= sx.cull_hi[1] && dmax(dmax(ay, by), cy) >= sx.cull_lo[1] &&
-               dmin(dmin(az, bz), cz) <= sx.cull_hi[2] && dmax(dmax(az, bz), cz) >= sx.cull_lo[2];
+        const double lo[3] = {dmin(dmin(ax, bx), cx), dmin(dmin(ay, by), cy), dmin(dmin(az, bz), cz)};
+        const double hi[3] = {dmax(dmax(ax, bx), cx), dmax(dmax(ay, by), cy), dmax(dmax(az, bz), cz)};
+        near = lo[0] <= sx.cull_hi[0] && hi[0] >= sx.cull_lo[0] && lo[1] <= sx.cull_hi[1] && hi[1] >= sx.cull_lo[1] &&
+               lo[2] <= sx.cull_hi[2] && hi[2] >= sx.cull_lo[2];
+        // Every sample the face's descent can take lies in its box; when the grid is
+        // provably above cd there, the reference ends with found = 0 (prune or descent),
+        // so the face is not descended at all (exact: no sample bound is violated).
+        if (near && grid.bmin && sample_lower_bound(grid, lo, hi) > sx.cd) near = false;
         if (near) { need[la] = 1; need[lb] = 1; need[lc] = 1; }
     }
     __syncthreads();
@@ -213,12 +218,12 @@ __global__ void __launch_bounds__(FACE_CHUNK) k_face_prep(const int2 *__restrict
 // A step is one descent iteration; the final gradient (contacts/_kernels.py:84)
 // is the next step's gradient, so it also runs in lockstep.
 template <bool COUNT, bool UNIFORM>
-__global__ void __launch_bounds__(PGD_BLOCK) k_face_pgd(const int2 *__restrict__ block_map,
+__global__ void __launch_bounds__(PGD_BLOCK, PGD_MINB) k_face_pgd(const int2 *__restrict__ block_map,
                                                         const EnvXf *__restrict__ xf,
                                                         const SdfDesc *__restrict__ sdfs,
                                                         const MeshDesc *__restrict__ meshes, Staging st,
                                                         unsigned long long *__restrict__ counter,
-                                                        const GridT<double> gu) {
+                                                        const PlanGrid gu) {
     __shared__ double sc[12][PGD_BLOCK];  // per lane: corners a, b, c (grid frame), phi at a, b, c
     const int t = threadIdx.x, lane = t & 31;
     const unsigned FULL = 0xffffffffu;
@@ -230,7 +235,7 @@ __global__ void __launch_bounds__(PGD_BLOCK) k_face_pgd(const int2 *__restrict__
     int64_t row = 0;
     unsigned long long ns = 0;
 
-    auto start = [&](unsigned idx, const GridT<double> &g) {
+    auto start = [&](unsigned idx, const PlanGrid &g) {
         const FaceWork *w = st.work + idx;
         row = w->row;
         blk = w->blk;
@@ -262,7 +267,7 @@ __global__ void __launch_bounds__(PGD_BLOCK) k_face_pgd(const int2 *__restrict__
         have_grad = false;
     };
 
-    auto step = [&](const GridT<double> &g) {
+    auto step = [&](const PlanGrid &g) {
         const GPoint p = gpoint(g, px, py, pz);
         double grx, gry, grz;
         gradient(g, p, grx, gry, grz);
@@ -344,7 +349,7 @@ __global__ void __launch_bounds__(PGD_BLOCK) k_face_pgd(const int2 *__restrict__
                     start(qb + rank, gu);
                 } else {
                     sdf = xf[__ldg(&block_map[st.work[qb + rank].blk].x)].sdf;
-                    start(qb + rank, sdfs[sdf].g64);
+                    start(qb + rank, sdfs[sdf].gp);
                 }
                 active = true;
             }
@@ -354,7 +359,7 @@ __global__ void __launch_bounds__(PGD_BLOCK) k_face_pgd(const int2 *__restrict__
         if (!__any_sync(FULL, active)) break;
         if (active) {
             if (UNIFORM) step(gu);
-            else step(sdfs[sdf].g64);
+            else step(sdfs[sdf].gp);
         }
     }
     if (COUNT) {
@@ -468,9 +473,9 @@ size_t face_prep_smem(int maxcv) { return (size_t)maxcv * (4 * sizeof(double) + 
 
 void launch_face_prep(int64_t nblocks, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs,
                       const MeshDesc *meshes, const int64_t *cand_base, const Staging &st, int maxcv,
-                      unsigned long long *counter, const GridT<double> *uniform, cudaStream_t s) {
+                      unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s) {
     if (nblocks <= 0) return;
-    const GridT<double> gu = uniform ? *uniform : GridT<double>{};
+    const PlanGrid gu = uniform ? *uniform : PlanGrid{};
     const unsigned nb = (unsigned)nblocks;
     const size_t sm = face_prep_smem(maxcv);
     if (uniform) {
@@ -491,9 +496,9 @@ int face_pgd_grid(int sm_count) {
 }
 
 void launch_face_pgd(int grid, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs, const MeshDesc *meshes,
-                     const Staging &st, unsigned long long *counter, const GridT<double> *uniform, cudaStream_t s) {
+                     const Staging &st, unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s) {
     if (grid <= 0) return;
-    const GridT<double> gu = uniform ? *uniform : GridT<double>{};
+    const PlanGrid gu = uniform ? *uniform : PlanGrid{};
     if (uniform) {
         if (counter) k_face_pgd<true, true><<<grid, PGD_BLOCK, 0, s>>>(block_map, xf, sdfs, meshes, st, counter, gu);
         else k_face_pgd<false, true><<<grid, PGD_BLOCK, 0, s>>>(block_map, xf, sdfs, meshes, st, nullptr, gu);

@@ -4,6 +4,12 @@
 namespace cs {
 
 constexpr int PGD_BLOCK = 128;
+#ifndef PGD_MINB
+#define PGD_MINB 5  // min resident k_face_pgd CTAs per SM: a 102-register budget (measured best)
+#endif
+#ifndef PREP_MINB
+#define PREP_MINB 4  // 64 registers
+#endif
 constexpr int PGD_GRAB = 64;  // work items a warp claims per atomic
 constexpr int COMPACT_BLOCK = 256;
 constexpr int MAX_MINIMIZE_ITERS = 12;  // generation.py:19
@@ -44,9 +50,9 @@ void launch_env_xf(int64_t E, const int32_t *env_sdf, const int32_t *env_mesh, c
                    int32_t *env_status, double *env_min_depth, unsigned *work_count, cudaStream_t s);
 void launch_face_prep(int64_t nblocks, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs,
                       const MeshDesc *meshes, const int64_t *cand_base, const Staging &st, int max_chunk_verts,
-                      unsigned long long *counter, const GridT<double> *uniform, cudaStream_t s);
+                      unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s);
 void launch_face_pgd(int grid, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs, const MeshDesc *meshes,
-                     const Staging &st, unsigned long long *counter, const GridT<double> *uniform, cudaStream_t s);
+                     const Staging &st, unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s);
 int face_pgd_grid(int sm_count);  // resident CTAs of k_face_pgd over the device
 size_t face_prep_smem(int max_chunk_verts);
 void launch_compact(int64_t E, const EnvXf *xf, const int64_t *cand_base, const int2 *block_map,
