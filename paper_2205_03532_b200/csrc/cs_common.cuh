@@ -81,7 +81,9 @@ struct GridT {
 };
 
 constexpr int BRICK = 2;                // cells per brick edge
-constexpr int BRICK_MAX_LOOKUPS = 64;   // larger face boxes skip the bound
+#ifndef BRICK_MAX_LOOKUPS
+#define BRICK_MAX_LOOKUPS 64  // larger face boxes skip the bound
+#endif
 
 template <class T>
 __host__ __device__ inline GridT<T> make_grid(const T *v, int nx, int ny, int nz, double ox, double oy, double oz,

@@ -154,9 +154,10 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int2 
         const double hi[3] = {dmax(dmax(ax, bx), cx), dmax(dmax(ay, by), cy), dmax(dmax(az, bz), cz)};
         near = lo[0] <= sx.cull_hi[0] && hi[0] >= sx.cull_lo[0] && lo[1] <= sx.cull_hi[1] && hi[1] >= sx.cull_lo[1] &&
                lo[2] <= sx.cull_hi[2] && hi[2] >= sx.cull_lo[2];
-        // Every sample the face's descent can take lies in its box; when the grid is
-        // provably above cd there, the reference ends with found = 0 (prune or descent),
-        // so the face is not descended at all (exact: no sample bound is violated).
+        // Every sample that can become the face's phi lies on the triangle, inside its
+        // box; when the grid is provably above cd there, the reference ends with
+        // found = 0 (prune or descent), so the face is not descended at all (exact:
+        // only a proof skips).
         if (near && grid.bmin && sample_lower_bound(grid, lo, hi) > sx.cd) near = false;
         if (near) { need[la] = 1; need[lb] = 1; need[lc] = 1; }
     }
