@@ -443,10 +443,10 @@ static int plan_buffers(cs_plan *P, const std::vector<int64_t> &cap) {
     if (P->stages & CS_STAGE_REDUCE) {
         A(io.order, tot); A(io.label, tot); A(io.su, tot); A(io.sv, tot); A(io.sp, tot);
         A(io.sh, 2 * tot + E * (4 * (int64_t)N + 4));
-        A(io.suv, tot); A(io.tu, tot); A(io.tv, tot); A(io.tk, tot);
+        A(io.suv, tot); A(io.tuv, tot); A(io.tpos, tot); A(io.tu, tot); A(io.tv, tot); A(io.tk, tot);
         A(io.hj, 4 * tot); A(io.hu, 4 * tot); A(io.hv, 4 * tot);
         A(io.hlen, 4 * E * N); A(io.pdeep, E * N); A(io.pnt, E * N); A(io.wenv, E * N);
-        A(io.jobs, 2 * E * N); A(io.njob, 4);
+        A(io.jobs, 64 * E * N); A(io.njob, 65);
         A(io.patch_off, E + 1);
         A(io.large_list, E * N); A(io.large_count, 1);
         A(io.n_patch, E); A(io.n_kept, E);

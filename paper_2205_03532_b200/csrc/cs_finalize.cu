@@ -13,7 +13,7 @@
 //                     monotone chain (reduction.py:214-223), lower and upper, over all
 //                     members (the area hull) and, when the kept selection uses them,
 //                     over the touching members (reduction.py:183-185); the pops of a
-//                     key are tested in parallel. A persistent queue, long patches first.
+//                     key are tested in parallel. Longest patches first.
 //   k_fin_kept        one warp per patch: hull assembly, kept selection
 //                     (reduction.py:172-199), hull area (reduction.py:227-236), rows.
 //   k_stats           per env stats (the multi-GPU all-gather payload).
@@ -24,7 +24,7 @@
 // position in that subset, which is monotone in the member position, so its order
 // is the all-members order (u, v, member) filtered to the touching members; the
 // projections are the same V3 gemv dot products either way.
-#include <cuda_pipeline.h>
+#include <cstdint>
 #include <stdint.h>
 
 #include "cs_reduce_util.cuh"
@@ -34,12 +34,15 @@ namespace cs {
 constexpr int FW_WARPS = 4;      // warp teams per k_fin_sort_warp CTA
 constexpr int FW_SMEM = 256;     // members per warp-path patch (all in shared memory)
 constexpr int FB_THREADS = 128;  // k_fin_sort_block
+constexpr int CH_BUCKETS = 64;   // chain jobs bucketed by length (16 keys per bucket)
+
+__device__ __forceinline__ int job_bucket(int len) { return max(0, CH_BUCKETS - 1 - len / 16); }  // longest first
 
 __global__ void k_patch_off(int64_t E, const int32_t *__restrict__ n_patch, int32_t *__restrict__ off,
                             int32_t *__restrict__ large_count, int32_t *__restrict__ njob) {
     __shared__ int ws[WS_INTS];
     if (threadIdx.x == 0) *large_count = 0;
-    if (threadIdx.x < 4) njob[threadIdx.x] = 0;
+    if (threadIdx.x <= CH_BUCKETS) njob[threadIdx.x] = 0;
     int running = 0;
     for (int64_t e0 = 0; e0 < E; e0 += blockDim.x) {
         int64_t e = e0 + threadIdx.x;
@@ -83,6 +86,11 @@ struct WarpTeam {
         return x;
     }
     __device__ bool any(bool b) const { return __any_sync(0xffffffffu, b); }
+    __device__ int excl_scan(int f, int *total) const {  // f in {0, 1}
+        const unsigned b = __ballot_sync(0xffffffffu, f != 0);
+        *total = __popc(b);
+        return __popc(b & ((1u << rank()) - 1u));
+    }
     // best (bk, bd) under depth_before over the team
     __device__ void best_depth(int &bk, double &bd) const {
 #pragma unroll
@@ -98,6 +106,7 @@ struct BlockTeam {
     ArgMax *am;    // 32 entries
     double *dred;  // 32 doubles
     int *ired;     // 32 ints
+    int *ws;       // WS_INTS ints
     __device__ int rank() const { return threadIdx.x; }
     __device__ int size() const { return blockDim.x; }
     __device__ void sync() const { __syncthreads(); }
@@ -125,6 +134,7 @@ struct BlockTeam {
         return r;
     }
     __device__ bool any(bool b) const { return __syncthreads_or(b) != 0; }
+    __device__ int excl_scan(int f, int *total) const { return block_excl_scan(f, ws, total); }
     __device__ void best_depth(int &bk, double &bd) const {
         int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
 #pragma unroll
@@ -300,18 +310,32 @@ __device__ void sort_patch(const Team &t, const ReduceIO &io, const ReduceParams
         io.pdeep[w] = am.i;
         io.pnt[w] = nt;
         io.wenv[w] = (int32_t)e;
-        if (hull) {  // chain job; long patches first (their chains are the critical path)
-            const int list = m > FW_SMEM ? 0 : 1;
-            io.jobs[(int64_t)list * io.E * N + atomicAdd(io.njob + list, 1)] = w;
+        if (hull) {  // chain job, bucketed by size (k_fin_chain runs the longest first)
+            const int k = job_bucket(m);
+            io.jobs[(int64_t)k * io.E * N + atomicAdd(io.njob + k, 1)] = w;
         }
     }
     t.sync();
     if (!hull) return;
     const Keys R = team_merge_sort(t, A, B, m) ? B : A;
-    for (int j = r; j < m; j += T) {
-        const int k = R.k[j];
-        io.suv[row0 + j] = make_double2(R.u[j], R.v[j]);
-        io.sp[row0 + j] = __ldg(D + mem[k]) >= 0.0 ? k : ~k;
+    // sorted keys -> rows (non-touching members as ~k), and the touching keys alone,
+    // in the same order, with their sorted positions (the touching chains' input)
+    int run = 0;
+    for (int j0 = 0; j0 < m; j0 += T) {
+        const int j = j0 + r;
+        bool touch = false;
+        double2 uv = make_double2(0.0, 0.0);
+        if (j < m) {
+            const int k = R.k[j];
+            uv = make_double2(R.u[j], R.v[j]);
+            touch = __ldg(D + mem[k]) >= 0.0;
+            io.suv[row0 + j] = uv;
+            io.sp[row0 + j] = touch ? k : ~k;
+        }
+        int tot;
+        const int pos = run + t.excl_scan(touch ? 1 : 0, &tot);
+        if (touch) { io.tuv[row0 + pos] = uv; io.tpos[row0 + pos] = j; }
+        run += tot;
     }
     t.sync();
 }
@@ -358,7 +382,8 @@ __global__ void __launch_bounds__(FB_THREADS) k_fin_sort_block(ReduceIO io, Redu
     __shared__ ArgMax s_am[32];
     __shared__ double s_dred[32];
     __shared__ int s_ired[32];
-    BlockTeam t{s_am, s_dred, s_ired};
+    __shared__ int s_ws[WS_INTS];
+    BlockTeam t{s_am, s_dred, s_ired, s_ws};
     const int64_t E = io.E;
     const int total = *io.large_count;
     for (int li = blockIdx.x; li < total; li += gridDim.x) {
@@ -380,125 +405,138 @@ __global__ void __launch_bounds__(FB_THREADS) k_fin_sort_block(ReduceIO io, Redu
 
 // ------------------------------------------------------------------ stage 2: chains
 
-constexpr int CH_WARPS = 4;  // warps per k_fin_chain CTA
-constexpr int CG = 8;        // lanes per half chain: the stack-top window
-constexpr int CR = 64;       // stack entries per half chain kept in shared memory
+// A global load the compiler may not hoist out of its branch (asm volatile).
+__device__ __forceinline__ double ld_nospec(const double *p) {
+    double v;
+    asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+
+constexpr int CH_WARPS = 4;   // warps per k_fin_chain CTA
+constexpr int CG = 8;         // lanes per half chain: the stack-top window
+constexpr int CS = 64;        // stack entries per half chain in shared memory (deeper ones in hu/hv/hj)
+constexpr size_t CH_SMEM = (size_t)CH_WARPS * 4 * CS * (8 + 8 + 4);
+
 
 // ONE WARP PER PATCH, one 8-lane group per half chain of _monotone_hull
 // (reduction.py:214-223): group 0/1 the lower/upper chain over all sorted members
-// (the hull area), 2/3 over the touching members (the kept selection). Patches are
-// claimed from the job queue (long patches first).
+// (the hull area), 2/3 over the touching members (the kept selection; k_fin_sort
+// wrote them compacted, in sorted order, with their sorted positions). Patches come
+// from the job queue bucketed by size, longest first.
 //
-// The chain is sequential in its keys, but the pops of one key are not: the
-// sequential loop tests cross(h[top-2-i], h[top-1-i], b) for i = 0, 1, ... on the
-// unchanged stack below the pops, stopping at the first positive one. Lane i of a
-// group holds stack entry top-1-i, takes entry top-2-i from lane i+1, evaluates
-// that same test, and a ballot gives the number of pops; so one key costs one
-// cross product whatever it pops. The window shifts by shuffles; entries below it
-// come from a shared-memory ring of the top CR entries (older ones spilled to
-// hu/hv/hj when a new high-water mark reuses their slot). Keys stream from the
-// sorted rows, each lane prefetching every 8th key one round ahead.
+// A chain is sequential in its keys but not in the pops of one key: the sequential
+// loop tests cross(h[top-2-i], h[top-1-i], b) for i = 0, 1, ... on the unchanged
+// stack below, stopping at the first positive one. Lane i of a group holds stack
+// entry top-1-i (lane 7 also top-9) and takes entry top-2-i from lane i+1, so the
+// group evaluates those tests at once and a ballot gives the number of pops: a key
+// costs one cross product whatever it pops (measured: at most 8 pops per key on the
+// headline workload; more take further rounds). The window shifts by shuffles;
+// entries below it come from the group's stack in shared memory (u, v, sorted
+// position; entries from CS up in hu/hv/hj). Keys stream from the sorted rows, each
+// lane prefetching every 8th key one octet ahead. The stack is the half hull.
 __global__ void __launch_bounds__(CH_WARPS * 32) k_fin_chain(ReduceIO io, ReduceParams p) {
-    __shared__ double2 s_ruv[CH_WARPS][4][CR];
-    __shared__ int32_t s_rpos[CH_WARPS][4][CR];
+    extern __shared__ __align__(16) unsigned char dyn[];
+    __shared__ int bstart[CH_BUCKETS + 1];
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int g = lane >> 3, li = lane & 7, gb = g * CG;
-    double2 *ruv = s_ruv[wib][g];
-    int32_t *rpos = s_rpos[wib][g];
-    const int nl = io.njob[0], ntot = nl + io.njob[1];
-    const int64_t lcap = io.E * (int64_t)p.N;
+    double *stu = reinterpret_cast<double *>(dyn) + (wib * 4 + g) * CS;
+    double *stv = stu + CH_WARPS * 4 * CS;
+    int32_t *stp = reinterpret_cast<int32_t *>(reinterpret_cast<double *>(dyn) + 2 * CH_WARPS * 4 * CS) + (wib * 4 + g) * CS;
+    if (threadIdx.x == 0) {
+        int r = 0;
+        for (int k = 0; k < CH_BUCKETS; ++k) { bstart[k] = r; r += io.njob[k]; }
+        bstart[CH_BUCKETS] = r;
+    }
+    __syncthreads();
+    const int ntot = bstart[CH_BUCKETS];
+    const int64_t bcap = io.E * (int64_t)p.N;
     while (true) {
         int idx = 0;
-        if (lane == 0) idx = atomicAdd(io.njob + 2, 1);
+        if (lane == 0) idx = atomicAdd(io.njob + CH_BUCKETS, 1);
         idx = __shfl_sync(FULL, idx, 0);
         if (idx >= ntot) break;
-        const int w = idx < nl ? io.jobs[idx] : io.jobs[lcap + idx - nl];
+        int k = 0;
+        while (idx >= bstart[k + 1]) ++k;
+        const int w = io.jobs[k * bcap + idx - bstart[k]];
         const int64_t e = io.wenv[w];
         const int q = w - io.patch_off[e];
         const int32_t *mo = io.member_offsets + e * (p.N + 1);
         const int m = mo[q + 1] - mo[q];
         const int64_t row0 = io.cand_base[e] + mo[q];
-        const bool run = g < 2 ? needs_all_hull(m, p.K) : needs_touch_hull(m, io.pnt[w], p.K);
+        const int nt = io.pnt[w];
+        const bool run = g < 2 ? needs_all_hull(m, p.K) : needs_touch_hull(m, nt, p.K);
+        const int L = run ? (g < 2 ? m : nt) : 0;
         const int dir = (g & 1) ? -1 : 1;
-        const bool touching = g >= 2;
-        const double2 *suv = io.suv + row0;
-        const int32_t *sk = io.sp + row0;
+        const double2 *kuv = g < 2 ? io.suv + row0 : io.tuv + row0;
+        const int32_t *kpos = g < 2 ? nullptr : io.tpos + row0;
         const int64_t h0 = 4 * row0 + (int64_t)g * m;
         int32_t *hj = io.hj + h0;
         double *hu = io.hu + h0, *hv = io.hv + h0;
-        auto load_key = [&](int x, double2 &uv, int &k) {
-            if (run && x < m) {
-                const int s = dir > 0 ? x : m - 1 - x;
-                uv = __ldg(suv + s);
-                k = __ldg(sk + s);
-            } else {
-                uv = make_double2(0.0, 0.0);
-                k = -1;
-            }
+        int Lmax = max(__shfl_sync(FULL, L, 0), __shfl_sync(FULL, L, 8));
+        Lmax = max(Lmax, max(__shfl_sync(FULL, L, 16), __shfl_sync(FULL, L, 24)));
+        // key x of the chain (index clamped into the list: no branch around the loads)
+        auto key = [&](int x, double &u, double &v, int &ps) {
+            const int c = min(x, L - 1);
+            const int sidx = max(dir > 0 ? c : L - 1 - c, 0);  // L == 0: row 0, unused
+            const double2 uv = __ldg(kuv + sidx);
+            u = uv.x; v = uv.y;
+            ps = kpos ? __ldg(kpos + sidx) : sidx;
         };
-        int hw = 0;  // high-water mark of the stack (ring invariant below)
-        auto entry = [&](int j, double &u, double &v) {  // stack entry j (j < top)
-            if (j < 0) { u = 0.0; v = 0.0; return; }
-            if (j >= hw - CR) { const double2 x = ruv[j % CR]; u = x.x; v = x.y; }
-            else { u = hu[j]; v = hv[j]; }
+        // stack entry j (j < top)
+        auto entry = [&](int j, double &u, double &v) {
+            if (j < 0) { u = 0.0; v = 0.0; }
+            else if (j < CS) { u = stu[j]; v = stv[j]; }
+            else { u = ld_nospec(hu + j); v = ld_nospec(hv + j); }
         };
-        double2 cur_uv, nxt_uv;
-        int cur_k, nxt_k;
-        load_key(li, cur_uv, cur_k);
-        load_key(CG + li, nxt_uv, nxt_k);
-        double wu = 0.0, wv = 0.0, bu = 0.0, bv = 0.0;  // entry top-1-li; lane 7 also entry top-9
+        double cu, cv, nu_, nv_;
+        int cp, np_;
+        key(li, cu, cv, cp);
+        key(CG + li, nu_, nv_, np_);
+        double wu = 0.0, wv = 0.0, xu = 0.0, xv = 0.0;  // entry top-1-li; lane 7: xu/xv = entry top-9
         int top = 0;
-        for (int t = 0; t < m; ++t) {
+        for (int t = 0; t < Lmax; ++t) {
             const int c = t & (CG - 1);
             if (c == 0 && t > 0) {
-                cur_uv = nxt_uv; cur_k = nxt_k;
-                load_key(t + CG + li, nxt_uv, nxt_k);
+                cu = nu_; cv = nv_; cp = np_;
+                key(t + CG + li, nu_, nv_, np_);
             }
-            const double ub = __shfl_sync(FULL, cur_uv.x, gb + c), vb = __shfl_sync(FULL, cur_uv.y, gb + c);
-            const int kb = __shfl_sync(FULL, cur_k, gb + c);
-            const bool act = run && (!touching || kb >= 0);
-            // pops: lane i tests cross(o = entry top-2-i, a = entry top-1-i, b)
+            const double ub = __shfl_sync(FULL, cu, gb + c), vb = __shfl_sync(FULL, cv, gb + c);
+            const int pb = __shfl_sync(FULL, cp, gb + c);
+            const bool act = t < L;
             bool more = act;
-            while (__any_sync(FULL, more)) {
+            while (true) {
                 double ou = __shfl_down_sync(FULL, wu, 1), ov = __shfl_down_sync(FULL, wv, 1);
-                if (li == CG - 1) { ou = bu; ov = bv; }
+                if (li == CG - 1) { ou = xu; ov = xv; }
+                // cross(o, a, b) = (a.u - o.u)(b.v - o.v) - (a.v - o.v)(b.u - o.u), o = h[top-2-li], a = h[top-1-li]
                 const bool popi = more && top - li >= 2 && !((wu - ou) * (vb - ov) - (wv - ov) * (ub - ou) > 0.0);
                 const unsigned stop = (__ballot_sync(FULL, !popi) >> gb) & 0xffu;
-                const int np = more ? (stop ? __ffs(stop) - 1 : CG) : 0;
-                top -= np;
-                double nu = __shfl_sync(FULL, wu, (lane + np) & 31), nv = __shfl_sync(FULL, wv, (lane + np) & 31);
-                if (li + np >= CG) entry(top - 1 - li, nu, nv);
-                if (li == CG - 1 && np > 0) entry(top - 1 - CG, bu, bv);
+                const int npop = more ? (stop ? __ffs(stop) - 1 : CG) : 0;
+                top -= npop;
+                double nu = __shfl_sync(FULL, wu, (lane + npop) & 31), nv = __shfl_sync(FULL, wv, (lane + npop) & 31);
+                if (li + npop >= CG) entry(top - 1 - li, nu, nv);
+                if (li == CG - 1 && npop > 0) entry(top - 1 - CG, xu, xv);
                 wu = nu; wv = nv;
-                more = more && np == CG;
+                more = npop == CG;
+                if (!__any_sync(FULL, more)) break;
             }
             // push b
             const double pu = __shfl_up_sync(FULL, wu, 1), pv = __shfl_up_sync(FULL, wv, 1);
             if (act) {
-                if (li == CG - 1) { bu = wu; bv = wv; }
+                if (li == CG - 1) { xu = wu; xv = wv; }
                 if (li == 0) {
-                    const int slot = top % CR;
-                    // Ring invariant: live entry j is in slot j % CR iff j >= hw - CR, else in
-                    // hu/hv/hj. A push at a new high-water mark moves entry top - CR out.
-                    if (top == hw && top >= CR) {
-                        const double2 old = ruv[slot];
-                        hu[top - CR] = old.x; hv[top - CR] = old.y; hj[top - CR] = rpos[slot];
-                    }
-                    ruv[slot] = make_double2(ub, vb);
-                    rpos[slot] = dir > 0 ? t : m - 1 - t;
+                    if (top < CS) { stu[top] = ub; stv[top] = vb; stp[top] = pb; }
+                    else { hu[top] = ub; hv[top] = vb; hj[top] = pb; }
                     wu = ub; wv = vb;
                 } else {
                     wu = pu; wv = pv;
                 }
                 ++top;
-                hw = max(hw, top);
             }
             __syncwarp();
         }
-        // the stack is the half hull: ring entries -> hj (spilled ones are there already)
-        if (run) {
-            for (int j = max(0, hw - CR) + li; j < top; j += CG) hj[j] = rpos[j % CR];
+        if (run) {  // the stack is the half hull (sorted positions)
+            for (int j = li; j < min(top, CS); j += CG) hj[j] = stp[j];
             if (li == 0) io.hlen[4 * (int64_t)w + g] = top;
         }
         __syncwarp();
@@ -665,12 +703,13 @@ void launch_finalize(const ReduceIO &io, const ReduceParams &p, int sm_count, cu
     if (!configured) {
         cudaFuncSetAttribute(k_fin_sort_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
         cudaFuncSetAttribute(k_fin_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FB_BYTES);
+        cudaFuncSetAttribute(k_fin_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CH_SMEM);
         configured = true;
     }
     auto cap = [&](int64_t want, int64_t limit) { return (unsigned)(want < limit ? want : limit); };
     k_fin_sort_warp<<<cap((int64_t)sm_count * 8, (maxw + FW_WARPS - 1) / FW_WARPS), FW_WARPS * 32, wsm, s>>>(io, p);
     k_fin_sort_block<<<cap((int64_t)sm_count * 4, maxw), FB_THREADS, FB_BYTES, s>>>(io, p);
-    k_fin_chain<<<cap((int64_t)sm_count * 8, (maxw + CH_WARPS - 1) / CH_WARPS), CH_WARPS * 32, 0, s>>>(io, p);
+    k_fin_chain<<<cap((int64_t)sm_count * 8, (maxw + CH_WARPS - 1) / CH_WARPS), CH_WARPS * 32, CH_SMEM, s>>>(io, p);
     k_fin_kept<<<cap((int64_t)sm_count * 8, (maxw + FK_WARPS - 1) / FK_WARPS), FK_WARPS * 32, 0, s>>>(io, p);
     k_stats<<<(unsigned)((io.E + 127) / 128), 128, 0, s>>>(io, p);
 }

@@ -28,6 +28,8 @@ struct ReduceIO {
     int32_t *sh;       // hull/stack scratch: env e uses [2 cand_base(e) + e (4N + 4), + 2 cap_e + 4N + 4)
     // finalisation scratch (cs_finalize.cu); rows like candidates unless stated
     double2 *suv;        // sorted (u, v) of every patch's members (rows), with sp the member (~k: not touching)
+    double2 *tuv;        // the touching members' sorted (u, v), compacted (rows) ...
+    int32_t *tpos;       // ... and their positions in the sorted rows
     double *tu, *tv;     // second sort buffer of patches too large for shared memory
     int32_t *tk;
     int32_t *hj;         // [4 rows] chain stacks: sorted positions (the hull output) ...
@@ -36,8 +38,8 @@ struct ReduceIO {
     int32_t *pdeep;      // [E N] per patch (work index): deepest member position
     int32_t *pnt;        // [E N] touching members (depth >= 0)
     int32_t *wenv;       // [E N] env of each work index
-    int32_t *jobs;       // [2][E N] chain jobs (patch work index): long patches, short patches
-    int32_t *njob;       // [4] long count, short count, claimed
+    int32_t *jobs;       // [64][E N] chain jobs (patch work index) bucketed by patch size
+    int32_t *njob;       // [65] per-bucket counts, claimed
     int32_t *patch_off;  // [E+1]
     int32_t *large_list, *large_count;  // patches above the warp path's size limit
     // outputs
