@@ -4,11 +4,12 @@
 //     * Assign (reduction.py:78-88): every batch position against every builder,
 //       in parallel over the CTA.
 //     * FindDeepest / BinReduce / AddPatch (reduction.py:63-73, 91-126): a
-//       sequential loop (one step per created patch, ~35 per env) run by warp 0
-//       alone -- shuffles and ballots, no block barriers -- over a compacted,
-//       order-preserving list of the still unassigned positions. One pass over
-//       that list bins against the seed AND finds the next seed (first argmax of
-//       depth among the survivors), so a step costs O(|unassigned| / 32).
+//       sequential loop (one step per created patch, ~35 per env), each step
+//       spread over the CTA: an order-preserving list of the still unassigned
+//       positions (block-scan compaction, ping-pong buffers); one pass over it
+//       bins against the seed AND finds the next seed (first argmax of depth
+//       among the survivors); the builder decision is a block argmax. The cold
+//       eviction path (reduction.py:111-126) runs in warp 0.
 //     * Members -> CSR by a stable counting sort (__match_any_sync) in warp 0.
 //   Builders (normals, order-encoded max depths) and the batch state live in
 //   shared memory; candidates are read through the read-only path.
@@ -22,10 +23,10 @@ namespace cs {
 constexpr int RED_T = 128;
 
 // Shared memory of one env: builders [N][3] f64, max depth [N] u64, counts [N] i32,
-// batch normals [SB][3] f64 and depths [SB] f64, batch -> candidate [SB] i32,
-// unassigned list [SB] i32, binned list [SB] i32, flags [SB] u8.
+// batch depths [SB] f64 (normals are read through L1), batch -> candidate [SB] i32,
+// unassigned lists [2][SB] i32, binned list [SB] i32, flags [SB] u8.
 __host__ __device__ inline size_t red_smem_bytes(int N, int SB) {
-    return (((size_t)N * (3 * 8 + 8 + 4) + 15) & ~(size_t)15) + (size_t)SB * (32 + 12) +
+    return (((size_t)N * (3 * 8 + 8 + 4) + 15) & ~(size_t)15) + (size_t)SB * (8 + 16) +
            (((size_t)SB + 15) & ~(size_t)15);
 }
 
@@ -66,18 +67,21 @@ __device__ double warp_hull_area_label(const int32_t *lab, int C, int L, const d
 __global__ void __launch_bounds__(RED_T) k_reduce(ReduceIO io, ReduceParams p, int SB) {
     extern __shared__ __align__(16) unsigned char dyn[];
     __shared__ int s_P;
+    __shared__ int s_ws[WS_INTS];
+    __shared__ ArgMax s_am[32];
+    __shared__ double s_dred[32];
     const int N = p.N;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
     double *bn = reinterpret_cast<double *>(dyn);                                  // [N][3]
     unsigned long long *bmx = reinterpret_cast<unsigned long long *>(bn + 3 * N);  // [N]
     int *hcnt = reinterpret_cast<int *>(bmx + N);                                  // [N]
-    double *bnrm = reinterpret_cast<double *>(dyn + (((size_t)N * 36 + 15) & ~(size_t)15));  // [SB][3]
-    double *bdep = bnrm + 3 * (size_t)SB;                                          // [SB]
+    double *bdep = reinterpret_cast<double *>(dyn + (((size_t)N * 36 + 15) & ~(size_t)15));  // [SB]
     int32_t *sbo = reinterpret_cast<int32_t *>(bdep + SB);                         // [SB]
     int32_t *ul = sbo + SB;                                                        // [SB] unassigned positions
     int32_t *bl = ul + SB;                                                         // [SB] binned positions
-    uint8_t *st = reinterpret_cast<uint8_t *>(bl + SB);                            // [SB]
+    int32_t *ul2 = bl + SB;                                                        // [SB] unassigned (ping-pong)
+    uint8_t *st = reinterpret_cast<uint8_t *>(ul2 + SB);                           // [SB]
 
     const int64_t e = blockIdx.x;
     const int64_t base = io.cand_base[e];
@@ -117,9 +121,6 @@ __global__ void __launch_bounds__(RED_T) k_reduce(ReduceIO io, ReduceParams p, i
         for (int k = tid; k < bsz; k += RED_T) {
             const int i = identity ? start + k : ord[start + k];
             sbo[k] = i;
-            bnrm[3 * k] = __ldg(nrm + 3 * (int64_t)i);
-            bnrm[3 * k + 1] = __ldg(nrm + 3 * (int64_t)i + 1);
-            bnrm[3 * k + 2] = __ldg(nrm + 3 * (int64_t)i + 2);
             bdep[k] = __ldg(dep + i);
         }
         __syncthreads();
@@ -130,7 +131,8 @@ __global__ void __launch_bounds__(RED_T) k_reduce(ReduceIO io, ReduceParams p, i
                 uint8_t s = 0;
                 if (P > 0) {
                     const int i = sbo[k];
-                    const double a[3] = {bnrm[3 * k], bnrm[3 * k + 1], bnrm[3 * k + 2]};
+                    const double a[3] = {__ldg(nrm + 3 * (int64_t)i), __ldg(nrm + 3 * (int64_t)i + 1),
+                                         __ldg(nrm + 3 * (int64_t)i + 2)};
                     int best = 0;
                     double bc = cosv(v3, a, bn);
                     for (int q = 1; q < P; ++q) {
@@ -148,108 +150,124 @@ __global__ void __launch_bounds__(RED_T) k_reduce(ReduceIO io, ReduceParams p, i
             }
         }
         __syncthreads();
-        if (wid == 0) {
-            // unassigned positions, ascending, and the first seed (first argmax of depth)
-            int nu = 0;
+        // Seed / BinReduce / AddPatch (reduction.py:63-73, 91-126), one step per created
+        // patch, each step spread over the CTA: the unassigned batch positions are kept
+        // as an ascending list (ordered block-scan compaction), so "first argmax" is
+        // numpy's, and the next seed comes out of the same pass as the bin.
+        int nu, dp;
+        {
+            int run = 0;
             ArgMax am = {0.0, -1, 0};
-            for (int c0 = 0; c0 < bsz; c0 += 32) {
-                const int k = c0 + lane;
-                const bool f = k < bsz && st[k] == 0;
-                const unsigned b = __ballot_sync(FULL, f);
-                if (f) {
-                    ul[nu + __popc(b & lt)] = k;
-                    am = argmax_combine(am, ArgMax{bdep[k], nu + __popc(b & lt), 1});
-                }
-                nu += __popc(b);
+            for (int r0 = 0; r0 < bsz; r0 += 32 * RED_T) {
+                const int rn = min(bsz - r0, 32 * RED_T);
+                const int c = (rn + RED_T - 1) / RED_T;
+                const int k0 = r0 + tid * c, k1 = min(k0 + c, r0 + rn);
+                int n = 0;
+                for (int k = k0; k < k1; ++k) n += st[k] == 0 ? 1 : 0;
+                int tot;
+                int pos = run + block_excl_scan(n, s_ws, &tot);
+                for (int k = k0; k < k1; ++k)
+                    if (st[k] == 0) {
+                        am = argmax_combine(am, ArgMax{bdep[k], pos, 1});
+                        ul[pos++] = k;
+                    }
+                run += tot;
             }
-            am = warp_argmax(am);
-            __syncwarp();
-            while (nu > 0) {
-                // FindDeepest: am.i indexes ul (ascending positions, so first max == numpy's)
-                const int dp = am.i;
-                const int sk = ul[dp];
-                const double sn[3] = {bnrm[3 * sk], bnrm[3 * sk + 1], bnrm[3 * sk + 2]};
-                const double sd = bdep[sk];
-                // BinReduce (reduction.py:67-69) fused with the next FindDeepest: one pass
-                const bool v3 = nu >= 2;
-                double lmax = -INFINITY;
-                int keep = 0, nbin = 0;
-                ArgMax nx = {0.0, -1, 0};
-                for (int c0 = 0; c0 < nu; c0 += 32) {
-                    const int j = c0 + lane;
-                    bool kept = false, binned = false;
-                    int k = 0;
-                    double d = 0.0;
-                    if (j < nu) {
-                        k = ul[j];
-                        const double n3[3] = {bnrm[3 * k], bnrm[3 * k + 1], bnrm[3 * k + 2]};
-                        d = bdep[k];
-                        binned = cosv(v3, n3, sn) >= p.cone || j == dp;
-                        kept = !binned;
-                    }
-                    const unsigned bb = __ballot_sync(FULL, binned);
-                    if (binned) {
+            am = block_argmax(am, s_am);
+            nu = run;
+            dp = am.i;
+        }
+        int32_t *ua = ul, *ub = ul2;
+        while (nu > 0) {
+            // FindDeepest: dp indexes ua (ascending positions)
+            const int sk = ua[dp];
+            const int64_t si = sbo[sk];
+            const double sn[3] = {__ldg(nrm + 3 * si), __ldg(nrm + 3 * si + 1), __ldg(nrm + 3 * si + 2)};
+            const double sd = bdep[sk];
+            // BinReduce (reduction.py:67-69) fused with the next FindDeepest. Each thread
+            // owns a contiguous span of the list (at most 32 positions per round of
+            // 32 RED_T), flags it in registers, and one block scan orders the writes.
+            const bool v3 = nu >= 2;
+            int keep = 0, nbin = 0;
+            double lmax = -INFINITY;
+            ArgMax nx = {0.0, -1, 0};
+            for (int r0 = 0; r0 < nu; r0 += 32 * RED_T) {
+                const int rn = min(nu - r0, 32 * RED_T);
+                const int c = (rn + RED_T - 1) / RED_T;
+                const int j0 = r0 + tid * c, j1 = min(j0 + c, r0 + rn);
+                unsigned bmask = 0;  // bit i: position j0 + i is binned
+                int nk = 0, nb = 0;
+                for (int j = j0; j < j1; ++j) {
+                    const int k = ua[j];
+                    const int64_t i = sbo[k];
+                    const double n3[3] = {__ldg(nrm + 3 * i), __ldg(nrm + 3 * i + 1), __ldg(nrm + 3 * i + 2)};
+                    const bool binned = cosv(v3, n3, sn) >= p.cone || j == dp;
+                    bmask |= (binned ? 1u : 0u) << (j - j0);
+                    nb += binned ? 1 : 0;
+                    nk += binned ? 0 : 1;
+                }
+                int tot;
+                const int pk = block_excl_scan(nk | (nb << 16), s_ws, &tot);
+                int kp = keep + (pk & 0xffff), bp = nbin + (pk >> 16);
+                for (int j = j0; j < j1; ++j) {
+                    const int k = ua[j];
+                    const double d = bdep[k];
+                    if ((bmask >> (j - j0)) & 1u) {
+                        bl[bp++] = k;
                         st[k] = 2;
-                        bl[nbin + __popc(bb & lt)] = k;
                         if (d > lmax) lmax = d;  // patch.max_depth: strict > over members, NaN ignored
+                    } else {
+                        nx = argmax_combine(nx, ArgMax{d, kp, 1});
+                        ub[kp++] = k;
                     }
-                    nbin += __popc(bb);
-                    const unsigned b = __ballot_sync(FULL, kept);
-                    if (kept) {
-                        const int pos = keep + __popc(b & lt);  // pos <= j: in-place compaction is safe
-                        ul[pos] = k;
-                        nx = argmax_combine(nx, ArgMax{d, pos, 1});
-                    }
-                    keep += __popc(b);
                 }
-                nx = warp_argmax(nx);
-                double pmax = sd;
-                if (isnan(sd)) {
+                keep += tot & 0xffff;
+                nbin += tot >> 16;
+            }
+            nx = block_argmax(nx, s_am);
+            double pmax = sd;
+            if (isnan(sd)) {
 #pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) lmax = fmax(lmax, __shfl_xor_sync(FULL, lmax, o));
-                    pmax = lmax;
+                for (int o = 16; o > 0; o >>= 1) lmax = fmax(lmax, __shfl_xor_sync(FULL, lmax, o));
+                if (lane == 0) s_dred[wid] = lmax;
+                __syncthreads();
+                pmax = -INFINITY;
+                for (int i = 0; i < RED_T / 32; ++i) pmax = fmax(pmax, s_dred[i]);
+                __syncthreads();
+            }
+            // _add_patch decision (reduction.py:91-110): reps @ patch.normal, first argmax
+            ArgMax bq = {0.0, -1, 0};
+            if (P > 0) {
+                const bool v3b = P >= 2;
+                for (int q = tid; q < P; q += RED_T) bq = argmax_combine(bq, ArgMax{cosv(v3b, bn + 3 * q, sn), q, 1});
+                bq = block_argmax(bq, s_am);
+            }
+            const int best = bq.i;
+            const double bc = bq.v;
+            const bool similar = P > 0 && bc >= p.cone;
+            if (similar && (bc >= MERGE_COS || P >= N)) {  // merge: deeper patch's normal, union members
+                const int t = best;
+                if (tid == 0 && pmax > dec_d(bmx[t])) { bn[3 * t] = sn[0]; bn[3 * t + 1] = sn[1]; bn[3 * t + 2] = sn[2]; }
+                __syncthreads();
+                for (int x = tid; x < nbin; x += RED_T) {
+                    const int k = bl[x], i = sbo[k];
+                    lab[i] = t;
+                    st[k] = 1;
+                    const double d = bdep[k];
+                    if (!isnan(d)) atomicMax(&bmx[t], enc_d(d));
                 }
-                // _add_patch decision (reduction.py:91-110): reps @ patch.normal, first argmax
-                int best = -1;
-                double bc = 0.0;
-                if (P > 0) {
-                    const bool v3b = P >= 2;
-                    for (int q = lane; q < P; q += 32) {
-                        const double c = cosv(v3b, bn + 3 * q, sn);
-                        if (best < 0 || amax_better(c, q, bc, best)) { bc = c; best = q; }
-                    }
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) {
-                        const double obc = __shfl_xor_sync(FULL, bc, o);
-                        const int ob = __shfl_xor_sync(FULL, best, o);
-                        if (ob >= 0 && (best < 0 || amax_better(obc, ob, bc, best))) { bc = obc; best = ob; }
-                    }
+            } else if (P < N) {  // append
+                if (tid == 0) {
+                    bn[3 * P] = sn[0]; bn[3 * P + 1] = sn[1]; bn[3 * P + 2] = sn[2];
+                    bmx[P] = enc_d(pmax);
                 }
-                __syncwarp();
-                const bool similar = P > 0 && bc >= p.cone;
-                if (similar && (bc >= MERGE_COS || P >= N)) {  // merge: deeper patch's normal, union members
-                    const int t = best;
-                    if (lane == 0 && pmax > dec_d(bmx[t])) { bn[3 * t] = sn[0]; bn[3 * t + 1] = sn[1]; bn[3 * t + 2] = sn[2]; }
-                    __syncwarp();
-                    for (int x = lane; x < nbin; x += 32) {
-                        const int k = bl[x], i = sbo[k];
-                        lab[i] = t;
-                        st[k] = 1;
-                        const double d = bdep[k];
-                        if (!isnan(d)) atomicMax(&bmx[t], enc_d(d));
-                    }
-                } else if (P < N) {  // append
-                    if (lane == 0) {
-                        bn[3 * P] = sn[0]; bn[3 * P + 1] = sn[1]; bn[3 * P + 2] = sn[2];
-                        bmx[P] = enc_d(pmax);
-                    }
-                    for (int x = lane; x < nbin; x += 32) {
-                        const int k = bl[x];
-                        lab[sbo[k]] = P;
-                        st[k] = 1;
-                    }
-                    ++P;
-                } else {  // evict the lowest-priority patch (reduction.py:111-126)
+                for (int x = tid; x < nbin; x += RED_T) {
+                    const int k = bl[x];
+                    lab[sbo[k]] = P;
+                    st[k] = 1;
+                }
+                ++P;
+            } else if (wid == 0) {  // evict the lowest-priority patch (reduction.py:111-126): cold, warp 0
                     for (int x = lane; x < nbin; x += 32) lab[sbo[bl[x]]] = -2;
                     __syncwarp();
                     double gm = dec_d(bmx[0]);
@@ -310,15 +328,12 @@ __global__ void __launch_bounds__(RED_T) k_reduce(ReduceIO io, ReduceParams p, i
                             }
                     }
                     for (int x = lane; x < nbin; x += 32) st[bl[x]] = 1;
-                }
-                __syncwarp();
-                nu = keep;
-                am = nx;
             }
-            if (lane == 0) s_P = P;
+            __syncthreads();
+            int32_t *tmp = ua; ua = ub; ub = tmp;
+            nu = keep;
+            dp = nx.i;
         }
-        __syncthreads();
-        P = s_P;
         __syncthreads();
     }
     // builders -> outputs
