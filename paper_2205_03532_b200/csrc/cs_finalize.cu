@@ -673,25 +673,36 @@ __global__ void __launch_bounds__(FK_WARPS * 32) k_fin_kept(ReduceIO io, ReduceP
         kept_patch(t, io, p, w, s_chosen[wib]);
 }
 
+// Per env stats, one warp per env (lanes over the patches).
 __global__ void k_stats(ReduceIO io, ReduceParams p) {
-    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (e >= io.E) return;
     const int N = p.N, K = p.K;
-    int P = io.n_patch[e], nk = 0;
+    const int P = io.n_patch[e];
+    int nk = 0;
     double mx = 0.0;  // StepReport.max_penetration = max(max(depth, 0)) (scene.py:160-161)
-    for (int q = 0; q < P; ++q) {
-        int k = io.patch_nkept[e * N + q];
+    for (int q = lane; q < P; q += 32) {
+        const int k = io.patch_nkept[e * N + q];
         nk += k;
         for (int j = 0; j < k; ++j) {
-            double d = io.kept_depth[(e * N + q) * K + j];
+            const double d = io.kept_depth[(e * N + q) * K + j];
             if (d > mx) mx = d;
         }
     }
-    io.n_kept[e] = nk;
-    io.stats[4 * e + 0] = (float)io.n_cand[e];
-    io.stats[4 * e + 1] = (float)P;
-    io.stats[4 * e + 2] = (float)nk;
-    io.stats[4 * e + 3] = (float)mx;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        nk += __shfl_xor_sync(0xffffffffu, nk, o);
+        const double om = __shfl_xor_sync(0xffffffffu, mx, o);
+        if (om > mx) mx = om;
+    }
+    if (lane == 0) {
+        io.n_kept[e] = nk;
+        io.stats[4 * e + 0] = (float)io.n_cand[e];
+        io.stats[4 * e + 1] = (float)P;
+        io.stats[4 * e + 2] = (float)nk;
+        io.stats[4 * e + 3] = (float)mx;
+    }
 }
 
 void launch_finalize(const ReduceIO &io, const ReduceParams &p, int sm_count, cudaStream_t s) {
@@ -711,7 +722,7 @@ void launch_finalize(const ReduceIO &io, const ReduceParams &p, int sm_count, cu
     k_fin_sort_block<<<cap((int64_t)sm_count * 4, maxw), FB_THREADS, FB_BYTES, s>>>(io, p);
     k_fin_chain<<<cap((int64_t)sm_count * 8, (maxw + CH_WARPS - 1) / CH_WARPS), CH_WARPS * 32, CH_SMEM, s>>>(io, p);
     k_fin_kept<<<cap((int64_t)sm_count * 8, (maxw + FK_WARPS - 1) / FK_WARPS), FK_WARPS * 32, 0, s>>>(io, p);
-    k_stats<<<(unsigned)((io.E + 127) / 128), 128, 0, s>>>(io, p);
+    k_stats<<<(unsigned)((io.E * 32 + 255) / 256), 256, 0, s>>>(io, p);
 }
 
 }  // namespace cs

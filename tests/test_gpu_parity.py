@@ -241,3 +241,42 @@ def test_empty_and_separated(P, grid64, nut):
     res = P.collide([P.register_sdf(grid64)], [P.register_mesh(nut)], [[0, 0, 0, 1.0, 0, 0, 0]],
                     [[1.0, 0, 0, 1.0, 0, 0, 0]], [1e-3])
     assert int(res.n_cand[0]) == 0 and int(res.n_patch[0]) == 0 and res.patches(0) == []
+
+
+def test_mixed_assets_per_env(P, grid64, nut, meshes):
+    """Configs 3/4 shape: envs with different SDF grids and meshes in one collide
+    call (M16 bolt grid + nut, peg grid + hole; moved SDF poses; a separated env),
+    each env against the oracle field by field."""
+    from oracle import oracle as O
+
+    g = np.load(os.path.join(GOLDEN, "grid_peg_r64.npz"))
+    peg_grid = P.SignedDistanceGrid(g["origin"], float(g["voxel"]), g["dims"], g["values"], (g["aabb_lo"], g["aabb_hi"]))
+    hole = P.TriMesh(meshes["hole_v"], meshes["hole_t"])
+    gen = np.load(os.path.join(GOLDEN, "gen_r64.npz"))
+    ident = np.array([0, 0, 0, 1.0, 0, 0, 0])
+    rng = np.random.default_rng(3)
+    envs = []  # (sdf grid, oracle grid, mesh, sdf pose, mesh pose, cd)
+    og_bolt = O.Grid.from_npz(np.load(os.path.join(GOLDEN, "grid_bolt_r64.npz")))
+    og_peg = O.Grid.from_npz(g)
+    for i in range(8):
+        if i % 2 == 0:
+            e = int(gen["envs"][(i // 2) % len(gen["envs"])])
+            envs.append((grid64, og_bolt, nut, meshes["nut_v"], meshes["nut_t"], gen[f"e{e}_sdf_pose"],
+                         gen[f"e{e}_mesh_pose"], 2.0 * grid64.voxel_size))
+        else:
+            dz = 0.05 if i == 7 else rng.uniform(0.0, 0.01)  # env 7: peg far above the hole
+            sp = np.array([rng.uniform(-3e-4, 3e-4), rng.uniform(-3e-4, 3e-4), dz, 1.0, 0, 0, 0])
+            envs.append((peg_grid, og_peg, hole, meshes["hole_v"], meshes["hole_t"], sp, ident,
+                         2.0 * peg_grid.voxel_size))
+    res = P.collide([P.register_sdf(x[0]) for x in envs], [P.register_mesh(x[2]) for x in envs],
+                    np.stack([x[5] for x in envs]), np.stack([x[6] for x in envs]), np.array([x[7] for x in envs]))
+    for i, (_, og, _, v, t, sp, mp, cd) in enumerate(envs):
+        ref = O.generate_contacts(og, v, t, sp, mp, cd)
+        cs = res.contact_set(i)
+        assert np.array_equal(cs.points, ref["points"]) and np.array_equal(cs.normals, ref["normals"]), i
+        assert np.array_equal(cs.depths, ref["depths"]) and np.array_equal(cs.face_indices, ref["faces"]), i
+        assert (len(cs) > 0) == (i != 7), i
+        r = O.reduce_contacts(ref["points"], ref["normals"], ref["depths"], ref["faces"], min_depth=-cd)
+        got = pack_patch_list(res.patches(i), 6)
+        for k in ("rep", "nkept", "members", "kept_faces", "wsum", "wp", "wn", "wt", "area", "maxd"):
+            assert np.array_equal(np.asarray(got[k]), np.asarray(r[k])), (i, k)
