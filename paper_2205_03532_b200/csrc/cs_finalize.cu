@@ -413,9 +413,9 @@ __device__ __forceinline__ double ld_nospec(const double *p) {
 }
 
 constexpr int CH_WARPS = 4;   // warps per k_fin_chain CTA
-constexpr int CG = 8;         // lanes per half chain: the stack-top window
+constexpr int CG = 8;         // lanes per half chain: pops tested per round
 constexpr int CS = 64;        // stack entries per half chain in shared memory (deeper ones in hu/hv/hj)
-constexpr size_t CH_SMEM = (size_t)CH_WARPS * 4 * CS * (8 + 8 + 4);
+constexpr size_t CH_SMEM = (size_t)CH_WARPS * 4 * CS * (16 + 4);
 
 
 // ONE WARP PER PATCH, one 8-lane group per half chain of _monotone_hull
@@ -426,23 +426,21 @@ constexpr size_t CH_SMEM = (size_t)CH_WARPS * 4 * CS * (8 + 8 + 4);
 //
 // A chain is sequential in its keys but not in the pops of one key: the sequential
 // loop tests cross(h[top-2-i], h[top-1-i], b) for i = 0, 1, ... on the unchanged
-// stack below, stopping at the first positive one. Lane i of a group holds stack
-// entry top-1-i (lane 7 also top-9) and takes entry top-2-i from lane i+1, so the
-// group evaluates those tests at once and a ballot gives the number of pops: a key
-// costs one cross product whatever it pops (measured: at most 8 pops per key on the
-// headline workload; more take further rounds). The window shifts by shuffles;
-// entries below it come from the group's stack in shared memory (u, v, sorted
-// position; entries from CS up in hu/hv/hj). Keys stream from the sorted rows, each
-// lane prefetching every 8th key one octet ahead. The stack is the half hull.
+// stack below, stopping at the first positive one. Lane i of a group reads stack
+// entries top-1-i and top-2-i and evaluates that same test, and a ballot gives the
+// number of pops, so a key costs one round whatever it pops (measured: at most 8
+// pops per key on the headline workload; more take further rounds). The stack
+// ((u, v) and sorted position) lives in shared memory (entries from CS up in
+// hu/hv/hj); pushing is one store. Keys stream from the sorted rows, each lane
+// prefetching every 8th key one octet ahead. The stack is the half hull.
 __global__ void __launch_bounds__(CH_WARPS * 32) k_fin_chain(ReduceIO io, ReduceParams p) {
     extern __shared__ __align__(16) unsigned char dyn[];
     __shared__ int bstart[CH_BUCKETS + 1];
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int g = lane >> 3, li = lane & 7, gb = g * CG;
-    double *stu = reinterpret_cast<double *>(dyn) + (wib * 4 + g) * CS;
-    double *stv = stu + CH_WARPS * 4 * CS;
-    int32_t *stp = reinterpret_cast<int32_t *>(reinterpret_cast<double *>(dyn) + 2 * CH_WARPS * 4 * CS) + (wib * 4 + g) * CS;
+    double2 *st = reinterpret_cast<double2 *>(dyn) + (wib * 4 + g) * CS;
+    int32_t *stp = reinterpret_cast<int32_t *>(reinterpret_cast<double2 *>(dyn) + CH_WARPS * 4 * CS) + (wib * 4 + g) * CS;
     if (threadIdx.x == 0) {
         int r = 0;
         for (int k = 0; k < CH_BUCKETS; ++k) { bstart[k] = r; r += io.njob[k]; }
@@ -483,17 +481,14 @@ __global__ void __launch_bounds__(CH_WARPS * 32) k_fin_chain(ReduceIO io, Reduce
             u = uv.x; v = uv.y;
             ps = kpos ? __ldg(kpos + sidx) : sidx;
         };
-        // stack entry j (j < top)
-        auto entry = [&](int j, double &u, double &v) {
-            if (j < 0) { u = 0.0; v = 0.0; }
-            else if (j < CS) { u = stu[j]; v = stv[j]; }
-            else { u = ld_nospec(hu + j); v = ld_nospec(hv + j); }
+        auto entry = [&](int j) -> double2 {  // stack entry j (0 <= j < top)
+            if (j < CS) return st[j];
+            return make_double2(ld_nospec(hu + j), ld_nospec(hv + j));
         };
         double cu, cv, nu_, nv_;
         int cp, np_;
         key(li, cu, cv, cp);
         key(CG + li, nu_, nv_, np_);
-        double wu = 0.0, wv = 0.0, xu = 0.0, xv = 0.0;  // entry top-1-li; lane 7: xu/xv = entry top-9
         int top = 0;
         for (int t = 0; t < Lmax; ++t) {
             const int c = t & (CG - 1);
@@ -506,30 +501,24 @@ __global__ void __launch_bounds__(CH_WARPS * 32) k_fin_chain(ReduceIO io, Reduce
             const bool act = t < L;
             bool more = act;
             while (true) {
-                double ou = __shfl_down_sync(FULL, wu, 1), ov = __shfl_down_sync(FULL, wv, 1);
-                if (li == CG - 1) { ou = xu; ov = xv; }
-                // cross(o, a, b) = (a.u - o.u)(b.v - o.v) - (a.v - o.v)(b.u - o.u), o = h[top-2-li], a = h[top-1-li]
-                const bool popi = more && top - li >= 2 && !((wu - ou) * (vb - ov) - (wv - ov) * (ub - ou) > 0.0);
+                // lane li: o = h[top-2-li], a = h[top-1-li];
+                // cross(o, a, b) = (a.u - o.u)(b.v - o.v) - (a.v - o.v)(b.u - o.u)
+                const bool valid = more && top - li >= 2;
+                bool popi = false;
+                if (valid) {
+                    const double2 a = entry(top - 1 - li), o = entry(top - 2 - li);
+                    popi = !((a.x - o.x) * (vb - o.y) - (a.y - o.y) * (ub - o.x) > 0.0);
+                }
                 const unsigned stop = (__ballot_sync(FULL, !popi) >> gb) & 0xffu;
                 const int npop = more ? (stop ? __ffs(stop) - 1 : CG) : 0;
                 top -= npop;
-                double nu = __shfl_sync(FULL, wu, (lane + npop) & 31), nv = __shfl_sync(FULL, wv, (lane + npop) & 31);
-                if (li + npop >= CG) entry(top - 1 - li, nu, nv);
-                if (li == CG - 1 && npop > 0) entry(top - 1 - CG, xu, xv);
-                wu = nu; wv = nv;
                 more = npop == CG;
                 if (!__any_sync(FULL, more)) break;
             }
-            // push b
-            const double pu = __shfl_up_sync(FULL, wu, 1), pv = __shfl_up_sync(FULL, wv, 1);
-            if (act) {
-                if (li == CG - 1) { xu = wu; xv = wv; }
+            if (act) {  // push b
                 if (li == 0) {
-                    if (top < CS) { stu[top] = ub; stv[top] = vb; stp[top] = pb; }
+                    if (top < CS) { st[top] = make_double2(ub, vb); stp[top] = pb; }
                     else { hu[top] = ub; hv[top] = vb; hj[top] = pb; }
-                    wu = ub; wv = vb;
-                } else {
-                    wu = pu; wv = pv;
                 }
                 ++top;
             }
