@@ -405,18 +405,29 @@ __global__ void __launch_bounds__(FB_THREADS) k_fin_sort_block(ReduceIO io, Redu
 
 // ------------------------------------------------------------------ stage 2: chains
 
-// A global load the compiler may not hoist out of its branch (asm volatile).
-__device__ __forceinline__ double ld_nospec(const double *p) {
-    double v;
-    asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
-    return v;
-}
 
 constexpr int CH_WARPS = 4;   // warps per k_fin_chain CTA
 constexpr int CG = 8;         // lanes per half chain: pops tested per round
-constexpr int CS = 64;        // stack entries per half chain in shared memory (deeper ones in hu/hv/hj)
-constexpr size_t CH_SMEM = (size_t)CH_WARPS * 4 * CS * (16 + 4);
+constexpr int CS = 64;        // stack entries per half chain in shared memory
 
+// One half of _monotone_hull (reduction.py:214-223) by one thread with its stack in
+// global memory: the fallback for the rare chains whose stack outgrows CS.
+__device__ int half_chain_global(const double2 *kuv, const int32_t *kpos, int L, int dir, int32_t *hj, double *hu,
+                                 double *hv) {
+    int top = 0;
+    for (int x = 0; x < L; ++x) {
+        const int s = dir > 0 ? x : L - 1 - x;
+        const double2 b = kuv[s];
+        while (top >= 2) {
+            const double ou = hu[top - 2], ov = hv[top - 2], au = hu[top - 1], av = hv[top - 1];
+            if ((au - ou) * (b.y - ov) - (av - ov) * (b.x - ou) > 0.0) break;
+            --top;
+        }
+        hu[top] = b.x; hv[top] = b.y; hj[top] = kpos ? kpos[s] : s;
+        ++top;
+    }
+    return top;
+}
 
 // ONE WARP PER PATCH, one 8-lane group per half chain of _monotone_hull
 // (reduction.py:214-223): group 0/1 the lower/upper chain over all sorted members
@@ -430,17 +441,20 @@ constexpr size_t CH_SMEM = (size_t)CH_WARPS * 4 * CS * (16 + 4);
 // entries top-1-i and top-2-i and evaluates that same test, and a ballot gives the
 // number of pops, so a key costs one round whatever it pops (measured: at most 8
 // pops per key on the headline workload; more take further rounds). The stack
-// ((u, v) and sorted position) lives in shared memory (entries from CS up in
-// hu/hv/hj); pushing is one store. Keys stream from the sorted rows, each lane
-// prefetching every 8th key one octet ahead. The stack is the half hull.
+// ((u, v) and sorted position) lives in shared memory; pushing is one store.
+// Measured stacks stay under 26 entries; a chain that would exceed CS is redone by
+// one thread with a global stack (half_chain_global). Keys stream from the sorted
+// rows, each lane prefetching every 8th key one octet ahead. The stack is the half
+// hull.
 __global__ void __launch_bounds__(CH_WARPS * 32) k_fin_chain(ReduceIO io, ReduceParams p) {
-    extern __shared__ __align__(16) unsigned char dyn[];
+    __shared__ double2 s_st[CH_WARPS * 4][CS];
+    __shared__ int32_t s_stp[CH_WARPS * 4][CS];
     __shared__ int bstart[CH_BUCKETS + 1];
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int g = lane >> 3, li = lane & 7, gb = g * CG;
-    double2 *st = reinterpret_cast<double2 *>(dyn) + (wib * 4 + g) * CS;
-    int32_t *stp = reinterpret_cast<int32_t *>(reinterpret_cast<double2 *>(dyn) + CH_WARPS * 4 * CS) + (wib * 4 + g) * CS;
+    double2 *st = s_st[wib * 4 + g];
+    int32_t *stp = s_stp[wib * 4 + g];
     if (threadIdx.x == 0) {
         int r = 0;
         for (int k = 0; k < CH_BUCKETS; ++k) { bstart[k] = r; r += io.njob[k]; }
@@ -455,7 +469,8 @@ __global__ void __launch_bounds__(CH_WARPS * 32) k_fin_chain(ReduceIO io, Reduce
         idx = __shfl_sync(FULL, idx, 0);
         if (idx >= ntot) break;
         int k = 0;
-        while (idx >= bstart[k + 1]) ++k;
+        for (int sz = CH_BUCKETS / 2; sz > 0; sz >>= 1)  // last k with bstart[k] <= idx
+            if (bstart[k + sz] <= idx) k += sz;
         const int w = io.jobs[k * bcap + idx - bstart[k]];
         const int64_t e = io.wenv[w];
         const int q = w - io.patch_off[e];
@@ -468,9 +483,6 @@ __global__ void __launch_bounds__(CH_WARPS * 32) k_fin_chain(ReduceIO io, Reduce
         const int dir = (g & 1) ? -1 : 1;
         const double2 *kuv = g < 2 ? io.suv + row0 : io.tuv + row0;
         const int32_t *kpos = g < 2 ? nullptr : io.tpos + row0;
-        const int64_t h0 = 4 * row0 + (int64_t)g * m;
-        int32_t *hj = io.hj + h0;
-        double *hu = io.hu + h0, *hv = io.hv + h0;
         int Lmax = max(__shfl_sync(FULL, L, 0), __shfl_sync(FULL, L, 8));
         Lmax = max(Lmax, max(__shfl_sync(FULL, L, 16), __shfl_sync(FULL, L, 24)));
         // key x of the chain (index clamped into the list: no branch around the loads)
@@ -481,15 +493,12 @@ __global__ void __launch_bounds__(CH_WARPS * 32) k_fin_chain(ReduceIO io, Reduce
             u = uv.x; v = uv.y;
             ps = kpos ? __ldg(kpos + sidx) : sidx;
         };
-        auto entry = [&](int j) -> double2 {  // stack entry j (0 <= j < top)
-            if (j < CS) return st[j];
-            return make_double2(ld_nospec(hu + j), ld_nospec(hv + j));
-        };
         double cu, cv, nu_, nv_;
         int cp, np_;
         key(li, cu, cv, cp);
         key(CG + li, nu_, nv_, np_);
         int top = 0;
+        bool ovf = false;  // the stack outgrew CS: redone by half_chain_global
         for (int t = 0; t < Lmax; ++t) {
             const int c = t & (CG - 1);
             if (c == 0 && t > 0) {
@@ -498,15 +507,14 @@ __global__ void __launch_bounds__(CH_WARPS * 32) k_fin_chain(ReduceIO io, Reduce
             }
             const double ub = __shfl_sync(FULL, cu, gb + c), vb = __shfl_sync(FULL, cv, gb + c);
             const int pb = __shfl_sync(FULL, cp, gb + c);
-            const bool act = t < L;
+            const bool act = t < L && !ovf;
             bool more = act;
             while (true) {
                 // lane li: o = h[top-2-li], a = h[top-1-li];
                 // cross(o, a, b) = (a.u - o.u)(b.v - o.v) - (a.v - o.v)(b.u - o.u)
-                const bool valid = more && top - li >= 2;
                 bool popi = false;
-                if (valid) {
-                    const double2 a = entry(top - 1 - li), o = entry(top - 2 - li);
+                if (more && top - li >= 2) {
+                    const double2 a = st[top - 1 - li], o = st[top - 2 - li];
                     popi = !((a.x - o.x) * (vb - o.y) - (a.y - o.y) * (ub - o.x) > 0.0);
                 }
                 const unsigned stop = (__ballot_sync(FULL, !popi) >> gb) & 0xffu;
@@ -516,16 +524,23 @@ __global__ void __launch_bounds__(CH_WARPS * 32) k_fin_chain(ReduceIO io, Reduce
                 if (!__any_sync(FULL, more)) break;
             }
             if (act) {  // push b
-                if (li == 0) {
-                    if (top < CS) { st[top] = make_double2(ub, vb); stp[top] = pb; }
-                    else { hu[top] = ub; hv[top] = vb; hj[top] = pb; }
+                if (top < CS) {
+                    if (li == 0) { st[top] = make_double2(ub, vb); stp[top] = pb; }
+                    ++top;
+                } else {
+                    ovf = true;
                 }
-                ++top;
             }
             __syncwarp();
         }
         if (run) {  // the stack is the half hull (sorted positions)
-            for (int j = li; j < min(top, CS); j += CG) hj[j] = stp[j];
+            const int64_t h0 = 4 * row0 + (int64_t)g * m;
+            int32_t *hj = io.hj + h0;
+            if (!ovf) {
+                for (int j = li; j < top; j += CG) hj[j] = stp[j];
+            } else if (li == 0) {
+                top = half_chain_global(kuv, kpos, L, dir, hj, io.hu + h0, io.hv + h0);
+            }
             if (li == 0) io.hlen[4 * (int64_t)w + g] = top;
         }
         __syncwarp();
@@ -703,13 +718,12 @@ void launch_finalize(const ReduceIO &io, const ReduceParams &p, int sm_count, cu
     if (!configured) {
         cudaFuncSetAttribute(k_fin_sort_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
         cudaFuncSetAttribute(k_fin_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FB_BYTES);
-        cudaFuncSetAttribute(k_fin_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CH_SMEM);
         configured = true;
     }
     auto cap = [&](int64_t want, int64_t limit) { return (unsigned)(want < limit ? want : limit); };
     k_fin_sort_warp<<<cap((int64_t)sm_count * 8, (maxw + FW_WARPS - 1) / FW_WARPS), FW_WARPS * 32, wsm, s>>>(io, p);
     k_fin_sort_block<<<cap((int64_t)sm_count * 4, maxw), FB_THREADS, FB_BYTES, s>>>(io, p);
-    k_fin_chain<<<cap((int64_t)sm_count * 8, (maxw + CH_WARPS - 1) / CH_WARPS), CH_WARPS * 32, CH_SMEM, s>>>(io, p);
+    k_fin_chain<<<cap((int64_t)sm_count * 8, (maxw + CH_WARPS - 1) / CH_WARPS), CH_WARPS * 32, 0, s>>>(io, p);
     k_fin_kept<<<cap((int64_t)sm_count * 8, (maxw + FK_WARPS - 1) / FK_WARPS), FK_WARPS * 32, 0, s>>>(io, p);
     k_stats<<<(unsigned)((io.E * 32 + 255) / 256), 256, 0, s>>>(io, p);
 }

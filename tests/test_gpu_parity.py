@@ -280,3 +280,25 @@ def test_mixed_assets_per_env(P, grid64, nut, meshes):
         got = pack_patch_list(res.patches(i), 6)
         for k in ("rep", "nkept", "members", "kept_faces", "wsum", "wp", "wn", "wt", "area", "maxd"):
             assert np.array_equal(np.asarray(got[k]), np.asarray(r[k])), (i, k)
+
+
+def test_reduce_deep_hull_stacks(P):
+    """Patches whose hull chains outgrow the kernel's shared-memory stack (points
+    on convex curves: every point stays on the chain), plus a touching/non-touching
+    mix, against the oracle."""
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(11)
+    for n, cap in ((300, 6), (1500, 6), (700, 3)):
+        s = np.sort(rng.uniform(-1.0, 1.0, n))
+        pts = np.stack([s * 1e-2, (s * s) * 1e-2, np.zeros(n)], axis=1)  # a parabola: all on the lower chain
+        pts[::7, 2] += 1e-9  # a few off-plane points
+        nrm = np.tile([0.0, 0.0, 1.0], (n, 1))
+        dep = rng.uniform(-1e-4, 2e-4, n)
+        faces = np.arange(n, dtype=np.int64)
+        cs = P.ContactSet(pts, nrm, dep, faces, 0, 1)
+        rp = P.ReductionParams(per_patch_cap=cap, min_depth=-1e-4)
+        got = pack_patch_list(P.reduce_contacts(cs, rp), cap)
+        r = O.reduce_contacts(pts, nrm, dep, faces, per_patch_cap=cap, min_depth=-1e-4)
+        for k in ("rep", "nkept", "members", "kept_faces", "wsum", "wp", "wn", "wt", "area", "maxd"):
+            assert np.array_equal(np.asarray(got[k]), np.asarray(r[k])), (n, k)
