@@ -86,6 +86,20 @@ struct WarpTeam {
         return x;
     }
     __device__ bool any(bool b) const { return __any_sync(0xffffffffu, b); }
+    // first argmax, max (NaN ignored here, flagged by nan), any NaN, count: one pass
+    __device__ void stats(ArgMax &am, double &mx, int &nan, int &cnt) const {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            ArgMax b;
+            b.v = __shfl_xor_sync(0xffffffffu, am.v, o);
+            b.i = __shfl_xor_sync(0xffffffffu, am.i, o);
+            b.cnt = 0;
+            am = argmax_combine(am, b);
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            nan |= __shfl_xor_sync(0xffffffffu, nan, o);
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        }
+    }
     __device__ int excl_scan(int f, int *total) const {  // f in {0, 1}
         const unsigned b = __ballot_sync(0xffffffffu, f != 0);
         *total = __popc(b);
@@ -135,6 +149,20 @@ struct BlockTeam {
     }
     __device__ bool any(bool b) const { return __syncthreads_or(b) != 0; }
     __device__ int excl_scan(int f, int *total) const { return block_excl_scan(f, ws, total); }
+    __device__ void stats(ArgMax &am, double &mx, int &nan, int &cnt) const {
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+        WarpTeam{nullptr}.stats(am, mx, nan, cnt);
+        if (lane == 0) { this->am[wid] = am; dred[wid] = mx; ired[wid] = cnt | (nan ? (1 << 30) : 0); }
+        __syncthreads();
+        am = this->am[0]; mx = dred[0]; cnt = ired[0] & ~(1 << 30); nan = ired[0] >> 30;
+        for (int i = 1; i < nw; ++i) {
+            am = argmax_combine(am, this->am[i]);
+            mx = fmax(mx, dred[i]);
+            cnt += ired[i] & ~(1 << 30);
+            nan |= ired[i] >> 30;
+        }
+        __syncthreads();
+    }
     __device__ void best_depth(int &bk, double &bd) const {
         int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
 #pragma unroll
@@ -263,13 +291,23 @@ __device__ void sort_patch(const Team &t, const ReduceIO &io, const ReduceParams
     double mx = -INFINITY, s = 0.0;
     bool anynan = false;
     int nt = 0;
+    // member data of this rank's next member, loaded one chunk ahead (the loads are
+    // DRAM latency: the candidate rows outgrow L2)
+    double fd = 0.0, fpx = 0.0, fpy = 0.0, fpz = 0.0, fnx = 0.0, fny = 0.0, fnz = 0.0;
+    auto fetch = [&](int k) {
+        if (k < m) {
+            const int64_t i = __ldg(mem + k);
+            fd = __ldg(D + i);
+            fpx = __ldg(P + 3 * i); fpy = __ldg(P + 3 * i + 1); fpz = __ldg(P + 3 * i + 2);
+            fnx = __ldg(Nn + 3 * i); fny = __ldg(Nn + 3 * i + 1); fnz = __ldg(Nn + 3 * i + 2);
+        }
+    };
+    fetch(r);
     for (int c0 = 0; c0 < m; c0 += T) {
         const int k = c0 + r;
         if (k < m) {
-            const int64_t i = mem[k];
-            const double d = __ldg(D + i);
-            const double px = __ldg(P + 3 * i), py = __ldg(P + 3 * i + 1), pz = __ldg(P + 3 * i + 2);
-            const double nx = __ldg(Nn + 3 * i), ny = __ldg(Nn + 3 * i + 1), nz = __ldg(Nn + 3 * i + 2);
+            const double d = fd, px = fpx, py = fpy, pz = fpz, nx = fnx, ny = fny, nz = fnz;
+            fetch(k + T);
             const double wk = weight_of(d);
             wb[k] = wk;
             am = argmax_combine(am, ArgMax{d, k, 1});
@@ -295,10 +333,11 @@ __device__ void sort_patch(const Team &t, const ReduceIO &io, const ReduceParams
         }
         t.sync();
     }
-    am = t.argmax(am);
-    mx = t.max(mx);
-    anynan = t.any(anynan);
-    nt = t.isum(nt);
+    {
+        int nan = anynan ? 1 : 0;
+        t.stats(am, mx, nan, nt);
+        anynan = nan != 0;
+    }
     if (r < 9) {
         const int kind = r / 3, c = r % 3;
         double *o = (kind == 0 ? io.wp_sum : kind == 1 ? io.wn_sum : io.wt_sum) + 3 * pq;
