@@ -140,6 +140,8 @@ typedef struct cs_outputs {
     double *max_depth;          /* [E,N] */
     int32_t *member_offsets;    /* [E,N+1] CSR into members (relative to cand_base[e]) */
     int32_t *members;           /* [cap] candidate indices, patch-major, ascending within a patch */
+    uint32_t *face_work;        /* [4] last step's face-descent workload: faces descended, -, faces moved
+                                 * by the first iteration, faces still moving after it (diagnostics) */
 } cs_outputs;
 
 typedef struct cs_plan cs_plan;

@@ -37,7 +37,7 @@ class OutputsC(ctypes.Structure):
         ("cand_point", _vp), ("cand_normal", _vp), ("cand_depth", _vp), ("cand_face", _vp),
         ("patch_normal", _vp), ("patch_nkept", _vp), ("kept_cand", _vp), ("kept_point", _vp), ("kept_normal", _vp),
         ("kept_depth", _vp), ("kept_face", _vp), ("w_sum", _vp), ("wp_sum", _vp), ("wn_sum", _vp), ("wt_sum", _vp),
-        ("area", _vp), ("max_depth", _vp), ("member_offsets", _vp), ("members", _vp),
+        ("area", _vp), ("max_depth", _vp), ("member_offsets", _vp), ("members", _vp), ("face_work", _vp),
     ]
 
 

@@ -100,6 +100,8 @@ class Plan:
         self.cand_normal = v("cand_normal", (cap, 3), "f8")
         self.cand_depth = v("cand_depth", (cap,), "f8")
         self.cand_face = v("cand_face", (cap,), "i4")
+        if o.face_work:
+            self.face_work = v("face_work", (4,), "i4")  # diagnostics of the last step's descent
         if stages & _native.CS_STAGE_REDUCE:
             self.n_patch = v("n_patch", (E,), "i4")
             self.n_kept = v("n_kept", (E,), "i4")

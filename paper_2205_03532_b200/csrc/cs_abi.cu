@@ -539,7 +539,10 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
     if (!r) r = P->alloc(&P->st.chunk_off, bmap.size());
     if (!r) r = P->alloc(&P->st.chunk_found, bmap.size());
     if (!r) r = P->alloc(&P->st.work, (size_t)P->total_cap);
-    if (!r) r = P->alloc(&P->st.work_count, 2);
+    if (!r) r = P->alloc(&P->st.work_count, 4);
+    if (!r) r = P->alloc(&P->st.alpha, (size_t)P->total_cap);
+    if (!r) r = P->alloc(&P->st.acc, (size_t)P->total_cap);
+    if (!r) r = P->alloc(&P->st.slow, (size_t)P->total_cap);
     if (!r) r = P->alloc(&P->chunk_first, chunk_first.size());
     if (!r) r = P->alloc(&P->st.point, 3 * (size_t)P->total_cap);
     if (!r) r = P->alloc(&P->st.phi, (size_t)P->total_cap);
@@ -550,6 +553,7 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
     }
     if (r) { delete P; return r; }
     P->nblocks = (int64_t)bmap.size();
+    P->out.face_work = P->st.work_count;
     cudaError_t ce = cudaMemcpy(P->env_sdf, sdf_handles, sizeof(int32_t) * (size_t)n_envs, cudaMemcpyHostToDevice);
     if (ce == cudaSuccess) ce = cudaMemcpy(P->env_mesh, mesh_handles, sizeof(int32_t) * (size_t)n_envs, cudaMemcpyHostToDevice);
     if (ce == cudaSuccess) ce = cudaMemcpy(P->block_map, bmap.data(), sizeof(int2) * bmap.size(), cudaMemcpyHostToDevice);
@@ -627,7 +631,7 @@ int cs_collide(cs_plan *P, const double *sdf_pose, const double *mesh_pose, int3
                      P->sample_counter, ug, s);
     CS_LAUNCHED();
     mark(2);
-    launch_face_pgd(P->pgd_grid, P->block_map, P->xf, d_sdfs, d_meshes, P->st,
+    launch_pgd_wave(g_sms > 0 ? g_sms : 148, P->block_map, P->xf, d_sdfs, d_meshes, P->st,
                     P->sample_counter ? P->sample_counter + 1 : nullptr, ug, s);
     CS_LAUNCHED();
     mark(3);

@@ -34,7 +34,7 @@ __global__ void k_env_xf(int64_t E, const int32_t *__restrict__ env_sdf, const i
                          EnvXf *__restrict__ xf, int32_t *__restrict__ env_status,
                          double *__restrict__ env_min_depth, unsigned *__restrict__ work_count) {
     int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (e == 0 && work_count) { work_count[0] = 0; work_count[1] = 0; }
+    if (e == 0 && work_count) { work_count[0] = 0; work_count[1] = 0; work_count[2] = 0; work_count[3] = 0; }
     if (e >= E) return;
     double Rs[9], Rm[9], ts[3], tm[3];
     int ok = 1;
@@ -205,10 +205,21 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int2 
     __syncthreads();
     if (survive) {
         FaceWork *w = st.work + sbase + pos;
-        w->row = cand_base[e] + f0 + pos;
+        const int64_t row = cand_base[e] + f0 + pos;
+        w->row = row;
         w->blk = (int32_t)blockIdx.x;
         w->face = (int32_t)f | (which << 30);
         w->phi[0] = pa; w->phi[1] = pb; w->phi[2] = pc; w->phi[3] = ps;
+        // the descent's start (contacts/_kernels.py:40-52) -> the staging row
+        const int l = which == 1 ? la : which == 2 ? lb : lc;
+        if (which == 0) {
+            st.point[3 * row + 0] = (vx[la] + vx[lb] + vx[lc]) / 3.0;
+            st.point[3 * row + 1] = (vy[la] + vy[lb] + vy[lc]) / 3.0;
+            st.point[3 * row + 2] = (vz[la] + vz[lb] + vz[lc]) / 3.0;
+        } else {
+            st.point[3 * row + 0] = vx[l]; st.point[3 * row + 1] = vy[l]; st.point[3 * row + 2] = vz[l];
+        }
+        st.phi[row] = ps;
     }
 }
 
@@ -369,6 +380,202 @@ __global__ void __launch_bounds__(PGD_BLOCK, PGD_MINB) k_face_pgd(const int2 *__
     }
 }
 
+// ---------------------------------------------------------------- the descent as a wavefront
+//
+// contacts/_kernels.py:44-87 for every surviving face, as a sequence of uniform
+// kernels over lists (the state -- point, phi, gradient, step -- lives in the face's
+// staging row):
+//   k_pgd_grad(stage 0)  gradient at the start point, every face
+//   k_pgd_first          iteration 0 after its gradient: normalise, up to four
+//                        backtracking projections; faces that do not move (or
+//                        have a vanishing gradient) are done; moved faces go to
+//                        the accepted list, flagged final when they moved less than
+//                        the tolerance
+//   k_pgd_grad(stage 1)  gradient at the moved point, accepted faces: the final
+//                        gradient of the final ones, iteration 1's of the others
+//   k_pgd_rest           the rest of the descent for the faces still moving (about
+//                        1%), one thread each
+// Same operations in the same order as the sequential loop; only the schedule
+// differs (uniform work per kernel instead of one divergent state machine).
+
+constexpr unsigned ACC_FINAL = 0x80000000u;  // accepted-list flag: the move ended the descent
+
+__device__ __forceinline__ void finish_face(const Staging &st, int64_t row, int blk, int face, double phi, double cd) {
+    const bool found = phi <= cd;  // contacts/_kernels.py:87
+    if (found) atomicAdd(st.chunk_found + blk, 1);
+    st.face[row] = found ? face : -1;
+}
+
+template <bool UNIFORM>
+__device__ __forceinline__ const PlanGrid &grid_of(const PlanGrid &gu, const SdfDesc *sdfs, const EnvXf *xf, int e) {
+    return UNIFORM ? gu : sdfs[xf[e].sdf].gp;
+}
+
+template <bool COUNT, bool UNIFORM>
+__global__ void __launch_bounds__(256, GRAD_MINB) k_pgd_grad(const int2 *__restrict__ block_map, const EnvXf *__restrict__ xf,
+                                                  const SdfDesc *__restrict__ sdfs, Staging st, int stage,
+                                                  unsigned long long *__restrict__ counter, const PlanGrid gu) {
+    const unsigned n = stage == 0 ? st.work_count[0] : st.work_count[2];
+    unsigned long long ns = 0;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        unsigned idx = i, flag = 0;
+        if (stage == 1) { const unsigned a = st.acc[i]; idx = a & ~ACC_FINAL; flag = a & ACC_FINAL; }
+        const FaceWork *w = st.work + idx;
+        const int64_t row = w->row;
+        const int blk = w->blk;
+        const int e = __ldg(&block_map[blk].x);
+        const PlanGrid &g = grid_of<UNIFORM>(gu, sdfs, xf, e);
+        double gx, gy, gz;
+        gradient(g, st.point[3 * row], st.point[3 * row + 1], st.point[3 * row + 2], gx, gy, gz);
+        if (COUNT) ns += 6;
+        st.grad[3 * row] = gx; st.grad[3 * row + 1] = gy; st.grad[3 * row + 2] = gz;
+        if (stage == 1) {
+            if (flag) finish_face(st, row, blk, w->face & 0x3fffffff, st.phi[row], xf[e].cd);
+            else st.slow[atomicAdd(st.work_count + 3, 1u)] = idx;
+        }
+    }
+    if (COUNT) {
+        for (int o = 16; o; o >>= 1) ns += __shfl_xor_sync(0xffffffffu, ns, o);
+        if ((threadIdx.x & 31) == 0 && ns) atomicAdd(counter, ns);
+    }
+}
+
+// The face's corners in the grid frame (generation.py:70-72), its vertex phis and start.
+struct FaceGeom {
+    double ax, ay, az, bx, by, bz, cx, cy, cz;
+};
+
+__device__ __forceinline__ FaceGeom face_geom(const EnvXf &X, const MeshDesc *meshes, int face) {
+    const MeshDesc &M = meshes[X.mesh];
+    const int4 tri = __ldg(M.tris + face);
+    const double3 a = to_grid(X, ld_vert(M.verts + tri.x));
+    const double3 b = to_grid(X, ld_vert(M.verts + tri.y));
+    const double3 c = to_grid(X, ld_vert(M.verts + tri.z));
+    return FaceGeom{a.x, a.y, a.z, b.x, b.y, b.z, c.x, c.y, c.z};
+}
+
+// One backtracking search (contacts/_kernels.py:64-75) from (p, phi) along -g/|g|.
+// Returns true on an accepted move (p, phi, alpha updated, moved set).
+template <bool COUNT, class G>
+__device__ __forceinline__ bool backtrack(const G &g, const FaceGeom &f, const double *vphi, double gx, double gy,
+                                          double gz, double &px, double &py, double &pz, double &phi, double &alpha,
+                                          double &moved, unsigned long long &ns) {
+    const double gnorm = sqrt(gx * gx + gy * gy + gz * gz);
+    // g / gnorm, correctly rounded: one reciprocal for the three (div_rn proves each
+    // quotient or falls back to the IEEE division)
+    const double rg = 1.0 / gnorm;
+    const double ux = div_rn(gx, gnorm, rg), uy = div_rn(gy, gnorm, rg), uz = div_rn(gz, gnorm, rg);
+    for (int bt = 0; bt < 4; ++bt) {
+        double qx, qy, qz;
+        closest_point(f.ax, f.ay, f.az, f.bx, f.by, f.bz, f.cx, f.cy, f.cz, px - alpha * ux, py - alpha * uy,
+                      pz - alpha * uz, qx, qy, qz);
+        // the projection often is the current point or a corner itself: identical
+        // inputs, so the sample's value is already known
+        double phi_new;
+        if (same3(qx, qy, qz, px, py, pz)) phi_new = phi;
+        else if (same3(qx, qy, qz, f.ax, f.ay, f.az)) phi_new = vphi[0];
+        else if (same3(qx, qy, qz, f.bx, f.by, f.bz)) phi_new = vphi[1];
+        else if (same3(qx, qy, qz, f.cx, f.cy, f.cz)) phi_new = vphi[2];
+        else {
+            phi_new = sample(g, qx, qy, qz);
+            if (COUNT) ns += 1;
+        }
+        if (phi_new < phi) {
+            moved = sqrt((qx - px) * (qx - px) + (qy - py) * (qy - py) + (qz - pz) * (qz - pz));
+            px = qx; py = qy; pz = qz;
+            phi = phi_new;
+            alpha = dmin(alpha * 1.5, 4.0 * g.voxel);
+            return true;
+        }
+        alpha *= 0.5;
+    }
+    moved = 0.0;
+    return false;
+}
+
+template <bool COUNT, bool UNIFORM>
+__global__ void __launch_bounds__(256, FIRST_MINB) k_pgd_first(const int2 *__restrict__ block_map, const EnvXf *__restrict__ xf,
+                                                   const SdfDesc *__restrict__ sdfs, const MeshDesc *__restrict__ meshes,
+                                                   Staging st, unsigned long long *__restrict__ counter, const PlanGrid gu) {
+    const unsigned n = st.work_count[0];
+    unsigned long long ns = 0;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const FaceWork *w = st.work + i;
+        const int64_t row = w->row;
+        const int blk = w->blk;
+        const int face = w->face & 0x3fffffff;
+        const int e = __ldg(&block_map[blk].x);
+        const EnvXf &X = xf[e];
+        const double gx = st.grad[3 * row], gy = st.grad[3 * row + 1], gz = st.grad[3 * row + 2];
+        double phi = w->phi[3];
+        if (sqrt(gx * gx + gy * gy + gz * gz) < 1e-12) {  // contacts/_kernels.py:61-62: break
+            finish_face(st, row, blk, face, phi, X.cd);
+            continue;
+        }
+        const PlanGrid &g = grid_of<UNIFORM>(gu, sdfs, xf, e);
+        const FaceGeom f = face_geom(X, meshes, face);
+        const double vphi[3] = {w->phi[0], w->phi[1], w->phi[2]};
+        double px = st.point[3 * row], py = st.point[3 * row + 1], pz = st.point[3 * row + 2];
+        double alpha = g.voxel, moved;
+        if (!backtrack<COUNT>(g, f, vphi, gx, gy, gz, px, py, pz, phi, alpha, moved, ns)) {
+            finish_face(st, row, blk, face, phi, X.cd);  // no move: this gradient is the final one
+            continue;
+        }
+        st.point[3 * row] = px; st.point[3 * row + 1] = py; st.point[3 * row + 2] = pz;
+        st.phi[row] = phi;
+        st.alpha[row] = alpha;
+        // moved < tol ends the descent (its final gradient is at the new point); 1 < max_iters
+        st.acc[atomicAdd(st.work_count + 2, 1u)] = i | (moved < X.tol ? ACC_FINAL : 0u);
+    }
+    if (COUNT) {
+        for (int o = 16; o; o >>= 1) ns += __shfl_xor_sync(0xffffffffu, ns, o);
+        if ((threadIdx.x & 31) == 0 && ns) atomicAdd(counter, ns);
+    }
+}
+
+// Iterations 1.. of the faces still moving (the gradient at their point is in the row).
+template <bool COUNT, bool UNIFORM>
+__global__ void __launch_bounds__(128, REST_MINB) k_pgd_rest(const int2 *__restrict__ block_map, const EnvXf *__restrict__ xf,
+                                                  const SdfDesc *__restrict__ sdfs, const MeshDesc *__restrict__ meshes,
+                                                  Staging st, unsigned long long *__restrict__ counter, const PlanGrid gu) {
+    const unsigned n = st.work_count[3];
+    unsigned long long ns = 0;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const unsigned idx = st.slow[i];
+        const FaceWork *w = st.work + idx;
+        const int64_t row = w->row;
+        const int blk = w->blk;
+        const int face = w->face & 0x3fffffff;
+        const int e = __ldg(&block_map[blk].x);
+        const EnvXf &X = xf[e];
+        const PlanGrid &g = grid_of<UNIFORM>(gu, sdfs, xf, e);
+        const FaceGeom f = face_geom(X, meshes, face);
+        const double vphi[3] = {w->phi[0], w->phi[1], w->phi[2]};
+        double px = st.point[3 * row], py = st.point[3 * row + 1], pz = st.point[3 * row + 2];
+        double phi = st.phi[row], alpha = st.alpha[row];
+        double gx = st.grad[3 * row], gy = st.grad[3 * row + 1], gz = st.grad[3 * row + 2];
+        for (int it = 1; it < MAX_MINIMIZE_ITERS; ++it) {
+            // (gx, gy, gz) is the gradient at p for this iteration
+            if (sqrt(gx * gx + gy * gy + gz * gz) < 1e-12) break;
+            double moved;
+            const bool acc = backtrack<COUNT>(g, f, vphi, gx, gy, gz, px, py, pz, phi, alpha, moved, ns);
+            if (acc) {  // the gradient at the new point: the next iteration's, or the final one
+                gradient(g, px, py, pz, gx, gy, gz);
+                if (COUNT) ns += 6;
+            }
+            if (moved < X.tol) break;
+        }
+        st.point[3 * row] = px; st.point[3 * row + 1] = py; st.point[3 * row + 2] = pz;
+        st.phi[row] = phi;
+        st.grad[3 * row] = gx; st.grad[3 * row + 1] = gy; st.grad[3 * row + 2] = gz;
+        finish_face(st, row, blk, face, phi, X.cd);
+    }
+    if (COUNT) {
+        for (int o = 16; o; o >>= 1) ns += __shfl_xor_sync(0xffffffffu, ns, o);
+        if ((threadIdx.x & 31) == 0 && ns) atomicAdd(counter, ns);
+    }
+}
+
 // Stitch the per-chunk survivor rows into the env's candidate list (found faces
 // in ascending face order) and apply the world-frame epilogue (generation.py:98-114).
 // One CTA per env: chunk offsets by a block scan of the found counts, then one
@@ -507,6 +714,25 @@ void launch_face_pgd(int grid, const int2 *block_map, const EnvXf *xf, const Sdf
         if (counter) k_face_pgd<true, false><<<grid, PGD_BLOCK, 0, s>>>(block_map, xf, sdfs, meshes, st, counter, gu);
         else k_face_pgd<false, false><<<grid, PGD_BLOCK, 0, s>>>(block_map, xf, sdfs, meshes, st, nullptr, gu);
     }
+}
+
+void launch_pgd_wave(int sm_count, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs, const MeshDesc *meshes,
+                     const Staging &st, unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s) {
+    const PlanGrid gu = uniform ? *uniform : PlanGrid{};
+    const unsigned g = (unsigned)sm_count * 8, gr = (unsigned)sm_count * REST_GRID;
+#define CS_WAVE(C, U)                                                                                 \
+    do {                                                                                              \
+        k_pgd_grad<C, U><<<g, 256, 0, s>>>(block_map, xf, sdfs, st, 0, counter, gu);                 \
+        k_pgd_first<C, U><<<g, 256, 0, s>>>(block_map, xf, sdfs, meshes, st, counter, gu);           \
+        k_pgd_grad<C, U><<<g, 256, 0, s>>>(block_map, xf, sdfs, st, 1, counter, gu);                 \
+        k_pgd_rest<C, U><<<gr, 128, 0, s>>>(block_map, xf, sdfs, meshes, st, counter, gu);           \
+    } while (0)
+    if (uniform) {
+        if (counter) CS_WAVE(true, true); else CS_WAVE(false, true);
+    } else {
+        if (counter) CS_WAVE(true, false); else CS_WAVE(false, false);
+    }
+#undef CS_WAVE
 }
 
 void launch_compact(int64_t E, const EnvXf *xf, const int64_t *cand_base, const int2 *block_map,

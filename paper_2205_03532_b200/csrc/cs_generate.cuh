@@ -7,6 +7,19 @@ constexpr int PGD_BLOCK = 128;
 #ifndef PGD_MINB
 #define PGD_MINB 5  // min resident k_face_pgd CTAs per SM: a 102-register budget (measured best)
 #endif
+// register budgets / grids of the descent wavefront (measured best, round 1)
+#ifndef FIRST_MINB
+#define FIRST_MINB 3
+#endif
+#ifndef GRAD_MINB
+#define GRAD_MINB 4
+#endif
+#ifndef REST_MINB
+#define REST_MINB 4
+#endif
+#ifndef REST_GRID
+#define REST_GRID 8
+#endif
 #ifndef PREP_MINB
 #define PREP_MINB 4  // 64 registers
 #endif
@@ -34,7 +47,10 @@ struct Staging {
     int32_t *chunk_found;  // [nblocks] found faces per block
     int32_t *chunk_off;    // [nblocks] candidate offset of the block's first found face
     FaceWork *work;        // [capacity] survivors, dense
-    unsigned *work_count;  // [0] survivors listed, [1] survivors claimed by k_face_pgd
+    double *alpha;         // [row] descent step of a moved face
+    uint32_t *acc;         // [capacity] work indices moved by k_pgd_first (| ACC_FINAL)
+    uint32_t *slow;        // [capacity] work indices still moving after iteration 0
+    unsigned *work_count;  // [0] survivors, [1] (k_face_pgd claims), [2] accepted, [3] slow
 };
 
 // Candidate arrays (row = cand_base[e] + candidate index).
@@ -53,7 +69,9 @@ void launch_face_prep(int64_t nblocks, const int2 *block_map, const EnvXf *xf, c
                       unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s);
 void launch_face_pgd(int grid, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs, const MeshDesc *meshes,
                      const Staging &st, unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s);
-int face_pgd_grid(int sm_count);  // resident CTAs of k_face_pgd over the device
+int face_pgd_grid(int sm_count);
+void launch_pgd_wave(int sm_count, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs, const MeshDesc *meshes,
+                     const Staging &st, unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s);  // resident CTAs of k_face_pgd over the device
 size_t face_prep_smem(int max_chunk_verts);
 void launch_compact(int64_t E, const EnvXf *xf, const int64_t *cand_base, const int2 *block_map,
                     const int32_t *chunk_first, const Staging &st, const Candidates &cs, int32_t *n_cand,

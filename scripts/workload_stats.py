@@ -38,6 +38,8 @@ def main():
         sel = sizes > lim
         print(f"  > {lim:5d}: {sel.sum():6d} patches ({100 * sel.mean():5.1f}%), {sizes[sel].sum():8d} members "
               f"({100 * sizes[sel].sum() / sizes.sum():5.1f}%)")
+    fw = plan.face_work.cpu().numpy()
+    print(f"face descent: {fw[0]} faces ({fw[0] / args.envs:.0f}/env), {fw[2]} moved by iteration 0, {fw[3]} still moving")
     nk = plan.patch_nkept.cpu().numpy()
     print("kept per env mean", nk.sum(1).mean())
 
