@@ -205,21 +205,10 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int2 
     __syncthreads();
     if (survive) {
         FaceWork *w = st.work + sbase + pos;
-        const int64_t row = cand_base[e] + f0 + pos;
-        w->row = row;
+        w->row = cand_base[e] + f0 + pos;
         w->blk = (int32_t)blockIdx.x;
         w->face = (int32_t)f | (which << 30);
         w->phi[0] = pa; w->phi[1] = pb; w->phi[2] = pc; w->phi[3] = ps;
-        // the descent's start (contacts/_kernels.py:40-52) -> the staging row
-        const int l = which == 1 ? la : which == 2 ? lb : lc;
-        if (which == 0) {
-            st.point[3 * row + 0] = (vx[la] + vx[lb] + vx[lc]) / 3.0;
-            st.point[3 * row + 1] = (vy[la] + vy[lb] + vy[lc]) / 3.0;
-            st.point[3 * row + 2] = (vz[la] + vz[lb] + vz[lc]) / 3.0;
-        } else {
-            st.point[3 * row + 0] = vx[l]; st.point[3 * row + 1] = vy[l]; st.point[3 * row + 2] = vz[l];
-        }
-        st.phi[row] = ps;
     }
 }
 
@@ -411,35 +400,6 @@ __device__ __forceinline__ const PlanGrid &grid_of(const PlanGrid &gu, const Sdf
     return UNIFORM ? gu : sdfs[xf[e].sdf].gp;
 }
 
-template <bool COUNT, bool UNIFORM>
-__global__ void __launch_bounds__(256, GRAD_MINB) k_pgd_grad(const int2 *__restrict__ block_map, const EnvXf *__restrict__ xf,
-                                                  const SdfDesc *__restrict__ sdfs, Staging st, int stage,
-                                                  unsigned long long *__restrict__ counter, const PlanGrid gu) {
-    const unsigned n = stage == 0 ? st.work_count[0] : st.work_count[2];
-    unsigned long long ns = 0;
-    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        unsigned idx = i, flag = 0;
-        if (stage == 1) { const unsigned a = st.acc[i]; idx = a & ~ACC_FINAL; flag = a & ACC_FINAL; }
-        const FaceWork *w = st.work + idx;
-        const int64_t row = w->row;
-        const int blk = w->blk;
-        const int e = __ldg(&block_map[blk].x);
-        const PlanGrid &g = grid_of<UNIFORM>(gu, sdfs, xf, e);
-        double gx, gy, gz;
-        gradient(g, st.point[3 * row], st.point[3 * row + 1], st.point[3 * row + 2], gx, gy, gz);
-        if (COUNT) ns += 6;
-        st.grad[3 * row] = gx; st.grad[3 * row + 1] = gy; st.grad[3 * row + 2] = gz;
-        if (stage == 1) {
-            if (flag) finish_face(st, row, blk, w->face & 0x3fffffff, st.phi[row], xf[e].cd);
-            else st.slow[atomicAdd(st.work_count + 3, 1u)] = idx;
-        }
-    }
-    if (COUNT) {
-        for (int o = 16; o; o >>= 1) ns += __shfl_xor_sync(0xffffffffu, ns, o);
-        if ((threadIdx.x & 31) == 0 && ns) atomicAdd(counter, ns);
-    }
-}
-
 // The face's corners in the grid frame (generation.py:70-72), its vertex phis and start.
 struct FaceGeom {
     double ax, ay, az, bx, by, bz, cx, cy, cz;
@@ -452,6 +412,55 @@ __device__ __forceinline__ FaceGeom face_geom(const EnvXf &X, const MeshDesc *me
     const double3 b = to_grid(X, ld_vert(M.verts + tri.y));
     const double3 c = to_grid(X, ld_vert(M.verts + tri.z));
     return FaceGeom{a.x, a.y, a.z, b.x, b.y, b.z, c.x, c.y, c.z};
+}
+
+// The descent's start (contacts/_kernels.py:40-52): the centroid, or the corner k_face_prep chose.
+__device__ __forceinline__ void face_start(const FaceGeom &f, int which, double &px, double &py, double &pz) {
+    if (which == 0) {
+        px = (f.ax + f.bx + f.cx) / 3.0; py = (f.ay + f.by + f.cy) / 3.0; pz = (f.az + f.bz + f.cz) / 3.0;
+    } else if (which == 1) {
+        px = f.ax; py = f.ay; pz = f.az;
+    } else if (which == 2) {
+        px = f.bx; py = f.by; pz = f.bz;
+    } else {
+        px = f.cx; py = f.cy; pz = f.cz;
+    }
+}
+
+template <bool COUNT, bool UNIFORM>
+__global__ void __launch_bounds__(256, GRAD_MINB) k_pgd_grad(const int2 *__restrict__ block_map, const EnvXf *__restrict__ xf,
+                                                  const SdfDesc *__restrict__ sdfs, const MeshDesc *__restrict__ meshes,
+                                                  Staging st, int stage,
+                                                  unsigned long long *__restrict__ counter, const PlanGrid gu) {
+    const unsigned n = stage == 0 ? st.work_count[0] : st.work_count[2];
+    unsigned long long ns = 0;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        unsigned idx = i, flag = 0;
+        if (stage == 1) { const unsigned a = st.acc[i]; idx = a & ~ACC_FINAL; flag = a & ACC_FINAL; }
+        const FaceWork *w = st.work + idx;
+        const int64_t row = w->row;
+        const int blk = w->blk;
+        const int e = __ldg(&block_map[blk].x);
+        const PlanGrid &g = grid_of<UNIFORM>(gu, sdfs, xf, e);
+        double px, py, pz;
+        if (stage == 0) {  // the start point, from the corners (not staged: recomputing is cheaper than the traffic)
+            face_start(face_geom(xf[e], meshes, w->face & 0x3fffffff), (int)((unsigned)w->face >> 30), px, py, pz);
+        } else {
+            px = st.point[3 * row]; py = st.point[3 * row + 1]; pz = st.point[3 * row + 2];
+        }
+        double gx, gy, gz;
+        gradient(g, px, py, pz, gx, gy, gz);
+        if (COUNT) ns += 6;
+        st.grad[3 * row] = gx; st.grad[3 * row + 1] = gy; st.grad[3 * row + 2] = gz;
+        if (stage == 1) {
+            if (flag) finish_face(st, row, blk, w->face & 0x3fffffff, st.phi[row], xf[e].cd);
+            else st.slow[atomicAdd(st.work_count + 3, 1u)] = idx;
+        }
+    }
+    if (COUNT) {
+        for (int o = 16; o; o >>= 1) ns += __shfl_xor_sync(0xffffffffu, ns, o);
+        if ((threadIdx.x & 31) == 0 && ns) atomicAdd(counter, ns);
+    }
 }
 
 // One backtracking search (contacts/_kernels.py:64-75) from (p, phi) along -g/|g|.
@@ -508,17 +517,24 @@ __global__ void __launch_bounds__(256, FIRST_MINB) k_pgd_first(const int2 *__res
         const EnvXf &X = xf[e];
         const double gx = st.grad[3 * row], gy = st.grad[3 * row + 1], gz = st.grad[3 * row + 2];
         double phi = w->phi[3];
-        if (sqrt(gx * gx + gy * gy + gz * gz) < 1e-12) {  // contacts/_kernels.py:61-62: break
+        const FaceGeom f = face_geom(X, meshes, face);
+        double px, py, pz;
+        face_start(f, (int)((unsigned)w->face >> 30), px, py, pz);
+        // a face that does not move ends here with this gradient: its point and phi go to
+        // the staging row only when it is found (the only rows k_compact reads)
+        auto done_here = [&]() {
+            if (phi <= X.cd) { st.point[3 * row] = px; st.point[3 * row + 1] = py; st.point[3 * row + 2] = pz; st.phi[row] = phi; }
             finish_face(st, row, blk, face, phi, X.cd);
+        };
+        if (sqrt(gx * gx + gy * gy + gz * gz) < 1e-12) {  // contacts/_kernels.py:61-62: break
+            done_here();
             continue;
         }
         const PlanGrid &g = grid_of<UNIFORM>(gu, sdfs, xf, e);
-        const FaceGeom f = face_geom(X, meshes, face);
         const double vphi[3] = {w->phi[0], w->phi[1], w->phi[2]};
-        double px = st.point[3 * row], py = st.point[3 * row + 1], pz = st.point[3 * row + 2];
         double alpha = g.voxel, moved;
         if (!backtrack<COUNT>(g, f, vphi, gx, gy, gz, px, py, pz, phi, alpha, moved, ns)) {
-            finish_face(st, row, blk, face, phi, X.cd);  // no move: this gradient is the final one
+            done_here();  // no move: this gradient is the final one
             continue;
         }
         st.point[3 * row] = px; st.point[3 * row + 1] = py; st.point[3 * row + 2] = pz;
@@ -722,9 +738,9 @@ void launch_pgd_wave(int sm_count, const int2 *block_map, const EnvXf *xf, const
     const unsigned g = (unsigned)sm_count * 8, gr = (unsigned)sm_count * REST_GRID;
 #define CS_WAVE(C, U)                                                                                 \
     do {                                                                                              \
-        k_pgd_grad<C, U><<<g, 256, 0, s>>>(block_map, xf, sdfs, st, 0, counter, gu);                 \
+        k_pgd_grad<C, U><<<g, 256, 0, s>>>(block_map, xf, sdfs, meshes, st, 0, counter, gu);         \
         k_pgd_first<C, U><<<g, 256, 0, s>>>(block_map, xf, sdfs, meshes, st, counter, gu);           \
-        k_pgd_grad<C, U><<<g, 256, 0, s>>>(block_map, xf, sdfs, st, 1, counter, gu);                 \
+        k_pgd_grad<C, U><<<g, 256, 0, s>>>(block_map, xf, sdfs, meshes, st, 1, counter, gu);         \
         k_pgd_rest<C, U><<<gr, 128, 0, s>>>(block_map, xf, sdfs, meshes, st, counter, gu);           \
     } while (0)
     if (uniform) {
