@@ -34,7 +34,9 @@ sys.path.insert(0, ROOT)
 METRIC = "SDF contact queries/s & collide-step ms, 1024 nut-bolt envs, 1/2/4/8 B200"
 UNIT = "queries/s"
 PAPER_QPS = 1024 * 17798 / 11e-3  # PAPER.md:227,584 (A5000, whole contact-handling step), derived
-LAUNCHES_PER_STEP = 8  # k_env_xf, k_face_prep, k_face_pgd, k_compact, k_reduce, k_patch_off, k_finalize, k_stats
+# k_env_xf, k_face_prep, k_pgd_grad x2, k_pgd_first, k_pgd_rest, k_compact, k_reduce, k_patch_off,
+# k_fin_sort_warp, k_fin_sort_block, k_fin_chain, k_fin_kept, k_stats
+LAUNCHES_PER_STEP = 14
 
 
 def parse():
@@ -109,9 +111,9 @@ def measured_peaks() -> dict:
 
 
 def ncu_traffic():
-    """dram bytes per k_face_pgd launch from the committed ncu capture, if present."""
+    """dram bytes per k_face_prep launch from the committed ncu capture, if present."""
     try:
-        with open(os.path.join(ROOT, "profiles", "k_face_pgd_ncu.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "k_face_prep_ncu.json")) as fh:
             return json.load(fh).get("dram_bytes_per_launch")
     except (OSError, ValueError):
         return None
@@ -272,13 +274,16 @@ def main():
     stats = gather_env_stats(plan.stats.clone(), E * world)
     plan.enable_timing(0)
 
-    # roofline of the dominant kernel (k_face_pgd): SURVEY §8(d) bytes / live event time
-    pgd_ms = float(phases[:, plan.PHASES.index("face_pgd")].mean())
-    alg_bytes = 32.0 * samples_pgd
+    # roofline of the dominant kernel (k_face_prep, the largest single launch of the
+    # step): SURVEY §8(d) bytes / its live event time. Per face query 48 B (3 corners
+    # f32 xyz + 3 indices) + 32 B per trilinear sample (8 float32 corners), samples
+    # counted exactly by the counting build.
+    prep_ms = float(phases[:, plan.PHASES.index("face_prep")].mean())
+    alg_bytes = 48.0 * E * F + 32.0 * samples_prep
     peaks = measured_peaks()
-    achieved = alg_bytes / (pgd_ms * 1e-3) / 1e9
-    faces_ms = pgd_ms + float(phases[:, plan.PHASES.index("face_prep")].mean())
-    faces_bytes = 48.0 * E * F + 32.0 * (samples_prep + samples_pgd)
+    achieved = alg_bytes / (prep_ms * 1e-3) / 1e9
+    pgd_ms = float(phases[:, plan.PHASES.index("face_pgd")].mean())
+    pgd_bytes = 32.0 * samples_pgd
     mean_phase = {n: float(phases[:, i].mean()) for i, n in enumerate(plan.PHASES)}
 
     # end-to-end through the public API with host buffers (H2D poses, D2H stats)
@@ -318,16 +323,16 @@ def main():
             "e2e": e2e,
             "gpu_launches": LAUNCHES_PER_STEP * args.steps,
             "phase_ms": mean_phase,
-            "roofline": {"kernel": "k_face_pgd", "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
+            "roofline": {"kernel": "k_face_prep", "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                          "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic(),
-                         "peak_source": peaks["source"],
-                         "alg_bytes_per_launch": alg_bytes, "samples_per_launch": samples_pgd,
-                         "basis": "32 B per trilinear sample (8 float32 corners, SURVEY §8(d)); samples counted "
-                                  "exactly by the counting build of k_face_pgd",
-                         "faces_phase": {"kernels": "k_face_prep + k_face_pgd", "ms": faces_ms,
-                                         "alg_bytes": faces_bytes, "samples": samples_prep + samples_pgd,
-                                         "achieved_gbs": faces_bytes / (faces_ms * 1e-3) / 1e9,
-                                         "basis": "48 B per face query + 32 B per trilinear sample"}},
+                         "peak_source": peaks["source"], "alg_bytes_per_launch": alg_bytes,
+                         "samples_per_launch": samples_prep,
+                         "basis": "48 B per face query (E x F) + 32 B per trilinear sample (8 float32 corners, "
+                                  "SURVEY §8(d)); samples counted exactly by the counting build of k_face_prep",
+                         "pgd_phase": {"kernels": "k_pgd_grad x2 + k_pgd_first + k_pgd_rest", "ms": pgd_ms,
+                                       "alg_bytes": pgd_bytes, "samples": samples_pgd,
+                                       "achieved_gbs": pgd_bytes / (pgd_ms * 1e-3) / 1e9,
+                                       "basis": "32 B per trilinear sample"}},
             "clocks": clk,
             "stats": {"candidates_per_env": float(stats[:, 0].double().mean()),
                       "patches_per_env": float(stats[:, 1].double().mean()),
