@@ -31,9 +31,15 @@
 
 namespace cs {
 
-constexpr int FW_WARPS = 4;      // warp teams per k_fin_sort_warp CTA
-constexpr int FW_SMEM = 256;     // members per warp-path patch (all in shared memory)
-constexpr int FB_THREADS = 128;  // k_fin_sort_block
+#ifndef FW_WARPS
+#define FW_WARPS 8      // warp teams per k_fin_sort_warp CTA
+#endif
+#ifndef FW_SMEM
+#define FW_SMEM 128     // members per warp-path patch (all in shared memory)
+#endif
+#ifndef FB_THREADS
+#define FB_THREADS 128  // k_fin_sort_block
+#endif
 constexpr int CH_BUCKETS = 64;   // chain jobs bucketed by length (16 keys per bucket)
 
 __device__ __forceinline__ int job_bucket(int len) { return max(0, CH_BUCKETS - 1 - len / 16); }  // longest first
