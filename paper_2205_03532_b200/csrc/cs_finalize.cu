@@ -278,7 +278,7 @@ __device__ __forceinline__ int64_t env_of(const int32_t *patch_off, int64_t E, i
 //   * a merge-path sort by (u, v, member) (lexsort, reduction.py:211), written to
 //     the patch's rows of suv/sp (non-touching members as ~k), and the patch's
 //     chain jobs queued (long patches and short patches in separate lists).
-template <class Team>
+template <bool FOLD, class Team>
 __device__ void sort_patch(const Team &t, const ReduceIO &io, const ReduceParams &p, int w, int64_t e, int q, Keys A,
                            Keys B, double *tile) {
     const int N = p.N, K = p.K;
@@ -314,41 +314,45 @@ __device__ void sort_patch(const Team &t, const ReduceIO &io, const ReduceParams
         if (k < m) {
             const double d = fd, px = fpx, py = fpy, pz = fpz, nx = fnx, ny = fny, nz = fnz;
             fetch(k + T);
-            const double wk = weight_of(d);
-            wb[k] = wk;
             am = argmax_combine(am, ArgMax{d, k, 1});
             anynan |= isnan(d);
             if (d > mx) mx = d;
             nt += d >= 0.0 ? 1 : 0;
-            tile[0 * T + r] = px * wk; tile[1 * T + r] = py * wk; tile[2 * T + r] = pz * wk;
-            tile[3 * T + r] = nx * wk; tile[4 * T + r] = ny * wk; tile[5 * T + r] = nz * wk;
-            tile[6 * T + r] = (py * nz - pz * ny) * wk;
-            tile[7 * T + r] = (pz * nx - px * nz) * wk;
-            tile[8 * T + r] = (px * ny - py * nx) * wk;
+            if (FOLD) {
+                const double wk = weight_of(d);
+                wb[k] = wk;
+                tile[0 * T + r] = px * wk; tile[1 * T + r] = py * wk; tile[2 * T + r] = pz * wk;
+                tile[3 * T + r] = nx * wk; tile[4 * T + r] = ny * wk; tile[5 * T + r] = nz * wk;
+                tile[6 * T + r] = (py * nz - pz * ny) * wk;
+                tile[7 * T + r] = (pz * nx - px * nz) * wk;
+                tile[8 * T + r] = (px * ny - py * nx) * wk;
+            }
             if (hull) {
                 A.u[k] = V3(px, py, pz, t1[0], t1[1], t1[2]);  // _project_2d: (n,3) @ (3,), n >= 2
                 A.v[k] = V3(px, py, pz, t2[0], t2[1], t2[2]);
                 A.k[k] = k;
             }
         }
-        t.sync();
-        if (r < 9) {
-            const int cnt = min(T, m - c0);
-            const double *row = tile + r * T;
-            for (int j = 0; j < cnt; ++j) s = (c0 + j == 0) ? row[j] : s + row[j];
+        if (FOLD) {
+            t.sync();
+            if (r < 9) {
+                const int cnt = min(T, m - c0);
+                const double *row = tile + r * T;
+                for (int j = 0; j < cnt; ++j) s = (c0 + j == 0) ? row[j] : s + row[j];
+            }
+            t.sync();
         }
-        t.sync();
     }
     {
         int nan = anynan ? 1 : 0;
         t.stats(am, mx, nan, nt);
         anynan = nan != 0;
     }
-    if (r < 9) {
+    if (FOLD && r < 9) {
         const int kind = r / 3, c = r % 3;
         double *o = (kind == 0 ? io.wp_sum : kind == 1 ? io.wn_sum : io.wt_sum) + 3 * pq;
         o[c] = s;
-    } else if (r == 9) {
+    } else if (FOLD && r == 9) {
         io.w_sum[pq] = 0.0 + pairwise([&](int k) { return wb[k]; }, 0, m);
     } else if (r == 10) {
         io.max_depth[pq] = anynan ? (double)NAN : mx;  // deps.max() propagates NaN
@@ -416,14 +420,13 @@ __global__ void __launch_bounds__(FW_WARPS * 32) k_fin_sort_warp(ReduceIO io, Re
             if ((threadIdx.x & 31) == 0) io.large_list[atomicAdd(io.large_count, 1)] = w;
             continue;
         }
-        sort_patch(t, io, p, w, e, q, A, B, tile);
+        sort_patch<true>(t, io, p, w, e, q, A, B, tile);
     }
 }
 
 // Larger patches: one CTA each; shared memory up to FB_SMEM members, global scratch rows beyond.
 __global__ void __launch_bounds__(FB_THREADS) k_fin_sort_block(ReduceIO io, ReduceParams p) {
     extern __shared__ __align__(16) unsigned char dyn[];
-    __shared__ double tile[9 * FB_THREADS];
     __shared__ ArgMax s_am[32];
     __shared__ double s_dred[32];
     __shared__ int s_ired[32];
@@ -444,7 +447,78 @@ __global__ void __launch_bounds__(FB_THREADS) k_fin_sort_block(ReduceIO io, Redu
             A = Keys{io.su + row0, io.sv + row0, io.sp + row0};
             B = Keys{io.tu + row0, io.tv + row0, io.tk + row0};
         }
-        sort_patch(t, io, p, w, e, q, A, B, tile);
+        sort_patch<false>(t, io, p, w, e, q, A, B, nullptr);
+    }
+}
+
+// The sequential sums of the larger patches (reduction.py:162-165), one warp per patch
+// (k_fin_sort_block leaves them out: 9 lanes folding while the CTA waits at a barrier
+// was a third of its time). Per chunk of 32 members the warp loads the rows (one
+// member per lane, the next chunk's loads in flight), writes the nine weighted
+// products (np.cross(pts, norms) * w etc.) to a shared tile, and lanes 0..8 fold
+// the tile in member order (numpy's axis-0 sums add row after row); the weights
+// are kept for lane 9's pairwise sum.
+constexpr int FL_WARPS = 4;
+constexpr int FL_W = 1024;  // weights per warp in shared memory (larger patches: global scratch)
+
+__global__ void __launch_bounds__(FL_WARPS * 32) k_fin_fold_large(ReduceIO io, ReduceParams p) {
+    __shared__ double s_tile[FL_WARPS][9 * 32];
+    __shared__ double s_w[FL_WARPS][FL_W];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    double *tile = s_tile[wib];
+    const int64_t E = io.E;
+    const int total = *io.large_count;
+    for (int li = blockIdx.x * FL_WARPS + wib; li < total; li += gridDim.x * FL_WARPS) {
+        const int w = io.large_list[li];
+        const int64_t e = env_of(io.patch_off, E, w);
+        const int q = w - io.patch_off[e];
+        const int64_t base = io.cand_base[e];
+        const int32_t *mo = io.member_offsets + e * (p.N + 1);
+        const int moff = mo[q], m = mo[q + 1] - moff;
+        const int32_t *mem = io.members + base + moff;
+        const double *P = io.point + 3 * base, *Nn = io.normal + 3 * base, *D = io.depth + base;
+        const int64_t pq = e * p.N + q;
+        double *wb = m <= FL_W ? s_w[wib] : io.tu + base + moff;
+        double fd = 0.0, fpx = 0.0, fpy = 0.0, fpz = 0.0, fnx = 0.0, fny = 0.0, fnz = 0.0;
+        auto fetch = [&](int k) {
+            if (k < m) {
+                const int64_t i = __ldg(mem + k);
+                fd = __ldg(D + i);
+                fpx = __ldg(P + 3 * i); fpy = __ldg(P + 3 * i + 1); fpz = __ldg(P + 3 * i + 2);
+                fnx = __ldg(Nn + 3 * i); fny = __ldg(Nn + 3 * i + 1); fnz = __ldg(Nn + 3 * i + 2);
+            }
+        };
+        fetch(lane);
+        double s = 0.0;
+        for (int c0 = 0; c0 < m; c0 += 32) {
+            const int k = c0 + lane;
+            if (k < m) {
+                const double px = fpx, py = fpy, pz = fpz, nx = fnx, ny = fny, nz = fnz;
+                const double wk = weight_of(fd);
+                fetch(k + 32);
+                wb[k] = wk;
+                tile[0 * 32 + lane] = px * wk; tile[1 * 32 + lane] = py * wk; tile[2 * 32 + lane] = pz * wk;
+                tile[3 * 32 + lane] = nx * wk; tile[4 * 32 + lane] = ny * wk; tile[5 * 32 + lane] = nz * wk;
+                tile[6 * 32 + lane] = (py * nz - pz * ny) * wk;
+                tile[7 * 32 + lane] = (pz * nx - px * nz) * wk;
+                tile[8 * 32 + lane] = (px * ny - py * nx) * wk;
+            }
+            __syncwarp();
+            if (lane < 9) {
+                const int cnt = min(32, m - c0);
+                const double *row = tile + lane * 32;
+                for (int j = 0; j < cnt; ++j) s = (c0 + j == 0) ? row[j] : s + row[j];
+            }
+            __syncwarp();
+        }
+        if (lane < 9) {
+            const int kind = lane / 3, c = lane % 3;
+            double *o = (kind == 0 ? io.wp_sum : kind == 1 ? io.wn_sum : io.wt_sum) + 3 * pq;
+            o[c] = s;
+        } else if (lane == 9) {
+            io.w_sum[pq] = 0.0 + pairwise([&](int k) { return wb[k]; }, 0, m);
+        }
+        __syncwarp();
     }
 }
 
@@ -768,6 +842,7 @@ void launch_finalize(const ReduceIO &io, const ReduceParams &p, int sm_count, cu
     auto cap = [&](int64_t want, int64_t limit) { return (unsigned)(want < limit ? want : limit); };
     k_fin_sort_warp<<<cap((int64_t)sm_count * 8, (maxw + FW_WARPS - 1) / FW_WARPS), FW_WARPS * 32, wsm, s>>>(io, p);
     k_fin_sort_block<<<cap((int64_t)sm_count * 4, maxw), FB_THREADS, FB_BYTES, s>>>(io, p);
+    k_fin_fold_large<<<cap((int64_t)sm_count * 4, (maxw + FL_WARPS - 1) / FL_WARPS), FL_WARPS * 32, 0, s>>>(io, p);
     k_fin_chain<<<cap((int64_t)sm_count * 8, (maxw + CH_WARPS - 1) / CH_WARPS), CH_WARPS * 32, 0, s>>>(io, p);
     k_fin_kept<<<cap((int64_t)sm_count * 8, (maxw + FK_WARPS - 1) / FK_WARPS), FK_WARPS * 32, 0, s>>>(io, p);
     k_stats<<<(unsigned)((io.E * 32 + 255) / 256), 256, 0, s>>>(io, p);
