@@ -446,7 +446,7 @@ static int plan_buffers(cs_plan *P, const std::vector<int64_t> &cap) {
         A(io.suv, tot); A(io.tuv, tot); A(io.tpos, tot); A(io.tu, tot); A(io.tv, tot); A(io.tk, tot);
         A(io.hj, 4 * tot); A(io.hu, 4 * tot); A(io.hv, 4 * tot);
         A(io.hlen, 4 * E * N); A(io.pdeep, E * N); A(io.pnt, E * N); A(io.wenv, E * N);
-        A(io.jobs, 64 * E * N); A(io.njob, 65);
+        A(io.jobs, 64 * 4 * E * N); A(io.njob, 65);
         A(io.patch_off, E + 1);
         A(io.large_list, E * N); A(io.large_count, 1);
         A(io.n_patch, E); A(io.n_kept, E);

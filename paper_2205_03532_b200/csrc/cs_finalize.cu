@@ -359,9 +359,16 @@ __device__ void sort_patch(const Team &t, const ReduceIO &io, const ReduceParams
         io.pdeep[w] = am.i;
         io.pnt[w] = nt;
         io.wenv[w] = (int32_t)e;
-        if (hull) {  // chain job, bucketed by size (k_fin_chain runs the longest first)
-            const int k = job_bucket(m);
-            io.jobs[(int64_t)k * io.E * N + atomicAdd(io.njob + k, 1)] = w;
+        if (hull) {  // chain jobs (4w + kind), bucketed by chain length (k_fin_chain: longest first)
+            const int64_t cap = 4 * io.E * N;
+            int k = job_bucket(m);
+            int32_t *J = io.jobs + (int64_t)k * cap + atomicAdd(io.njob + k, 2);
+            J[0] = 4 * w; J[1] = 4 * w + 1;
+            if (needs_touch_hull(m, nt, K)) {
+                k = job_bucket(nt);
+                J = io.jobs + (int64_t)k * cap + atomicAdd(io.njob + k, 2);
+                J[0] = 4 * w + 2; J[1] = 4 * w + 3;
+            }
         }
     }
     t.sync();
@@ -548,11 +555,12 @@ __device__ int half_chain_global(const double2 *kuv, const int32_t *kpos, int L,
     return top;
 }
 
-// ONE WARP PER PATCH, one 8-lane group per half chain of _monotone_hull
-// (reduction.py:214-223): group 0/1 the lower/upper chain over all sorted members
-// (the hull area), 2/3 over the touching members (the kept selection; k_fin_sort
-// wrote them compacted, in sorted order, with their sorted positions). Patches come
-// from the job queue bucketed by size, longest first.
+// ONE 8-LANE GROUP PER HALF CHAIN of _monotone_hull (reduction.py:214-223), four
+// chains per warp. Job 4w + kind: kind 0/1 the lower/upper chain over patch w's
+// sorted members (the hull area), 2/3 over its touching members (the kept
+// selection; k_fin_sort wrote them compacted, in sorted order, with their sorted
+// positions). Jobs come bucketed by chain length, longest first; a warp takes four
+// consecutive ones, so its groups step through chains of similar length.
 //
 // A chain is sequential in its keys but not in the pops of one key: the sequential
 // loop tests cross(h[top-2-i], h[top-1-i], b) for i = 0, 1, ... on the unchanged
@@ -581,27 +589,34 @@ __global__ void __launch_bounds__(CH_WARPS * 32) k_fin_chain(ReduceIO io, Reduce
     }
     __syncthreads();
     const int ntot = bstart[CH_BUCKETS];
-    const int64_t bcap = io.E * (int64_t)p.N;
+    const int64_t bcap = 4 * io.E * (int64_t)p.N;
     while (true) {
-        int idx = 0;
-        if (lane == 0) idx = atomicAdd(io.njob + CH_BUCKETS, 1);
-        idx = __shfl_sync(FULL, idx, 0);
-        if (idx >= ntot) break;
-        int k = 0;
-        for (int sz = CH_BUCKETS / 2; sz > 0; sz >>= 1)  // last k with bstart[k] <= idx
-            if (bstart[k + sz] <= idx) k += sz;
-        const int w = io.jobs[k * bcap + idx - bstart[k]];
-        const int64_t e = io.wenv[w];
-        const int q = w - io.patch_off[e];
-        const int32_t *mo = io.member_offsets + e * (p.N + 1);
-        const int m = mo[q + 1] - mo[q];
-        const int64_t row0 = io.cand_base[e] + mo[q];
-        const int nt = io.pnt[w];
-        const bool run = g < 2 ? needs_all_hull(m, p.K) : needs_touch_hull(m, nt, p.K);
-        const int L = run ? (g < 2 ? m : nt) : 0;
-        const int dir = (g & 1) ? -1 : 1;
-        const double2 *kuv = g < 2 ? io.suv + row0 : io.tuv + row0;
-        const int32_t *kpos = g < 2 ? nullptr : io.tpos + row0;
+        int base = 0;
+        if (lane == 0) base = atomicAdd(io.njob + CH_BUCKETS, 4);
+        base = __shfl_sync(FULL, base, 0);
+        if (base >= ntot) break;
+        // this group's chain: job base + g (4 consecutive jobs: similar lengths)
+        const int idx = base + g;
+        bool run = idx < ntot;
+        int w = 0, kind = 0, L = 0, m = 0;
+        int64_t row0 = 0;
+        if (run) {
+            int k = 0;
+            for (int sz = CH_BUCKETS / 2; sz > 0; sz >>= 1)  // last k with bstart[k] <= idx
+                if (bstart[k + sz] <= idx) k += sz;
+            const int jw = io.jobs[k * bcap + idx - bstart[k]];
+            w = jw >> 2;
+            kind = jw & 3;
+            const int64_t e = io.wenv[w];
+            const int q = w - io.patch_off[e];
+            const int32_t *mo = io.member_offsets + e * (p.N + 1);
+            m = mo[q + 1] - mo[q];
+            row0 = io.cand_base[e] + mo[q];
+            L = kind < 2 ? m : io.pnt[w];
+        }
+        const int dir = (kind & 1) ? -1 : 1;
+        const double2 *kuv = kind < 2 ? io.suv + row0 : io.tuv + row0;
+        const int32_t *kpos = kind < 2 ? nullptr : io.tpos + row0;
         int Lmax = max(__shfl_sync(FULL, L, 0), __shfl_sync(FULL, L, 8));
         Lmax = max(Lmax, max(__shfl_sync(FULL, L, 16), __shfl_sync(FULL, L, 24)));
         // key x of the chain (index clamped into the list: no branch around the loads)
@@ -653,14 +668,14 @@ __global__ void __launch_bounds__(CH_WARPS * 32) k_fin_chain(ReduceIO io, Reduce
             __syncwarp();
         }
         if (run) {  // the stack is the half hull (sorted positions)
-            const int64_t h0 = 4 * row0 + (int64_t)g * m;
+            const int64_t h0 = 4 * row0 + (int64_t)kind * m;
             int32_t *hj = io.hj + h0;
             if (!ovf) {
                 for (int j = li; j < top; j += CG) hj[j] = stp[j];
             } else if (li == 0) {
                 top = half_chain_global(kuv, kpos, L, dir, hj, io.hu + h0, io.hv + h0);
             }
-            if (li == 0) io.hlen[4 * (int64_t)w + g] = top;
+            if (li == 0) io.hlen[4 * (int64_t)w + kind] = top;
         }
         __syncwarp();
     }

@@ -38,7 +38,7 @@ struct ReduceIO {
     int32_t *pdeep;      // [E N] per patch (work index): deepest member position
     int32_t *pnt;        // [E N] touching members (depth >= 0)
     int32_t *wenv;       // [E N] env of each work index
-    int32_t *jobs;       // [64][E N] chain jobs (patch work index) bucketed by patch size
+    int32_t *jobs;       // [64][4 E N] chain jobs (4 w + kind) bucketed by chain length
     int32_t *njob;       // [65] per-bucket counts, claimed
     int32_t *patch_off;  // [E+1]
     int32_t *large_list, *large_count;  // patches above the warp path's size limit
