@@ -53,6 +53,7 @@ struct SdfEntry {
     bool live = false;
     float *values = nullptr;
     float *bmin = nullptr;  // brick minima (GridT::bmin)
+    float *bwin = nullptr;  // window minima (GridT::bwin)
     size_t bytes = 0;
     SdfDesc desc{};
 };
@@ -205,6 +206,27 @@ int cs_sdf_register(const float *values, int values_on_device, int32_t nx, int32
                 }
         CS_CUDA(cudaMalloc(&s.bmin, bm.size() * sizeof(float)));
         CS_CUDA(cudaMemcpy(s.bmin, bm.data(), bm.size() * sizeof(float), cudaMemcpyHostToDevice));
+        // window tables: widths {1, 2} per axis, window [b, b + w - 1] clamped to the last brick
+        const size_t nb = bm.size();
+        std::vector<float> bw(8 * nb);
+        for (int t = 0; t < 8; ++t) {
+            const int wx = 1 + (t & 1), wy = 1 + ((t >> 1) & 1), wz = 1 + ((t >> 2) & 1);
+            for (int z = 0; z < bz; ++z)
+                for (int y = 0; y < by; ++y)
+                    for (int x = 0; x < bx; ++x) {
+                        float m = INFINITY;
+                        for (int dz = 0; dz < wz; ++dz)
+                            for (int dy = 0; dy < wy; ++dy)
+                                for (int dx = 0; dx < wx; ++dx) {
+                                    const int xx = std::min(x + dx, bx - 1), yy = std::min(y + dy, by - 1),
+                                              zz = std::min(z + dz, bz - 1);
+                                    m = std::fmin(m, bm[(size_t)xx + (size_t)bx * ((size_t)yy + (size_t)by * zz)]);
+                                }
+                        bw[(size_t)t * nb + (size_t)x + (size_t)bx * ((size_t)y + (size_t)by * z)] = m;
+                    }
+        }
+        CS_CUDA(cudaMalloc(&s.bwin, bw.size() * sizeof(float)));
+        CS_CUDA(cudaMemcpy(s.bwin, bw.data(), bw.size() * sizeof(float), cudaMemcpyHostToDevice));
     }
     SdfDesc &d = s.desc;
     d.values = s.values;
@@ -214,6 +236,7 @@ int cs_sdf_register(const float *values, int values_on_device, int32_t nx, int32
     for (int k = 0; k < 3; ++k) { d.lo[k] = aabb_lo[k]; d.hi[k] = aabb_hi[k]; }
     d.gp = cs::make_grid<float>(s.values, nx, ny, nz, origin[0], origin[1], origin[2], voxel);
     d.gp.bmin = s.bmin;
+    d.gp.bwin = s.bwin;
     CS_CUDA(cudaMemcpy(d_sdfs + h, &d, sizeof(SdfDesc), cudaMemcpyHostToDevice));
     s.live = true;
     *handle = h;
@@ -226,6 +249,7 @@ int cs_sdf_free(int32_t handle) {
     SdfEntry &s = g_sdf[handle];
     CS_CUDA(cudaFree(s.values));
     CS_CUDA(cudaFree(s.bmin));
+    CS_CUDA(cudaFree(s.bwin));
     s = SdfEntry{};
     return CS_OK;
 }

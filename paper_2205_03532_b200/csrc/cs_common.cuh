@@ -78,6 +78,9 @@ struct GridT {
     // [BRICK b, BRICK b + BRICK) -- a lower bound of any sample in those cells.
     const float *__restrict__ bmin;
     int bnx, bny, bnz;
+    // bwin[t][b], t = (wx - 1) + 2 (wy - 1) + 4 (wz - 1), w in {1, 2}: the minimum of bmin
+    // over the bricks [b, b + w - 1] per axis (clamped at the grid's last brick)
+    const float *__restrict__ bwin;
 };
 
 constexpr int BRICK = 2;                // cells per brick edge
@@ -101,6 +104,7 @@ __host__ __device__ inline GridT<T> make_grid(const T *v, int nx, int ny, int nz
     g.nm2[0] = nx - 2.0; g.nm2[1] = ny - 2.0; g.nm2[2] = nz - 2.0;
     g.n2[0] = nx - 2; g.n2[1] = ny - 2; g.n2[2] = nz - 2;
     g.bmin = nullptr;
+    g.bwin = nullptr;
     g.bnx = (nx - 2) / BRICK + 1; g.bny = (ny - 2) / BRICK + 1; g.bnz = (nz - 2) / BRICK + 1;
     return g;
 }
@@ -261,16 +265,29 @@ __device__ __forceinline__ double sample_lower_bound(const GridT<T> &g, const do
         n *= b1[k] - b0[k] + 1;
     }
     if (n > BRICK_MAX_LOOKUPS) return -INFINITY;
-    const int sx = b1[0] - b0[0] + 1;
-    float m = INFINITY;
-    for (int z = b0[2]; z <= b1[2]; ++z)
-        for (int y = b0[1]; y <= b1[1]; ++y) {
-            const float *row = g.bmin + b0[0] + g.bnx * (y + g.bny * z);
+    // The same minimum from the window tables: per axis, a range of one brick is one
+    // width-1 window, a longer one is covered by width-2 windows (overlapping at the
+    // end; min is idempotent), e.g. 3 bricks -> 2 lookups instead of 3.
+    int w[3], step[3], last[3];
 #pragma unroll
-            for (int x = 0; x < 4; ++x)  // a row's loads are independent: four in flight
-                if (x < sx) m = fminf(m, __ldg(row + x));
-            for (int x = 4; x < sx; ++x) m = fminf(m, __ldg(row + x));
+    for (int k = 0; k < 3; ++k) {
+        w[k] = b1[k] > b0[k] ? 2 : 1;
+        last[k] = b1[k] - w[k] + 1;  // start of the last window
+        step[k] = 2;
+    }
+    const float *tab = g.bwin + (size_t)((w[0] - 1) + 2 * (w[1] - 1) + 4 * (w[2] - 1)) * g.bnx * g.bny * g.bnz;
+    float m = INFINITY;
+    for (int z = b0[2];; z = min(z + step[2], last[2])) {
+        for (int y = b0[1];; y = min(y + step[1], last[1])) {
+            const float *row = tab + g.bnx * (y + g.bny * z);
+            for (int x = b0[0];; x = min(x + step[0], last[0])) {
+                m = fminf(m, __ldg(row + x));
+                if (x >= last[0]) break;
+            }
+            if (y >= last[1]) break;
         }
+        if (z >= last[2]) break;
+    }
     const double md = (double)m;
     return md - fabs(md) * 0x1p-40 - 1e-300;
 }
