@@ -52,8 +52,8 @@ constexpr int MAX_HANDLES = 4096;
 struct SdfEntry {
     bool live = false;
     float *values = nullptr;
-    float *bmin = nullptr;  // brick minima (GridT::bmin)
-    float *bwin = nullptr;  // window minima (GridT::bwin)
+    float *cwin = nullptr;  // cell-window minima (GridT::cwin)
+    float *bwin = nullptr;  // brick-window minima (GridT::bwin)
     size_t bytes = 0;
     SdfDesc desc{};
 };
@@ -184,7 +184,7 @@ int cs_sdf_register(const float *values, int values_on_device, int32_t nx, int32
     CS_CUDA(cudaMalloc(&s.values, s.bytes));
     CS_CUDA(cudaMemcpy(s.values, values, s.bytes, values_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
     GridT<float> probe = cs::make_grid<float>(nullptr, nx, ny, nz, origin[0], origin[1], origin[2], voxel);
-    {   // brick minima of the face lower bound (cs_common.cuh: sample_lower_bound)
+    {   // brick-window minima: the first pass of the face lower bound (cs_common.cuh: sample_lower_bound)
         std::vector<float> h32((size_t)n);
         CS_CUDA(cudaMemcpy(h32.data(), s.values, s.bytes, cudaMemcpyDeviceToHost));
         const int bx = probe.bnx, by = probe.bny, bz = probe.bnz;
@@ -204,8 +204,6 @@ int cs_sdf_register(const float *values, int values_on_device, int32_t nx, int32
                                 o = std::fmin(o, v);
                             }
                 }
-        CS_CUDA(cudaMalloc(&s.bmin, bm.size() * sizeof(float)));
-        CS_CUDA(cudaMemcpy(s.bmin, bm.data(), bm.size() * sizeof(float), cudaMemcpyHostToDevice));
         // window tables: widths {1, 2} per axis, window [b, b + w - 1] clamped to the last brick
         const size_t nb = bm.size();
         std::vector<float> bw(8 * nb);
@@ -228,6 +226,16 @@ int cs_sdf_register(const float *values, int values_on_device, int32_t nx, int32
         CS_CUDA(cudaMalloc(&s.bwin, bw.size() * sizeof(float)));
         CS_CUDA(cudaMemcpy(s.bwin, bw.data(), bw.size() * sizeof(float), cudaMemcpyHostToDevice));
     }
+    {   // cell-window minima of the exact face bound (cs_common.cuh: sample_lower_bound)
+        const int64_t nc = (int64_t)(nx - 1) * (ny - 1) * (nz - 1);
+        float *tmp = nullptr;
+        CS_CUDA(cudaMalloc(&s.cwin, (size_t)CWIN_LEVELS * nc * sizeof(float)));
+        CS_CUDA(cudaMalloc(&tmp, (size_t)nc * sizeof(float)));
+        build_cell_windows(s.values, nx, ny, nz, s.cwin, tmp, 0);
+        CS_CUDA(cudaGetLastError());
+        CS_CUDA(cudaDeviceSynchronize());
+        CS_CUDA(cudaFree(tmp));
+    }
     SdfDesc &d = s.desc;
     d.values = s.values;
     d.nx = nx; d.ny = ny; d.nz = nz; d.pad = 0;
@@ -235,7 +243,7 @@ int cs_sdf_register(const float *values, int values_on_device, int32_t nx, int32
     d.voxel = voxel;
     for (int k = 0; k < 3; ++k) { d.lo[k] = aabb_lo[k]; d.hi[k] = aabb_hi[k]; }
     d.gp = cs::make_grid<float>(s.values, nx, ny, nz, origin[0], origin[1], origin[2], voxel);
-    d.gp.bmin = s.bmin;
+    d.gp.cwin = s.cwin;
     d.gp.bwin = s.bwin;
     CS_CUDA(cudaMemcpy(d_sdfs + h, &d, sizeof(SdfDesc), cudaMemcpyHostToDevice));
     s.live = true;
@@ -248,7 +256,7 @@ int cs_sdf_free(int32_t handle) {
     if (handle < 0 || handle >= (int)g_sdf.size() || !g_sdf[handle].live) return fail(CS_ERR_HANDLE, "bad SDF handle %d", handle);
     SdfEntry &s = g_sdf[handle];
     CS_CUDA(cudaFree(s.values));
-    CS_CUDA(cudaFree(s.bmin));
+    CS_CUDA(cudaFree(s.cwin));
     CS_CUDA(cudaFree(s.bwin));
     s = SdfEntry{};
     return CS_OK;

@@ -73,20 +73,23 @@ struct GridT {
     double nm1[3];      // n - 1 (clamp bound, sdf/_kernels.py:302-304)
     double nm2[3];      // n - 2 (cell clamp, sdf/_kernels.py:261-270)
     int n2[3];
-    // Brick minima (optional): bmin[bx + bnx (by + bny bz)] = min of the grid values at
-    // nodes [BRICK b, BRICK b + BRICK] per axis, i.e. of every corner of the cells
-    // [BRICK b, BRICK b + BRICK) -- a lower bound of any sample in those cells.
-    const float *__restrict__ bmin;
-    int bnx, bny, bnz;
-    // bwin[t][b], t = (wx - 1) + 2 (wy - 1) + 4 (wz - 1), w in {1, 2}: the minimum of bmin
-    // over the bricks [b, b + w - 1] per axis (clamped at the grid's last brick)
+    // Cell-window minima (optional), for the exact face bound (sample_lower_bound):
+    // cwin[l][c], c = cx + (nx - 1) (cy + (ny - 1) cz), l = 0..3: the minimum grid value
+    // over the corners of the cells [c, c + 2^l - 1] per axis (the window is only read
+    // inside the grid).
+    const float *__restrict__ cwin;
+    // Brick windows (optional), the cheap first pass of the same bound: bwin[t][b],
+    // t = (wx - 1) + 2 (wy - 1) + 4 (wz - 1), w in {1, 2}: the minimum grid value over the
+    // corners of the cells of bricks [b, b + w - 1] per axis (BRICK cells per brick edge).
     const float *__restrict__ bwin;
+    int bnx, bny, bnz;
 };
 
-constexpr int BRICK = 2;                // cells per brick edge
-#ifndef BRICK_MAX_LOOKUPS
-#define BRICK_MAX_LOOKUPS 64  // larger face boxes skip the bound
+constexpr int BRICK = 2;  // cells per brick edge
+#ifndef CWIN_MAX_LOOKUPS
+#define CWIN_MAX_LOOKUPS 16  // face boxes needing more window lookups skip the bound (measured best)
 #endif
+constexpr int CWIN_LEVELS = 4;  // window widths 1, 2, 4, 8 cells
 
 template <class T>
 __host__ __device__ inline GridT<T> make_grid(const T *v, int nx, int ny, int nz, double ox, double oy, double oz,
@@ -103,7 +106,7 @@ __host__ __device__ inline GridT<T> make_grid(const T *v, int nx, int ny, int nz
     g.nm1[0] = nx - 1.0; g.nm1[1] = ny - 1.0; g.nm1[2] = nz - 1.0;
     g.nm2[0] = nx - 2.0; g.nm2[1] = ny - 2.0; g.nm2[2] = nz - 2.0;
     g.n2[0] = nx - 2; g.n2[1] = ny - 2; g.n2[2] = nz - 2;
-    g.bmin = nullptr;
+    g.cwin = nullptr;
     g.bwin = nullptr;
     g.bnx = (nx - 2) / BRICK + 1; g.bny = (ny - 2) / BRICK + 1; g.bnz = (nz - 2) / BRICK + 1;
     return g;
@@ -245,44 +248,85 @@ __device__ __forceinline__ void gradient(const GridT<T> &g, double px, double py
 }
 
 // A lower bound of every trilinear sample (sdf/_kernels.py:253-309) at points of
-// the box [lo, hi] (grid frame, metres), from the brick minima; -inf (no bound)
-// when the box spans more than BRICK_MAX_LOOKUPS bricks. A sample is a convex
-// combination of its cell's corners (weights f and 1 - f, evaluated in float64)
-// plus a non-negative outside term, and points outside the grid sample a clamped
-// boundary cell, so no sample in the box's cells is below the minimum corner
-// minus the lerps' rounding (a few ulps; margin 2^-40 relative). The box is
-// widened by 1e-6 voxel so roundings of the points themselves stay inside.
+// the box [lo, hi] (grid frame, metres); -inf (no bound) when it would take more
+// than CWIN_MAX_LOOKUPS window lookups. A sample is a convex combination of its
+// cell's 8 corners (weights f and 1 - f, evaluated in float64) plus a non-negative
+// outside term, and points outside the grid sample a clamped boundary cell, so no
+// sample in the box's cells is below the minimum corner value over those cells,
+// less the lerps' rounding (a few ulps; margin 2^-40 relative). The box is widened
+// by 1e-6 voxel so roundings of the points themselves stay inside. cd_hint: a
+// looser bound above it is returned early. The minimum over
+// the box's cells is read from the window tables: with w = the largest power of two
+// (<= 8) not above any axis' cell count, each axis is covered by windows of w cells
+// (overlapping at the end; min is idempotent), so the bound is exactly the minimum
+// over the box's cells.
 template <class T>
-__device__ __forceinline__ double sample_lower_bound(const GridT<T> &g, const double lo[3], const double hi[3]) {
-    int b0[3], b1[3], n = 1;
+__device__ __forceinline__ double sample_lower_bound(const GridT<T> &g, const double lo[3], const double hi[3],
+                                                    double cd_hint) {
+    int c0[3], c1[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         const double a = (lo[k] - g.o[k]) * g.rv - 1e-6, b = (hi[k] - g.o[k]) * g.rv + 1e-6;
-        const int c0 = a < 0.0 ? 0 : (a > g.nm2[k] ? g.n2[k] : (int)a);
-        const int c1 = b < 0.0 ? 0 : (b > g.nm2[k] ? g.n2[k] : (int)b);
-        b0[k] = c0 / BRICK;
-        b1[k] = c1 / BRICK;
-        n *= b1[k] - b0[k] + 1;
+        c0[k] = a < 0.0 ? 0 : (a > g.nm2[k] ? g.n2[k] : (int)a);
+        c1[k] = b < 0.0 ? 0 : (b > g.nm2[k] ? g.n2[k] : (int)b);
     }
-    if (n > BRICK_MAX_LOOKUPS) return -INFINITY;
-    // The same minimum from the window tables: per axis, a range of one brick is one
-    // width-1 window, a longer one is covered by width-2 windows (overlapping at the
-    // end; min is idempotent), e.g. 3 bricks -> 2 lookups instead of 3.
-    int w[3], step[3], last[3];
+    const int cnx = g.nx - 1, cny = g.ny - 1;
+    const size_t ntab = (size_t)cnx * cny * (g.nz - 1);
+    // First a cheap pass over the box's bricks (a superset of its cells: a lower bound
+    // too), from the brick windows: per axis one width-1 window or width-2 windows
+    // (overlapping at the end; min is idempotent). Faces it cannot settle take the exact
+    // pass over the cells.
+    if (g.bwin) {
+        int b0[3], w[3], last[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            b0[k] = c0[k] / BRICK;
+            const int b1 = c1[k] / BRICK;
+            w[k] = b1 > b0[k] ? 2 : 1;
+            last[k] = b1 - w[k] + 1;
+        }
+        const float *tab = g.bwin + (size_t)((w[0] - 1) + 2 * (w[1] - 1) + 4 * (w[2] - 1)) * g.bnx * g.bny * g.bnz;
+        float m = INFINITY;
+        for (int z = b0[2];; z = min(z + 2, last[2])) {
+            for (int y = b0[1];; y = min(y + 2, last[1])) {
+                const float *row = tab + g.bnx * (y + g.bny * z);
+                for (int x = b0[0];; x = min(x + 2, last[0])) {
+                    m = fminf(m, __ldg(row + x));
+                    if (x >= last[0]) break;
+                }
+                if (y >= last[1]) break;
+            }
+            if (z >= last[2]) break;
+        }
+        const double md = (double)m;
+        const double lb = md - fabs(md) * 0x1p-40 - 1e-300;
+        if (lb > cd_hint) return lb;
+    }
+    const int rmin = min(c1[0] - c0[0], min(c1[1] - c0[1], c1[2] - c0[2])) + 1;
+    const int lvl = rmin >= 8 ? 3 : rmin >= 4 ? 2 : rmin >= 2 ? 1 : 0, w = 1 << lvl;
+    int n = 1, last[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        w[k] = b1[k] > b0[k] ? 2 : 1;
-        last[k] = b1[k] - w[k] + 1;  // start of the last window
-        step[k] = 2;
+        last[k] = c1[k] - w + 1;  // start of the last window
+        n *= (last[k] - c0[k] + w - 1) / w + 1;
     }
-    const float *tab = g.bwin + (size_t)((w[0] - 1) + 2 * (w[1] - 1) + 4 * (w[2] - 1)) * g.bnx * g.bny * g.bnz;
+    if (n > CWIN_MAX_LOOKUPS) return -INFINITY;
+    const float *tab = g.cwin + (size_t)lvl * ntab;
     float m = INFINITY;
-    for (int z = b0[2];; z = min(z + step[2], last[2])) {
-        for (int y = b0[1];; y = min(y + step[1], last[1])) {
-            const float *row = tab + g.bnx * (y + g.bny * z);
-            for (int x = b0[0];; x = min(x + step[0], last[0])) {
-                m = fminf(m, __ldg(row + x));
-                if (x >= last[0]) break;
+    const int nxw = (last[0] - c0[0] + w - 1) / w + 1;  // windows per row
+    for (int z = c0[2];; z = min(z + w, last[2])) {
+        for (int y = c0[1];; y = min(y + w, last[1])) {
+            const float *row = tab + (size_t)cnx * (y + (size_t)cny * z);
+            if (nxw <= 4) {  // the usual case: four loads issued together (repeats of the last are harmless)
+                float r = __ldg(row + c0[0]);
+#pragma unroll
+                for (int i = 1; i < 4; ++i) r = fminf(r, __ldg(row + min(c0[0] + i * w, last[0])));
+                m = fminf(m, r);
+            } else {
+                for (int x = c0[0];; x = min(x + w, last[0])) {
+                    m = fminf(m, __ldg(row + x));
+                    if (x >= last[0]) break;
+                }
             }
             if (y >= last[1]) break;
         }

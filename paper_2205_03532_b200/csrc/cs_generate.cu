@@ -10,6 +10,8 @@
 //                  epilogue (generation.py:98-114)
 //   k_face_contacts / k_sdf_sample / k_sdf_gradient: per-pair drop-ins for the
 //                  reference's numba kernels.
+#include <algorithm>
+
 #include "cs_generate.cuh"
 
 namespace cs {
@@ -158,7 +160,7 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int2 
         // box; when the grid is provably above cd there, the reference ends with
         // found = 0 (prune or descent), so the face is not descended at all (exact:
         // only a proof skips).
-        if (near && grid.bmin && sample_lower_bound(grid, lo, hi) > sx.cd) near = false;
+        if (near && grid.cwin && sample_lower_bound(grid, lo, hi, sx.cd) > sx.cd) near = false;
         if (near) { need[la] = 1; need[lb] = 1; need[lc] = 1; }
     }
     __syncthreads();
@@ -749,6 +751,51 @@ void launch_pgd_wave(int sm_count, const int2 *block_map, const EnvXf *xf, const
         if (counter) CS_WAVE(true, false); else CS_WAVE(false, false);
     }
 #undef CS_WAVE
+}
+
+// ---------------------------------------------------------------- cell-window minima
+// (GridT::cwin; built once at SDF registration)
+
+__global__ void k_cell_min(const float *__restrict__ v, int nx, int ny, int nz, float *__restrict__ out) {
+    const int cnx = nx - 1, cny = ny - 1, cnz = nz - 1;
+    const int64_t nc = (int64_t)cnx * cny * cnz;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x) {
+        const int x = (int)(c % cnx), y = (int)((c / cnx) % cny), z = (int)(c / ((int64_t)cnx * cny));
+        const float *p = v + x + (int64_t)nx * (y + (int64_t)ny * z);
+        const int64_t sy = nx, sz = (int64_t)nx * ny;
+        out[c] = fminf(fminf(fminf(p[0], p[1]), fminf(p[sy], p[sy + 1])),
+                       fminf(fminf(p[sz], p[sz + 1]), fminf(p[sy + sz], p[sy + sz + 1])));
+    }
+}
+
+// out[c] = min(in[c], in[c + h along axis]) (the second term dropped past the last cell)
+__global__ void k_min_shift(const float *__restrict__ in, float *__restrict__ out, int cnx, int cny, int cnz, int axis,
+                            int h) {
+    const int64_t nc = (int64_t)cnx * cny * cnz;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x) {
+        const int x = (int)(c % cnx), y = (int)((c / cnx) % cny), z = (int)(c / ((int64_t)cnx * cny));
+        const int pos = axis == 0 ? x : axis == 1 ? y : z, n = axis == 0 ? cnx : axis == 1 ? cny : cnz;
+        const int64_t stride = axis == 0 ? 1 : axis == 1 ? (int64_t)cnx : (int64_t)cnx * cny;
+        float m = in[c];
+        if (pos + h < n) m = fminf(m, in[c + h * stride]);
+        out[c] = m;
+    }
+}
+
+// tables: CWIN_LEVELS x (nx-1)(ny-1)(nz-1) floats; tmp: one table
+void build_cell_windows(const float *values, int nx, int ny, int nz, float *tables, float *tmp, cudaStream_t s) {
+    const int cnx = nx - 1, cny = ny - 1, cnz = nz - 1;
+    const int64_t nc = (int64_t)cnx * cny * cnz;
+    const unsigned grid = (unsigned)std::min<int64_t>((nc + 255) / 256, 148 * 32);
+    k_cell_min<<<grid, 256, 0, s>>>(values, nx, ny, nz, tables);
+    for (int l = 1; l < CWIN_LEVELS; ++l) {  // width 2^l from width 2^(l-1): shift by half per axis
+        const int h = 1 << (l - 1);
+        const float *prev = tables + (int64_t)(l - 1) * nc;
+        float *cur = tables + (int64_t)l * nc;
+        k_min_shift<<<grid, 256, 0, s>>>(prev, cur, cnx, cny, cnz, 0, h);
+        k_min_shift<<<grid, 256, 0, s>>>(cur, tmp, cnx, cny, cnz, 1, h);
+        k_min_shift<<<grid, 256, 0, s>>>(tmp, cur, cnx, cny, cnz, 2, h);
+    }
 }
 
 void launch_compact(int64_t E, const EnvXf *xf, const int64_t *cand_base, const int2 *block_map,
