@@ -694,7 +694,10 @@ struct HullView {
 
 // One patch per warp: hull assembly, kept selection (reduction.py:172-199), hull
 // area (reduction.py:227-236), the kept rows.
-__device__ void kept_patch(const WarpTeam &t, const ReduceIO &io, const ReduceParams &p, int w, int *chosen) {
+constexpr int KH = 256;  // hull entries a k_fin_kept warp stages in shared memory (longer hulls: read in place)
+
+__device__ void kept_patch(const WarpTeam &t, const ReduceIO &io, const ReduceParams &p, int w, int *chosen,
+                           double2 *huv, int *hk) {
     const int N = p.N, K = p.K;
     const int64_t e = io.wenv[w];
     const int q = w - io.patch_off[e];
@@ -710,10 +713,19 @@ __device__ void kept_patch(const WarpTeam &t, const ReduceIO &io, const ReducePa
     const int4 len = *reinterpret_cast<const int4 *>(io.hlen + 4 * (int64_t)w);
     const int lane = t.rank();
     double area = 0.0;
-    if (lane == 0 && m >= 3) {
+    if (m >= 3) {
         const HullView h{hj, hj + m, len.x, (len.x - 1) + (len.y - 1)};
-        if (h.H >= 3) {
-            const int H = h.H;
+        const int H = h.H;
+        if (H >= 3 && H <= KH) {  // the hull's (u, v) staged by the warp, the sums in lane 0
+            for (int k = lane; k < H; k += 32) huv[k] = suv[h.at(k)];
+            __syncwarp();
+            if (lane == 0) {
+                const double d1 = ddot_x2(H, [&](int k) { return huv[k].x; }, [&](int k) { return huv[(k + 1) % H].y; });
+                const double d2 = ddot_x2(H, [&](int k) { return huv[k].y; }, [&](int k) { return huv[(k + 1) % H].x; });
+                area = 0.5 * fabs(d1 - d2);
+            }
+            __syncwarp();
+        } else if (H >= 3 && lane == 0) {
             const double d1 = ddot_x2(H, [&](int k) { return suv[h.at(k)].x; }, [&](int k) { return suv[h.at((k + 1) % H)].y; });
             const double d2 = ddot_x2(H, [&](int k) { return suv[h.at(k)].y; }, [&](int k) { return suv[h.at((k + 1) % H)].x; });
             area = 0.5 * fabs(d1 - d2);
@@ -724,17 +736,30 @@ __device__ void kept_patch(const WarpTeam &t, const ReduceIO &io, const ReducePa
         for (int k = lane; k < m; k += 32) chosen[k] = k;
         nc = m;
     } else {
+        const HullView hb = needs_touch_hull(m, nt, K)  // base = touching members, else all
+                                ? HullView{hj + 2 * m, hj + 3 * m, len.z, (len.z - 1) + (len.w - 1)}
+                                : HullView{hj, hj + m, len.x, (len.x - 1) + (len.y - 1)};
+        const bool staged = hb.H <= KH;  // the hull's members staged by the warp
+        if (staged) {
+            for (int k = lane; k < hb.H; k += 32) hk[k] = dec_k(sk[hb.at(k)]);
+            __syncwarp();
+        }
         if (lane == 0) {
-            const HullView h = needs_touch_hull(m, nt, K)  // base = touching members, else all
-                                   ? HullView{hj + 2 * m, hj + 3 * m, len.z, (len.z - 1) + (len.w - 1)}
-                                   : HullView{hj, hj + m, len.x, (len.x - 1) + (len.y - 1)};
+            struct {
+                const HullView &h;
+                const int32_t *sk;
+                const int *hk;
+                bool staged;
+                __device__ int at(int j) const { return staged ? hk[j] : dec_k(sk[h.at(j)]); }
+                int H;
+            } h{hb, sk, hk, staged, hb.H};
             int nh = 0;  // hull members other than the deepest
-            for (int j = 0; j < h.H; ++j) nh += dec_k(sk[h.at(j)]) != deepest;
+            for (int j = 0; j < h.H; ++j) nh += h.at(j) != deepest;
             chosen[0] = deepest;
             int c = 1;
             if (nh <= K - 1) {
                 for (int j = 0; j < h.H; ++j) {
-                    const int k = dec_k(sk[h.at(j)]);
+                    const int k = h.at(j);
                     if (k != deepest) chosen[c++] = k;
                 }
             } else {  // picks = linspace(0, len(hull), K-1, endpoint=False).astype(int), strictly increasing
@@ -743,7 +768,7 @@ __device__ void kept_patch(const WarpTeam &t, const ReduceIO &io, const ReducePa
                 for (int pk = 0; pk < K - 1; ++pk) {
                     const int target = (int)((double)pk * step + 0.0);
                     while (f < target) {
-                        k = dec_k(sk[h.at(++j)]);
+                        k = h.at(++j);
                         if (k != deepest) ++f;
                     }
                     chosen[c++] = k;
@@ -804,11 +829,13 @@ constexpr int FK_WARPS = 4;
 __global__ void __launch_bounds__(FK_WARPS * 32) k_fin_kept(ReduceIO io, ReduceParams p) {
     __shared__ int s_chosen[FK_WARPS][MAX_KEPT];
     __shared__ int s_misc[FK_WARPS][4];
+    __shared__ double2 s_huv[FK_WARPS][KH];
+    __shared__ int s_hk[FK_WARPS][KH];
     const int wib = threadIdx.x >> 5;
     WarpTeam t{s_misc[wib]};
     const int total = io.patch_off[io.E];
     for (int w = blockIdx.x * FK_WARPS + wib; w < total; w += gridDim.x * FK_WARPS)
-        kept_patch(t, io, p, w, s_chosen[wib]);
+        kept_patch(t, io, p, w, s_chosen[wib], s_huv[wib], s_hk[wib]);
 }
 
 // Per env stats, one warp per env (lanes over the patches).
