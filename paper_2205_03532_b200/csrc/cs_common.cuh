@@ -276,6 +276,7 @@ __device__ __forceinline__ double sample_lower_bound(const GridT<T> &g, const do
     // too), from the brick windows: per axis one width-1 window or width-2 windows
     // (overlapping at the end; min is idempotent). Faces it cannot settle take the exact
     // pass over the cells.
+#ifndef NO_BWIN
     if (g.bwin) {
         int b0[3], w[3], last[3];
 #pragma unroll
@@ -287,21 +288,32 @@ __device__ __forceinline__ double sample_lower_bound(const GridT<T> &g, const do
         }
         const float *tab = g.bwin + (size_t)((w[0] - 1) + 2 * (w[1] - 1) + 4 * (w[2] - 1)) * g.bnx * g.bny * g.bnz;
         float m = INFINITY;
-        for (int z = b0[2];; z = min(z + 2, last[2])) {
-            for (int y = b0[1];; y = min(y + 2, last[1])) {
-                const float *row = tab + g.bnx * (y + g.bny * z);
-                for (int x = b0[0];; x = min(x + 2, last[0])) {
-                    m = fminf(m, __ldg(row + x));
-                    if (x >= last[0]) break;
+        if (last[0] - b0[0] <= 2 && last[1] - b0[1] <= 2 && last[2] - b0[2] <= 2) {
+            // at most two windows per axis (the usual case): eight independent loads in
+            // flight together (repeats when one window suffices)
+            const int x1 = last[0], y0 = g.bnx * b0[1], y1 = g.bnx * last[1];
+            const int z0 = g.bnx * g.bny * b0[2], z1 = g.bnx * g.bny * last[2];
+            const float *r00 = tab + y0 + z0, *r01 = tab + y0 + z1, *r10 = tab + y1 + z0, *r11 = tab + y1 + z1;
+            m = fminf(fminf(fminf(__ldg(r00 + b0[0]), __ldg(r00 + x1)), fminf(__ldg(r10 + b0[0]), __ldg(r10 + x1))),
+                      fminf(fminf(__ldg(r01 + b0[0]), __ldg(r01 + x1)), fminf(__ldg(r11 + b0[0]), __ldg(r11 + x1))));
+        } else {
+            for (int z = b0[2];; z = min(z + 2, last[2])) {
+                for (int y = b0[1];; y = min(y + 2, last[1])) {
+                    const float *row = tab + g.bnx * (y + g.bny * z);
+                    for (int x = b0[0];; x = min(x + 2, last[0])) {
+                        m = fminf(m, __ldg(row + x));
+                        if (x >= last[0]) break;
+                    }
+                    if (y >= last[1]) break;
                 }
-                if (y >= last[1]) break;
+                if (z >= last[2]) break;
             }
-            if (z >= last[2]) break;
         }
         const double md = (double)m;
         const double lb = md - fabs(md) * 0x1p-40 - 1e-300;
         if (lb > cd_hint) return lb;
     }
+#endif
     const int rmin = min(c1[0] - c0[0], min(c1[1] - c0[1], c1[2] - c0[2])) + 1;
     const int lvl = rmin >= 8 ? 3 : rmin >= 4 ? 2 : rmin >= 2 ? 1 : 0, w = 1 << lvl;
     int n = 1, last[3];
@@ -314,24 +326,18 @@ __device__ __forceinline__ double sample_lower_bound(const GridT<T> &g, const do
     const float *tab = g.cwin + (size_t)lvl * ntab;
     float m = INFINITY;
     const int nxw = (last[0] - c0[0] + w - 1) / w + 1;  // windows per row
-    for (int z = c0[2];; z = min(z + w, last[2])) {
-        for (int y = c0[1];; y = min(y + w, last[1])) {
-            const float *row = tab + (size_t)cnx * (y + (size_t)cny * z);
-            if (nxw <= 4) {  // the usual case: four loads issued together (repeats of the last are harmless)
-                float r = __ldg(row + c0[0]);
+    const int nyw = (last[1] - c0[1] + w - 1) / w + 1;
+    // all lookups issued together: (ix, iy, iz) walks the windows, loads are predicated
+    int ix = 0, iy = 0, iz = 0;
+    float r[CWIN_MAX_LOOKUPS];
 #pragma unroll
-                for (int i = 1; i < 4; ++i) r = fminf(r, __ldg(row + min(c0[0] + i * w, last[0])));
-                m = fminf(m, r);
-            } else {
-                for (int x = c0[0];; x = min(x + w, last[0])) {
-                    m = fminf(m, __ldg(row + x));
-                    if (x >= last[0]) break;
-                }
-            }
-            if (y >= last[1]) break;
-        }
-        if (z >= last[2]) break;
+    for (int i = 0; i < CWIN_MAX_LOOKUPS; ++i) {
+        const int x = min(c0[0] + ix * w, last[0]), y = min(c0[1] + iy * w, last[1]), z = min(c0[2] + iz * w, last[2]);
+        r[i] = i < n ? __ldg(tab + x + (size_t)cnx * (y + (size_t)cny * z)) : INFINITY;
+        if (++ix == nxw) { ix = 0; if (++iy == nyw) { iy = 0; ++iz; } }
     }
+#pragma unroll
+    for (int i = 0; i < CWIN_MAX_LOOKUPS; ++i) m = fminf(m, r[i]);
     const double md = (double)m;
     return md - fabs(md) * 0x1p-40 - 1e-300;
 }

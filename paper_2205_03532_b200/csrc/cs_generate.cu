@@ -92,6 +92,21 @@ __device__ __forceinline__ double3 to_grid(const EnvXf &X, double4 v) {
     return r;
 }
 
+#ifdef PREP_STATS
+#define PREP_PROF
+#define PREP_CONST
+#else
+#define PREP_CONST const
+#endif
+#ifdef PREP_PROF
+__device__ unsigned long long g_prep_prof[16];
+#define PREP_MARK(i) do { if (threadIdx.x == 0) { const long long t_ = clock64(); atomicAdd(&g_prep_prof[i], (unsigned long long)(t_ - t_last)); t_last = t_; } } while (0)
+extern "C" int cs_debug_prep_prof(unsigned long long *out) { return (int)cudaMemcpyFromSymbol(out, g_prep_prof, sizeof(g_prep_prof)); }
+#else
+#define PREP_MARK(i) do {} while (0)
+#endif
+constexpr int FACE_ITEM = 1 << 30;  // sample-list code of a face centre (else a vertex slot)
+
 // k_face_prep: one CTA per (env, chunk of FACE_CHUNK faces). The chunk's distinct
 // vertices are transformed and (where a face needs them) sampled once into shared
 // memory; each thread then culls one face (generation.py:74-83), applies the
@@ -113,11 +128,15 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int2 
     __shared__ PlanGrid sg;
     __shared__ int ws[WS_INTS];
     __shared__ unsigned sbase;
+#ifdef PREP_PROF
+    long long t_last = clock64();
+#endif
     const int2 bm = block_map[blockIdx.x];
     const int e = bm.x, f0 = bm.y;
     if (threadIdx.x < sizeof(EnvXf) / 8)
         reinterpret_cast<double *>(&sx)[threadIdx.x] = reinterpret_cast<const double *>(xf + e)[threadIdx.x];
     __syncthreads();
+    PREP_MARK(0);
     if (sx.status != 0) {  // non-finite pose or cd < 0: nothing is generated
         if (threadIdx.x == 0) { st.chunk_count[blockIdx.x] = 0; st.chunk_found[blockIdx.x] = 0; }
         return;
@@ -134,20 +153,32 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int2 
     const int chunk = f0 / FACE_CHUNK;
     const int v0 = __ldg(meshes[sx.mesh].chunk_voff + chunk);
     const int ncv = __ldg(meshes[sx.mesh].chunk_voff + chunk + 1) - v0;
-    double *vx = dsm, *vy = dsm + maxcv, *vz = dsm + 2 * maxcv, *vphi = dsm + 3 * maxcv;
-    unsigned char *need = reinterpret_cast<unsigned char *>(dsm + 4 * maxcv);
+    // shared: vertex x/y/z/phi [maxcv], centre phi [FACE_CHUNK], face corner slots
+    // [FACE_CHUNK], the sample list [maxcv + FACE_CHUNK], vertex flags [maxcv]
+    double *vx = dsm, *vy = dsm + maxcv, *vz = dsm + 2 * maxcv, *vphi = dsm + 3 * maxcv, *cphi = dsm + 4 * maxcv;
+    uint2 *sloc = reinterpret_cast<uint2 *>(cphi + FACE_CHUNK);
+    int *list = reinterpret_cast<int *>(sloc + FACE_CHUNK);
+    unsigned char *need = reinterpret_cast<unsigned char *>(list + maxcv + FACE_CHUNK);
+    __shared__ int s_nl;
+    const int64_t f = (int64_t)f0 + threadIdx.x;
+    const uint2 loc = f < nt ? __ldg(meshes[sx.mesh].face_loc + f) : make_uint2(0, 0);  // in flight during the transform
     // verts_grid = to_grid.apply(vertices) (generation.py:70), per distinct vertex
     for (int j = threadIdx.x; j < ncv; j += FACE_CHUNK) {
         const double3 p = to_grid(sx, ld_vert(verts + __ldg(cverts + v0 + j)));
         vx[j] = p.x; vy[j] = p.y; vz[j] = p.z;
         need[j] = 0;
     }
+    if (threadIdx.x == 0) s_nl = 0;
     __syncthreads();
-    const int64_t f = (int64_t)f0 + threadIdx.x;
+    PREP_MARK(1);
+    const int lane = threadIdx.x & 31;
     int la = 0, lb = 0, lc = 0;
     bool near = false;
+#ifdef PREP_STATS
+    bool bcull = false;
+#endif
     if (f < nt) {
-        const uint2 loc = __ldg(meshes[sx.mesh].face_loc + f);
+        sloc[threadIdx.x] = loc;
         la = (int)(loc.x & 0xffffu); lb = (int)(loc.x >> 16); lc = (int)loc.y;
         const double ax = vx[la], bx = vx[lb], cx = vx[lc];
         const double ay = vy[la], by = vy[lb], cy = vy[lc];
@@ -160,17 +191,61 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int2 
         // box; when the grid is provably above cd there, the reference ends with
         // found = 0 (prune or descent), so the face is not descended at all (exact:
         // only a proof skips).
+#ifdef PREP_STATS
+        bcull = near && grid.cwin && sample_lower_bound(grid, lo, hi, sx.cd) > sx.cd;
+        atomicAdd(&g_prep_prof[8], 1ull);
+        if (near) atomicAdd(&g_prep_prof[9], 1ull);
+        if (bcull) atomicAdd(&g_prep_prof[10], 1ull);
+#else
         if (near && grid.cwin && sample_lower_bound(grid, lo, hi, sx.cd) > sx.cd) near = false;
+#endif
         if (near) { need[la] = 1; need[lb] = 1; need[lc] = 1; }
     }
+    {   // near faces queue their centre sample
+        const unsigned b = __ballot_sync(0xffffffffu, near);
+        int base = 0;
+        if (lane == 0 && b) base = atomicAdd(&s_nl, __popc(b));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (near) list[base + __popc(b & ((1u << lane) - 1))] = FACE_ITEM | threadIdx.x;
+    }
     __syncthreads();
-    int ns = 0;
-    for (int j = threadIdx.x; j < ncv; j += FACE_CHUNK)
-        if (need[j]) {
-            vphi[j] = sample(grid, vx[j], vy[j], vz[j]);
-            ++ns;
+    PREP_MARK(2);
+    for (int j0 = threadIdx.x & ~31; j0 < ncv; j0 += FACE_CHUNK) {  // needed vertices queue theirs
+        const int j = j0 + lane;
+        const bool q = j < ncv && need[j];
+        const unsigned b = __ballot_sync(0xffffffffu, q);
+        int base = 0;
+        if (lane == 0 && b) base = atomicAdd(&s_nl, __popc(b));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (q) list[base + __popc(b & ((1u << lane) - 1))] = j;
+    }
+    __syncthreads();
+    PREP_MARK(3);
+    // One dense pass over the queued samples: every needed vertex (phi at the vertices,
+    // generation.py:92) and the centre of every near face (the centroid start point;
+    // only used when the face survives the Lipschitz prune below).
+    const int nl = s_nl;
+    for (int i = threadIdx.x; i < nl; i += FACE_CHUNK) {
+        const int code = list[i];
+        double px, py, pz;
+        if (code & FACE_ITEM) {
+            const uint2 loc = sloc[code & 0xffff];
+            const int a = (int)(loc.x & 0xffffu), b = (int)(loc.x >> 16), c = (int)loc.y;
+            px = (vx[a] + vx[b] + vx[c]) / 3.0;
+            py = (vy[a] + vy[b] + vy[c]) / 3.0;
+            pz = (vz[a] + vz[b] + vz[c]) / 3.0;
+        } else {
+            px = vx[code]; py = vy[code]; pz = vz[code];
         }
+        const double r = sample(grid, px, py, pz);
+        if (code & FACE_ITEM) cphi[code & 0xffff] = r;
+        else vphi[code] = r;
+    }
     __syncthreads();
+    PREP_MARK(4);
+    int ns = 0;
+    if (COUNT)
+        for (int j = threadIdx.x; j < ncv; j += FACE_CHUNK) ns += need[j];
     bool survive = false;
     int which = 0;
     double pa = 0.0, pb = 0.0, pc = 0.0, ps = 0.0;
@@ -183,9 +258,16 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int2 
         const double e1 = sqrt((cx - bx) * (cx - bx) + (cy - by) * (cy - by) + (cz - bz) * (cz - bz));
         const double e2 = sqrt((ax - cx) * (ax - cx) + (ay - cy) * (ay - cy) + (az - cz) * (az - cz));
         const double diam = dmax(e0, dmax(e1, e2));
-        const double phi_min = dmin(pa, dmin(pb, pc));
+        PREP_CONST double phi_min = dmin(pa, dmin(pb, pc));
+#ifdef PREP_STATS
+        const bool pcull = phi_min - diam > sx.cd;
+        if (pcull) atomicAdd(&g_prep_prof[11], 1ull);
+        if (pcull && bcull) atomicAdd(&g_prep_prof[12], 1ull);
+        if (!pcull && !bcull) atomicAdd(&g_prep_prof[13], 1ull);
+        if (bcull) phi_min = sx.cd + diam + 1.0;
+#endif
         if (!(phi_min - diam > sx.cd)) {
-            ps = sample(grid, (ax + bx + cx) / 3.0, (ay + by + cy) / 3.0, (az + bz + cz) / 3.0);
+            ps = cphi[threadIdx.x];
             ++ns;
             if (pa < ps) { ps = pa; which = 1; }
             if (pb < ps) { ps = pb; which = 2; }
@@ -212,6 +294,7 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int2 
         w->face = (int32_t)f | (which << 30);
         w->phi[0] = pa; w->phi[1] = pb; w->phi[2] = pc; w->phi[3] = ps;
     }
+    PREP_MARK(5);
 }
 
 // k_face_pgd: the projected-gradient descent of every surviving face
@@ -695,7 +778,9 @@ void launch_env_xf(int64_t E, const int32_t *env_sdf, const int32_t *env_mesh, c
                                                           pose_format, cd, xf, env_status, env_min_depth, work_count);
 }
 
-size_t face_prep_smem(int maxcv) { return (size_t)maxcv * (4 * sizeof(double) + 1); }
+size_t face_prep_smem(int maxcv) {
+    return (size_t)maxcv * (4 * sizeof(double) + sizeof(int) + 1) + (size_t)FACE_CHUNK * (sizeof(double) + sizeof(uint2) + sizeof(int));
+}
 
 void launch_face_prep(int64_t nblocks, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs,
                       const MeshDesc *meshes, const int64_t *cand_base, const Staging &st, int maxcv,

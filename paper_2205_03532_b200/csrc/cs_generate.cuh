@@ -21,7 +21,7 @@ constexpr int PGD_BLOCK = 128;
 #define REST_GRID 8
 #endif
 #ifndef PREP_MINB
-#define PREP_MINB 4  // 64 registers
+#define PREP_MINB 5  // 48 registers (measured best; 4 and 6 are slower)
 #endif
 constexpr int PGD_GRAB = 64;  // work items a warp claims per atomic
 constexpr int COMPACT_BLOCK = 256;
