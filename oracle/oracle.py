@@ -2,7 +2,9 @@
 
 ctypes front end for oracle/cs_oracle.c, the plain-C restatement of the
 reference hot path (contactsim generate_contacts / reduce_contacts and the
-SDF sampling kernels). Imported only by tests/, __graft_entry__.smoke() and
+SDF sampling kernels), and oracle/cs_oracle_solver.c, the contact solver that
+consumes its output (dynamics/solver.py ContactConstraints.build,
+dynamics/_kernels.py gauss_seidel_sweeps). Imported only by tests/, __graft_entry__.smoke() and
 bench.py's CPU-baseline leg, as the checker. The product package never imports
 this module.
 
@@ -32,7 +34,8 @@ def build() -> str:
 def lib():
     global _lib
     if _lib is None:
-        if not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(os.path.join(_HERE, "cs_oracle.c")):
+        srcs = [os.path.join(_HERE, f) for f in ("cs_oracle.c", "cs_oracle_solver.c")]
+        if not os.path.exists(_SO) or os.path.getmtime(_SO) < max(os.path.getmtime(f) for f in srcs if os.path.exists(f)):
             build()
         _lib = ctypes.CDLL(_SO)
         _lib.og_generate_contacts.restype = ctypes.c_int64
@@ -215,3 +218,56 @@ def collide_batched(grid: Grid, vertices, triangles, sdf_pose7, mesh_pose7, cont
 
 def num_threads() -> int:
     return int(lib().og_num_threads())
+
+
+# ---------------------------------------------------------------- contact solver (cs_oracle_solver.c)
+
+def _i64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def constraints_build(body_a, body_b, point, normal, depth, restitution, slop, ref, w_mat, vel, h, bias_factor):
+    """ContactConstraints.build (dynamics/solver.py:105-141) for one system; rows in
+    sweep order. Returns dict of ra, rb, tan1, tan2, kn, kt1, kt2, bias_target,
+    restitution_target."""
+    m = len(depth)
+    ba, bb = _i64(body_a), _i64(body_b)
+    pt, nr = _f64(point).reshape(m, 3), _f64(normal).reshape(m, 3)
+    dep = _f64(depth)
+    rest = _f64(np.broadcast_to(np.asarray(restitution, dtype=np.float64), (m,)))
+    sl = _f64(np.broadcast_to(np.asarray(slop, dtype=np.float64), (m,)))
+    ref_, W, v = _f64(ref), _f64(w_mat), _f64(vel)
+    out = {k: np.zeros((m, 3)) for k in ("ra", "rb", "tan1", "tan2")}
+    out.update({k: np.zeros(m) for k in ("kn", "kt1", "kt2", "bias_target", "restitution_target")})
+    lib().og_constraints_build(ctypes.c_int64(m), _p(ba), _p(bb), _p(pt), _p(nr), _p(dep), _p(rest), _p(sl),
+                               _p(ref_), _p(W), _p(v), ctypes.c_double(h), ctypes.c_double(bias_factor),
+                               *(_p(out[k]) for k in ("ra", "rb", "tan1", "tan2", "kn", "kt1", "kt2", "bias_target",
+                                                       "restitution_target")))
+    return out
+
+
+def gauss_seidel_sweeps(iters, w_mat, vel, imp, body_a, body_b, ra, rb, nrm, tan1, tan2, kn, kt1, kt2, target_vn,
+                        mu, lam_n, lam_t1, lam_t2, with_friction):
+    """dynamics/_kernels.py:52-115, same argument list; vel, imp, lam_* are updated
+    in place (they must be C-contiguous float64 arrays)."""
+    m = len(kn)
+    for a in (vel, imp, lam_n, lam_t1, lam_t2):
+        assert a.dtype == np.float64 and a.flags.c_contiguous
+    ba, bb = _i64(body_a), _i64(body_b)
+    args = [_f64(x) for x in (ra, rb, nrm, tan1, tan2, kn, kt1, kt2, target_vn,
+                              np.broadcast_to(np.asarray(mu, dtype=np.float64), (m,)))]
+    W = _f64(w_mat)
+    lib().og_gauss_seidel_sweeps(ctypes.c_int64(iters), _p(W), _p(vel), _p(imp), ctypes.c_int64(m), _p(ba),
+                                 _p(bb), *(_p(a) for a in args), _p(lam_n), _p(lam_t1), _p(lam_t2),
+                                 ctypes.c_int(1 if with_friction else 0))
+
+
+def body_wrenches(n_bodies, body_a, body_b, ra, rb, nrm, tan1, tan2, lam_n, lam_vel, lam_t1, lam_t2, h):
+    """ContactConstraints.body_wrenches (dynamics/solver.py:154-163)."""
+    m = len(lam_n)
+    out = np.zeros((n_bodies, 6))
+    ba, bb = _i64(body_a), _i64(body_b)
+    arrs = [_f64(x) for x in (ra, rb, nrm, tan1, tan2, lam_n, lam_vel, lam_t1, lam_t2)]
+    lib().og_body_wrenches(ctypes.c_int64(m), _p(ba), _p(bb), *(_p(a) for a in arrs),
+                           ctypes.c_double(h), _p(out))
+    return out
