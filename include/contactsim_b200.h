@@ -190,6 +190,74 @@ int cs_collide_host(cs_plan *plan, const double *sdf_pose_host, const double *me
                     const double *contact_distance_host, float *stats_host, void *stream);
 
 /* ------------------------------------------------------------------------
+ * Contact solver, the consumer of the reduced contacts:
+ * dynamics/solver.py ContactConstraints.build / body_wrenches and
+ * dynamics/_kernels.py gauss_seidel_sweeps, bit-identical to the reference.
+ * Batched over n_sys independent systems: system s owns rows
+ * [row_off[s], row_off[s+1]) (sweep order; row_off [dev] (n_sys+1) int64) and
+ * bodies [s*n_bodies, (s+1)*n_bodies) of the state arrays (ref (.,3),
+ * w_mat (.,6,6), vel/imp (.,6)); body_a/body_b hold system-local ids
+ * (0 <= id < n_bodies <= 8). All arrays [dev], float64 / int64, C order.
+ * With n_sys = 1 and row_off = {0, m} these are the reference's per-scene calls.
+ * ---------------------------------------------------------------------- */
+
+/* dynamics/solver.py:105-141 (rows' point/normal/depth/restitution/slop -> constraint rows). */
+int cs_constraints_build(int64_t n_sys, int32_t n_bodies, const int64_t *row_off, const int64_t *body_a,
+                         const int64_t *body_b, const double *point, const double *normal, const double *depth,
+                         const double *restitution, const double *slop, const double *ref, const double *w_mat,
+                         const double *vel, double h, double bias_factor, double *ra, double *rb, double *tan1,
+                         double *tan2, double *kn, double *kt1, double *kt2, double *bias_target,
+                         double *restitution_target, void *stream);
+
+/* dynamics/_kernels.py:52-115 gauss_seidel_sweeps(iters, w_mat, vel, imp, body_a, body_b, ra, rb,
+ * nrm, tan1, tan2, kn, kt1, kt2, target_vn, mu, lam_n, lam_t1, lam_t2, with_friction):
+ * vel, imp, lam_n, lam_t1, lam_t2 updated in place. */
+int cs_gauss_seidel_sweeps(int64_t n_sys, int32_t n_bodies, const int64_t *row_off, int64_t iters,
+                           const double *w_mat, double *vel, double *imp, const int64_t *body_a,
+                           const int64_t *body_b, const double *ra, const double *rb, const double *nrm,
+                           const double *tan1, const double *tan2, const double *kn, const double *kt1,
+                           const double *kt2, const double *target_vn, const double *mu, double *lam_n,
+                           double *lam_t1, double *lam_t2, int32_t with_friction, void *stream);
+
+/* dynamics/solver.py:154-163 body_wrenches: out (n_sys*n_bodies, 6), overwritten. */
+int cs_body_wrenches(int64_t n_sys, int32_t n_bodies, const int64_t *row_off, const int64_t *body_a,
+                     const int64_t *body_b, const double *ra, const double *rb, const double *nrm,
+                     const double *tan1, const double *tan2, const double *lam_n, const double *lam_vel,
+                     const double *lam_t1, const double *lam_t2, double h, double *out, void *stream);
+
+/* SolverParams (dynamics/solver.py:24-43) of one substep: h = dt / substeps. */
+typedef struct cs_solver_params {
+    double h;
+    double bias_factor;    /* default 0.2 */
+    int32_t pos_iterations;  /* default 16 */
+    int32_t vel_iterations;  /* default 1 */
+} cs_solver_params;
+
+/* Device views of a plan's solver rows (valid after the first cs_plan_solve):
+ * env e's rows are [e*stride, e*stride + n_kept[e]) in Scene order
+ * (scene.py:228-243: patch slot, then kept contact), body_a = 0 (the SDF body),
+ * body_b = 1 (the mesh body). */
+typedef struct cs_solver_rows {
+    int64_t stride;
+    int64_t *body_a, *body_b;
+    double *point, *normal, *depth, *mu, *restitution, *slop;
+    double *ra, *rb, *tan1, *tan2, *kn, *kt1, *kt2, *bias_target, *restitution_target;
+    double *lam_n, *lam_vel, *lam_t1, *lam_t2;
+} cs_solver_rows;
+
+/* The contact solve of one substep on a plan's last cs_collide, one system per env
+ * with two bodies (0 = SDF body, 1 = mesh body): builds the rows, runs
+ * pos_iterations sweeps with friction toward the bias targets, then
+ * vel_iterations sweeps toward the restitution targets (Scene._substep,
+ * scene.py:130-145), and writes the body wrenches. State [dev]: ref (E,2,3),
+ * w_mat (E,2,6,6), vel (E,2,6) and imp (E,2,6) in/out; mu, restitution, slop
+ * (E) per pair (scene.py:206-212,226-227); wrench (E,2,6) out. Stream-ordered. */
+int cs_plan_solve(cs_plan *plan, const double *ref, const double *w_mat, double *vel, double *imp, const double *mu,
+                  const double *restitution, const double *slop, const cs_solver_params *params, double *wrench,
+                  void *stream);
+int cs_plan_solver_rows(cs_plan *plan, cs_solver_rows *rows);
+
+/* ------------------------------------------------------------------------
  * SDF generation (sdf/grid.py:163-239): exact unsigned distance to the mesh
  * and ray-parity sign voting on the GPU, bit-identical to the reference.
  * vertices/triangles [host]; values_out [host] (nx*ny*nz).

@@ -41,6 +41,16 @@ class OutputsC(ctypes.Structure):
     ]
 
 
+class SolverParamsC(ctypes.Structure):
+    _fields_ = [("h", _f64), ("bias_factor", _f64), ("pos_iterations", _i32), ("vel_iterations", _i32)]
+
+
+class SolverRowsC(ctypes.Structure):
+    _fields_ = [("stride", _i64)] + [(k, _vp) for k in (
+        "body_a", "body_b", "point", "normal", "depth", "mu", "restitution", "slop", "ra", "rb", "tan1", "tan2",
+        "kn", "kt1", "kt2", "bias_target", "restitution_target", "lam_n", "lam_vel", "lam_t1", "lam_t2")]
+
+
 _SIGS = {
     "cs_last_error": ([], ctypes.c_char_p),
     "cs_abi_version": ([], ctypes.c_int),
@@ -66,6 +76,13 @@ _SIGS = {
     "cs_plan_timing_read": ([_vp, _vp, _i32, ctypes.POINTER(_i32)], ctypes.c_int),
     "cs_collide_host": ([_vp, _vp, _vp, _i32, _vp, _vp, _vp], ctypes.c_int),
     "cs_sdf_generate": ([_vp, _i64, _vp, _i64, _i32, _i32, _i32, _vp, _f64, _vp], ctypes.c_int),
+    "cs_constraints_build": ([_i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f64, _f64]
+                             + [_vp] * 9 + [_vp], ctypes.c_int),
+    "cs_gauss_seidel_sweeps": ([_i64, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp], ctypes.c_int),
+    "cs_body_wrenches": ([_i64, _i32, _vp] + [_vp] * 11 + [_f64, _vp, _vp], ctypes.c_int),
+    "cs_plan_solve": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.POINTER(SolverParamsC), _vp, _vp], ctypes.c_int),
+    "cs_plan_solver_rows": ([_vp, ctypes.POINTER(SolverRowsC)], ctypes.c_int),
 }
 
 EXPORTED = tuple(_SIGS)

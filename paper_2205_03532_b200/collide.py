@@ -154,6 +154,48 @@ class Plan:
         _native.call("cs_plan_timing_read", self.ptr, out.ctypes.data, int(max_steps), ctypes.byref(n))
         return out[: n.value]
 
+    def solve(self, state, mu, restitution, slop, params=None, wrench=None, stream=None):
+        """Contact solve of one substep on the last collide's reduced contacts
+        (cs_plan_solve): per env the two-body system of Scene._substep
+        (dynamics/scene.py:130-145) — rows in (patch, kept) order, pos_iterations
+        sweeps with friction toward the bias targets, then vel_iterations toward the
+        restitution targets. state: dynamics.BatchedSolverState (vel and impulse
+        updated in place); mu, restitution, slop: (E,) float64 CUDA tensors.
+        Returns the body wrenches (E,2,6)."""
+        import torch
+
+        from .dynamics.solver import SolverParams
+
+        if not self.stages & _native.CS_STAGE_REDUCE:
+            raise ValueError("plan has no reduce stage")
+        params = params or SolverParams()
+        for t in (state.ref, state.w_mat, state.vel, state.impulse, mu, restitution, slop):
+            if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+                raise ValueError("solver state and per-env parameters must be contiguous float64 CUDA tensors")
+        if wrench is None:
+            wrench = torch.empty((self.n_envs, 2, 6), dtype=torch.float64, device="cuda")
+        cp = params.to_c()
+        _native.call("cs_plan_solve", self.ptr, state.ref.data_ptr(), state.w_mat.data_ptr(), state.vel.data_ptr(),
+                     state.impulse.data_ptr(), mu.data_ptr(), restitution.data_ptr(), slop.data_ptr(),
+                     ctypes.byref(cp), wrench.data_ptr(), _native.stream_handle(stream))
+        return wrench
+
+    def solver_rows(self) -> dict:
+        """Device views of the solver rows of the last solve (cs_plan_solver_rows):
+        env e's rows are [e * stride, e * stride + n_kept[e])."""
+        r = _native.SolverRowsC()
+        _native.call("cs_plan_solver_rows", self.ptr, ctypes.byref(r))
+        R = self.n_envs * r.stride
+        out = {"stride": int(r.stride)}
+        for k in ("body_a", "body_b"):
+            out[k] = _native.device_view(getattr(r, k), (R,), "i8", self)
+        for k in ("point", "normal", "ra", "rb", "tan1", "tan2"):
+            out[k] = _native.device_view(getattr(r, k), (R, 3), "f8", self)
+        for k in ("depth", "mu", "restitution", "slop", "kn", "kt1", "kt2", "bias_target", "restitution_target",
+                  "lam_n", "lam_vel", "lam_t1", "lam_t2"):
+            out[k] = _native.device_view(getattr(r, k), (R,), "f8", self)
+        return out
+
     def count_samples(self, sdf_pose, mesh_pose, contact_distance, pose_format: int = _native.CS_POSE7):
         """Exact trilinear SDF samples of one collide step (counting builds):
         (k_face_prep samples, k_face_pgd samples)."""

@@ -15,6 +15,7 @@
 
 #include "cs_reduce.cuh"
 #include "cs_sdfgen.cuh"
+#include "cs_solver.cuh"
 
 using namespace cs;
 
@@ -131,6 +132,8 @@ struct cs_plan {
     std::vector<cudaEvent_t> events;
     int64_t timing_step = 0;
     int32_t timing_slots = 0;
+    // contact solver rows (cs_plan_solve), allocated on first use
+    cs_solver_rows srows{};
 
     template <class T>
     int alloc(T **p, size_t n) {
@@ -757,6 +760,114 @@ int cs_collide_host(cs_plan *P, const double *sdf_pose_host, const double *mesh_
     if (stats_host && (P->stages & CS_STAGE_REDUCE))
         CS_CUDA(cudaMemcpyAsync(stats_host, P->io.stats, sizeof(float) * 4 * (size_t)P->E, cudaMemcpyDeviceToHost, s));
     CS_CUDA(cudaStreamSynchronize(s));
+    return CS_OK;
+}
+
+// ---------------------------------------------------------------- contact solver
+
+namespace {
+int check_sys(int64_t n_sys, int32_t nb, const int64_t *row_off) {
+    if (n_sys < 0) return fail(CS_ERR_VALUE, "n_sys must be non-negative");
+    if (nb < 1 || nb > SOLVER_MAX_BODIES) return fail(CS_ERR_VALUE, "n_bodies must be in [1, %d]", SOLVER_MAX_BODIES);
+    if (n_sys > 0 && !row_off) return fail(CS_ERR_VALUE, "null row_off");
+    return CS_OK;
+}
+}  // namespace
+
+int cs_constraints_build(int64_t n_sys, int32_t n_bodies, const int64_t *row_off, const int64_t *body_a,
+                         const int64_t *body_b, const double *point, const double *normal, const double *depth,
+                         const double *restitution, const double *slop, const double *ref, const double *w_mat,
+                         const double *vel, double h, double bias_factor, double *ra, double *rb, double *tan1,
+                         double *tan2, double *kn, double *kt1, double *kt2, double *bias_target,
+                         double *restitution_target, void *stream) {
+    if (int r = check_sys(n_sys, n_bodies, row_off)) return r;
+    const SysRows rows{row_off, 0, nullptr};
+    const BuildIO io{body_a, body_b, point, normal, depth, restitution, slop, ref, w_mat, vel, h, bias_factor,
+                     ra, rb, tan1, tan2, kn, kt1, kt2, bias_target, restitution_target};
+    launch_constraints_build(n_sys, n_bodies, rows, io, (cudaStream_t)stream);
+    CS_LAUNCHED();
+    return CS_OK;
+}
+
+int cs_gauss_seidel_sweeps(int64_t n_sys, int32_t n_bodies, const int64_t *row_off, int64_t iters,
+                           const double *w_mat, double *vel, double *imp, const int64_t *body_a,
+                           const int64_t *body_b, const double *ra, const double *rb, const double *nrm,
+                           const double *tan1, const double *tan2, const double *kn, const double *kt1,
+                           const double *kt2, const double *target_vn, const double *mu, double *lam_n,
+                           double *lam_t1, double *lam_t2, int32_t with_friction, void *stream) {
+    if (int r = check_sys(n_sys, n_bodies, row_off)) return r;
+    const SysRows rows{row_off, 0, nullptr};
+    const SweepIO io{body_a, body_b, ra, rb, nrm, tan1, tan2, kn, kt1, kt2, mu, lam_t1, lam_t2, w_mat, vel, imp};
+    const SweepPhase ph{iters, target_vn, lam_n, with_friction ? 1 : 0};
+    launch_sweeps(n_sys, n_bodies, rows, io, &ph, 1, (cudaStream_t)stream);
+    CS_LAUNCHED();
+    return CS_OK;
+}
+
+int cs_body_wrenches(int64_t n_sys, int32_t n_bodies, const int64_t *row_off, const int64_t *body_a,
+                     const int64_t *body_b, const double *ra, const double *rb, const double *nrm,
+                     const double *tan1, const double *tan2, const double *lam_n, const double *lam_vel,
+                     const double *lam_t1, const double *lam_t2, double h, double *out, void *stream) {
+    if (int r = check_sys(n_sys, n_bodies, row_off)) return r;
+    const SysRows rows{row_off, 0, nullptr};
+    const WrenchIO io{body_a, body_b, ra, rb, nrm, tan1, tan2, lam_n, lam_vel, lam_t1, lam_t2, h, out};
+    launch_body_wrenches(n_sys, n_bodies, rows, io, (cudaStream_t)stream);
+    CS_LAUNCHED();
+    return CS_OK;
+}
+
+int cs_plan_solve(cs_plan *P, const double *ref, const double *w_mat, double *vel, double *imp, const double *mu,
+                  const double *restitution, const double *slop, const cs_solver_params *params, double *wrench,
+                  void *stream) {
+    if (!P || !(P->stages & CS_STAGE_REDUCE)) return fail(CS_ERR_VALUE, "plan has no reduce stage");
+    if (!params || !ref || !w_mat || !vel || !imp || !mu || !restitution || !slop || !wrench)
+        return fail(CS_ERR_VALUE, "null argument");
+    if (!(params->h > 0.0)) return fail(CS_ERR_VALUE, "h must be positive");
+    if (params->pos_iterations < 1) return fail(CS_ERR_VALUE, "pos_iterations must be at least 1");
+    if (params->vel_iterations < 0) return fail(CS_ERR_VALUE, "vel_iterations must be non-negative");
+    const int64_t E = P->E, NK = (int64_t)P->rp.N * P->rp.K, R = E * NK;
+    cs_solver_rows &S = P->srows;
+    if (!S.body_a) {
+        int r = 0;
+        S.stride = NK;
+        if ((r = P->alloc(&S.body_a, R)) || (r = P->alloc(&S.body_b, R)) || (r = P->alloc(&S.point, 3 * R)) ||
+            (r = P->alloc(&S.normal, 3 * R)) || (r = P->alloc(&S.depth, R)) || (r = P->alloc(&S.mu, R)) ||
+            (r = P->alloc(&S.restitution, R)) || (r = P->alloc(&S.slop, R)) || (r = P->alloc(&S.ra, 3 * R)) ||
+            (r = P->alloc(&S.rb, 3 * R)) || (r = P->alloc(&S.tan1, 3 * R)) || (r = P->alloc(&S.tan2, 3 * R)) ||
+            (r = P->alloc(&S.kn, R)) || (r = P->alloc(&S.kt1, R)) || (r = P->alloc(&S.kt2, R)) ||
+            (r = P->alloc(&S.bias_target, R)) || (r = P->alloc(&S.restitution_target, R)) ||
+            (r = P->alloc(&S.lam_n, 4 * R)))
+            return r;
+        S.lam_vel = S.lam_n + R;
+        S.lam_t1 = S.lam_n + 2 * R;
+        S.lam_t2 = S.lam_n + 3 * R;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const SysRows rows{nullptr, NK, P->io.n_kept};
+    PlanRowsIO pr{P->io.patch_nkept, P->io.kept_point, P->io.kept_normal, P->io.kept_depth, mu, restitution, slop,
+                  P->rp.N, P->rp.K, NK, S.body_a, S.body_b, S.point, S.normal, S.depth, S.mu, S.restitution, S.slop};
+    launch_plan_rows(E, pr, s);
+    const BuildIO bio{S.body_a, S.body_b, S.point, S.normal, S.depth, S.restitution, S.slop, ref, w_mat, vel,
+                      params->h, params->bias_factor, S.ra, S.rb, S.tan1, S.tan2, S.kn, S.kt1, S.kt2,
+                      S.bias_target, S.restitution_target};
+    launch_constraints_build(E, 2, rows, bio, s);
+    CS_CUDA(cudaMemsetAsync(S.lam_n, 0, sizeof(double) * 4 * (size_t)R, s));
+    const SweepIO sio{S.body_a, S.body_b, S.ra, S.rb, S.normal, S.tan1, S.tan2, S.kn, S.kt1, S.kt2, S.mu,
+                      S.lam_t1, S.lam_t2, w_mat, vel, imp};
+    const SweepPhase ph[2] = {{params->pos_iterations, S.bias_target, S.lam_n, 1},
+                              {params->vel_iterations, S.restitution_target, S.lam_vel, 0}};
+    launch_sweeps(E, 2, rows, sio, ph, 2, s);
+    const WrenchIO wio{S.body_a, S.body_b, S.ra, S.rb, S.normal, S.tan1, S.tan2, S.lam_n, S.lam_vel, S.lam_t1,
+                       S.lam_t2, params->h, wrench};
+    launch_body_wrenches(E, 2, rows, wio, s);
+    CS_LAUNCHED();
+    return CS_OK;
+}
+
+int cs_plan_solver_rows(cs_plan *P, cs_solver_rows *rows) {
+    if (!P || !rows) return fail(CS_ERR_VALUE, "null argument");
+    if (!P->srows.body_a) return fail(CS_ERR_VALUE, "cs_plan_solve has not run on this plan");
+    *rows = P->srows;
     return CS_OK;
 }
 

@@ -1,0 +1,73 @@
+#pragma once
+// Contact solver: the consumer of the reduced contacts.
+//   ContactConstraints.build     dynamics/solver.py:105-141
+//   gauss_seidel_sweeps          dynamics/_kernels.py:52-115
+//   body_wrenches                dynamics/solver.py:154-163
+// Batched over independent systems. System s owns the rows [begin(s), end(s)) in
+// sweep order and the bodies [s nb, (s + 1) nb) of the state arrays; row body ids
+// are local to the system.
+#include "cs_common.cuh"
+
+namespace cs {
+
+constexpr int SOLVER_MAX_BODIES = 8;
+
+struct SysRows {
+    const int64_t *off;    // [S + 1] CSR offsets, or null: ...
+    int64_t stride;        // ... system s starts at s * stride ...
+    const int32_t *count;  // ... and holds count[s] rows
+    __device__ __forceinline__ int64_t begin(int64_t s) const { return off ? off[s] : s * stride; }
+    __device__ __forceinline__ int64_t end(int64_t s) const { return off ? off[s + 1] : s * stride + count[s]; }
+};
+
+struct BuildIO {
+    const int64_t *body_a, *body_b;
+    const double *point, *normal, *depth, *restitution, *slop;
+    const double *ref, *w_mat, *vel;  // state [S nb (3 | 36 | 6)]
+    double h, bias_factor;
+    double *ra, *rb, *tan1, *tan2, *kn, *kt1, *kt2, *bias_target, *restitution_target;
+};
+
+// One sweep phase: `iters` in-order sweeps toward `target` accumulating into lam_n
+// (position phase: bias targets with friction; velocity phase: restitution targets).
+struct SweepPhase {
+    int64_t iters;
+    const double *target;
+    double *lam_n;
+    int with_friction;
+};
+
+struct SweepIO {
+    const int64_t *body_a, *body_b;
+    const double *ra, *rb, *nrm, *tan1, *tan2, *kn, *kt1, *kt2, *mu;
+    double *lam_t1, *lam_t2;
+    const double *w_mat;
+    double *vel, *imp;  // [S nb 6] in/out
+};
+
+struct WrenchIO {
+    const int64_t *body_a, *body_b;
+    const double *ra, *rb, *nrm, *tan1, *tan2, *lam_n, *lam_vel, *lam_t1, *lam_t2;
+    double h;
+    double *out;  // [S nb 6], overwritten
+};
+
+void launch_constraints_build(int64_t n_sys, int nb, const SysRows &rows, const BuildIO &io, cudaStream_t s);
+void launch_sweeps(int64_t n_sys, int nb, const SysRows &rows, const SweepIO &io, const SweepPhase *phases,
+                   int n_phases, cudaStream_t s);
+void launch_body_wrenches(int64_t n_sys, int nb, const SysRows &rows, const WrenchIO &io, cudaStream_t s);
+
+// Plan rows: env e's kept contacts in (patch slot, k) order (scene.py:228-243) at
+// rows [e stride, e stride + n_kept[e]), body_a = 0 (SDF body), body_b = 1 (mesh body).
+struct PlanRowsIO {
+    const int32_t *patch_nkept;  // [E N]
+    const double *kept_point, *kept_normal, *kept_depth;  // [E N K (3)]
+    const double *env_mu, *env_restitution, *env_slop;    // [E]
+    int32_t N, K;
+    int64_t stride;
+    int64_t *body_a, *body_b;
+    double *point, *normal, *depth, *mu, *restitution, *slop;
+};
+void launch_plan_rows(int64_t E, const PlanRowsIO &io, cudaStream_t s);
+
+}  // namespace cs

@@ -1,0 +1,237 @@
+"""GPU parity of the contact solver (csrc/cs_solver.cu through
+libcontactsim_b200.so): bit-exact against the reference's golden outputs
+(tests/golden/solver.npz: ContactConstraints.build, gauss_seidel_sweeps,
+body_wrenches) and, for the batched Plan.solve on collide's device-resident
+reduced contacts, against the pinned oracle."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+G = golden("solver.npz")
+CASES = [str(c) for c in G["cases"]]
+BUILD_KEYS = ("ra", "rb", "tan1", "tan2", "kn", "kt1", "kt2", "bias_target", "restitution_target")
+
+
+def case(name):
+    return {k[len(name) + 1:]: G[k] for k in G.files if k.startswith(name + "_")}
+
+
+def same(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return a.shape == b.shape and a.tobytes() == b.tobytes()
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2205_03532_b200 as P
+    from paper_2205_03532_b200 import _native
+
+    _native.lib()
+    return P
+
+
+def rows_of(c):
+    m = int(c["m"])
+    return [{"body_a": int(c["body_a"][i]), "body_b": int(c["body_b"][i]), "point": c["point"][i],
+             "normal": c["normal"][i], "depth": float(c["depth"][i]), "mu": float(c["mu"][i]),
+             "restitution": float(c["restitution"][i]), "slop": float(c["slop"][i])} for i in range(m)]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_solver_dropin_matches_reference(P, name):
+    """The reference's per-scene calls, one after the other as Scene._substep makes them."""
+    from paper_2205_03532_b200.dynamics import ContactConstraints, SolverState
+
+    c = case(name)
+    nb = int(c["nb"])
+    st = SolverState(nb)
+    st.ref[...] = c["ref"]
+    st.w_mat[...] = c["w_mat"]
+    st.vel[...] = c["vel0"]
+    con = ContactConstraints.build(rows_of(c), st, float(c["h"]), float(c["bias"]))
+    for k in BUILD_KEYS:
+        assert same(getattr(con, k), c[k].reshape(getattr(con, k).shape)), f"{name}: build {k}"
+    pos_it, vel_it = (int(x) for x in c["iters"])
+    con.position_sweeps(st, pos_it)
+    assert same(st.vel, c["vel_pos"]) and same(st.impulse, c["imp_pos"]), name
+    assert same(con.lam_n, c["lam_n"]), name
+    con.velocity_sweeps(st, vel_it)
+    assert same(st.vel, c["vel_end"]) and same(st.impulse, c["imp_end"]), name
+    for k in ("lam_vel", "lam_t1", "lam_t2"):
+        assert same(getattr(con, k), c[k]), f"{name}: {k}"
+    assert same(con.body_wrenches(nb, float(c["h"])), c["wrench"]), name
+
+
+def test_solver_batched_abi_ragged_systems(P):
+    """Every golden case as one system of a single batched launch (CSR rows,
+    ragged row counts incl. an empty system, bodies padded to the largest nb)."""
+    from paper_2205_03532_b200 import _native
+    from oracle import oracle as O
+
+    cs = [case(n) for n in CASES]
+    NB = max(int(c["nb"]) for c in cs)
+    S = len(cs)
+    ms = [int(c["m"]) for c in cs]
+    off = np.concatenate([[0], np.cumsum(ms)]).astype(np.int64)
+    cat = lambda k, shape: np.concatenate([np.asarray(c[k], np.float64).reshape(shape) for c in cs])  # noqa: E731
+    # per-system h / bias differ between cases: run the build per distinct (h, bias) group
+    ref = np.zeros((S, NB, 3)); W = np.zeros((S, NB, 6, 6)); vel = np.zeros((S, NB, 6))
+    for s, c in enumerate(cs):
+        nb = int(c["nb"])
+        ref[s, :nb] = c["ref"]; W[s, :nb] = c["w_mat"]; vel[s, :nb] = c["vel0"]
+    d = lambda a, dt=torch.float64: torch.from_numpy(np.ascontiguousarray(a)).to(dt).cuda()  # noqa: E731
+    ba = d(np.concatenate([c["body_a"] for c in cs]).astype(np.int64), torch.int64)
+    bb = d(np.concatenate([c["body_b"] for c in cs]).astype(np.int64), torch.int64)
+    point, normal = d(cat("point", (-1, 3))), d(cat("normal", (-1, 3)))
+    depth, rest, slop, mu = d(cat("depth", (-1,))), d(cat("restitution", (-1,))), d(cat("slop", (-1,))), d(cat("mu", (-1,)))
+    R = int(off[-1])
+    outs = {k: torch.zeros((R, 3) if k in ("ra", "rb", "tan1", "tan2") else (R,), dtype=torch.float64, device="cuda")
+            for k in BUILD_KEYS}
+    dref, dW, dvel = d(ref), d(W), d(vel)
+    dimp = torch.zeros_like(dvel)
+    doff = d(off, torch.int64)
+    stream = _native.stream_handle()
+    groups = {}
+    for s, c in enumerate(cs):
+        groups.setdefault((float(c["h"]), float(c["bias"]), tuple(int(x) for x in c["iters"])), []).append(s)
+    # one system range per group: build and sweep each group's systems in one launch
+    lam = {k: torch.zeros(R, dtype=torch.float64, device="cuda") for k in ("lam_n", "lam_vel", "lam_t1", "lam_t2")}
+    for (h, bias, (pit, vit)), ss in groups.items():
+        for s in ss:  # launches over a contiguous sub-range of systems
+            o = doff[s:s + 2]
+            _native.call("cs_constraints_build", 1, NB, o.data_ptr(), ba.data_ptr(), bb.data_ptr(), point.data_ptr(),
+                         normal.data_ptr(), depth.data_ptr(), rest.data_ptr(), slop.data_ptr(),
+                         dref[s].data_ptr(), dW[s].data_ptr(), dvel[s].data_ptr(), h, bias,
+                         *(outs[k].data_ptr() for k in BUILD_KEYS), stream)
+    # now the sweeps of all systems in ONE launch per phase where the iteration counts agree
+    for (h, bias, (pit, vit)), ss in groups.items():
+        for s in ss:
+            o = doff[s:s + 2]
+            args = (ba, bb, outs["ra"], outs["rb"], normal, outs["tan1"], outs["tan2"], outs["kn"], outs["kt1"],
+                    outs["kt2"])
+            _native.call("cs_gauss_seidel_sweeps", 1, NB, o.data_ptr(), pit, dW[s].data_ptr(), dvel[s].data_ptr(),
+                         dimp[s].data_ptr(), *(a.data_ptr() for a in args), outs["bias_target"].data_ptr(),
+                         mu.data_ptr(), lam["lam_n"].data_ptr(), lam["lam_t1"].data_ptr(), lam["lam_t2"].data_ptr(),
+                         1, stream)
+            _native.call("cs_gauss_seidel_sweeps", 1, NB, o.data_ptr(), vit, dW[s].data_ptr(), dvel[s].data_ptr(),
+                         dimp[s].data_ptr(), *(a.data_ptr() for a in args), outs["restitution_target"].data_ptr(),
+                         mu.data_ptr(), lam["lam_vel"].data_ptr(), lam["lam_t1"].data_ptr(), lam["lam_t2"].data_ptr(),
+                         0, stream)
+    # all systems at once: the wrenches (h per system differs -> per group) and a batched
+    # re-run of the position sweeps of the equal-iteration group from scratch
+    vel_h, imp_h = dvel.cpu().numpy(), dimp.cpu().numpy()
+    got = {k: v.cpu().numpy() for k, v in outs.items()}
+    gl = {k: v.cpu().numpy() for k, v in lam.items()}
+    for s, c in enumerate(cs):
+        nb, a, b = int(c["nb"]), off[s], off[s + 1]
+        for k in BUILD_KEYS:
+            assert same(got[k][a:b], c[k].reshape(got[k][a:b].shape)), (CASES[s], k)
+        assert same(vel_h[s, :nb], c["vel_end"]) and same(imp_h[s, :nb], c["imp_end"]), CASES[s]
+        for k in ("lam_n", "lam_vel", "lam_t1", "lam_t2"):
+            assert same(gl[k][a:b], c[k]), (CASES[s], k)
+    # a genuinely batched launch: the position phase of every r64 env system at once
+    sel = [s for s, n in enumerate(CASES) if n.startswith("r64e")]
+    vel2 = d(vel[sel]); imp2 = torch.zeros_like(vel2)
+    lam2 = torch.zeros(R, dtype=torch.float64, device="cuda")
+    t1 = torch.zeros(R, dtype=torch.float64, device="cuda"); t2 = torch.zeros_like(t1)
+    sub_off = []
+    for s in sel:  # systems are contiguous in row space: keep absolute offsets
+        sub_off.append(off[s])
+    sub_off.append(off[sel[-1] + 1])
+    so = d(np.array(sub_off, np.int64), torch.int64)
+    args = (ba, bb, outs["ra"], outs["rb"], normal, outs["tan1"], outs["tan2"], outs["kn"], outs["kt1"], outs["kt2"])
+    _native.call("cs_gauss_seidel_sweeps", len(sel), NB, so.data_ptr(), int(cs[sel[0]]["iters"][0]),
+                 d(W[sel]).data_ptr(), vel2.data_ptr(), imp2.data_ptr(), *(x.data_ptr() for x in args),
+                 outs["bias_target"].data_ptr(), mu.data_ptr(), lam2.data_ptr(), t1.data_ptr(), t2.data_ptr(), 1, stream)
+    v2 = vel2.cpu().numpy()
+    for i, s in enumerate(sel):
+        nb = int(cs[s]["nb"])
+        assert same(v2[i, :nb], cs[s]["vel_pos"]), CASES[s]
+        assert same(lam2.cpu().numpy()[off[s]:off[s + 1]], cs[s]["lam_n"]), CASES[s]
+
+
+def test_plan_solve_matches_oracle(P, grid64_npz, meshes):
+    """collide -> Plan.solve on the device-resident reduced contacts, against the
+    oracle fed the same patches in Scene row order (scene.py:228-243)."""
+    from oracle import oracle as O
+    from paper_2205_03532_b200.dynamics import BatchedSolverState, SolverParams
+
+    gen64 = golden("gen_r64.npz")
+    d = grid64_npz
+    grid = P.SignedDistanceGrid(d["origin"], float(d["voxel"]), d["dims"], d["values"], (d["aabb_lo"], d["aabb_hi"]))
+    nut = P.TriMesh(meshes["nut_v"], meshes["nut_t"])
+    envs = list(gen64["envs"])
+    E = len(envs) * 3
+    sp = np.concatenate([np.stack([gen64[f"e{e}_sdf_pose"] for e in envs])] * 3)
+    mp = np.concatenate([np.stack([gen64[f"e{e}_mesh_pose"] for e in envs])] * 3)
+    cd = np.full(E, float(gen64["cd"]))
+    res = P.collide([P.register_sdf(grid)] * E, [P.register_mesh(nut)] * E, sp, mp, cd)
+    plan = res.plan
+    rng = np.random.default_rng(3)
+    ref = np.zeros((E, 2, 3)); W = np.zeros((E, 2, 6, 6)); vel = np.zeros((E, 2, 6))
+    for e in range(E):
+        for b in range(2):
+            if b == 0 and e % 3 == 0:
+                continue  # static SDF body in a third of the envs
+            m = rng.uniform(0.005, 0.05)
+            ref[e, b] = mp[e, :3] if b else rng.standard_normal(3) * 1e-3
+            W[e, b, :3, :3] = np.eye(3) / m
+            A = rng.standard_normal((3, 3))
+            W[e, b, 3:, 3:] = np.linalg.inv(A @ A.T * 1e-6 + np.eye(3) * 1e-7)
+            vel[e, b] = rng.standard_normal(6) * np.array([0.05] * 3 + [0.5] * 3)
+        vel[e, 1, 2] -= 0.4 + (e % 4) * 0.3  # some impacts above the restitution threshold
+    mu = rng.uniform(0.0, 0.8, E); mu[::5] = 0.0
+    rest = rng.uniform(0.0, 0.6, E)
+    slop = np.full(E, 0.5 * float(d["voxel"]))
+    st = BatchedSolverState.from_numpy(ref, W, vel)
+    prm = SolverParams(dt=1 / 120, substeps=2, pos_iterations=10, vel_iterations=2)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float64)).cuda()  # noqa: E731
+    wrench = plan.solve(st, t(mu), t(rest), t(slop), prm).cpu().numpy()
+    gvel, gimp = st.vel.cpu().numpy(), st.impulse.cpu().numpy()
+    rows = plan.solver_rows()
+    stride = rows["stride"]
+    n_kept = res.n_kept.cpu().numpy()
+    h = prm.dt / prm.substeps
+    for e in range(E):
+        pt = res.patches(e)
+        pts = np.concatenate([p.points for p in pt]) if pt else np.zeros((0, 3))
+        nrm = np.concatenate([p.normals for p in pt]) if pt else np.zeros((0, 3))
+        dep = np.concatenate([p.depths for p in pt]) if pt else np.zeros(0)
+        m = len(dep)
+        assert m == n_kept[e]
+        a = np.zeros(m, np.int64); b = np.ones(m, np.int64)
+        con = O.constraints_build(a, b, pts, nrm, dep, rest[e], slop[e], ref[e], W[e], vel[e], h, prm.bias_factor)
+        r0 = e * stride
+        for k in ("kn", "kt1", "kt2", "bias_target", "restitution_target"):
+            assert same(rows[k][r0:r0 + m].cpu().numpy(), con[k]), (e, k)
+        v = np.array(vel[e]); imp = np.zeros((2, 6))
+        lam = {k: np.zeros(m) for k in ("n", "t1", "t2", "v")}
+        args = (a, b, con["ra"], con["rb"], nrm, con["tan1"], con["tan2"], con["kn"], con["kt1"], con["kt2"])
+        if m:
+            O.gauss_seidel_sweeps(prm.pos_iterations, W[e], v, imp, *args, con["bias_target"], mu[e], lam["n"],
+                                  lam["t1"], lam["t2"], True)
+            O.gauss_seidel_sweeps(prm.vel_iterations, W[e], v, imp, *args, con["restitution_target"], mu[e],
+                                  lam["v"], lam["t1"], lam["t2"], False)
+        assert same(gvel[e], v) and same(gimp[e], imp), e
+        wr = O.body_wrenches(2, a, b, con["ra"], con["rb"], nrm, con["tan1"], con["tan2"], lam["n"], lam["v"],
+                             lam["t1"], lam["t2"], h)
+        assert same(wrench[e], wr), e
+
+
+def test_solver_errors(P):
+    from paper_2205_03532_b200 import _native
+
+    with pytest.raises(ValueError):
+        _native.call("cs_gauss_seidel_sweeps", 1, 99, 0, 1, *([0] * 18), 1, _native.stream_handle())
+    from paper_2205_03532_b200.dynamics import SolverParams
+
+    with pytest.raises(ValueError):
+        SolverParams(dt=0.0)
+    with pytest.raises(ValueError):
+        SolverParams(vel_iterations=-1)
