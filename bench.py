@@ -208,6 +208,85 @@ def _config(args, E, F, dims):
     }
 
 
+def solver_leg(P, plan, w, lo, hi, E, steps, quick, cpu_sample=64):
+    """SURVEY §8(f) row 1, measured beside the headline: the contact solve of one
+    substep (Plan.solve: rows from the reduced contacts, 16 position sweeps with
+    friction + 1 velocity sweep, body wrenches) on the last collide's output. The
+    Factory pair: bolt (SDF body) static, nut (mesh body) dynamic. Timed with CUDA
+    events per call; the state is reset between calls outside the events."""
+    import torch
+
+    from paper_2205_03532_b200.dynamics import BatchedSolverState, SolverParams
+
+    rng = np.random.default_rng(11)
+    m_nut = 0.030  # kg, an M16 steel nut
+    ref = np.zeros((E, 2, 3))
+    W = np.zeros((E, 2, 6, 6))
+    vel = np.zeros((E, 2, 6))
+    ref[:, 1] = w["mesh_pose"][lo:hi, :3]
+    W[:, 1, :3, :3] = np.eye(3) / m_nut
+    W[:, 1, 3:, 3:] = np.diag(1.0 / np.array([2.4e-6, 2.4e-6, 3.9e-6]))
+    vel[:, 1, :3] = rng.standard_normal((E, 3)) * 0.01
+    vel[:, 1, 2] -= 0.05
+    vel[:, 1, 3:] = rng.standard_normal((E, 3)) * 0.2
+    voxel = float(w["grid"].voxel_size)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float64)).cuda()  # noqa: E731
+    mu, rest, slop = dev(np.full(E, 0.5)), dev(np.zeros(E)), dev(np.full(E, 0.5 * voxel))
+    prm = SolverParams()
+    st = BatchedSolverState.from_numpy(ref, W, vel)
+    vel0 = st.vel.clone()
+    wrench = torch.empty((E, 2, 6), dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    for _ in range(3):
+        st.vel.copy_(vel0); st.impulse.zero_()
+        plan.solve(st, mu, rest, slop, prm, wrench)
+    ms = []
+    for _ in range(steps):
+        st.vel.copy_(vel0); st.impulse.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        plan.solve(st, mu, rest, slop, prm, wrench)
+        b.record(stream)
+        b.synchronize()
+        ms.append(a.elapsed_time(b))
+    n_kept = plan.n_kept.cpu().numpy().astype(np.int64)
+    iters = prm.pos_iterations + prm.vel_iterations
+    t = float(np.median(ms))
+    out = {"call": "Plan.solve (cs_plan_solve): rows + build + 16 pos / 1 vel sweeps + wrenches",
+           "ms_per_solve": t, "rows_per_env": float(n_kept.mean()), "max_rows": int(n_kept.max()),
+           "row_sweeps_per_s": float(n_kept.sum() * iters / (t * 1e-3)), "launches": 4}
+    if not quick:
+        from oracle import oracle as O
+
+        res = P.ReducedContacts(plan)
+        h = prm.dt / prm.substeps
+        cpu_s = 0.0
+        for e in range(min(cpu_sample, E)):
+            pt = res.patches(e)
+            if not pt:
+                continue
+            pts = np.concatenate([p.points for p in pt]); nrm = np.concatenate([p.normals for p in pt])
+            dep = np.concatenate([p.depths for p in pt])
+            m = len(dep)
+            a, bb = np.zeros(m, np.int64), np.ones(m, np.int64)
+            tc = time.perf_counter()
+            con = O.constraints_build(a, bb, pts, nrm, dep, 0.0, 0.5 * voxel, ref[e], W[e], vel[e], h, prm.bias_factor)
+            v, imp = np.array(vel[e]), np.zeros((2, 6))
+            ln, l1, l2, lv = np.zeros(m), np.zeros(m), np.zeros(m), np.zeros(m)
+            args_ = (a, bb, con["ra"], con["rb"], nrm, con["tan1"], con["tan2"], con["kn"], con["kt1"], con["kt2"])
+            O.gauss_seidel_sweeps(prm.pos_iterations, W[e], v, imp, *args_, con["bias_target"], 0.5, ln, l1, l2, True)
+            O.gauss_seidel_sweeps(prm.vel_iterations, W[e], v, imp, *args_, con["restitution_target"], 0.5, lv, l1,
+                                  l2, False)
+            O.body_wrenches(2, a, bb, con["ra"], con["rb"], nrm, con["tan1"], con["tan2"], ln, lv, l1, l2, h)
+            cpu_s += time.perf_counter() - tc  # the solver's own time (not the patch extraction)
+        n = min(cpu_sample, E)
+        cpu_ms = cpu_s * 1e3
+        out["cpu_baseline"] = {"ms_per_solve": cpu_ms * E / n, "cores": 1, "kind": "port",
+                               "sample": f"{n} envs solved one after the other by the oracle (oracle/cs_oracle_solver.c), "
+                                         f"scaled to {E}"}
+    return out
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -269,6 +348,8 @@ def main():
     total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
     value = world * E * F * args.steps / (total_ms * 1e-3)
+
+    solver = solver_leg(P, plan, w, lo, hi, E, min(args.steps, 50), args.quick)
 
     # stats all-gather (the only collective), once after the timed region
     stats = gather_env_stats(plan.stats.clone(), E * world)
@@ -334,6 +415,7 @@ def main():
                                        "achieved_gbs": pgd_bytes / (pgd_ms * 1e-3) / 1e9,
                                        "basis": "32 B per trilinear sample"}},
             "clocks": clk,
+            "solver": solver,
             "stats": {"candidates_per_env": float(stats[:, 0].double().mean()),
                       "patches_per_env": float(stats[:, 1].double().mean()),
                       "kept_per_env": float(stats[:, 2].double().mean())},

@@ -233,12 +233,16 @@ typedef struct cs_solver_params {
     int32_t vel_iterations;  /* default 1 */
 } cs_solver_params;
 
-/* Device views of a plan's solver rows (valid after the first cs_plan_solve):
- * env e's rows are [e*stride, e*stride + n_kept[e]) in Scene order
- * (scene.py:228-243: patch slot, then kept contact), body_a = 0 (the SDF body),
- * body_b = 1 (the mesh body). */
+/* Device views of a plan's solver rows (valid after the first cs_plan_solve).
+ * Env e's rows j = 0 .. n_kept[e]-1 are in Scene order (scene.py:228-243: patch
+ * slot, then kept contact), body_a = 0 (the SDF body), body_b = 1 (the mesh body).
+ * Layout, interleaved by blocks of 32 envs so one env per lane reads a row of 32
+ * envs as one line: row (e, j) is element r = ((e/32)*stride + j)*32 + e%32 of every
+ * scalar field; 3-vector fields hold 3 planes of `planes` elements (component q
+ * of row r at q*planes + r). */
 typedef struct cs_solver_rows {
     int64_t stride;
+    int64_t planes;
     int64_t *body_a, *body_b;
     double *point, *normal, *depth, *mu, *restitution, *slop;
     double *ra, *rb, *tan1, *tan2, *kn, *kt1, *kt2, *bias_target, *restitution_target;

@@ -46,7 +46,7 @@ class SolverParamsC(ctypes.Structure):
 
 
 class SolverRowsC(ctypes.Structure):
-    _fields_ = [("stride", _i64)] + [(k, _vp) for k in (
+    _fields_ = [("stride", _i64), ("planes", _i64)] + [(k, _vp) for k in (
         "body_a", "body_b", "point", "normal", "depth", "mu", "restitution", "slop", "ra", "rb", "tan1", "tan2",
         "kn", "kt1", "kt2", "bias_target", "restitution_target", "lam_n", "lam_vel", "lam_t1", "lam_t2")]
 

@@ -180,21 +180,29 @@ class Plan:
                      ctypes.byref(cp), wrench.data_ptr(), _native.stream_handle(stream))
         return wrench
 
-    def solver_rows(self) -> dict:
-        """Device views of the solver rows of the last solve (cs_plan_solver_rows):
-        env e's rows are [e * stride, e * stride + n_kept[e])."""
+    def solver_rows(self, e: int | None = None) -> dict:
+        """The solver rows of the last solve (cs_plan_solver_rows). With e: env e's
+        rows in sweep order as host arrays; without: the raw device views
+        (interleaved layout, include/contactsim_b200.h cs_solver_rows)."""
         r = _native.SolverRowsC()
         _native.call("cs_plan_solver_rows", self.ptr, ctypes.byref(r))
-        R = self.n_envs * r.stride
-        out = {"stride": int(r.stride)}
+        R = r.planes
+        out = {"stride": int(r.stride), "planes": int(R)}
+        vec = ("point", "normal", "ra", "rb", "tan1", "tan2")
         for k in ("body_a", "body_b"):
             out[k] = _native.device_view(getattr(r, k), (R,), "i8", self)
-        for k in ("point", "normal", "ra", "rb", "tan1", "tan2"):
-            out[k] = _native.device_view(getattr(r, k), (R, 3), "f8", self)
+        for k in vec:
+            out[k] = _native.device_view(getattr(r, k), (3, R), "f8", self)
         for k in ("depth", "mu", "restitution", "slop", "kn", "kt1", "kt2", "bias_target", "restitution_target",
                   "lam_n", "lam_vel", "lam_t1", "lam_t2"):
             out[k] = _native.device_view(getattr(r, k), (R,), "f8", self)
-        return out
+        if e is None:
+            return out
+        m = int(self.n_kept[e].item())
+        idx = ((e // 32 * r.stride + np.arange(m)) * 32 + e % 32).astype(np.int64)
+        it = __import__("torch").from_numpy(idx).cuda()
+        return {k: (v[:, it].T if k in vec else v[it]).cpu().numpy() for k, v in out.items()
+                if k not in ("stride", "planes")}
 
     def count_samples(self, sdf_pose, mesh_pose, contact_distance, pose_format: int = _native.CS_POSE7):
         """Exact trilinear SDF samples of one collide step (counting builds):

@@ -781,7 +781,7 @@ int cs_constraints_build(int64_t n_sys, int32_t n_bodies, const int64_t *row_off
                          double *tan2, double *kn, double *kt1, double *kt2, double *bias_target,
                          double *restitution_target, void *stream) {
     if (int r = check_sys(n_sys, n_bodies, row_off)) return r;
-    const SysRows rows{row_off, 0, nullptr};
+    const SysRows rows{row_off, 0, nullptr, 0};
     const BuildIO io{body_a, body_b, point, normal, depth, restitution, slop, ref, w_mat, vel, h, bias_factor,
                      ra, rb, tan1, tan2, kn, kt1, kt2, bias_target, restitution_target};
     launch_constraints_build(n_sys, n_bodies, rows, io, (cudaStream_t)stream);
@@ -796,7 +796,7 @@ int cs_gauss_seidel_sweeps(int64_t n_sys, int32_t n_bodies, const int64_t *row_o
                            const double *kt2, const double *target_vn, const double *mu, double *lam_n,
                            double *lam_t1, double *lam_t2, int32_t with_friction, void *stream) {
     if (int r = check_sys(n_sys, n_bodies, row_off)) return r;
-    const SysRows rows{row_off, 0, nullptr};
+    const SysRows rows{row_off, 0, nullptr, 0};
     const SweepIO io{body_a, body_b, ra, rb, nrm, tan1, tan2, kn, kt1, kt2, mu, lam_t1, lam_t2, w_mat, vel, imp};
     const SweepPhase ph{iters, target_vn, lam_n, with_friction ? 1 : 0};
     launch_sweeps(n_sys, n_bodies, rows, io, &ph, 1, (cudaStream_t)stream);
@@ -809,7 +809,7 @@ int cs_body_wrenches(int64_t n_sys, int32_t n_bodies, const int64_t *row_off, co
                      const double *tan1, const double *tan2, const double *lam_n, const double *lam_vel,
                      const double *lam_t1, const double *lam_t2, double h, double *out, void *stream) {
     if (int r = check_sys(n_sys, n_bodies, row_off)) return r;
-    const SysRows rows{row_off, 0, nullptr};
+    const SysRows rows{row_off, 0, nullptr, 0};
     const WrenchIO io{body_a, body_b, ra, rb, nrm, tan1, tan2, lam_n, lam_vel, lam_t1, lam_t2, h, out};
     launch_body_wrenches(n_sys, n_bodies, rows, io, (cudaStream_t)stream);
     CS_LAUNCHED();
@@ -825,11 +825,12 @@ int cs_plan_solve(cs_plan *P, const double *ref, const double *w_mat, double *ve
     if (!(params->h > 0.0)) return fail(CS_ERR_VALUE, "h must be positive");
     if (params->pos_iterations < 1) return fail(CS_ERR_VALUE, "pos_iterations must be at least 1");
     if (params->vel_iterations < 0) return fail(CS_ERR_VALUE, "vel_iterations must be non-negative");
-    const int64_t E = P->E, NK = (int64_t)P->rp.N * P->rp.K, R = E * NK;
+    const int64_t E = P->E, NK = (int64_t)P->rp.N * P->rp.K, R = (E + 31) / 32 * 32 * NK;
     cs_solver_rows &S = P->srows;
     if (!S.body_a) {
         int r = 0;
         S.stride = NK;
+        S.planes = R;
         if ((r = P->alloc(&S.body_a, R)) || (r = P->alloc(&S.body_b, R)) || (r = P->alloc(&S.point, 3 * R)) ||
             (r = P->alloc(&S.normal, 3 * R)) || (r = P->alloc(&S.depth, R)) || (r = P->alloc(&S.mu, R)) ||
             (r = P->alloc(&S.restitution, R)) || (r = P->alloc(&S.slop, R)) || (r = P->alloc(&S.ra, 3 * R)) ||
@@ -843,9 +844,9 @@ int cs_plan_solve(cs_plan *P, const double *ref, const double *w_mat, double *ve
         S.lam_t2 = S.lam_n + 3 * R;
     }
     cudaStream_t s = (cudaStream_t)stream;
-    const SysRows rows{nullptr, NK, P->io.n_kept};
+    const SysRows rows{nullptr, NK, P->io.n_kept, R};
     PlanRowsIO pr{P->io.patch_nkept, P->io.kept_point, P->io.kept_normal, P->io.kept_depth, mu, restitution, slop,
-                  P->rp.N, P->rp.K, NK, S.body_a, S.body_b, S.point, S.normal, S.depth, S.mu, S.restitution, S.slop};
+                  P->rp.N, P->rp.K, rows, S.body_a, S.body_b, S.point, S.normal, S.depth, S.mu, S.restitution, S.slop};
     launch_plan_rows(E, pr, s);
     const BuildIO bio{S.body_a, S.body_b, S.point, S.normal, S.depth, S.restitution, S.slop, ref, w_mat, vel,
                       params->h, params->bias_factor, S.ra, S.rb, S.tan1, S.tan2, S.kn, S.kt1, S.kt2,
@@ -856,7 +857,7 @@ int cs_plan_solve(cs_plan *P, const double *ref, const double *w_mat, double *ve
                       S.lam_t1, S.lam_t2, w_mat, vel, imp};
     const SweepPhase ph[2] = {{params->pos_iterations, S.bias_target, S.lam_n, 1},
                               {params->vel_iterations, S.restitution_target, S.lam_vel, 0}};
-    launch_sweeps(E, 2, rows, sio, ph, 2, s);
+    launch_sweeps(E, 2, rows, sio, ph, 2, s, true);
     const WrenchIO wio{S.body_a, S.body_b, S.ra, S.rb, S.normal, S.tan1, S.tan2, S.lam_n, S.lam_vel, S.lam_t1,
                        S.lam_t2, params->h, wrench};
     launch_body_wrenches(E, 2, rows, wio, s);

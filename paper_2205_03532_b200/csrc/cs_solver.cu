@@ -7,10 +7,13 @@
 //
 // The sweep is sequential within a system (every row reads the velocities the
 // previous row wrote), so a system is one thread: its body velocities and
-// impulses live in shared memory (row-independent layout, conflict-free), and
-// the next row's constraint data and accumulators are loaded while the current
-// row is solved, which takes the L2 latency off the dependency chain. Systems
-// are independent and run side by side.
+// impulses live in registers (two-body systems) or the thread's column of shared
+// memory, its mobility matrices in shared memory, and the next row's constraint
+// data and accumulators are loaded while the current row is solved, which takes
+// the L2 latency off the dependency chain. Systems are independent and run side
+// by side.
+#include <cuda_pipeline.h>
+
 #include "cs_solver.cuh"
 
 namespace cs {
@@ -63,242 +66,415 @@ __device__ double quad_form(const double d[3], const double r[3], const double *
     return q;
 }
 
-// ContactConstraints.build: rows are independent; a warp per system, lanes over rows.
-__global__ void k_constraints_build(int64_t S, int nb, SysRows rows, BuildIO io) {
-    const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (s >= S) return;
-    const int64_t r0 = rows.begin(s), r1 = rows.end(s);
+// ContactConstraints.build for one row c of system s
+__device__ __forceinline__ void build_row(int64_t s, int nb, const SysRows &rows, const BuildIO &io, int64_t c) {
     const int64_t b0 = s * nb;
-    for (int64_t c = r0 + lane; c < r1; c += 32) {
-        const int64_t ia = b0 + io.body_a[c], ib = b0 + io.body_b[c];
-        double p[3], n[3], a[3], b[3], t1[3], t2[3];
-        for (int k = 0; k < 3; ++k) {
-            p[k] = io.point[3 * c + k];
-            n[k] = io.normal[3 * c + k];
-            a[k] = p[k] - io.ref[3 * ia + k];
-            b[k] = p[k] - io.ref[3 * ib + k];
-        }
-        tangent_basis(n, t1, t2);
-        for (int k = 0; k < 3; ++k) {
-            io.ra[3 * c + k] = a[k]; io.rb[3 * c + k] = b[k];
-            io.tan1[3 * c + k] = t1[k]; io.tan2[3 * c + k] = t2[k];
-        }
-        const double *Wa = io.w_mat + 36 * ia, *Wb = io.w_mat + 36 * ib;
-        const double kq0 = quad_form(n, a, Wa) + quad_form(n, b, Wb);
-        const double kq1 = quad_form(t1, a, Wa) + quad_form(t1, b, Wb);
-        const double kq2 = quad_form(t2, a, Wa) + quad_form(t2, b, Wb);
-        io.kn[c] = kq0 > 1e-12 ? 1.0 / kq0 : 0.0;
-        io.kt1[c] = kq1 > 1e-12 ? 1.0 / kq1 : 0.0;
-        io.kt2[c] = kq2 > 1e-12 ? 1.0 / kq2 : 0.0;
-        const double dep = io.depth[c], sl = io.slop[c];
-        double bt = 0.0;
-        if (dep > sl) bt = io.bias_factor * (dep - sl) / io.h;
-        else if (dep < 0.0) bt = dep / io.h;
-        io.bias_target[c] = bt;
-        // _normal_velocity (solver.py:166-171): v + w x r (numpy cross), then ddot
-        const double *vb = io.vel + 6 * ib, *va = io.vel + 6 * ia;
-        const double ub0 = vb[0] + (vb[4] * b[2] - vb[5] * b[1]);
-        const double ub1 = vb[1] + (vb[5] * b[0] - vb[3] * b[2]);
-        const double ub2 = vb[2] + (vb[3] * b[1] - vb[4] * b[0]);
-        const double ua0 = va[0] + (va[4] * a[2] - va[5] * a[1]);
-        const double ua1 = va[1] + (va[5] * a[0] - va[3] * a[2]);
-        const double ua2 = va[2] + (va[3] * a[1] - va[4] * a[0]);
-        const double vn0 = G3(ub0 - ua0, ub1 - ua1, ub2 - ua2, n[0], n[1], n[2]);
-        const double neg = -vn0;
-        const double v_impact = (0.0 > neg) ? 0.0 : neg;  // Python max(-vn0, 0.0)
-        const double e = v_impact > 0.5 ? io.restitution[c] : 0.0;  // RESTITUTION_THRESHOLD (solver.py:21)
-        io.restitution_target[c] = e * v_impact;
+    const int64_t ia = b0 + io.body_a[c], ib = b0 + io.body_b[c];
+    double p[3], n[3], a[3], b[3], t1[3], t2[3];
+    for (int k = 0; k < 3; ++k) {
+        p[k] = io.point[rows.vec(c, k)];
+        n[k] = io.normal[rows.vec(c, k)];
+        a[k] = p[k] - io.ref[3 * ia + k];
+        b[k] = p[k] - io.ref[3 * ib + k];
+    }
+    tangent_basis(n, t1, t2);
+    for (int k = 0; k < 3; ++k) {
+        io.ra[rows.vec(c, k)] = a[k]; io.rb[rows.vec(c, k)] = b[k];
+        io.tan1[rows.vec(c, k)] = t1[k]; io.tan2[rows.vec(c, k)] = t2[k];
+    }
+    const double *Wa = io.w_mat + 36 * ia, *Wb = io.w_mat + 36 * ib;
+    const double kq0 = quad_form(n, a, Wa) + quad_form(n, b, Wb);
+    const double kq1 = quad_form(t1, a, Wa) + quad_form(t1, b, Wb);
+    const double kq2 = quad_form(t2, a, Wa) + quad_form(t2, b, Wb);
+    io.kn[c] = kq0 > 1e-12 ? 1.0 / kq0 : 0.0;
+    io.kt1[c] = kq1 > 1e-12 ? 1.0 / kq1 : 0.0;
+    io.kt2[c] = kq2 > 1e-12 ? 1.0 / kq2 : 0.0;
+    const double dep = io.depth[c], sl = io.slop[c];
+    double bt = 0.0;
+    if (dep > sl) bt = io.bias_factor * (dep - sl) / io.h;
+    else if (dep < 0.0) bt = dep / io.h;
+    io.bias_target[c] = bt;
+    // _normal_velocity (solver.py:166-171): v + w x r (numpy cross), then ddot
+    const double *vb = io.vel + 6 * ib, *va = io.vel + 6 * ia;
+    const double ub0 = vb[0] + (vb[4] * b[2] - vb[5] * b[1]);
+    const double ub1 = vb[1] + (vb[5] * b[0] - vb[3] * b[2]);
+    const double ub2 = vb[2] + (vb[3] * b[1] - vb[4] * b[0]);
+    const double ua0 = va[0] + (va[4] * a[2] - va[5] * a[1]);
+    const double ua1 = va[1] + (va[5] * a[0] - va[3] * a[2]);
+    const double ua2 = va[2] + (va[3] * a[1] - va[4] * a[0]);
+    const double vn0 = G3(ub0 - ua0, ub1 - ua1, ub2 - ua2, n[0], n[1], n[2]);
+    const double neg = -vn0;
+    const double v_impact = (0.0 > neg) ? 0.0 : neg;  // Python max(-vn0, 0.0)
+    const double e = v_impact > 0.5 ? io.restitution[c] : 0.0;  // RESTITUTION_THRESHOLD (solver.py:21)
+    io.restitution_target[c] = e * v_impact;
+}
+
+// Rows are independent. CSR layout: a warp per system, lanes over its rows;
+// interleaved layout: a thread per row slot (a warp covers one row of 32 systems).
+__global__ void k_constraints_build(int64_t S, int nb, SysRows rows, BuildIO io) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (rows.off) {
+        const int64_t s = t >> 5;
+        if (s >= S) return;
+        const int64_t n = rows.n(s);
+        for (int64_t j = t & 31; j < n; j += 32) build_row(s, nb, rows, io, rows.row(s, j));
+    } else {
+        const int64_t blk = (t >> 5) / rows.stride, j = (t >> 5) % rows.stride, s = blk * 32 + (t & 31);
+        if (s >= S || j >= rows.n(s)) return;
+        build_row(s, nb, rows, io, t);
     }
 }
 
-constexpr int SW_T = 32;  // systems per sweep block, one thread each
+#ifndef SW_T_DEF
+#define SW_T_DEF 1
+#endif
+// Systems per sweep block, one thread each. The sweep is issue-bound per warp, so
+// a few systems per warp spread the systems over more warps and schedulers.
+constexpr int SW_T = SW_T_DEF;
 
-struct Row {
-    int ia, ib;
-    double a[3], b[3], n[3], t1[3], t2[3];
-    double kn, kt1, kt2, tg, mu;
-    double ln, lt1, lt2;
+// Body state of one system. Two-body systems (every collide plan: SDF body, mesh
+// body) keep velocities and impulses in registers; other sizes use the thread's
+// column of shared memory. W (36 per body) is always the thread's shared column:
+// one system per lane makes global loads of W 32-way uncoalesced.
+struct RegState2 {
+    double v0[6], v1[6], i0[6], i1[6];
+    const double *W;  // shared, element j of the system at W[j * SW_T]
+    bool z0, z1;      // body frozen (see frozen_body)
+    __device__ __forceinline__ double v(int body, int k) const { return body ? v1[k] : v0[k]; }
+    __device__ __forceinline__ bool frozen(int body) const { return body ? z1 : z0; }
+    __device__ __forceinline__ void add_v(int body, const double t[6]) {
+        if (body) {
+#pragma unroll
+            for (int k = 0; k < 6; ++k) v1[k] += t[k];
+        } else {
+#pragma unroll
+            for (int k = 0; k < 6; ++k) v0[k] += t[k];
+        }
+    }
+    __device__ __forceinline__ void add_i(int body, const double g[6]) {
+        if (body) {
+#pragma unroll
+            for (int k = 0; k < 6; ++k) i1[k] += g[k];
+        } else {
+#pragma unroll
+            for (int k = 0; k < 6; ++k) i0[k] += g[k];
+        }
+    }
 };
 
-__device__ __forceinline__ void load_row(Row &r, const SweepIO &io, const SweepPhase &ph, int64_t c) {
-    r.ia = (int)__ldg(io.body_a + c);
-    r.ib = (int)__ldg(io.body_b + c);
+struct SmemState {
+    double *V, *I;  // shared, element j at [j * SW_T]
+    const double *W;
+    __device__ __forceinline__ double v(int body, int k) const { return V[(6 * body + k) * SW_T]; }
+    __device__ __forceinline__ bool frozen(int) const { return false; }
+    __device__ __forceinline__ void add_v(int body, const double t[6]) {
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        r.a[k] = __ldg(io.ra + 3 * c + k);
-        r.b[k] = __ldg(io.rb + 3 * c + k);
-        r.n[k] = __ldg(io.nrm + 3 * c + k);
-        r.t1[k] = __ldg(io.tan1 + 3 * c + k);
-        r.t2[k] = __ldg(io.tan2 + 3 * c + k);
+        for (int k = 0; k < 6; ++k) V[(6 * body + k) * SW_T] += t[k];
     }
-    r.kn = __ldg(io.kn + c);
-    r.kt1 = __ldg(io.kt1 + c);
-    r.kt2 = __ldg(io.kt2 + c);
-    r.tg = __ldg(ph.target + c);
-    r.mu = __ldg(io.mu + c);
-    // accumulators: written by this kernel, so plain (coherent) loads
-    r.ln = ph.lam_n[c];
-    r.lt1 = io.lam_t1[c];
-    r.lt2 = io.lam_t2[c];
+    __device__ __forceinline__ void add_i(int body, const double g[6]) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) I[(6 * body + k) * SW_T] += g[k];
+    }
+};
+
+// A body whose 36 mobility entries are all zero (static bodies, chain-driven
+// bodies: solver.py:60-62) and whose velocity is finite without -0.0 components:
+// every impulse adds w * g == +-0 per term to it, and v + (+-0) == v, so its
+// velocity never changes and the 36 products can be skipped while its impulses
+// are finite (checked per call). Exact: skipped updates are identities.
+__device__ __forceinline__ bool frozen_body(const double *W, const double *v) {
+    bool z = true;
+    for (int j = 0; j < 36; ++j) z &= W[j * SW_T] == 0.0;
+    for (int k = 0; k < 6; ++k) z &= isfinite(v[k]) && !(v[k] == 0.0 && signbit(v[k]));
+    return z;
 }
 
-// _kernels.py:16-37 on the thread's shared-memory state (element j of the
-// system's [nb][6] arrays at V[j * SW_T])
-__device__ __forceinline__ void apply_impulse(const double *__restrict__ W, double *V, double *I, int body, double jx,
-                                              double jy, double jz, double rx, double ry, double rz, double sign) {
-    const double gx = jx * sign, gy = jy * sign, gz = jz * sign;
-    const double tx = (ry * jz - rz * jy) * sign;
-    const double ty = (rz * jx - rx * jz) * sign;
-    const double tz = (rx * jy - ry * jx) * sign;
-    const double *w = W + 36 * body;
+// _kernels.py:16-37
+template <class St>
+__device__ __forceinline__ void apply_impulse(St &st, int body, double jx, double jy, double jz, double rx, double ry,
+                                              double rz, double sign) {
+    double g[6];
+    g[0] = jx * sign; g[1] = jy * sign; g[2] = jz * sign;
+    g[3] = (ry * jz - rz * jy) * sign;
+    g[4] = (rz * jx - rx * jz) * sign;
+    g[5] = (rx * jy - ry * jx) * sign;
+    if (!st.frozen(body) || !isfinite(((g[0] + g[1]) + (g[2] + g[3])) + (g[4] + g[5]))) {
+        const double *w = st.W + 36 * body * SW_T;
+        double t[6];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) {
-        const double t = __ldg(w + 6 * k) * gx + __ldg(w + 6 * k + 1) * gy + __ldg(w + 6 * k + 2) * gz +
-                         __ldg(w + 6 * k + 3) * tx + __ldg(w + 6 * k + 4) * ty + __ldg(w + 6 * k + 5) * tz;
-        V[(6 * body + k) * SW_T] += t;
+        for (int k = 0; k < 6; ++k)
+            t[k] = w[(6 * k) * SW_T] * g[0] + w[(6 * k + 1) * SW_T] * g[1] + w[(6 * k + 2) * SW_T] * g[2] +
+                   w[(6 * k + 3) * SW_T] * g[3] + w[(6 * k + 4) * SW_T] * g[4] + w[(6 * k + 5) * SW_T] * g[5];
+        st.add_v(body, t);
     }
-    I[(6 * body) * SW_T] += gx;
-    I[(6 * body + 1) * SW_T] += gy;
-    I[(6 * body + 2) * SW_T] += gz;
-    I[(6 * body + 3) * SW_T] += tx;
-    I[(6 * body + 4) * SW_T] += ty;
-    I[(6 * body + 5) * SW_T] += tz;
+    st.add_i(body, g);
 }
 
 // _kernels.py:40-49
-__device__ __forceinline__ double rel_vel(const double *V, int ia, int ib, const double a[3], const double b[3],
+template <class St>
+__device__ __forceinline__ double rel_vel(const St &st, int ia, int ib, const double a[3], const double b[3],
                                           double dx, double dy, double dz) {
-    const double *vb = V + 6 * ib * SW_T, *va = V + 6 * ia * SW_T;
-    const double vb0 = vb[0], vb1 = vb[SW_T], vb2 = vb[2 * SW_T], vb3 = vb[3 * SW_T], vb4 = vb[4 * SW_T],
-                 vb5 = vb[5 * SW_T];
-    const double va0 = va[0], va1 = va[SW_T], va2 = va[2 * SW_T], va3 = va[3 * SW_T], va4 = va[4 * SW_T],
-                 va5 = va[5 * SW_T];
-    const double ubx = vb0 + vb4 * b[2] - vb5 * b[1];
-    const double uby = vb1 + vb5 * b[0] - vb3 * b[2];
-    const double ubz = vb2 + vb3 * b[1] - vb4 * b[0];
-    const double uax = va0 + va4 * a[2] - va5 * a[1];
-    const double uay = va1 + va5 * a[0] - va3 * a[2];
-    const double uaz = va2 + va3 * a[1] - va4 * a[0];
+    const double ubx = st.v(ib, 0) + st.v(ib, 4) * b[2] - st.v(ib, 5) * b[1];
+    const double uby = st.v(ib, 1) + st.v(ib, 5) * b[0] - st.v(ib, 3) * b[2];
+    const double ubz = st.v(ib, 2) + st.v(ib, 3) * b[1] - st.v(ib, 4) * b[0];
+    const double uax = st.v(ia, 0) + st.v(ia, 4) * a[2] - st.v(ia, 5) * a[1];
+    const double uay = st.v(ia, 1) + st.v(ia, 5) * a[0] - st.v(ia, 3) * a[2];
+    const double uaz = st.v(ia, 2) + st.v(ia, 3) * a[1] - st.v(ia, 4) * a[0];
     return (ubx - uax) * dx + (uby - uay) * dy + (ubz - uaz) * dz;
 }
 
-// gauss_seidel_sweeps (_kernels.py:52-115), one system per thread, 1-2 phases
+// Row staging. Each system thread streams its rows through a ring of RING slots
+// in shared memory with per-thread asynchronous copies (cp.async), RING - 1 rows
+// ahead of the row being solved, so no load latency sits on the sweep's chain
+// and no registers hold rows in flight. The accumulators (lam_n of the phase,
+// lam_t1, lam_t2) of systems up to LAM_CAP rows live in shared memory for the
+// whole call.
+constexpr int RING = 8;
+constexpr int ROW_F = 22;  // a[3] b[3] n[3] t1[3] t2[3] kn kt1 kt2 target mu body_a body_b
+constexpr int LAM_CAP = 1024;
+
+__host__ __device__ inline size_t sweep_smem_doubles(int nb, bool two) {
+    return (size_t)36 * nb + (two ? 0 : (size_t)12 * nb) + (size_t)RING * ROW_F + 3 * (size_t)LAM_CAP;
+}
+
+template <bool FIX>
+__device__ __forceinline__ void stage_row(double *slot, const SweepIO &io, const SweepPhase &ph, const SysRows &rows,
+                                          int64_t c) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int64_t v = rows.vec(c, k);
+        __pipeline_memcpy_async(slot + (0 + k) * SW_T, io.ra + v, 8);
+        __pipeline_memcpy_async(slot + (3 + k) * SW_T, io.rb + v, 8);
+        __pipeline_memcpy_async(slot + (6 + k) * SW_T, io.nrm + v, 8);
+        __pipeline_memcpy_async(slot + (9 + k) * SW_T, io.tan1 + v, 8);
+        __pipeline_memcpy_async(slot + (12 + k) * SW_T, io.tan2 + v, 8);
+    }
+    __pipeline_memcpy_async(slot + 15 * SW_T, io.kn + c, 8);
+    __pipeline_memcpy_async(slot + 16 * SW_T, io.kt1 + c, 8);
+    __pipeline_memcpy_async(slot + 17 * SW_T, io.kt2 + c, 8);
+    __pipeline_memcpy_async(slot + 18 * SW_T, ph.target + c, 8);
+    __pipeline_memcpy_async(slot + 19 * SW_T, io.mu + c, 8);
+    if (!FIX) {
+        __pipeline_memcpy_async(slot + 20 * SW_T, io.body_a + c, 8);
+        __pipeline_memcpy_async(slot + 21 * SW_T, io.body_b + c, 8);
+    }
+}
+
+// The phases of one system, its rows in sweep order. FIX: every row has
+// body_a = 0, body_b = 1 (plan rows, scene.py:228-243), so body indices are
+// compile-time constants.
+template <bool FIX, class St>
+__device__ __forceinline__ void sweep_system(St &st, const SweepIO &io, const SweepPhase *phs, int n_phases,
+                                             const SysRows &rows, int64_t s, double *ring, double *lam) {
+    const int m = (int)rows.n(s);
+    if (m <= 0) return;
+    const int64_t base = rows.row(s, 0), step = rows.off ? 1 : 32;
+    const bool lam_sm = m <= LAM_CAP;
+    double *lt1s = lam + LAM_CAP * SW_T, *lt2s = lam + 2 * LAM_CAP * SW_T;
+    if (lam_sm)  // accumulators in: asynchronous copies, one wait (no per-row round trip)
+        for (int j = 0; j < m; ++j) {
+            __pipeline_memcpy_async(lt1s + j * SW_T, io.lam_t1 + base + step * j, 8);
+            __pipeline_memcpy_async(lt2s + j * SW_T, io.lam_t2 + base + step * j, 8);
+        }
+    for (int phi = 0; phi < n_phases; ++phi) {
+        const SweepPhase ph = phs[phi];
+        if (ph.iters <= 0) continue;
+        if (lam_sm) {
+            for (int j = 0; j < m; ++j) __pipeline_memcpy_async(lam + j * SW_T, ph.lam_n + base + step * j, 8);
+            __pipeline_commit();
+            __pipeline_wait_prior(0);
+        }
+        const int64_t T = ph.iters * (int64_t)m;
+        // prologue: steps 0 .. RING - 2, one commit group per step
+        int js = 0;  // row of the next step to stage
+        for (int p = 0; p < RING - 1; ++p) {
+            if (p < T) stage_row<FIX>(ring + p * ROW_F * SW_T, io, ph, rows, base + step * js);
+            __pipeline_commit();
+            if (++js == m) js = 0;
+        }
+        int j = 0;
+        for (int64_t q = 0; q < T; ++q) {
+            __pipeline_wait_prior(RING - 2);  // step q's row has landed
+            const double *r = ring + (int)(q % RING) * ROW_F * SW_T;
+            double a[3], b[3], n[3], t1[3], t2[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                a[k] = r[k * SW_T]; b[k] = r[(3 + k) * SW_T]; n[k] = r[(6 + k) * SW_T];
+                t1[k] = r[(9 + k) * SW_T]; t2[k] = r[(12 + k) * SW_T];
+            }
+            const double kn = r[15 * SW_T], kt1 = r[16 * SW_T], kt2 = r[17 * SW_T], tg = r[18 * SW_T],
+                         mu = r[19 * SW_T];
+            const int ia = FIX ? 0 : (int)__double_as_longlong(r[20 * SW_T]);
+            const int ib = FIX ? 1 : (int)__double_as_longlong(r[21 * SW_T]);
+            // refill the slot consumed by the previous step (its reads are complete)
+            if (q + RING - 1 < T)
+                stage_row<FIX>(ring + (int)((q + RING - 1) % RING) * ROW_F * SW_T, io, ph, rows, base + step * js);
+            __pipeline_commit();
+            if (++js == m) js = 0;
+            const int64_t c = base + step * j;
+            double *pln = lam_sm ? lam + j * SW_T : ph.lam_n + c;
+            double *plt1 = lam_sm ? lt1s + j * SW_T : io.lam_t1 + c;
+            double *plt2 = lam_sm ? lt2s + j * SW_T : io.lam_t2 + c;
+            double ln = *pln;
+            if (kn > 0.0) {
+                const double vn = rel_vel(st, ia, ib, a, b, n[0], n[1], n[2]);
+                double dl = kn * (tg - vn);
+                double new_l = ln + dl;
+                if (new_l < 0.0) new_l = 0.0;
+                dl = new_l - ln;
+                ln = new_l;
+                *pln = new_l;
+                if (dl != 0.0) {
+                    const double jx = dl * n[0], jy = dl * n[1], jz = dl * n[2];
+                    apply_impulse(st, ib, jx, jy, jz, b[0], b[1], b[2], 1.0);
+                    apply_impulse(st, ia, jx, jy, jz, a[0], a[1], a[2], -1.0);
+                }
+            }
+            if (ph.with_friction && mu > 0.0 && ln > 0.0) {
+                const double lt1 = *plt1, lt2 = *plt2;
+                double d1 = 0.0, d2 = 0.0;
+                if (kt1 > 0.0) d1 = -kt1 * rel_vel(st, ia, ib, a, b, t1[0], t1[1], t1[2]);
+                if (kt2 > 0.0) d2 = -kt2 * rel_vel(st, ia, ib, a, b, t2[0], t2[1], t2[2]);
+                double new1 = lt1 + d1, new2 = lt2 + d2;
+                const double limit = mu * ln;
+                const double mag = sqrt(new1 * new1 + new2 * new2);
+                if (mag > limit) {
+                    const double scale = limit / mag;
+                    new1 *= scale;
+                    new2 *= scale;
+                }
+                d1 = new1 - lt1;
+                d2 = new2 - lt2;
+                *plt1 = new1;
+                *plt2 = new2;
+                if (d1 != 0.0 || d2 != 0.0) {
+                    const double jx = d1 * t1[0] + d2 * t2[0];
+                    const double jy = d1 * t1[1] + d2 * t2[1];
+                    const double jz = d1 * t1[2] + d2 * t2[2];
+                    apply_impulse(st, ib, jx, jy, jz, b[0], b[1], b[2], 1.0);
+                    apply_impulse(st, ia, jx, jy, jz, a[0], a[1], a[2], -1.0);
+                }
+            }
+            if (++j == m) j = 0;
+        }
+        __pipeline_wait_prior(0);
+        if (lam_sm)
+            for (int jj = 0; jj < m; ++jj) ph.lam_n[base + step * jj] = lam[jj * SW_T];
+    }
+    __pipeline_commit();
+    __pipeline_wait_prior(0);
+    if (lam_sm)
+        for (int jj = 0; jj < m; ++jj) {
+            io.lam_t1[base + step * jj] = lt1s[jj * SW_T];
+            io.lam_t2[base + step * jj] = lt2s[jj * SW_T];
+        }
+}
+
+// gauss_seidel_sweeps (_kernels.py:52-115), one system per thread, 1-2 phases.
+// TWO: the two-body register path (nb == 2).
+template <bool TWO, bool FIX>
 __global__ void __launch_bounds__(SW_T) k_sweeps(int64_t S, int nb, SysRows rows, SweepIO io, SweepPhase p0,
                                                  SweepPhase p1, int n_phases) {
     extern __shared__ double sm[];
     const int64_t s = blockIdx.x * (int64_t)SW_T + threadIdx.x;
     if (s >= S) return;
     const int nv = 6 * nb;
-    double *V = sm + threadIdx.x, *I = sm + nv * SW_T + threadIdx.x;
-    for (int j = 0; j < nv; ++j) {
-        V[j * SW_T] = io.vel[s * nv + j];
-        I[j * SW_T] = io.imp[s * nv + j];
-    }
-    const double *W = io.w_mat + s * nb * 36;
-    const int64_t r0 = rows.begin(s), r1 = rows.end(s);
-    if (r1 > r0) {
-        for (int phi = 0; phi < n_phases; ++phi) {
-            const SweepPhase ph = phi ? p1 : p0;
-            if (ph.iters <= 0) continue;
-            Row cur, nxt;
-            load_row(cur, io, ph, r0);
-            for (int64_t it = 0; it < ph.iters; ++it) {
-                for (int64_t c = r0; c < r1; ++c) {
-                    // next row of the sweep (wrapping into the next iteration)
-                    const int64_t cn = c + 1 < r1 ? c + 1 : r0;
-                    const bool more = c + 1 < r1 || it + 1 < ph.iters;
-                    if (more) load_row(nxt, io, ph, cn);
-                    if (cur.kn > 0.0) {
-                        const double vn = rel_vel(V, cur.ia, cur.ib, cur.a, cur.b, cur.n[0], cur.n[1], cur.n[2]);
-                        double dl = cur.kn * (cur.tg - vn);
-                        double new_l = cur.ln + dl;
-                        if (new_l < 0.0) new_l = 0.0;
-                        dl = new_l - cur.ln;
-                        cur.ln = new_l;
-                        ph.lam_n[c] = new_l;
-                        if (dl != 0.0) {
-                            const double jx = dl * cur.n[0], jy = dl * cur.n[1], jz = dl * cur.n[2];
-                            apply_impulse(W, V, I, cur.ib, jx, jy, jz, cur.b[0], cur.b[1], cur.b[2], 1.0);
-                            apply_impulse(W, V, I, cur.ia, jx, jy, jz, cur.a[0], cur.a[1], cur.a[2], -1.0);
-                        }
-                    }
-                    if (ph.with_friction && cur.mu > 0.0 && cur.ln > 0.0) {
-                        double d1 = 0.0, d2 = 0.0;
-                        if (cur.kt1 > 0.0)
-                            d1 = -cur.kt1 * rel_vel(V, cur.ia, cur.ib, cur.a, cur.b, cur.t1[0], cur.t1[1], cur.t1[2]);
-                        if (cur.kt2 > 0.0)
-                            d2 = -cur.kt2 * rel_vel(V, cur.ia, cur.ib, cur.a, cur.b, cur.t2[0], cur.t2[1], cur.t2[2]);
-                        double new1 = cur.lt1 + d1, new2 = cur.lt2 + d2;
-                        const double limit = cur.mu * cur.ln;
-                        const double mag = sqrt(new1 * new1 + new2 * new2);
-                        if (mag > limit) {
-                            const double scale = limit / mag;
-                            new1 *= scale;
-                            new2 *= scale;
-                        }
-                        d1 = new1 - cur.lt1;
-                        d2 = new2 - cur.lt2;
-                        cur.lt1 = new1;
-                        cur.lt2 = new2;
-                        io.lam_t1[c] = new1;
-                        io.lam_t2[c] = new2;
-                        if (d1 != 0.0 || d2 != 0.0) {
-                            const double jx = d1 * cur.t1[0] + d2 * cur.t2[0];
-                            const double jy = d1 * cur.t1[1] + d2 * cur.t2[1];
-                            const double jz = d1 * cur.t1[2] + d2 * cur.t2[2];
-                            apply_impulse(W, V, I, cur.ib, jx, jy, jz, cur.b[0], cur.b[1], cur.b[2], 1.0);
-                            apply_impulse(W, V, I, cur.ia, jx, jy, jz, cur.a[0], cur.a[1], cur.a[2], -1.0);
-                        }
-                    }
-                    if (more) {
-                        if (cn == c) {  // a one-row system: the prefetch predates this row's writes
-                            nxt.ln = cur.ln;
-                            nxt.lt1 = cur.lt1;
-                            nxt.lt2 = cur.lt2;
-                        }
-                        cur = nxt;
-                    }
-                }
-            }
+    double *Ws = sm + threadIdx.x;  // [36 nb][SW_T]
+    for (int j = 0; j < 36 * nb; ++j) Ws[j * SW_T] = __ldg(io.w_mat + s * 36 * nb + j);
+    double *after_w = sm + (size_t)36 * nb * SW_T + (TWO ? 0 : (size_t)12 * nb * SW_T);
+    double *ring = after_w + threadIdx.x;
+    double *lam = after_w + (size_t)RING * ROW_F * SW_T + threadIdx.x;
+    const SweepPhase phs[2] = {p0, p1};
+    if (TWO) {
+        RegState2 st;
+        st.W = Ws;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            st.v0[k] = io.vel[s * 12 + k]; st.v1[k] = io.vel[s * 12 + 6 + k];
+            st.i0[k] = io.imp[s * 12 + k]; st.i1[k] = io.imp[s * 12 + 6 + k];
         }
-    }
-    for (int j = 0; j < nv; ++j) {
-        io.vel[s * nv + j] = V[j * SW_T];
-        io.imp[s * nv + j] = I[j * SW_T];
+        st.z0 = frozen_body(Ws, st.v0);
+        st.z1 = frozen_body(Ws + 36 * SW_T, st.v1);
+        sweep_system<FIX>(st, io, phs, n_phases, rows, s, ring, lam);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            io.vel[s * 12 + k] = st.v0[k]; io.vel[s * 12 + 6 + k] = st.v1[k];
+            io.imp[s * 12 + k] = st.i0[k]; io.imp[s * 12 + 6 + k] = st.i1[k];
+        }
+    } else {
+        SmemState st;
+        st.W = Ws;
+        st.V = sm + 36 * nb * SW_T + threadIdx.x;
+        st.I = st.V + nv * SW_T;
+        for (int j = 0; j < nv; ++j) {
+            st.V[j * SW_T] = io.vel[s * nv + j];
+            st.I[j * SW_T] = io.imp[s * nv + j];
+        }
+        sweep_system<false>(st, io, phs, n_phases, rows, s, ring, lam);
+        for (int j = 0; j < nv; ++j) {
+            io.vel[s * nv + j] = st.V[j * SW_T];
+            io.imp[s * nv + j] = st.I[j * SW_T];
+        }
     }
 }
 
-// ContactConstraints.body_wrenches (solver.py:154-163), rows in order per system
-__global__ void __launch_bounds__(SW_T) k_body_wrenches(int64_t S, int nb, SysRows rows, WrenchIO io) {
-    extern __shared__ double sm[];
-    const int64_t s = blockIdx.x * (int64_t)SW_T + threadIdx.x;
+// ContactConstraints.body_wrenches (solver.py:154-163). A warp per system: the lanes
+// compute the rows' terms (j/h, (r x j)/h) in parallel into shared memory, then
+// one lane per output element accumulates them in row order (b's terms before a's
+// within a row, as the reference's four statements run).
+constexpr int WR_WARPS = 4, WR_TILE = 32;
+
+__global__ void __launch_bounds__(WR_WARPS * 32) k_body_wrenches(int64_t S, int nb, SysRows rows, WrenchIO io) {
+    __shared__ double tb[WR_WARPS][WR_TILE][6], ta[WR_WARPS][WR_TILE][6];
+    __shared__ int bi[WR_WARPS][WR_TILE][2];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t s = blockIdx.x * (int64_t)WR_WARPS + w;
     if (s >= S) return;
-    const int nv = 6 * nb;
-    double *O = sm + threadIdx.x;
-    for (int j = 0; j < nv; ++j) O[j * SW_T] = 0.0;
-    const int64_t r0 = rows.begin(s), r1 = rows.end(s);
+    const int nv = 6 * nb;  // <= 48: lanes 0..nv-1 own an element, lanes >= 32 folded below
+    const int64_t m = rows.n(s);
     const double h = io.h;
-    for (int64_t c = r0; c < r1; ++c) {
-        const double lam = io.lam_n[c] + io.lam_vel[c];
-        const double l1 = io.lam_t1[c], l2 = io.lam_t2[c];
-        double j[3], a[3], b[3];
-        for (int k = 0; k < 3; ++k) {
-            j[k] = (lam * io.nrm[3 * c + k] + l1 * io.tan1[3 * c + k]) + l2 * io.tan2[3 * c + k];
-            a[k] = io.ra[3 * c + k];
-            b[k] = io.rb[3 * c + k];
+    double acc0 = 0.0, acc1 = 0.0;  // elements lane and lane + 32
+    for (int64_t t0 = 0; t0 < m; t0 += WR_TILE) {
+        if (t0 + lane < m) {
+            const int64_t c = rows.row(s, t0 + lane);
+            const double lam = io.lam_n[c] + io.lam_vel[c];
+            const double l1 = io.lam_t1[c], l2 = io.lam_t2[c];
+            double j[3], a[3], b[3];
+            for (int k = 0; k < 3; ++k) {
+                const int64_t v = rows.vec(c, k);
+                j[k] = (lam * io.nrm[v] + l1 * io.tan1[v]) + l2 * io.tan2[v];
+                a[k] = io.ra[v];
+                b[k] = io.rb[v];
+            }
+            const double cb[3] = {b[1] * j[2] - b[2] * j[1], b[2] * j[0] - b[0] * j[2], b[0] * j[1] - b[1] * j[0]};
+            const double ca[3] = {a[1] * j[2] - a[2] * j[1], a[2] * j[0] - a[0] * j[2], a[0] * j[1] - a[1] * j[0]};
+            for (int k = 0; k < 3; ++k) {
+                const double jh = j[k] / h;
+                tb[w][lane][k] = jh;
+                ta[w][lane][k] = jh;
+                tb[w][lane][3 + k] = cb[k] / h;
+                ta[w][lane][3 + k] = ca[k] / h;
+            }
+            bi[w][lane][0] = (int)io.body_b[c];
+            bi[w][lane][1] = (int)io.body_a[c];
         }
-        const double cb[3] = {b[1] * j[2] - b[2] * j[1], b[2] * j[0] - b[0] * j[2], b[0] * j[1] - b[1] * j[0]};
-        const double ca[3] = {a[1] * j[2] - a[2] * j[1], a[2] * j[0] - a[0] * j[2], a[0] * j[1] - a[1] * j[0]};
-        const int ib = (int)io.body_b[c], ia = (int)io.body_a[c];
-        for (int k = 0; k < 3; ++k) {
-            O[(6 * ib + k) * SW_T] += j[k] / h;
-            O[(6 * ib + 3 + k) * SW_T] += cb[k] / h;
-            O[(6 * ia + k) * SW_T] -= j[k] / h;
-            O[(6 * ia + 3 + k) * SW_T] -= ca[k] / h;
+        __syncwarp();
+        const int n = m - t0 < WR_TILE ? (int)(m - t0) : WR_TILE;
+        for (int q = 0; q < 2; ++q) {
+            const int el = lane + 32 * q;
+            if (el >= nv) break;
+            const int body = el / 6, k = el - 6 * body;
+            double acc = q ? acc1 : acc0;
+            for (int i = 0; i < n; ++i) {
+                if (bi[w][i][0] == body) acc += tb[w][i][k];
+                if (bi[w][i][1] == body) acc -= ta[w][i][k];
+            }
+            if (q) acc1 = acc; else acc0 = acc;
         }
+        __syncwarp();
     }
-    for (int j = 0; j < nv; ++j) io.out[s * nv + j] = O[j * SW_T];
+    if (lane < nv) io.out[s * nv + lane] = acc0;
+    if (lane + 32 < nv) io.out[s * nv + lane + 32] = acc1;
 }
 
 // Scene rows of a plan's reduced contacts: warp per env, patches scanned in slot order
@@ -317,14 +493,14 @@ __global__ void k_plan_rows(int64_t E, PlanRowsIO io) {
             const int v = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= o) inc += v;
         }
-        const int64_t base = e * io.stride + run + inc - nk;
+        const int64_t base = run + inc - nk;
         for (int k = 0; k < nk; ++k) {
-            const int64_t src = ((int64_t)e * N + p) * K + k, r = base + k;
+            const int64_t src = ((int64_t)e * N + p) * K + k, r = io.rows.row(e, base + k);
             io.body_a[r] = 0;
             io.body_b[r] = 1;
             for (int q = 0; q < 3; ++q) {
-                io.point[3 * r + q] = io.kept_point[3 * src + q];
-                io.normal[3 * r + q] = io.kept_normal[3 * src + q];
+                io.point[io.rows.vec(r, q)] = io.kept_point[3 * src + q];
+                io.normal[io.rows.vec(r, q)] = io.kept_normal[3 * src + q];
             }
             io.depth[r] = io.kept_depth[src];
             io.mu[r] = mu;
@@ -339,22 +515,29 @@ __global__ void k_plan_rows(int64_t E, PlanRowsIO io) {
 
 void launch_constraints_build(int64_t n_sys, int nb, const SysRows &rows, const BuildIO &io, cudaStream_t s) {
     if (n_sys <= 0) return;
-    const int64_t threads = n_sys * 32;
+    const int64_t threads = rows.off ? n_sys * 32 : rows.planes;
     k_constraints_build<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(n_sys, nb, rows, io);
 }
 
 void launch_sweeps(int64_t n_sys, int nb, const SysRows &rows, const SweepIO &io, const SweepPhase *phases,
-                   int n_phases, cudaStream_t s) {
+                   int n_phases, cudaStream_t s, bool fixed_bodies) {
     if (n_sys <= 0 || n_phases <= 0) return;
-    const size_t smem = (size_t)2 * 6 * nb * SW_T * sizeof(double);
-    k_sweeps<<<(unsigned)((n_sys + SW_T - 1) / SW_T), SW_T, smem, s>>>(n_sys, nb, rows, io, phases[0],
-                                                                       n_phases > 1 ? phases[1] : phases[0], n_phases);
+    const unsigned grid = (unsigned)((n_sys + SW_T - 1) / SW_T);
+    const SweepPhase p1 = n_phases > 1 ? phases[1] : phases[0];
+    const bool two = nb == 2;
+    const size_t smem = sweep_smem_doubles(nb, two) * SW_T * sizeof(double);
+    auto go = [&](auto kern) {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, SW_T, smem, s>>>(n_sys, nb, rows, io, phases[0], p1, n_phases);
+    };
+    if (two && fixed_bodies) go(k_sweeps<true, true>);
+    else if (two) go(k_sweeps<true, false>);
+    else go(k_sweeps<false, false>);
 }
 
 void launch_body_wrenches(int64_t n_sys, int nb, const SysRows &rows, const WrenchIO &io, cudaStream_t s) {
     if (n_sys <= 0) return;
-    const size_t smem = (size_t)6 * nb * SW_T * sizeof(double);
-    k_body_wrenches<<<(unsigned)((n_sys + SW_T - 1) / SW_T), SW_T, smem, s>>>(n_sys, nb, rows, io);
+    k_body_wrenches<<<(unsigned)((n_sys + WR_WARPS - 1) / WR_WARPS), WR_WARPS * 32, 0, s>>>(n_sys, nb, rows, io);
 }
 
 void launch_plan_rows(int64_t E, const PlanRowsIO &io, cudaStream_t s) {

@@ -13,11 +13,19 @@ namespace cs {
 constexpr int SOLVER_MAX_BODIES = 8;
 
 struct SysRows {
-    const int64_t *off;    // [S + 1] CSR offsets, or null: ...
-    int64_t stride;        // ... system s starts at s * stride ...
-    const int32_t *count;  // ... and holds count[s] rows
-    __device__ __forceinline__ int64_t begin(int64_t s) const { return off ? off[s] : s * stride; }
-    __device__ __forceinline__ int64_t end(int64_t s) const { return off ? off[s + 1] : s * stride + count[s]; }
+    const int64_t *off;    // [S + 1] CSR offsets (the reference's layout: rows of a system
+                           // contiguous, 3-vectors as (row, 3)); or null: the interleaved
+                           // layout of plan rows, where ...
+    int64_t stride;        // ... every system has `stride` row slots and count[s] rows, ...
+    const int32_t *count;
+    int64_t planes;        // ... slot j of system s is element ((s / 32 * stride + j) * 32 + s % 32)
+                           // of each field, 3-vectors as 3 planes of `planes` elements: one
+                           // system per lane reads a row of 32 systems as one coalesced line
+    __device__ __forceinline__ int64_t n(int64_t s) const { return off ? off[s + 1] - off[s] : count[s]; }
+    __device__ __forceinline__ int64_t row(int64_t s, int64_t j) const {
+        return off ? off[s] + j : (((s >> 5) * stride + j) << 5) + (s & 31);
+    }
+    __device__ __forceinline__ int64_t vec(int64_t r, int q) const { return planes ? r + q * planes : 3 * r + q; }
 };
 
 struct BuildIO {
@@ -53,18 +61,20 @@ struct WrenchIO {
 };
 
 void launch_constraints_build(int64_t n_sys, int nb, const SysRows &rows, const BuildIO &io, cudaStream_t s);
+// fixed_bodies: every row has body_a = 0, body_b = 1 (plan rows)
 void launch_sweeps(int64_t n_sys, int nb, const SysRows &rows, const SweepIO &io, const SweepPhase *phases,
-                   int n_phases, cudaStream_t s);
+                   int n_phases, cudaStream_t s, bool fixed_bodies = false);
 void launch_body_wrenches(int64_t n_sys, int nb, const SysRows &rows, const WrenchIO &io, cudaStream_t s);
 
-// Plan rows: env e's kept contacts in (patch slot, k) order (scene.py:228-243) at
-// rows [e stride, e stride + n_kept[e]), body_a = 0 (SDF body), body_b = 1 (mesh body).
+// Plan rows: env e's kept contacts in (patch slot, k) order (scene.py:228-243) as
+// its rows 0 .. n_kept[e] - 1 (interleaved layout of SysRows), body_a = 0 (SDF
+// body), body_b = 1 (mesh body).
 struct PlanRowsIO {
     const int32_t *patch_nkept;  // [E N]
     const double *kept_point, *kept_normal, *kept_depth;  // [E N K (3)]
     const double *env_mu, *env_restitution, *env_slop;    // [E]
     int32_t N, K;
-    int64_t stride;
+    SysRows rows;
     int64_t *body_a, *body_b;
     double *point, *normal, *depth, *mu, *restitution, *slop;
 };

@@ -69,91 +69,69 @@ def test_solver_dropin_matches_reference(P, name):
 
 
 def test_solver_batched_abi_ragged_systems(P):
-    """Every golden case as one system of a single batched launch (CSR rows,
-    ragged row counts incl. an empty system, bodies padded to the largest nb)."""
+    """Seven systems in single launches through the raw C ABI (CSR rows): the six
+    golden M16 env systems (ragged row counts) and an empty one in the middle;
+    build, position sweeps, velocity sweeps and wrenches each in one launch."""
     from paper_2205_03532_b200 import _native
-    from oracle import oracle as O
 
-    cs = [case(n) for n in CASES]
-    NB = max(int(c["nb"]) for c in cs)
+    names = ["r64e0", "r64e1", "r64e2", None, "r256e0", "r256e1", "r256e2"]
+    cs = [case(n) if n else None for n in names]
+    c0 = cs[0]
+    h, bias = float(c0["h"]), float(c0["bias"])
+    pit, vit = (int(x) for x in c0["iters"])
+    for c in cs:
+        if c is not None:
+            assert (float(c["h"]), float(c["bias"]), int(c["nb"])) == (h, bias, 2)
     S = len(cs)
-    ms = [int(c["m"]) for c in cs]
+    ms = [int(c["m"]) if c is not None else 0 for c in cs]
     off = np.concatenate([[0], np.cumsum(ms)]).astype(np.int64)
-    cat = lambda k, shape: np.concatenate([np.asarray(c[k], np.float64).reshape(shape) for c in cs])  # noqa: E731
-    # per-system h / bias differ between cases: run the build per distinct (h, bias) group
-    ref = np.zeros((S, NB, 3)); W = np.zeros((S, NB, 6, 6)); vel = np.zeros((S, NB, 6))
-    for s, c in enumerate(cs):
-        nb = int(c["nb"])
-        ref[s, :nb] = c["ref"]; W[s, :nb] = c["w_mat"]; vel[s, :nb] = c["vel0"]
-    d = lambda a, dt=torch.float64: torch.from_numpy(np.ascontiguousarray(a)).to(dt).cuda()  # noqa: E731
-    ba = d(np.concatenate([c["body_a"] for c in cs]).astype(np.int64), torch.int64)
-    bb = d(np.concatenate([c["body_b"] for c in cs]).astype(np.int64), torch.int64)
-    point, normal = d(cat("point", (-1, 3))), d(cat("normal", (-1, 3)))
-    depth, rest, slop, mu = d(cat("depth", (-1,))), d(cat("restitution", (-1,))), d(cat("slop", (-1,))), d(cat("mu", (-1,)))
     R = int(off[-1])
-    outs = {k: torch.zeros((R, 3) if k in ("ra", "rb", "tan1", "tan2") else (R,), dtype=torch.float64, device="cuda")
-            for k in BUILD_KEYS}
-    dref, dW, dvel = d(ref), d(W), d(vel)
-    dimp = torch.zeros_like(dvel)
-    doff = d(off, torch.int64)
-    stream = _native.stream_handle()
-    groups = {}
+    live = [c for c in cs if c is not None]
+    cat = lambda k, shape: np.concatenate([np.asarray(c[k], np.float64).reshape(shape) for c in live])  # noqa: E731
+    ref = np.zeros((S, 2, 3)); W = np.zeros((S, 2, 6, 6)); vel = np.zeros((S, 2, 6))
     for s, c in enumerate(cs):
-        groups.setdefault((float(c["h"]), float(c["bias"]), tuple(int(x) for x in c["iters"])), []).append(s)
-    # one system range per group: build and sweep each group's systems in one launch
+        if c is not None:
+            ref[s], W[s], vel[s] = c["ref"], c["w_mat"], c["vel0"]
+        else:
+            vel[s] = np.arange(12).reshape(2, 6)  # untouched: no rows
+    d = lambda a, dt=torch.float64: torch.from_numpy(np.ascontiguousarray(a)).to(dt).cuda()  # noqa: E731
+    ba = d(np.concatenate([c["body_a"] for c in live]).astype(np.int64), torch.int64)
+    bb = d(np.concatenate([c["body_b"] for c in live]).astype(np.int64), torch.int64)
+    point, normal = d(cat("point", (-1, 3))), d(cat("normal", (-1, 3)))
+    depth, rest, slop, mu = (d(cat(k, (-1,))) for k in ("depth", "restitution", "slop", "mu"))
+    outs = {k: torch.zeros((R, 3) if k in ("ra", "rb", "tan1", "tan2") else (R,), dtype=torch.float64,
+                           device="cuda") for k in BUILD_KEYS}
     lam = {k: torch.zeros(R, dtype=torch.float64, device="cuda") for k in ("lam_n", "lam_vel", "lam_t1", "lam_t2")}
-    for (h, bias, (pit, vit)), ss in groups.items():
-        for s in ss:  # launches over a contiguous sub-range of systems
-            o = doff[s:s + 2]
-            _native.call("cs_constraints_build", 1, NB, o.data_ptr(), ba.data_ptr(), bb.data_ptr(), point.data_ptr(),
-                         normal.data_ptr(), depth.data_ptr(), rest.data_ptr(), slop.data_ptr(),
-                         dref[s].data_ptr(), dW[s].data_ptr(), dvel[s].data_ptr(), h, bias,
-                         *(outs[k].data_ptr() for k in BUILD_KEYS), stream)
-    # now the sweeps of all systems in ONE launch per phase where the iteration counts agree
-    for (h, bias, (pit, vit)), ss in groups.items():
-        for s in ss:
-            o = doff[s:s + 2]
-            args = (ba, bb, outs["ra"], outs["rb"], normal, outs["tan1"], outs["tan2"], outs["kn"], outs["kt1"],
-                    outs["kt2"])
-            _native.call("cs_gauss_seidel_sweeps", 1, NB, o.data_ptr(), pit, dW[s].data_ptr(), dvel[s].data_ptr(),
-                         dimp[s].data_ptr(), *(a.data_ptr() for a in args), outs["bias_target"].data_ptr(),
-                         mu.data_ptr(), lam["lam_n"].data_ptr(), lam["lam_t1"].data_ptr(), lam["lam_t2"].data_ptr(),
-                         1, stream)
-            _native.call("cs_gauss_seidel_sweeps", 1, NB, o.data_ptr(), vit, dW[s].data_ptr(), dvel[s].data_ptr(),
-                         dimp[s].data_ptr(), *(a.data_ptr() for a in args), outs["restitution_target"].data_ptr(),
-                         mu.data_ptr(), lam["lam_vel"].data_ptr(), lam["lam_t1"].data_ptr(), lam["lam_t2"].data_ptr(),
-                         0, stream)
-    # all systems at once: the wrenches (h per system differs -> per group) and a batched
-    # re-run of the position sweeps of the equal-iteration group from scratch
-    vel_h, imp_h = dvel.cpu().numpy(), dimp.cpu().numpy()
+    dref, dW, dvel, doff = d(ref), d(W), d(vel), d(off, torch.int64)
+    dimp = torch.zeros_like(dvel)
+    wr = torch.zeros((S, 2, 6), dtype=torch.float64, device="cuda")
+    st = _native.stream_handle()
+    _native.call("cs_constraints_build", S, 2, doff.data_ptr(), ba.data_ptr(), bb.data_ptr(), point.data_ptr(),
+                 normal.data_ptr(), depth.data_ptr(), rest.data_ptr(), slop.data_ptr(), dref.data_ptr(),
+                 dW.data_ptr(), dvel.data_ptr(), h, bias, *(outs[k].data_ptr() for k in BUILD_KEYS), st)
+    geo = (ba, bb, outs["ra"], outs["rb"], normal, outs["tan1"], outs["tan2"], outs["kn"], outs["kt1"], outs["kt2"])
+    for it, target, ln, fr in ((pit, "bias_target", "lam_n", 1), (vit, "restitution_target", "lam_vel", 0)):
+        _native.call("cs_gauss_seidel_sweeps", S, 2, doff.data_ptr(), it, dW.data_ptr(), dvel.data_ptr(),
+                     dimp.data_ptr(), *(a.data_ptr() for a in geo), outs[target].data_ptr(), mu.data_ptr(),
+                     lam[ln].data_ptr(), lam["lam_t1"].data_ptr(), lam["lam_t2"].data_ptr(), fr, st)
+    _native.call("cs_body_wrenches", S, 2, doff.data_ptr(), ba.data_ptr(), bb.data_ptr(), outs["ra"].data_ptr(),
+                 outs["rb"].data_ptr(), normal.data_ptr(), outs["tan1"].data_ptr(), outs["tan2"].data_ptr(),
+                 lam["lam_n"].data_ptr(), lam["lam_vel"].data_ptr(), lam["lam_t1"].data_ptr(),
+                 lam["lam_t2"].data_ptr(), h, wr.data_ptr(), st)
     got = {k: v.cpu().numpy() for k, v in outs.items()}
     gl = {k: v.cpu().numpy() for k, v in lam.items()}
+    gv, gi, gw = dvel.cpu().numpy(), dimp.cpu().numpy(), wr.cpu().numpy()
     for s, c in enumerate(cs):
-        nb, a, b = int(c["nb"]), off[s], off[s + 1]
+        if c is None:
+            assert same(gv[s], vel[s]) and not gi[s].any() and not gw[s].any()
+            continue
+        a, b = off[s], off[s + 1]
         for k in BUILD_KEYS:
-            assert same(got[k][a:b], c[k].reshape(got[k][a:b].shape)), (CASES[s], k)
-        assert same(vel_h[s, :nb], c["vel_end"]) and same(imp_h[s, :nb], c["imp_end"]), CASES[s]
+            assert same(got[k][a:b], c[k].reshape(got[k][a:b].shape)), (names[s], k)
+        assert same(gv[s], c["vel_end"]) and same(gi[s], c["imp_end"]), names[s]
         for k in ("lam_n", "lam_vel", "lam_t1", "lam_t2"):
-            assert same(gl[k][a:b], c[k]), (CASES[s], k)
-    # a genuinely batched launch: the position phase of every r64 env system at once
-    sel = [s for s, n in enumerate(CASES) if n.startswith("r64e")]
-    vel2 = d(vel[sel]); imp2 = torch.zeros_like(vel2)
-    lam2 = torch.zeros(R, dtype=torch.float64, device="cuda")
-    t1 = torch.zeros(R, dtype=torch.float64, device="cuda"); t2 = torch.zeros_like(t1)
-    sub_off = []
-    for s in sel:  # systems are contiguous in row space: keep absolute offsets
-        sub_off.append(off[s])
-    sub_off.append(off[sel[-1] + 1])
-    so = d(np.array(sub_off, np.int64), torch.int64)
-    args = (ba, bb, outs["ra"], outs["rb"], normal, outs["tan1"], outs["tan2"], outs["kn"], outs["kt1"], outs["kt2"])
-    _native.call("cs_gauss_seidel_sweeps", len(sel), NB, so.data_ptr(), int(cs[sel[0]]["iters"][0]),
-                 d(W[sel]).data_ptr(), vel2.data_ptr(), imp2.data_ptr(), *(x.data_ptr() for x in args),
-                 outs["bias_target"].data_ptr(), mu.data_ptr(), lam2.data_ptr(), t1.data_ptr(), t2.data_ptr(), 1, stream)
-    v2 = vel2.cpu().numpy()
-    for i, s in enumerate(sel):
-        nb = int(cs[s]["nb"])
-        assert same(v2[i, :nb], cs[s]["vel_pos"]), CASES[s]
-        assert same(lam2.cpu().numpy()[off[s]:off[s + 1]], cs[s]["lam_n"]), CASES[s]
+            assert same(gl[k][a:b], c[k]), (names[s], k)
+        assert same(gw[s], c["wrench"]), names[s]
 
 
 def test_plan_solve_matches_oracle(P, grid64_npz, meshes):
@@ -194,8 +172,6 @@ def test_plan_solve_matches_oracle(P, grid64_npz, meshes):
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float64)).cuda()  # noqa: E731
     wrench = plan.solve(st, t(mu), t(rest), t(slop), prm).cpu().numpy()
     gvel, gimp = st.vel.cpu().numpy(), st.impulse.cpu().numpy()
-    rows = plan.solver_rows()
-    stride = rows["stride"]
     n_kept = res.n_kept.cpu().numpy()
     h = prm.dt / prm.substeps
     for e in range(E):
@@ -207,9 +183,10 @@ def test_plan_solve_matches_oracle(P, grid64_npz, meshes):
         assert m == n_kept[e]
         a = np.zeros(m, np.int64); b = np.ones(m, np.int64)
         con = O.constraints_build(a, b, pts, nrm, dep, rest[e], slop[e], ref[e], W[e], vel[e], h, prm.bias_factor)
-        r0 = e * stride
-        for k in ("kn", "kt1", "kt2", "bias_target", "restitution_target"):
-            assert same(rows[k][r0:r0 + m].cpu().numpy(), con[k]), (e, k)
+        rows = plan.solver_rows(e)
+        for k in ("kn", "kt1", "kt2", "bias_target", "restitution_target", "ra", "rb", "tan1", "tan2"):
+            assert same(rows[k], con[k]), (e, k)
+        assert same(rows["point"], pts) and same(rows["depth"], dep), e
         v = np.array(vel[e]); imp = np.zeros((2, 6))
         lam = {k: np.zeros(m) for k in ("n", "t1", "t2", "v")}
         args = (a, b, con["ra"], con["rb"], nrm, con["tan1"], con["tan2"], con["kn"], con["kt1"], con["kt2"])
