@@ -34,7 +34,7 @@ def build() -> str:
 def lib():
     global _lib
     if _lib is None:
-        srcs = [os.path.join(_HERE, f) for f in ("cs_oracle.c", "cs_oracle_solver.c")]
+        srcs = [os.path.join(_HERE, f) for f in ("cs_oracle.c", "cs_oracle_solver.c", "cs_oracle_broadphase.c")]
         if not os.path.exists(_SO) or os.path.getmtime(_SO) < max(os.path.getmtime(f) for f in srcs if os.path.exists(f)):
             build()
         _lib = ctypes.CDLL(_SO)
@@ -42,6 +42,7 @@ def lib():
         _lib.og_reduce_contacts.restype = ctypes.c_int
         _lib.og_num_threads.restype = ctypes.c_int
         _lib.og_sum.restype = ctypes.c_double
+        _lib.og_broadphase.restype = ctypes.c_int64
     return _lib
 
 
@@ -271,3 +272,26 @@ def body_wrenches(n_bodies, body_a, body_b, ra, rb, nrm, tan1, tan2, lam_n, lam_
     lib().og_body_wrenches(ctypes.c_int64(m), _p(ba), _p(bb), *(_p(a) for a in arrs),
                            ctypes.c_double(h), _p(out))
     return out
+
+
+# ---------------------------------------------------------------- broadphase (cs_oracle_broadphase.c)
+
+def world_aabb(mesh_lo, mesh_hi, pose7):
+    """RigidBody.world_aabb (dynamics/body.py:77-83) for n bodies: (lo, hi) (n, 3)."""
+    ml, mh, p = _f64(mesh_lo).reshape(-1, 3), _f64(mesh_hi).reshape(-1, 3), _f64(pose7).reshape(-1, 7)
+    n = len(ml)
+    lo, hi = np.zeros((n, 3)), np.zeros((n, 3))
+    lib().og_world_aabb(ctypes.c_int64(n), _p(ml), _p(mh), _p(p), _p(lo), _p(hi))
+    return lo, hi
+
+
+def broadphase_pairs(lo, hi, ids, margin):
+    """geometry/broadphase.py:25-44 for one scene: (P, 2) int64 sorted (id_a, id_b)."""
+    lo_, hi_ = _f64(lo).reshape(-1, 3), _f64(hi).reshape(-1, 3)
+    ids_ = _i64(ids)
+    n = len(ids_)
+    out = np.zeros((max(n * (n - 1) // 2, 1), 2), np.int64)
+    k = lib().og_broadphase(ctypes.c_int64(n), _p(lo_), _p(hi_), _p(ids_), ctypes.c_double(margin), _p(out))
+    if k < 0:
+        raise ValueError("non-finite AABB in broadphase input")
+    return out[:k]
