@@ -116,7 +116,7 @@ typedef struct cs_outputs {
     int32_t max_patches, per_patch_cap;
     int64_t total_capacity;
     const int64_t *cand_base;   /* [E] */
-    int32_t *env_status;        /* [E] 0 ok, 1 non-finite pose, 2 cd < 0 */
+    int32_t *env_status;        /* [E] 0 ok, 1 non-finite pose, 2 cd < 0, 3 inactive (cs_collide_active) */
     int32_t *n_cand;            /* [E] candidates (ContactSet length) */
     int32_t *n_patch;           /* [E] */
     int32_t *n_kept;            /* [E] sum of kept contacts over patches */
@@ -260,6 +260,42 @@ int cs_plan_solve(cs_plan *plan, const double *ref, const double *w_mat, double 
                   const double *restitution, const double *slop, const cs_solver_params *params, double *wrench,
                   void *stream);
 int cs_plan_solver_rows(cs_plan *plan, cs_solver_rows *rows);
+
+/* ------------------------------------------------------------------------
+ * Broadphase and multi-pair scenes, bit-identical to the
+ * reference. All arrays [dev].
+ * ---------------------------------------------------------------------- */
+
+/* dynamics/body.py:77-83 RigidBody.world_aabb (no margin) for n bodies: mesh AABBs
+ * (n,3) + poses (n,7) (px,py,pz,qw,qx,qy,qz) -> world lo/hi (n,3). */
+int cs_world_aabb(int64_t n, const double *mesh_lo, const double *mesh_hi, const double *pose7, double *lo,
+                  double *hi, void *stream);
+
+/* geometry/broadphase.py:25-68 broadphase_pairs over n_scenes independent scenes:
+ * scene s owns bodies [body_off[s], body_off[s+1]) of lo/hi (.,3) and ids (unique
+ * within the scene), inflated by margin[s]. Its pairs (id_a < id_b, sorted) go to
+ * rows [pair_off[s], pair_off[s] + n_pairs[s]) of pairs (.,2) int64; the capacity
+ * of scene s is pair_off[s+1] - pair_off[s]. status[s]: 0 ok, 1 non-finite box (the
+ * reference raises ValueError), 2 capacity exceeded, 3 more than 2048 bodies,
+ * 4 duplicate ids. Up to 64 bodies the all-pairs test, above it the sweep-and-prune
+ * test, as the reference (they differ only on inverted boxes). */
+int cs_broadphase(int64_t n_scenes, const int64_t *body_off, const double *lo, const double *hi, const int64_t *ids,
+                  const double *margin, const int64_t *pair_off, int64_t *pairs, int32_t *n_pairs, int32_t *status,
+                  void *stream);
+
+/* Pair slots -> active mask: active[t] = (slot_pair[t,0], slot_pair[t,1]) is among
+ * the broadphase pairs of scene slot_scene[t] (cs_broadphase output). */
+int cs_pair_slots_active(int64_t n_slots, const int64_t *slot_scene, const int64_t *slot_pair,
+                         const int64_t *pair_off, const int64_t *pairs, const int32_t *n_pairs, int32_t *active,
+                         void *stream);
+
+/* cs_collide with an active mask [dev] (E) int32: envs with active[e] == 0 are
+ * skipped (env_status 3, no candidates, no patches; their poses are not
+ * validated). A plan over every candidate pair slot of a set of multi-body
+ * scenes plus this mask from cs_pair_slots_active runs Scene._collect_contacts'
+ * pair loop (scene.py:188-227) for the pairs the broadphase reports. */
+int cs_collide_active(cs_plan *plan, const double *sdf_pose, const double *mesh_pose, int32_t pose_format,
+                      const double *contact_distance, const int32_t *active, void *stream);
 
 /* ------------------------------------------------------------------------
  * SDF generation (sdf/grid.py:163-239): exact unsigned distance to the mesh

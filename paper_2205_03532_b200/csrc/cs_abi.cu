@@ -16,6 +16,7 @@
 #include "cs_reduce.cuh"
 #include "cs_sdfgen.cuh"
 #include "cs_solver.cuh"
+#include "cs_broadphase.cuh"
 
 using namespace cs;
 
@@ -647,6 +648,11 @@ static int run_reduce(cs_plan *P, cudaStream_t s) {
 
 int cs_collide(cs_plan *P, const double *sdf_pose, const double *mesh_pose, int32_t pose_format,
                const double *contact_distance, void *stream) {
+    return cs_collide_active(P, sdf_pose, mesh_pose, pose_format, contact_distance, nullptr, stream);
+}
+
+int cs_collide_active(cs_plan *P, const double *sdf_pose, const double *mesh_pose, int32_t pose_format,
+                      const double *contact_distance, const int32_t *active, void *stream) {
     if (!P || !(P->stages & CS_STAGE_GENERATE)) return fail(CS_ERR_VALUE, "plan has no generate stage");
     if (pose_format != CS_POSE7 && pose_format != CS_POSE12) return fail(CS_ERR_VALUE, "bad pose format");
     cudaStream_t s = (cudaStream_t)stream;
@@ -658,7 +664,7 @@ int cs_collide(cs_plan *P, const double *sdf_pose, const double *mesh_pose, int3
     auto mark = [&](int i) { if (ev) cudaEventRecord(ev[i], s); };
     mark(0);
     launch_env_xf(P->E, P->env_sdf, P->env_mesh, d_sdfs, sdf_pose, mesh_pose, pose_format, contact_distance, P->xf,
-                  P->status, P->env_min_depth, P->st.work_count, s);
+                  P->status, P->env_min_depth, P->st.work_count, s, active);
     CS_LAUNCHED();
     mark(1);
     const PlanGrid *ug = P->uniform_sdf ? &P->uniform_grid : nullptr;
@@ -869,6 +875,38 @@ int cs_plan_solver_rows(cs_plan *P, cs_solver_rows *rows) {
     if (!P || !rows) return fail(CS_ERR_VALUE, "null argument");
     if (!P->srows.body_a) return fail(CS_ERR_VALUE, "cs_plan_solve has not run on this plan");
     *rows = P->srows;
+    return CS_OK;
+}
+
+// ---------------------------------------------------------------- broadphase
+
+int cs_world_aabb(int64_t n, const double *mesh_lo, const double *mesh_hi, const double *pose7, double *lo,
+                  double *hi, void *stream) {
+    if (n < 0) return fail(CS_ERR_VALUE, "n must be non-negative");
+    if (n > 0 && (!mesh_lo || !mesh_hi || !pose7 || !lo || !hi)) return fail(CS_ERR_VALUE, "null argument");
+    launch_world_aabb(n, mesh_lo, mesh_hi, pose7, lo, hi, (cudaStream_t)stream);
+    CS_LAUNCHED();
+    return CS_OK;
+}
+
+int cs_broadphase(int64_t n_scenes, const int64_t *body_off, const double *lo, const double *hi, const int64_t *ids,
+                  const double *margin, const int64_t *pair_off, int64_t *pairs, int32_t *n_pairs, int32_t *status,
+                  void *stream) {
+    if (n_scenes < 0) return fail(CS_ERR_VALUE, "n_scenes must be non-negative");
+    if (n_scenes > 0 && (!body_off || !lo || !hi || !ids || !margin || !pair_off || !pairs || !n_pairs || !status))
+        return fail(CS_ERR_VALUE, "null argument");
+    const BroadIO io{body_off, lo, hi, ids, margin, pair_off, pairs, n_pairs, status};
+    launch_broadphase(n_scenes, io, (cudaStream_t)stream);
+    CS_LAUNCHED();
+    return CS_OK;
+}
+
+int cs_pair_slots_active(int64_t n_slots, const int64_t *slot_scene, const int64_t *slot_pair,
+                         const int64_t *pair_off, const int64_t *pairs, const int32_t *n_pairs, int32_t *active,
+                         void *stream) {
+    if (n_slots < 0) return fail(CS_ERR_VALUE, "n_slots must be non-negative");
+    launch_pair_slots(n_slots, slot_scene, slot_pair, pair_off, pairs, n_pairs, active, (cudaStream_t)stream);
+    CS_LAUNCHED();
     return CS_OK;
 }
 

@@ -33,6 +33,20 @@ __device__ __forceinline__ double V3(double a0, double a1, double a2, double b0,
     return __fma_rn(a2, b2, __fma_rn(a0, b0, __dmul_rn(a1, b1)));
 }
 
+__host__ __device__ __forceinline__ void quat_to_matrix(const double *q, double *R) {
+    // math3d.py:45-53, float64 scalar arithmetic
+    double w = q[0], x = q[1], y = q[2], z = q[3];
+    R[0] = 1.0 - 2.0 * (y * y + z * z);
+    R[1] = 2.0 * (x * y - w * z);
+    R[2] = 2.0 * (x * z + w * y);
+    R[3] = 2.0 * (x * y + w * z);
+    R[4] = 1.0 - 2.0 * (x * x + z * z);
+    R[5] = 2.0 * (y * z - w * x);
+    R[6] = 2.0 * (x * z - w * y);
+    R[7] = 2.0 * (y * z + w * x);
+    R[8] = 1.0 - 2.0 * (x * x + y * y);
+}
+
 // Faces are processed in chunks of FACE_CHUNK consecutive triangles; each chunk
 // carries the sorted list of the distinct vertices it references and, per face,
 // the three corners as indices into that list (so a chunk samples every vertex once).

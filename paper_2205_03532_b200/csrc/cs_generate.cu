@@ -16,25 +16,12 @@
 
 namespace cs {
 
-__device__ __forceinline__ void quat_to_matrix(const double *q, double *R) {
-    // math3d.py:45-53, float64 scalar arithmetic
-    double w = q[0], x = q[1], y = q[2], z = q[3];
-    R[0] = 1.0 - 2.0 * (y * y + z * z);
-    R[1] = 2.0 * (x * y - w * z);
-    R[2] = 2.0 * (x * z + w * y);
-    R[3] = 2.0 * (x * y + w * z);
-    R[4] = 1.0 - 2.0 * (x * x + z * z);
-    R[5] = 2.0 * (y * z - w * x);
-    R[6] = 2.0 * (x * z - w * y);
-    R[7] = 2.0 * (y * z + w * x);
-    R[8] = 1.0 - 2.0 * (x * x + y * y);
-}
-
 __global__ void k_env_xf(int64_t E, const int32_t *__restrict__ env_sdf, const int32_t *__restrict__ env_mesh,
                          const SdfDesc *__restrict__ sdfs, const double *__restrict__ sdf_pose,
                          const double *__restrict__ mesh_pose, int pose_format, const double *__restrict__ cdv,
                          EnvXf *__restrict__ xf, int32_t *__restrict__ env_status,
-                         double *__restrict__ env_min_depth, unsigned *__restrict__ work_count) {
+                         double *__restrict__ env_min_depth, unsigned *__restrict__ work_count,
+                         const int32_t *__restrict__ active) {
     int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e == 0 && work_count) { work_count[0] = 0; work_count[1] = 0; work_count[2] = 0; work_count[3] = 0; }
     if (e >= E) return;
@@ -68,7 +55,9 @@ __global__ void k_env_xf(int64_t E, const int32_t *__restrict__ env_sdf, const i
     X.tol = 0.1 * S.voxel;  // CONVERGENCE_TOL_VOXELS * voxel (generation.py:20,91)
     double margin = cd + 2.0 * S.voxel;
     for (int k = 0; k < 3; ++k) { X.cull_lo[k] = S.lo[k] - margin; X.cull_hi[k] = S.hi[k] + margin; }
-    X.status = ok ? (cd < 0.0 ? 2 : 0) : 1;
+    // an inactive pair slot (active[e] == 0: no broadphase overlap this step) generates
+    // nothing and its pose is not validated
+    X.status = (active && !active[e]) ? 3 : (ok ? (cd < 0.0 ? 2 : 0) : 1);
     X.sdf = env_sdf[e];
     X.mesh = env_mesh[e];
     X.pad = 0;
@@ -772,10 +761,12 @@ __global__ void k_sdf_gradient(GridView g, const double *__restrict__ p, int64_t
 
 void launch_env_xf(int64_t E, const int32_t *env_sdf, const int32_t *env_mesh, const SdfDesc *sdfs,
                    const double *sdf_pose, const double *mesh_pose, int pose_format, const double *cd, EnvXf *xf,
-                   int32_t *env_status, double *env_min_depth, unsigned *work_count, cudaStream_t s) {
+                   int32_t *env_status, double *env_min_depth, unsigned *work_count, cudaStream_t s,
+                   const int32_t *active) {
     int bs = 128;
     k_env_xf<<<(unsigned)((E + bs - 1) / bs), bs, 0, s>>>(E, env_sdf, env_mesh, sdfs, sdf_pose, mesh_pose,
-                                                          pose_format, cd, xf, env_status, env_min_depth, work_count);
+                                                          pose_format, cd, xf, env_status, env_min_depth, work_count,
+                                                          active);
 }
 
 size_t face_prep_smem(int maxcv) {
