@@ -261,6 +261,22 @@ int cs_plan_solve(cs_plan *plan, const double *ref, const double *w_mat, double 
                   void *stream);
 int cs_plan_solver_rows(cs_plan *plan, cs_solver_rows *rows);
 
+/* The contact solve of one substep for multi-pair scenes (cs_collide_active plans):
+ * system s = scene s with n_bodies bodies, owning the pair slots (plan envs)
+ * [slot_off[s], slot_off[s+1]) (at most max_slots); its rows are the slots' kept
+ * contacts slot by slot in Scene order (scene.py:228-243) with body_a =
+ * slot_a[e] (the slot's SDF body) and body_b = slot_b[e] (its mesh body), both
+ * local to the scene; inactive slots contribute none. State [dev] per body
+ * (S*n_bodies): ref (.,3), w_mat (.,6,6), vel/imp (.,6) in/out; mu, restitution,
+ * slop [dev] per slot (E); wrench (S*n_bodies, 6) out. slot_off, slot_a, slot_b
+ * [dev] int64. Row views: cs_plan_multipair_rows (stride = max_slots*N*K,
+ * counts per system in n_rows). */
+int cs_multipair_solve(cs_plan *plan, int64_t n_sys, int32_t n_bodies, const int64_t *slot_off,
+                       const int64_t *slot_a, const int64_t *slot_b, int32_t max_slots, const double *ref,
+                       const double *w_mat, double *vel, double *imp, const double *mu, const double *restitution,
+                       const double *slop, const cs_solver_params *params, double *wrench, void *stream);
+int cs_plan_multipair_rows(cs_plan *plan, cs_solver_rows *rows, const int32_t **n_rows);
+
 /* ------------------------------------------------------------------------
  * Broadphase and multi-pair scenes, bit-identical to the
  * reference. All arrays [dev].

@@ -83,6 +83,9 @@ _SIGS = {
     "cs_body_wrenches": ([_i64, _i32, _vp] + [_vp] * 11 + [_f64, _vp, _vp], ctypes.c_int),
     "cs_plan_solve": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.POINTER(SolverParamsC), _vp, _vp], ctypes.c_int),
     "cs_plan_solver_rows": ([_vp, ctypes.POINTER(SolverRowsC)], ctypes.c_int),
+    "cs_multipair_solve": ([_vp, _i64, _i32, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                            ctypes.POINTER(SolverParamsC), _vp, _vp], ctypes.c_int),
+    "cs_plan_multipair_rows": ([_vp, ctypes.POINTER(SolverRowsC), ctypes.POINTER(_vp)], ctypes.c_int),
     "cs_world_aabb": ([_i64, _vp, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
     "cs_broadphase": ([_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
     "cs_pair_slots_active": ([_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),

@@ -133,8 +133,10 @@ struct cs_plan {
     std::vector<cudaEvent_t> events;
     int64_t timing_step = 0;
     int32_t timing_slots = 0;
-    // contact solver rows (cs_plan_solve), allocated on first use
-    cs_solver_rows srows{};
+    // contact solver rows (cs_plan_solve / cs_multipair_solve), allocated on first use
+    cs_solver_rows srows{}, mrows{};
+    int32_t *mrow_count = nullptr;
+    int64_t mrows_sys = 0;
 
     template <class T>
     int alloc(T **p, size_t n) {
@@ -822,59 +824,115 @@ int cs_body_wrenches(int64_t n_sys, int32_t n_bodies, const int64_t *row_off, co
     return CS_OK;
 }
 
-int cs_plan_solve(cs_plan *P, const double *ref, const double *w_mat, double *vel, double *imp, const double *mu,
-                  const double *restitution, const double *slop, const cs_solver_params *params, double *wrench,
-                  void *stream) {
-    if (!P || !(P->stages & CS_STAGE_REDUCE)) return fail(CS_ERR_VALUE, "plan has no reduce stage");
-    if (!params || !ref || !w_mat || !vel || !imp || !mu || !restitution || !slop || !wrench)
-        return fail(CS_ERR_VALUE, "null argument");
-    if (!(params->h > 0.0)) return fail(CS_ERR_VALUE, "h must be positive");
-    if (params->pos_iterations < 1) return fail(CS_ERR_VALUE, "pos_iterations must be at least 1");
-    if (params->vel_iterations < 0) return fail(CS_ERR_VALUE, "vel_iterations must be non-negative");
-    const int64_t E = P->E, NK = (int64_t)P->rp.N * P->rp.K, R = (E + 31) / 32 * 32 * NK;
-    cs_solver_rows &S = P->srows;
-    if (!S.body_a) {
-        int r = 0;
-        S.stride = NK;
-        S.planes = R;
-        if ((r = P->alloc(&S.body_a, R)) || (r = P->alloc(&S.body_b, R)) || (r = P->alloc(&S.point, 3 * R)) ||
-            (r = P->alloc(&S.normal, 3 * R)) || (r = P->alloc(&S.depth, R)) || (r = P->alloc(&S.mu, R)) ||
-            (r = P->alloc(&S.restitution, R)) || (r = P->alloc(&S.slop, R)) || (r = P->alloc(&S.ra, 3 * R)) ||
-            (r = P->alloc(&S.rb, 3 * R)) || (r = P->alloc(&S.tan1, 3 * R)) || (r = P->alloc(&S.tan2, 3 * R)) ||
-            (r = P->alloc(&S.kn, R)) || (r = P->alloc(&S.kt1, R)) || (r = P->alloc(&S.kt2, R)) ||
-            (r = P->alloc(&S.bias_target, R)) || (r = P->alloc(&S.restitution_target, R)) ||
-            (r = P->alloc(&S.lam_n, 4 * R)))
-            return r;
-        S.lam_vel = S.lam_n + R;
-        S.lam_t1 = S.lam_n + 2 * R;
-        S.lam_t2 = S.lam_n + 3 * R;
-    }
-    cudaStream_t s = (cudaStream_t)stream;
-    const SysRows rows{nullptr, NK, P->io.n_kept, R};
-    PlanRowsIO pr{P->io.patch_nkept, P->io.kept_point, P->io.kept_normal, P->io.kept_depth, mu, restitution, slop,
-                  P->rp.N, P->rp.K, rows, S.body_a, S.body_b, S.point, S.normal, S.depth, S.mu, S.restitution, S.slop};
-    launch_plan_rows(E, pr, s);
+namespace {
+int alloc_rows(cs_plan *P, cs_solver_rows &S, int64_t stride, int64_t R) {
+    int r = 0;
+    S.stride = stride;
+    S.planes = R;
+    if ((r = P->alloc(&S.body_a, R)) || (r = P->alloc(&S.body_b, R)) || (r = P->alloc(&S.point, 3 * R)) ||
+        (r = P->alloc(&S.normal, 3 * R)) || (r = P->alloc(&S.depth, R)) || (r = P->alloc(&S.mu, R)) ||
+        (r = P->alloc(&S.restitution, R)) || (r = P->alloc(&S.slop, R)) || (r = P->alloc(&S.ra, 3 * R)) ||
+        (r = P->alloc(&S.rb, 3 * R)) || (r = P->alloc(&S.tan1, 3 * R)) || (r = P->alloc(&S.tan2, 3 * R)) ||
+        (r = P->alloc(&S.kn, R)) || (r = P->alloc(&S.kt1, R)) || (r = P->alloc(&S.kt2, R)) ||
+        (r = P->alloc(&S.bias_target, R)) || (r = P->alloc(&S.restitution_target, R)) ||
+        (r = P->alloc(&S.lam_n, 4 * R)))
+        return r;
+    S.lam_vel = S.lam_n + R;
+    S.lam_t1 = S.lam_n + 2 * R;
+    S.lam_t2 = S.lam_n + 3 * R;
+    return CS_OK;
+}
+
+// rows -> build -> sweeps (position with friction, then velocity) -> wrenches
+int solve_rows(cs_plan *P, const cs_solver_rows &S, const SysRows &rows, int64_t n_sys, int nb, bool fixed,
+               const double *ref, const double *w_mat, double *vel, double *imp, const cs_solver_params *params,
+               double *wrench, cudaStream_t s) {
     const BuildIO bio{S.body_a, S.body_b, S.point, S.normal, S.depth, S.restitution, S.slop, ref, w_mat, vel,
                       params->h, params->bias_factor, S.ra, S.rb, S.tan1, S.tan2, S.kn, S.kt1, S.kt2,
                       S.bias_target, S.restitution_target};
-    launch_constraints_build(E, 2, rows, bio, s);
-    CS_CUDA(cudaMemsetAsync(S.lam_n, 0, sizeof(double) * 4 * (size_t)R, s));
+    launch_constraints_build(n_sys, nb, rows, bio, s);
+    CS_CUDA(cudaMemsetAsync(S.lam_n, 0, sizeof(double) * 4 * (size_t)S.planes, s));
     const SweepIO sio{S.body_a, S.body_b, S.ra, S.rb, S.normal, S.tan1, S.tan2, S.kn, S.kt1, S.kt2, S.mu,
                       S.lam_t1, S.lam_t2, w_mat, vel, imp};
     const SweepPhase ph[2] = {{params->pos_iterations, S.bias_target, S.lam_n, 1},
                               {params->vel_iterations, S.restitution_target, S.lam_vel, 0}};
-    launch_sweeps(E, 2, rows, sio, ph, 2, s, true);
+    launch_sweeps(n_sys, nb, rows, sio, ph, 2, s, fixed);
     const WrenchIO wio{S.body_a, S.body_b, S.ra, S.rb, S.normal, S.tan1, S.tan2, S.lam_n, S.lam_vel, S.lam_t1,
                        S.lam_t2, params->h, wrench};
-    launch_body_wrenches(E, 2, rows, wio, s);
+    launch_body_wrenches(n_sys, nb, rows, wio, s);
     CS_LAUNCHED();
     return CS_OK;
+}
+
+int check_solver_params(const cs_solver_params *params) {
+    if (!params) return fail(CS_ERR_VALUE, "null argument");
+    if (!(params->h > 0.0)) return fail(CS_ERR_VALUE, "h must be positive");
+    if (params->pos_iterations < 1) return fail(CS_ERR_VALUE, "pos_iterations must be at least 1");
+    if (params->vel_iterations < 0) return fail(CS_ERR_VALUE, "vel_iterations must be non-negative");
+    return CS_OK;
+}
+}  // namespace
+
+int cs_plan_solve(cs_plan *P, const double *ref, const double *w_mat, double *vel, double *imp, const double *mu,
+                  const double *restitution, const double *slop, const cs_solver_params *params, double *wrench,
+                  void *stream) {
+    if (!P || !(P->stages & CS_STAGE_REDUCE)) return fail(CS_ERR_VALUE, "plan has no reduce stage");
+    if (!ref || !w_mat || !vel || !imp || !mu || !restitution || !slop || !wrench)
+        return fail(CS_ERR_VALUE, "null argument");
+    if (int r = check_solver_params(params)) return r;
+    const int64_t E = P->E, NK = (int64_t)P->rp.N * P->rp.K, R = (E + 31) / 32 * 32 * NK;
+    cs_solver_rows &S = P->srows;
+    if (!S.body_a)
+        if (int r = alloc_rows(P, S, NK, R)) return r;
+    cudaStream_t s = (cudaStream_t)stream;
+    const SysRows rows{nullptr, NK, P->io.n_kept, R};
+    PlanRowsIO pr{P->io.patch_nkept, P->io.n_patch, P->io.kept_point, P->io.kept_normal, P->io.kept_depth, mu,
+                  restitution, slop, nullptr, nullptr, nullptr, P->rp.N, P->rp.K, rows, nullptr, S.body_a,
+                  S.body_b, S.point, S.normal, S.depth, S.mu, S.restitution, S.slop};
+    launch_plan_rows(E, pr, s);
+    return solve_rows(P, S, rows, E, 2, true, ref, w_mat, vel, imp, params, wrench, s);
 }
 
 int cs_plan_solver_rows(cs_plan *P, cs_solver_rows *rows) {
     if (!P || !rows) return fail(CS_ERR_VALUE, "null argument");
     if (!P->srows.body_a) return fail(CS_ERR_VALUE, "cs_plan_solve has not run on this plan");
     *rows = P->srows;
+    return CS_OK;
+}
+
+int cs_multipair_solve(cs_plan *P, int64_t n_sys, int32_t nb, const int64_t *slot_off, const int64_t *slot_a,
+                       const int64_t *slot_b, int32_t max_slots, const double *ref, const double *w_mat, double *vel,
+                       double *imp, const double *mu, const double *restitution, const double *slop,
+                       const cs_solver_params *params, double *wrench, void *stream) {
+    if (!P || !(P->stages & CS_STAGE_REDUCE)) return fail(CS_ERR_VALUE, "plan has no reduce stage");
+    if (n_sys < 1 || max_slots < 1) return fail(CS_ERR_VALUE, "n_sys and max_slots must be positive");
+    if (nb < 1 || nb > SOLVER_MAX_BODIES) return fail(CS_ERR_VALUE, "n_bodies must be in [1, %d]", SOLVER_MAX_BODIES);
+    if (!slot_off || !slot_a || !slot_b || !ref || !w_mat || !vel || !imp || !mu || !restitution || !slop || !wrench)
+        return fail(CS_ERR_VALUE, "null argument");
+    if (int r = check_solver_params(params)) return r;
+    const int64_t stride = (int64_t)max_slots * P->rp.N * P->rp.K, R = (n_sys + 31) / 32 * 32 * stride;
+    cs_solver_rows &S = P->mrows;
+    if (S.body_a && (P->mrows_sys != n_sys || S.stride != stride))
+        return fail(CS_ERR_VALUE, "a plan serves one multi-pair layout (n_sys / max_slots changed)");
+    if (!S.body_a) {
+        if (int r = alloc_rows(P, S, stride, R)) return r;
+        if (int r = P->alloc(&P->mrow_count, n_sys)) return r;
+        P->mrows_sys = n_sys;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const SysRows rows{nullptr, stride, P->mrow_count, R};
+    PlanRowsIO pr{P->io.patch_nkept, P->io.n_patch, P->io.kept_point, P->io.kept_normal, P->io.kept_depth, mu,
+                  restitution, slop, slot_off, slot_a, slot_b, P->rp.N, P->rp.K, rows, P->mrow_count, S.body_a,
+                  S.body_b, S.point, S.normal, S.depth, S.mu, S.restitution, S.slop};
+    launch_plan_rows(n_sys, pr, s);
+    return solve_rows(P, S, rows, n_sys, nb, false, ref, w_mat, vel, imp, params, wrench, s);
+}
+
+int cs_plan_multipair_rows(cs_plan *P, cs_solver_rows *rows, const int32_t **n_rows) {
+    if (!P || !rows || !n_rows) return fail(CS_ERR_VALUE, "null argument");
+    if (!P->mrows.body_a) return fail(CS_ERR_VALUE, "cs_multipair_solve has not run on this plan");
+    *rows = P->mrows;
+    *n_rows = P->mrow_count;
     return CS_OK;
 }
 

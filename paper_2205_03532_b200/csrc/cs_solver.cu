@@ -477,38 +477,45 @@ __global__ void __launch_bounds__(WR_WARPS * 32) k_body_wrenches(int64_t S, int 
     if (lane + 32 < nv) io.out[s * nv + lane + 32] = acc1;
 }
 
-// Scene rows of a plan's reduced contacts: warp per env, patches scanned in slot order
-__global__ void k_plan_rows(int64_t E, PlanRowsIO io) {
-    const int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+// Scene rows of a plan's reduced contacts: warp per system; its pair slots in
+// order, each slot's patches (up to n_patch: later slots are stale) in slot order
+__global__ void k_plan_rows(int64_t S, PlanRowsIO io) {
+    const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (e >= E) return;
+    if (s >= S) return;
     const int N = io.N, K = io.K;
-    const double mu = io.env_mu[e], rest = io.env_restitution[e], slop = io.env_slop[e];
+    const int64_t t0 = io.slot_off ? io.slot_off[s] : s, t1 = io.slot_off ? io.slot_off[s + 1] : s + 1;
     int run = 0;
-    for (int p0 = 0; p0 < N; p0 += 32) {
-        const int p = p0 + lane;
-        const int nk = p < N ? io.patch_nkept[e * N + p] : 0;
-        int inc = nk;
-        for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += v;
-        }
-        const int64_t base = run + inc - nk;
-        for (int k = 0; k < nk; ++k) {
-            const int64_t src = ((int64_t)e * N + p) * K + k, r = io.rows.row(e, base + k);
-            io.body_a[r] = 0;
-            io.body_b[r] = 1;
-            for (int q = 0; q < 3; ++q) {
-                io.point[io.rows.vec(r, q)] = io.kept_point[3 * src + q];
-                io.normal[io.rows.vec(r, q)] = io.kept_normal[3 * src + q];
+    for (int64_t e = t0; e < t1; ++e) {
+        const double mu = io.env_mu[e], rest = io.env_restitution[e], slop = io.env_slop[e];
+        const int64_t ba = io.slot_a ? io.slot_a[e] : 0, bb = io.slot_b ? io.slot_b[e] : 1;
+        const int np = io.n_patch[e];
+        for (int p0 = 0; p0 < np; p0 += 32) {
+            const int p = p0 + lane;
+            const int nk = p < np ? io.patch_nkept[e * N + p] : 0;
+            int inc = nk;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += v;
             }
-            io.depth[r] = io.kept_depth[src];
-            io.mu[r] = mu;
-            io.restitution[r] = rest;
-            io.slop[r] = slop;
+            const int64_t base = run + inc - nk;
+            for (int k = 0; k < nk; ++k) {
+                const int64_t src = ((int64_t)e * N + p) * K + k, r = io.rows.row(s, base + k);
+                io.body_a[r] = ba;
+                io.body_b[r] = bb;
+                for (int q = 0; q < 3; ++q) {
+                    io.point[io.rows.vec(r, q)] = io.kept_point[3 * src + q];
+                    io.normal[io.rows.vec(r, q)] = io.kept_normal[3 * src + q];
+                }
+                io.depth[r] = io.kept_depth[src];
+                io.mu[r] = mu;
+                io.restitution[r] = rest;
+                io.slop[r] = slop;
+            }
+            run += __shfl_sync(0xffffffffu, inc, 31);
         }
-        run += __shfl_sync(0xffffffffu, inc, 31);
     }
+    if (io.count_out && lane == 0) io.count_out[s] = run;
 }
 
 }  // namespace
@@ -540,9 +547,9 @@ void launch_body_wrenches(int64_t n_sys, int nb, const SysRows &rows, const Wren
     k_body_wrenches<<<(unsigned)((n_sys + WR_WARPS - 1) / WR_WARPS), WR_WARPS * 32, 0, s>>>(n_sys, nb, rows, io);
 }
 
-void launch_plan_rows(int64_t E, const PlanRowsIO &io, cudaStream_t s) {
-    if (E <= 0) return;
-    k_plan_rows<<<(unsigned)((E * 32 + 255) / 256), 256, 0, s>>>(E, io);
+void launch_plan_rows(int64_t S, const PlanRowsIO &io, cudaStream_t s) {
+    if (S <= 0) return;
+    k_plan_rows<<<(unsigned)((S * 32 + 255) / 256), 256, 0, s>>>(S, io);
 }
 
 }  // namespace cs

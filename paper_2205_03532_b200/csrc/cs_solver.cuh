@@ -66,15 +66,19 @@ void launch_sweeps(int64_t n_sys, int nb, const SysRows &rows, const SweepIO &io
                    int n_phases, cudaStream_t s, bool fixed_bodies = false);
 void launch_body_wrenches(int64_t n_sys, int nb, const SysRows &rows, const WrenchIO &io, cudaStream_t s);
 
-// Plan rows: env e's kept contacts in (patch slot, k) order (scene.py:228-243) as
-// its rows 0 .. n_kept[e] - 1 (interleaved layout of SysRows), body_a = 0 (SDF
-// body), body_b = 1 (mesh body).
+// Plan rows: system s's rows are the kept contacts of its pair slots (plan envs)
+// [slot_off[s], slot_off[s + 1]) (one slot e = s when slot_off is null), slot by
+// slot, each in (patch slot, k) order (scene.py:228-243), with body_a / body_b the
+// slot's SDF / mesh body within the system (0 / 1 when null), in the interleaved
+// layout of `rows`. count_out (optional) receives each system's row count.
 struct PlanRowsIO {
-    const int32_t *patch_nkept;  // [E N]
+    const int32_t *patch_nkept, *n_patch;                 // [E N], [E]
     const double *kept_point, *kept_normal, *kept_depth;  // [E N K (3)]
-    const double *env_mu, *env_restitution, *env_slop;    // [E]
+    const double *env_mu, *env_restitution, *env_slop;    // [E] per pair slot
+    const int64_t *slot_off, *slot_a, *slot_b;            // [S + 1], [E], [E] or null
     int32_t N, K;
     SysRows rows;
+    int32_t *count_out;
     int64_t *body_a, *body_b;
     double *point, *normal, *depth, *mu, *restitution, *slop;
 };

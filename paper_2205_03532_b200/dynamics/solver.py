@@ -175,24 +175,25 @@ def solve_contact_sweep(constraints: ContactConstraints, state: SolverState) -> 
 
 
 class BatchedSolverState:
-    """Device state of E two-body systems for Plan.solve: body 0 is each env's SDF
-    body, body 1 its mesh body (scene.py:228-243). float64 CUDA tensors:
-    ref (E,2,3), w_mat (E,2,6,6), vel (E,2,6), impulse (E,2,6)."""
+    """Device SolverState of E systems of n_bodies each (float64 CUDA tensors:
+    ref (E,nb,3), w_mat (E,nb,6,6), vel (E,nb,6), impulse (E,nb,6)). For Plan.solve
+    nb = 2: body 0 is each env's SDF body, body 1 its mesh body (scene.py:228-243);
+    for MultiPairScenes.solve the scene's bodies in order."""
 
-    def __init__(self, n_envs: int):
+    def __init__(self, n_envs: int, n_bodies: int = 2):
         import torch
 
         z = lambda *s: torch.zeros(s, dtype=torch.float64, device="cuda")  # noqa: E731
-        self.ref = z(n_envs, 2, 3)
-        self.w_mat = z(n_envs, 2, 6, 6)
-        self.vel = z(n_envs, 2, 6)
-        self.impulse = z(n_envs, 2, 6)
+        self.ref = z(n_envs, n_bodies, 3)
+        self.w_mat = z(n_envs, n_bodies, 6, 6)
+        self.vel = z(n_envs, n_bodies, 6)
+        self.impulse = z(n_envs, n_bodies, 6)
 
     @classmethod
     def from_numpy(cls, ref, w_mat, vel, impulse=None) -> "BatchedSolverState":
         import torch
 
-        st = cls(len(ref))
+        st = cls(len(ref), np.asarray(ref).shape[1])
         st.ref.copy_(torch.from_numpy(np.ascontiguousarray(ref, np.float64)))
         st.w_mat.copy_(torch.from_numpy(np.ascontiguousarray(w_mat, np.float64)))
         st.vel.copy_(torch.from_numpy(np.ascontiguousarray(vel, np.float64)))

@@ -18,6 +18,7 @@ reference's pair order (sorted by body id).
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -44,6 +45,8 @@ class SceneBody:
     voxel: float | None = None
     sdf_enabled: bool = False
     fixed: bool = False
+    friction: float = 0.5      # RigidBody defaults (dynamics/body.py:27-28)
+    restitution: float = 0.0
 
 
 class MultiPairScenes:
@@ -71,6 +74,7 @@ class MultiPairScenes:
             margins.append(contact_distance or 2.0 * mv or 1e-3)
         # candidate pair slots, in the reference's pair order
         slot_scene, slot_pair, sdf_idx, mesh_idx, sdf_h, mesh_h, cd = [], [], [], [], [], [], []
+        slot_a, slot_b, slot_mu, slot_e, slot_voxel = [], [], [], [], []
         for s, bodies in enumerate(scenes):
             by_id = {b.body_id: (k, b) for k, b in enumerate(bodies)}
             order = sorted(by_id)
@@ -95,6 +99,12 @@ class MultiPairScenes:
                     sdf_h.append(sb.sdf_handle)
                     mesh_h.append(mb.mesh_handle)
                     cd.append(contact_distance or 2.0 * sb.voxel)
+                    # solver rows of this pair (scene.py:224-243): body_a = SDF body
+                    slot_a.append(ks)
+                    slot_b.append(km)
+                    slot_mu.append(float(np.sqrt(sb.friction * mb.friction)))
+                    slot_e.append(max(sb.restitution, mb.restitution))
+                    slot_voxel.append(sb.voxel)
         self.n_slots = len(slot_scene)
         if self.n_slots == 0:
             raise ValueError("no candidate pairs")
@@ -121,6 +131,16 @@ class MultiPairScenes:
         self.d_mesh_idx = dev(np.array(mesh_idx, np.int64), torch.int64)
         self.d_cd = dev(np.array(cd, np.float64), torch.float64)
         self.active = torch.zeros(self.n_slots, dtype=torch.int32, device="cuda")
+        # solver: scenes' slots are contiguous, in pair order
+        slot_off = np.searchsorted(self.slot_scene, np.arange(S + 1)).astype(np.int64)
+        self.max_slots = int(np.diff(slot_off).max())
+        self.max_bodies = int(np.diff(body_off).max())
+        self.d_slot_off = dev(slot_off, torch.int64)
+        self.d_slot_a = dev(np.array(slot_a, np.int64), torch.int64)
+        self.d_slot_b = dev(np.array(slot_b, np.int64), torch.int64)
+        self.d_slot_mu = dev(np.array(slot_mu, np.float64), torch.float64)
+        self.d_slot_e = dev(np.array(slot_e, np.float64), torch.float64)
+        self.slot_voxel = np.array(slot_voxel, np.float64)
         self.world_lo = torch.zeros((self.n_bodies, 3), dtype=torch.float64, device="cuda")
         self.world_hi = torch.zeros_like(self.world_lo)
 
@@ -154,6 +174,35 @@ class MultiPairScenes:
                 raise ValueError("non-finite AABB in broadphase input")
             res.check()
         return res
+
+    def solve(self, state, params=None, wrench=None, stream=None):
+        """The contact solve of one substep (Scene._substep, scene.py:130-160) for
+        every scene on the last step's reduced contacts: system s = scene s, its
+        rows the active pairs' kept contacts in pair order with body_a the pair's
+        SDF body, mu = sqrt(f_a f_b), e = max(e_a, e_b), slop = penetration_slop or
+        0.5 voxel of the pair's grid (scene.py:207-212,226-227).
+        state: dynamics.BatchedSolverState(n_scenes, max bodies per scene), bodies
+        in scene order (vel, impulse updated in place). Returns wrenches (S, nb, 6)."""
+        import torch
+
+        from .dynamics.solver import SolverParams
+
+        params = params or SolverParams()
+        S, nb = len(self.scenes), state.vel.shape[1]
+        if state.vel.shape[0] != S or nb < self.max_bodies:
+            raise ValueError("state must hold (n_scenes, >= bodies per scene) systems")
+        slop = np.full(self.n_slots, params.penetration_slop) if params.penetration_slop is not None \
+            else 0.5 * self.slot_voxel
+        d_slop = torch.from_numpy(slop.astype(np.float64)).cuda()
+        if wrench is None:
+            wrench = torch.empty((S, nb, 6), dtype=torch.float64, device="cuda")
+        cp = params.to_c()
+        _native.call("cs_multipair_solve", self.plan.ptr, S, nb, self.d_slot_off.data_ptr(), self.d_slot_a.data_ptr(),
+                     self.d_slot_b.data_ptr(), self.max_slots, state.ref.data_ptr(), state.w_mat.data_ptr(),
+                     state.vel.data_ptr(), state.impulse.data_ptr(), self.d_slot_mu.data_ptr(),
+                     self.d_slot_e.data_ptr(), d_slop.data_ptr(), ctypes.byref(cp), wrench.data_ptr(),
+                     _native.stream_handle(stream))
+        return wrench
 
     def scene_pairs(self, s: int) -> list[tuple[int, int]]:
         """Scene s's broadphase pairs of the last step (sorted (id_a, id_b))."""

@@ -141,3 +141,47 @@ def test_multipair_scenes_match_oracle(P, grid64_npz, meshes):
             for q, p in enumerate(pt):
                 assert np.array_equal(p.face_indices, red["kept_faces"][q, :len(p)])
     assert n_active > S  # bolt-nut in every scene plus touching pads
+
+    # the substep's contact solve over each whole scene (4 bodies; rows of its active
+    # pairs in pair order, body_a = the pair's SDF body), against the oracle
+    from paper_2205_03532_b200.dynamics import BatchedSolverState, SolverParams
+
+    rng = np.random.default_rng(9)
+    ref_pt = np.zeros((S, 4, 3)); W = np.zeros((S, 4, 6, 6)); vel = np.zeros((S, 4, 6))
+    ref_pt[:, 1] = poses[:, 1, :3]
+    W[:, 1, :3, :3] = np.eye(3) / 0.03
+    W[:, 1, 3:, 3:] = np.diag(1.0 / np.array([2.4e-6, 2.4e-6, 3.9e-6]))
+    vel[:, 1] = rng.standard_normal((S, 6)) * 0.05
+    vel[:, 1, 2] -= 0.3
+    st = BatchedSolverState.from_numpy(ref_pt, W, vel)
+    prm = SolverParams(pos_iterations=8, vel_iterations=2)
+    wrench = mps.solve(st, prm).cpu().numpy()
+    gv = st.vel.cpu().numpy()
+    h = prm.dt / prm.substeps
+    for i in range(S):
+        pts, nrm, dep, ba, bb, mu, rs, sl = [], [], [], [], [], [], [], []
+        for t in np.nonzero(mps.slot_scene == i)[0]:
+            if not active[t]:
+                continue
+            sb, mb = int(mps.slot_sdf_body[t]), int(mps.slot_mesh_body[t])
+            for p in res.patches(int(t)):
+                pts.append(p.points); nrm.append(p.normals); dep.append(p.depths)
+                k = len(p.depths)
+                ba += [sb] * k; bb += [mb] * k
+                mu += [0.5] * k; rs += [0.0] * k
+                sl += [0.5 * (bolt_grid.voxel_size if sb == 0 else pad_grid.voxel_size)] * k
+        m = len(ba)
+        pts, nrm, dep = np.concatenate(pts), np.concatenate(nrm), np.concatenate(dep)
+        a, b = np.array(ba, np.int64), np.array(bb, np.int64)
+        con = O.constraints_build(a, b, pts, nrm, dep, np.array(rs), np.array(sl), ref_pt[i], W[i], vel[i], h,
+                                  prm.bias_factor)
+        v, imp = np.array(vel[i]), np.zeros((4, 6))
+        ln, l1, l2, lv = (np.zeros(m) for _ in range(4))
+        geo = (a, b, con["ra"], con["rb"], nrm, con["tan1"], con["tan2"], con["kn"], con["kt1"], con["kt2"])
+        O.gauss_seidel_sweeps(prm.pos_iterations, W[i], v, imp, *geo, con["bias_target"], np.array(mu), ln, l1, l2,
+                              True)
+        O.gauss_seidel_sweeps(prm.vel_iterations, W[i], v, imp, *geo, con["restitution_target"], np.array(mu), lv,
+                              l1, l2, False)
+        wr = O.body_wrenches(4, a, b, con["ra"], con["rb"], nrm, con["tan1"], con["tan2"], ln, lv, l1, l2, h)
+        assert np.array_equal(gv[i], v), i
+        assert np.array_equal(wrench[i], wr), i
