@@ -700,29 +700,45 @@ __global__ void __launch_bounds__(COMPACT_BLOCK) k_compact(const EnvXf *__restri
         const int cnt = st.chunk_count[c0 + j];
         const int64_t src0 = base + block_map[c0 + j].y;
         int64_t dst = base + st.chunk_off[c0 + j];
-        for (int i0 = 0; i0 < cnt; i0 += 32) {
-            const int i = i0 + lane;
-            const int64_t s = src0 + i;
-            const int fidx = i < cnt ? st.face[s] : -1;
-            const unsigned bal = __ballot_sync(0xffffffffu, fidx >= 0);
-            if (fidx >= 0) {
-                const int64_t d = dst + __popc(bal & ((1u << lane) - 1u));
-                double px = st.point[3 * s], py = st.point[3 * s + 1], pz = st.point[3 * s + 2];
-                double gx = st.grad[3 * s], gy = st.grad[3 * s + 1], gz = st.grad[3 * s + 2];
-                double nrm = sqrt(gx * gx + gy * gy + gz * gz);  // np.linalg.norm(axis=1): ((x2+y2)+z2)
-                if (nrm < 1e-12) { gx = 0.0; gy = 0.0; gz = 1.0; nrm = 1.0; }
-                const double nx = gx / nrm, ny = gy / nrm, nz = gz / nrm;
-                for (int k = 0; k < 3; ++k) {
-                    const double *rr = sx.Rs + 3 * k;
-                    cs.normal[3 * d + k] =
-                        gemm ? G3(nx, ny, nz, rr[0], rr[1], rr[2]) : V3(nx, ny, nz, rr[0], rr[1], rr[2]);
-                    cs.point[3 * d + k] =
-                        (gemm ? G3(px, py, pz, rr[0], rr[1], rr[2]) : V3(px, py, pz, rr[0], rr[1], rr[2])) + sx.ts[k];
+        // two groups of 32 rows per round, every load of both in flight at once (rows
+        // not found carry stale values that are never used)
+        for (int i0 = 0; i0 < cnt; i0 += 64) {
+            int fidx[2];
+            double px[2], py[2], pz[2], gx[2], gy[2], gz[2], phi[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int i = i0 + 32 * h + lane;
+                const int64_t s = src0 + i;
+                fidx[h] = -1;
+                px[h] = py[h] = pz[h] = gx[h] = gy[h] = gz[h] = phi[h] = 0.0;
+                if (i < cnt) {
+                    fidx[h] = st.face[s];
+                    px[h] = st.point[3 * s]; py[h] = st.point[3 * s + 1]; pz[h] = st.point[3 * s + 2];
+                    gx[h] = st.grad[3 * s]; gy[h] = st.grad[3 * s + 1]; gz[h] = st.grad[3 * s + 2];
+                    phi[h] = st.phi[s];
                 }
-                cs.depth[d] = -st.phi[s];
-                cs.face[d] = fidx;
             }
-            dst += __popc(bal);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const unsigned bal = __ballot_sync(0xffffffffu, fidx[h] >= 0);
+                if (fidx[h] >= 0) {
+                    const int64_t d = dst + __popc(bal & ((1u << lane) - 1u));
+                    double ux = gx[h], uy = gy[h], uz = gz[h];
+                    double nrm = sqrt(ux * ux + uy * uy + uz * uz);  // np.linalg.norm(axis=1): ((x2+y2)+z2)
+                    if (nrm < 1e-12) { ux = 0.0; uy = 0.0; uz = 1.0; nrm = 1.0; }
+                    const double nx = ux / nrm, ny = uy / nrm, nz = uz / nrm;
+                    for (int k = 0; k < 3; ++k) {
+                        const double *rr = sx.Rs + 3 * k;
+                        cs.normal[3 * d + k] =
+                            gemm ? G3(nx, ny, nz, rr[0], rr[1], rr[2]) : V3(nx, ny, nz, rr[0], rr[1], rr[2]);
+                        cs.point[3 * d + k] = (gemm ? G3(px[h], py[h], pz[h], rr[0], rr[1], rr[2])
+                                                    : V3(px[h], py[h], pz[h], rr[0], rr[1], rr[2])) + sx.ts[k];
+                    }
+                    cs.depth[d] = -phi[h];
+                    cs.face[d] = fidx[h];
+                }
+                dst += __popc(bal);
+            }
         }
     }
     if (threadIdx.x == 0) n_cand[e] = C;
