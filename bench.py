@@ -48,7 +48,9 @@ def parse():
     ap.add_argument("--envs", type=int, default=1024, help="envs per GPU")
     ap.add_argument("--res", type=int, default=256)
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--no-l2-pin", action="store_true")
+    ap.add_argument("--l2-pin", action="store_true",
+                    help="pin the grid in L2 (persisting window); measured slower: the carve-out costs the step's "
+                         "staging traffic more than the grid gathers gain")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=256, help="envs in the CPU-baseline sample")
     ap.add_argument("--ref-sample", type=int, default=32, help="envs per reference-arm step")
@@ -204,7 +206,7 @@ def _config(args, E, F, dims):
         "envs_total": int(E), "envs_per_gpu": args.envs, "mesh_faces": int(F), "sdf_dims": [int(d) for d in dims],
         "reduction": "ReductionParams() defaults, min_depth = -cd (Scene semantics)",
         "l2": "flushed between timed steps (256 MiB write, untimed)" if not args.no_flush else "not flushed",
-        "l2_pin": not args.no_l2_pin, "parallelism": f"env shards, {args.gpus} rank(s)",
+        "l2_pin": bool(args.l2_pin), "parallelism": f"env shards, {args.gpus} rank(s)",
     }
 
 
@@ -317,7 +319,7 @@ def main():
     mp = torch.from_numpy(np.ascontiguousarray(w["mesh_pose"][lo:hi])).cuda()
     cd = torch.from_numpy(np.ascontiguousarray(w["cd"][lo:hi])).cuda()
     stream = torch.cuda.current_stream()
-    if not args.no_l2_pin:
+    if args.l2_pin:
         P.pin_sdf_in_l2(grid, 1.0, stream)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
