@@ -302,3 +302,46 @@ def test_reduce_deep_hull_stacks(P):
         r = O.reduce_contacts(pts, nrm, dep, faces, per_patch_cap=cap, min_depth=-1e-4)
         for k in ("rep", "nkept", "members", "kept_faces", "wsum", "wp", "wn", "wt", "area", "maxd"):
             assert np.array_equal(np.asarray(got[k]), np.asarray(r[k])), (n, k)
+
+
+def test_config3_suite_4096_envs_vs_oracle(P):
+    """Config 3 at full size: 4096 envs over pegs 4/8/12/16 mm in
+    tight holes and M4..M20 nuts on bolts (9 assets, res-256 grids), one collide
+    call with per-env handles; every env's stats against the oracle, two envs per
+    asset field by field."""
+    from oracle import oracle as O
+    from paper_2205_03532_b200.scenes import suite_workload
+
+    E = 4096
+    w = suite_workload(E, seed=1)
+    A, asset = w["assets"], w["asset"]
+    hs = [P.register_sdf(a["grid"]) for a in A]
+    hm = [P.register_mesh(a["mesh"]) for a in A]
+    res = P.collide([hs[k] for k in asset], [hm[k] for k in asset], w["sdf_pose"], w["mesh_pose"], w["cd"])
+    n_cand = res.n_cand.cpu().numpy()
+    n_patch = res.n_patch.cpu().numpy()
+    stats = res.stats.cpu().numpy()
+    rng = np.random.default_rng(5)
+    for k, a in enumerate(A):
+        idx = np.nonzero(asset == k)[0]
+        g = a["grid"]
+        og = O.Grid(g.values, g.dims, g.origin, g.voxel_size, *g.mesh_aabb)
+        m = a["mesh"]
+        ost = O.collide_batched(og, m.vertices, m.triangles, w["sdf_pose"][idx], w["mesh_pose"][idx], w["cd"][idx])
+        assert np.array_equal(n_cand[idx], ost[:, 0].astype(np.int64)), a["name"]
+        assert np.array_equal(n_patch[idx], ost[:, 1].astype(np.int64)), a["name"]
+        assert np.array_equal(stats[idx, 2], ost[:, 2].astype(np.float32)), a["name"]
+        assert np.array_equal(stats[idx, 3], ost[:, 3].astype(np.float32)), a["name"]
+        assert (n_cand[idx] > 0).mean() > 0.5, a["name"]  # the poses engage the parts
+        for e in rng.choice(idx, size=2, replace=False):
+            e = int(e)
+            ref = O.generate_contacts(og, m.vertices, m.triangles, w["sdf_pose"][e], w["mesh_pose"][e],
+                                      float(w["cd"][e]))
+            cs = res.contact_set(e)
+            assert np.array_equal(cs.points, ref["points"]) and np.array_equal(cs.normals, ref["normals"]), e
+            assert np.array_equal(cs.depths, ref["depths"]) and np.array_equal(cs.face_indices, ref["faces"]), e
+            r = O.reduce_contacts(ref["points"], ref["normals"], ref["depths"], ref["faces"],
+                                  min_depth=-float(w["cd"][e]))
+            got = pack_patch_list(res.patches(e), 6)
+            for key in ("rep", "nkept", "members", "kept_faces", "wsum", "wp", "wn", "wt", "area", "maxd"):
+                assert np.array_equal(np.asarray(got[key]), np.asarray(r[key])), (e, key)
