@@ -345,3 +345,30 @@ def test_config3_suite_4096_envs_vs_oracle(P):
             got = pack_patch_list(res.patches(e), 6)
             for key in ("rep", "nkept", "members", "kept_faces", "wsum", "wp", "wn", "wt", "area", "maxd"):
                 assert np.array_equal(np.asarray(got[key]), np.asarray(r[key])), (e, key)
+
+
+def test_config5_res512_vs_oracle(P):
+    """Config 5's largest grid: the M16 bolt at res 512 (~400 MB,
+    above L2), generated on the GPU, 8 envs against the oracle field by field."""
+    from oracle import oracle as O
+    from paper_2205_03532_b200.scenes import m16_meshes, m16_workload
+    from paper_2205_03532_b200.sdf.grid import SdfResolutionSpec, generate_sdf
+
+    nut, bolt, _ = m16_meshes()
+    grid = generate_sdf(bolt, SdfResolutionSpec(512, 4))
+    assert max(grid.dims) == 512 and grid.values.nbytes > 300e6
+    E = 8
+    w = m16_workload(E, seed=4, grid=grid)
+    res = P.collide([P.register_sdf(grid)] * E, [P.register_mesh(nut)] * E, w["sdf_pose"], w["mesh_pose"], w["cd"])
+    og = O.Grid(grid.values, grid.dims, grid.origin, grid.voxel_size, *grid.mesh_aabb)
+    assert (res.n_cand.cpu().numpy() > 0).sum() >= E // 2  # the poses engage the threads
+    for e in range(E):
+        cd = float(w["cd"][e])
+        ref = O.generate_contacts(og, nut.vertices, nut.triangles, w["sdf_pose"][e], w["mesh_pose"][e], cd)
+        cs = res.contact_set(e)
+        assert np.array_equal(cs.points, ref["points"]) and np.array_equal(cs.normals, ref["normals"]), e
+        assert np.array_equal(cs.depths, ref["depths"]) and np.array_equal(cs.face_indices, ref["faces"]), e
+        r = O.reduce_contacts(ref["points"], ref["normals"], ref["depths"], ref["faces"], min_depth=-cd)
+        got = pack_patch_list(res.patches(e), 6)
+        for key in ("rep", "nkept", "members", "kept_faces", "wsum", "area", "maxd"):
+            assert np.array_equal(np.asarray(got[key]), np.asarray(r[key])), (e, key)
