@@ -162,6 +162,43 @@ struct RegState2 {
     }
 };
 
+// Up to four bodies in registers (multi-pair scenes): body indices are per row, so
+// every access selects among the NB register sets with compile-time indices.
+template <int NB>
+struct RegStateN {
+    double v_[NB][6], i_[NB][6];
+    const double *W;
+    bool z_[NB];
+    __device__ __forceinline__ double v(int body, int k) const {
+        double r = v_[0][k];
+#pragma unroll
+        for (int b = 1; b < NB; ++b) r = body == b ? v_[b][k] : r;
+        return r;
+    }
+    __device__ __forceinline__ bool frozen(int body) const {
+        bool r = z_[0];
+#pragma unroll
+        for (int b = 1; b < NB; ++b) r = body == b ? z_[b] : r;
+        return r;
+    }
+    __device__ __forceinline__ void add_v(int body, const double t[6]) {
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+            if (body == b) {
+#pragma unroll
+                for (int k = 0; k < 6; ++k) v_[b][k] += t[k];
+            }
+    }
+    __device__ __forceinline__ void add_i(int body, const double g[6]) {
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+            if (body == b) {
+#pragma unroll
+                for (int k = 0; k < 6; ++k) i_[b][k] += g[k];
+            }
+    }
+};
+
 struct SmemState {
     double *V, *I;  // shared, element j at [j * SW_T]
     const double *W;
@@ -372,7 +409,7 @@ __device__ __forceinline__ void sweep_system(St &st, const SweepIO &io, const Sw
 
 // gauss_seidel_sweeps (_kernels.py:52-115), one system per thread, 1-2 phases.
 // TWO: the two-body register path (nb == 2).
-template <bool TWO, bool FIX>
+template <int MODE, bool FIX>
 __global__ void __launch_bounds__(SW_T) k_sweeps(int64_t S, int nb, SysRows rows, SweepIO io, SweepPhase p0,
                                                  SweepPhase p1, int n_phases) {
     extern __shared__ double sm[];
@@ -381,7 +418,8 @@ __global__ void __launch_bounds__(SW_T) k_sweeps(int64_t S, int nb, SysRows rows
     const int nv = 6 * nb;
     double *Ws = sm + threadIdx.x;  // [36 nb][SW_T]
     for (int j = 0; j < 36 * nb; ++j) Ws[j * SW_T] = __ldg(io.w_mat + s * 36 * nb + j);
-    double *after_w = sm + (size_t)36 * nb * SW_T + (TWO ? 0 : (size_t)12 * nb * SW_T);
+    constexpr bool TWO = MODE == 2;
+    double *after_w = sm + (size_t)36 * nb * SW_T + (MODE ? 0 : (size_t)12 * nb * SW_T);
     double *ring = after_w + threadIdx.x;
     double *lam = after_w + (size_t)RING * ROW_F * SW_T + threadIdx.x;
     const SweepPhase phs[2] = {p0, p1};
@@ -401,6 +439,27 @@ __global__ void __launch_bounds__(SW_T) k_sweeps(int64_t S, int nb, SysRows rows
             io.vel[s * 12 + k] = st.v0[k]; io.vel[s * 12 + 6 + k] = st.v1[k];
             io.imp[s * 12 + k] = st.i0[k]; io.imp[s * 12 + 6 + k] = st.i1[k];
         }
+    } else if (MODE == 4) {
+        RegStateN<4> st;
+        st.W = Ws;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                st.v_[b][k] = b < nb ? io.vel[s * nv + 6 * b + k] : 0.0;
+                st.i_[b][k] = b < nb ? io.imp[s * nv + 6 * b + k] : 0.0;
+            }
+            st.z_[b] = b < nb ? frozen_body(Ws + 36 * b * SW_T, st.v_[b]) : true;
+        }
+        sweep_system<false>(st, io, phs, n_phases, rows, s, ring, lam);
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+            if (b < nb)
+#pragma unroll
+                for (int k = 0; k < 6; ++k) {
+                    io.vel[s * nv + 6 * b + k] = st.v_[b][k];
+                    io.imp[s * nv + 6 * b + k] = st.i_[b][k];
+                }
     } else {
         SmemState st;
         st.W = Ws;
@@ -531,15 +590,16 @@ void launch_sweeps(int64_t n_sys, int nb, const SysRows &rows, const SweepIO &io
     if (n_sys <= 0 || n_phases <= 0) return;
     const unsigned grid = (unsigned)((n_sys + SW_T - 1) / SW_T);
     const SweepPhase p1 = n_phases > 1 ? phases[1] : phases[0];
-    const bool two = nb == 2;
-    const size_t smem = sweep_smem_doubles(nb, two) * SW_T * sizeof(double);
+    const bool two = nb == 2, regs = nb <= 4;
+    const size_t smem = sweep_smem_doubles(nb, regs) * SW_T * sizeof(double);
     auto go = [&](auto kern) {
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<grid, SW_T, smem, s>>>(n_sys, nb, rows, io, phases[0], p1, n_phases);
     };
-    if (two && fixed_bodies) go(k_sweeps<true, true>);
-    else if (two) go(k_sweeps<true, false>);
-    else go(k_sweeps<false, false>);
+    if (two && fixed_bodies) go(k_sweeps<2, true>);
+    else if (two) go(k_sweeps<2, false>);
+    else if (regs) go(k_sweeps<4, false>);
+    else go(k_sweeps<0, false>);
 }
 
 void launch_body_wrenches(int64_t n_sys, int nb, const SysRows &rows, const WrenchIO &io, cudaStream_t s) {
