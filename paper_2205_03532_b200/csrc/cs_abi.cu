@@ -117,7 +117,6 @@ struct cs_plan {
     int2 *block_map = nullptr;       // k_face_prep block -> (env, first face of the chunk)
     int32_t *chunk_first = nullptr;  // [E+1] first k_face_prep block of each env
     int32_t max_chunk_verts = 1;     // largest chunk vertex list over the plan's meshes
-    int pgd_grid = 0;                // persistent k_face_pgd CTAs
     EnvXf *xf = nullptr;
     Staging st{};
     Candidates cands{};
@@ -560,7 +559,6 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
     P->uniform_sdf = uniform;
     P->uniform_grid = ugrid;
     P->max_chunk_verts = maxcv;
-    P->pgd_grid = face_pgd_grid(g_sms > 0 ? g_sms : 148);
     if (stages & CS_STAGE_REDUCE) {
         P->rp.N = params->max_patches; P->rp.K = params->per_patch_cap; P->rp.batch_size = params->batch_size;
         P->rp.has_min_depth = params->has_min_depth; P->rp.cone = params->normal_cone_cos; P->rp.min_depth = params->min_depth;

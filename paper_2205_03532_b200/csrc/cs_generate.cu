@@ -4,8 +4,8 @@
 //                  (generation.py:64-83, math3d.py:45-53,168-179)
 //   k_face_prep    per (env, chunk): grid-frame vertices, AABB cull, Lipschitz
 //                  prune, descent start (generation.py:70-96, contacts/_kernels.py:20-43)
-//   k_face_pgd     persistent warps: projected-gradient descent per surviving face
-//                  (contacts/_kernels.py:44-87)
+//   k_pgd_grad / k_pgd_first / k_pgd_rest: the projected-gradient descent
+//                  (contacts/_kernels.py:44-87) as a wavefront over the survivors
 //   k_compact      per env: ordered compaction of found faces + world-frame
 //                  epilogue (generation.py:98-114)
 //   k_face_contacts / k_sdf_sample / k_sdf_gradient: per-pair drop-ins for the
@@ -284,163 +284,6 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int2 
         w->phi[0] = pa; w->phi[1] = pb; w->phi[2] = pc; w->phi[3] = ps;
     }
     PREP_MARK(5);
-}
-
-// k_face_pgd: the projected-gradient descent of every surviving face
-// (contacts/_kernels.py:44-87), one face per lane. Warps are persistent: a lane
-// that finishes its face takes the next one from the warp's claimed block of the
-// work list, so the warp's lanes stay busy whatever the per-face iteration count.
-// A step is one descent iteration; the final gradient (contacts/_kernels.py:84)
-// is the next step's gradient, so it also runs in lockstep.
-template <bool COUNT, bool UNIFORM>
-__global__ void __launch_bounds__(PGD_BLOCK, PGD_MINB) k_face_pgd(const int2 *__restrict__ block_map,
-                                                        const EnvXf *__restrict__ xf,
-                                                        const SdfDesc *__restrict__ sdfs,
-                                                        const MeshDesc *__restrict__ meshes, Staging st,
-                                                        unsigned long long *__restrict__ counter,
-                                                        const PlanGrid gu) {
-    __shared__ double sc[12][PGD_BLOCK];  // per lane: corners a, b, c (grid frame), phi at a, b, c
-    const int t = threadIdx.x, lane = t & 31;
-    const unsigned FULL = 0xffffffffu;
-    const unsigned n = st.work_count[0];
-    bool active = false, exhausted = false, final_step = false, have_grad = false;
-    unsigned qb = 0, qe = 0;
-    double px = 0.0, py = 0.0, pz = 0.0, phi = 0.0, alpha = 0.0, cd = 0.0, tol = 0.0;
-    int it = 0, face = 0, blk = 0, sdf = 0;
-    int64_t row = 0;
-    unsigned long long ns = 0;
-
-    auto start = [&](unsigned idx, const PlanGrid &g) {
-        const FaceWork *w = st.work + idx;
-        row = w->row;
-        blk = w->blk;
-        const int fw = w->face;
-        face = fw & 0x3fffffff;
-        const int which = (int)((unsigned)fw >> 30);
-        const EnvXf &X = xf[__ldg(&block_map[blk].x)];
-        cd = X.cd;
-        tol = X.tol;
-        const MeshDesc &M = meshes[X.mesh];
-        const int4 tri = __ldg(M.tris + face);
-        const double3 a = to_grid(X, ld_vert(M.verts + tri.x));
-        const double3 b = to_grid(X, ld_vert(M.verts + tri.y));
-        const double3 c = to_grid(X, ld_vert(M.verts + tri.z));
-        sc[0][t] = a.x; sc[1][t] = a.y; sc[2][t] = a.z;
-        sc[3][t] = b.x; sc[4][t] = b.y; sc[5][t] = b.z;
-        sc[6][t] = c.x; sc[7][t] = c.y; sc[8][t] = c.z;
-        sc[9][t] = w->phi[0]; sc[10][t] = w->phi[1]; sc[11][t] = w->phi[2];
-        phi = w->phi[3];
-        if (which == 0) {
-            px = (a.x + b.x + c.x) / 3.0; py = (a.y + b.y + c.y) / 3.0; pz = (a.z + b.z + c.z) / 3.0;
-        } else {
-            const double3 s = which == 1 ? a : which == 2 ? b : c;
-            px = s.x; py = s.y; pz = s.z;
-        }
-        alpha = g.voxel;
-        it = 0;
-        final_step = false;
-        have_grad = false;
-    };
-
-    auto step = [&](const PlanGrid &g) {
-        const GPoint p = gpoint(g, px, py, pz);
-        double grx, gry, grz;
-        gradient(g, p, grx, gry, grz);
-        if (COUNT) ns += 6;
-        bool done = final_step;
-        if (!done) {
-            have_grad = true;
-            const double gnorm = sqrt(grx * grx + gry * gry + grz * grz);
-            if (gnorm < 1e-12) {
-                done = true;
-            } else {
-                const double ux = grx / gnorm, uy = gry / gnorm, uz = grz / gnorm;
-                const double ax = sc[0][t], ay = sc[1][t], az = sc[2][t];
-                const double bx = sc[3][t], by = sc[4][t], bz = sc[5][t];
-                const double cx = sc[6][t], cy = sc[7][t], cz = sc[8][t];
-                double moved = 0.0;
-                for (int bt = 0; bt < 4; ++bt) {
-                    double qx, qy, qz;
-                    closest_point(ax, ay, az, bx, by, bz, cx, cy, cz, px - alpha * ux, py - alpha * uy,
-                                  pz - alpha * uz, qx, qy, qz);
-                    // the projection often is the current point or a corner itself:
-                    // identical inputs, so the sample's value is already known
-                    double phi_new;
-                    if (same3(qx, qy, qz, px, py, pz)) phi_new = phi;
-                    else if (same3(qx, qy, qz, ax, ay, az)) phi_new = sc[9][t];
-                    else if (same3(qx, qy, qz, bx, by, bz)) phi_new = sc[10][t];
-                    else if (same3(qx, qy, qz, cx, cy, cz)) phi_new = sc[11][t];
-                    else {
-                        phi_new = sample(g, qx, qy, qz);
-                        if (COUNT) ns += 1;
-                    }
-                    if (phi_new < phi) {
-                        moved = sqrt((qx - px) * (qx - px) + (qy - py) * (qy - py) + (qz - pz) * (qz - pz));
-                        px = qx; py = qy; pz = qz;
-                        phi = phi_new;
-                        have_grad = false;
-                        alpha = dmin(alpha * 1.5, 4.0 * g.voxel);
-                        break;
-                    }
-                    alpha *= 0.5;
-                }
-                if (moved < tol || ++it >= MAX_MINIMIZE_ITERS) {
-                    if (have_grad) done = true;
-                    else final_step = true;  // the next step's gradient is the final one
-                }
-            }
-        }
-        if (done) {
-            const bool found = phi <= cd;
-            if (found) {
-                st.point[3 * row + 0] = px; st.point[3 * row + 1] = py; st.point[3 * row + 2] = pz;
-                st.phi[row] = phi;
-                st.grad[3 * row + 0] = grx; st.grad[3 * row + 1] = gry; st.grad[3 * row + 2] = grz;
-                atomicAdd(st.chunk_found + blk, 1);
-            }
-            st.face[row] = found ? face : -1;
-            active = false;
-        }
-    };
-
-    while (true) {
-        unsigned need = __ballot_sync(FULL, !active && !exhausted);
-        while (need) {
-            if (qb >= qe) {
-                unsigned b = 0;
-                if (lane == 0) b = atomicAdd(st.work_count + 1, (unsigned)PGD_GRAB);
-                b = __shfl_sync(FULL, b, 0);
-                if (b >= n) {
-                    if (!active) exhausted = true;
-                    break;
-                }
-                qb = b;
-                qe = min(b + (unsigned)PGD_GRAB, n);
-            }
-            const unsigned avail = qe - qb;
-            const unsigned rank = __popc(need & ((1u << lane) - 1u));
-            if (((need >> lane) & 1u) && rank < avail) {
-                if (UNIFORM) {
-                    start(qb + rank, gu);
-                } else {
-                    sdf = xf[__ldg(&block_map[st.work[qb + rank].blk].x)].sdf;
-                    start(qb + rank, sdfs[sdf].gp);
-                }
-                active = true;
-            }
-            qb += min((unsigned)__popc(need), avail);
-            need = __ballot_sync(FULL, !active && !exhausted);
-        }
-        if (!__any_sync(FULL, active)) break;
-        if (active) {
-            if (UNIFORM) step(gu);
-            else step(sdfs[sdf].gp);
-        }
-    }
-    if (COUNT) {
-        for (int o = 16; o; o >>= 1) ns += __shfl_xor_sync(FULL, ns, o);
-        if (lane == 0 && ns) atomicAdd(counter, ns);
-    }
 }
 
 // ---------------------------------------------------------------- the descent as a wavefront
@@ -802,27 +645,6 @@ void launch_face_prep(int64_t nblocks, const int2 *block_map, const EnvXf *xf, c
     } else {
         if (counter) k_face_prep<true, false><<<nb, FACE_CHUNK, sm, s>>>(block_map, xf, sdfs, meshes, cand_base, st, maxcv, counter, gu);
         else k_face_prep<false, false><<<nb, FACE_CHUNK, sm, s>>>(block_map, xf, sdfs, meshes, cand_base, st, maxcv, nullptr, gu);
-    }
-}
-
-int face_pgd_grid(int sm_count) {
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_face_pgd<false, true>, PGD_BLOCK, 0) != cudaSuccess ||
-        per_sm < 1)
-        per_sm = 1;
-    return per_sm * sm_count;
-}
-
-void launch_face_pgd(int grid, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs, const MeshDesc *meshes,
-                     const Staging &st, unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s) {
-    if (grid <= 0) return;
-    const PlanGrid gu = uniform ? *uniform : PlanGrid{};
-    if (uniform) {
-        if (counter) k_face_pgd<true, true><<<grid, PGD_BLOCK, 0, s>>>(block_map, xf, sdfs, meshes, st, counter, gu);
-        else k_face_pgd<false, true><<<grid, PGD_BLOCK, 0, s>>>(block_map, xf, sdfs, meshes, st, nullptr, gu);
-    } else {
-        if (counter) k_face_pgd<true, false><<<grid, PGD_BLOCK, 0, s>>>(block_map, xf, sdfs, meshes, st, counter, gu);
-        else k_face_pgd<false, false><<<grid, PGD_BLOCK, 0, s>>>(block_map, xf, sdfs, meshes, st, nullptr, gu);
     }
 }
 

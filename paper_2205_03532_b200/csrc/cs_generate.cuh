@@ -3,10 +3,6 @@
 
 namespace cs {
 
-constexpr int PGD_BLOCK = 128;
-#ifndef PGD_MINB
-#define PGD_MINB 5  // min resident k_face_pgd CTAs per SM: a 102-register budget (measured best)
-#endif
 // register budgets / grids of the descent wavefront (measured best, round 1)
 #ifndef FIRST_MINB
 #define FIRST_MINB 3
@@ -28,7 +24,7 @@ constexpr int COMPACT_BLOCK = 256;
 constexpr int MAX_MINIMIZE_ITERS = 12;  // generation.py:19
 
 // One face that survived the cull and the Lipschitz prune (k_face_prep), waiting
-// for its projected-gradient descent (k_face_pgd).
+// for its projected-gradient descent (the k_pgd_* wavefront).
 struct FaceWork {
     int64_t row;        // staging row: cand_base[e] + f0 + rank among the chunk's survivors
     int32_t blk;        // k_face_prep block (env, chunk)
@@ -50,7 +46,7 @@ struct Staging {
     double *alpha;         // [row] descent step of a moved face
     uint32_t *acc;         // [capacity] work indices moved by k_pgd_first (| ACC_FINAL)
     uint32_t *slow;        // [capacity] work indices still moving after iteration 0
-    unsigned *work_count;  // [0] survivors, [1] (k_face_pgd claims), [2] accepted, [3] slow
+    unsigned *work_count;  // [0] survivors, [1] (unused), [2] accepted, [3] slow
 };
 
 // Candidate arrays (row = cand_base[e] + candidate index).
@@ -68,11 +64,8 @@ void launch_env_xf(int64_t E, const int32_t *env_sdf, const int32_t *env_mesh, c
 void launch_face_prep(int64_t nblocks, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs,
                       const MeshDesc *meshes, const int64_t *cand_base, const Staging &st, int max_chunk_verts,
                       unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s);
-void launch_face_pgd(int grid, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs, const MeshDesc *meshes,
-                     const Staging &st, unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s);
-int face_pgd_grid(int sm_count);
 void launch_pgd_wave(int sm_count, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs, const MeshDesc *meshes,
-                     const Staging &st, unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s);  // resident CTAs of k_face_pgd over the device
+                     const Staging &st, unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s);
 size_t face_prep_smem(int max_chunk_verts);
 void launch_compact(int64_t E, const EnvXf *xf, const int64_t *cand_base, const int2 *block_map,
                     const int32_t *chunk_first, const Staging &st, const Candidates &cs, int32_t *n_cand,
