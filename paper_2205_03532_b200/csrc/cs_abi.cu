@@ -134,6 +134,7 @@ struct cs_plan {
     int32_t timing_slots = 0;
     // contact solver rows (cs_plan_solve / cs_multipair_solve), allocated on first use
     cs_solver_rows srows{}, mrows{};
+    double *spacked = nullptr, *mpacked = nullptr;  // packed sweep records (launch_sweeps_packed)
     int32_t *mrow_count = nullptr;
     int64_t mrows_sys = 0;
 
@@ -844,7 +845,7 @@ int alloc_rows(cs_plan *P, cs_solver_rows &S, int64_t stride, int64_t R) {
 // rows -> build -> sweeps (position with friction, then velocity) -> wrenches
 int solve_rows(cs_plan *P, const cs_solver_rows &S, const SysRows &rows, int64_t n_sys, int nb, bool fixed,
                const double *ref, const double *w_mat, double *vel, double *imp, const cs_solver_params *params,
-               double *wrench, cudaStream_t s) {
+               double *wrench, cudaStream_t s, double *packed) {
     const BuildIO bio{S.body_a, S.body_b, S.point, S.normal, S.depth, S.restitution, S.slop, ref, w_mat, vel,
                       params->h, params->bias_factor, S.ra, S.rb, S.tan1, S.tan2, S.kn, S.kt1, S.kt2,
                       S.bias_target, S.restitution_target};
@@ -854,7 +855,8 @@ int solve_rows(cs_plan *P, const cs_solver_rows &S, const SysRows &rows, int64_t
                       S.lam_t1, S.lam_t2, w_mat, vel, imp};
     const SweepPhase ph[2] = {{params->pos_iterations, S.bias_target, S.lam_n, 1},
                               {params->vel_iterations, S.restitution_target, S.lam_vel, 0}};
-    launch_sweeps(n_sys, nb, rows, sio, ph, 2, s, fixed);
+    if (packed) launch_sweeps_packed(n_sys, nb, rows, sio, ph, 2, packed, s, fixed);
+    else launch_sweeps(n_sys, nb, rows, sio, ph, 2, s, fixed);
     const WrenchIO wio{S.body_a, S.body_b, S.ra, S.rb, S.normal, S.tan1, S.tan2, S.lam_n, S.lam_vel, S.lam_t1,
                        S.lam_t2, params->h, wrench};
     launch_body_wrenches(n_sys, nb, rows, wio, s);
@@ -880,15 +882,17 @@ int cs_plan_solve(cs_plan *P, const double *ref, const double *w_mat, double *ve
     if (int r = check_solver_params(params)) return r;
     const int64_t E = P->E, NK = (int64_t)P->rp.N * P->rp.K, R = (E + 31) / 32 * 32 * NK;
     cs_solver_rows &S = P->srows;
-    if (!S.body_a)
+    if (!S.body_a) {
         if (int r = alloc_rows(P, S, NK, R)) return r;
+        if (int r = P->alloc(&P->spacked, (size_t)E * NK * 22)) return r;
+    }
     cudaStream_t s = (cudaStream_t)stream;
     const SysRows rows{nullptr, NK, P->io.n_kept, R};
     PlanRowsIO pr{P->io.patch_nkept, P->io.n_patch, P->io.kept_point, P->io.kept_normal, P->io.kept_depth, mu,
                   restitution, slop, nullptr, nullptr, nullptr, P->rp.N, P->rp.K, rows, nullptr, S.body_a,
                   S.body_b, S.point, S.normal, S.depth, S.mu, S.restitution, S.slop};
     launch_plan_rows(E, pr, s);
-    return solve_rows(P, S, rows, E, 2, true, ref, w_mat, vel, imp, params, wrench, s);
+    return solve_rows(P, S, rows, E, 2, true, ref, w_mat, vel, imp, params, wrench, s, P->spacked);
 }
 
 int cs_plan_solver_rows(cs_plan *P, cs_solver_rows *rows) {
@@ -915,6 +919,7 @@ int cs_multipair_solve(cs_plan *P, int64_t n_sys, int32_t nb, const int64_t *slo
     if (!S.body_a) {
         if (int r = alloc_rows(P, S, stride, R)) return r;
         if (int r = P->alloc(&P->mrow_count, n_sys)) return r;
+        if (int r = P->alloc(&P->mpacked, (size_t)n_sys * stride * 22)) return r;
         P->mrows_sys = n_sys;
     }
     cudaStream_t s = (cudaStream_t)stream;
@@ -923,7 +928,7 @@ int cs_multipair_solve(cs_plan *P, int64_t n_sys, int32_t nb, const int64_t *slo
                   restitution, slop, slot_off, slot_a, slot_b, P->rp.N, P->rp.K, rows, P->mrow_count, S.body_a,
                   S.body_b, S.point, S.normal, S.depth, S.mu, S.restitution, S.slop};
     launch_plan_rows(n_sys, pr, s);
-    return solve_rows(P, S, rows, n_sys, nb, false, ref, w_mat, vel, imp, params, wrench, s);
+    return solve_rows(P, S, rows, n_sys, nb, false, ref, w_mat, vel, imp, params, wrench, s, P->mpacked);
 }
 
 int cs_plan_multipair_rows(cs_plan *P, cs_solver_rows *rows, const int32_t **n_rows) {

@@ -297,6 +297,55 @@ __device__ __forceinline__ void stage_row(double *slot, const SweepIO &io, const
     }
 }
 
+// One row of the sweep (_kernels.py:71-115) on the system state st; the row's
+// accumulators are read and written through pln / plt1 / plt2.
+template <class St>
+__device__ __forceinline__ void solve_row(St &st, int ia, int ib, const double a[3], const double b[3],
+                                          const double n[3], const double t1[3], const double t2[3], double kn,
+                                          double kt1, double kt2, double tg, double mu, double *pln, double *plt1,
+                                          double *plt2, int with_friction) {
+    double ln = *pln;
+    if (kn > 0.0) {
+        const double vn = rel_vel(st, ia, ib, a, b, n[0], n[1], n[2]);
+        double dl = kn * (tg - vn);
+        double new_l = ln + dl;
+        if (new_l < 0.0) new_l = 0.0;
+        dl = new_l - ln;
+        ln = new_l;
+        *pln = new_l;
+        if (dl != 0.0) {
+            const double jx = dl * n[0], jy = dl * n[1], jz = dl * n[2];
+            apply_impulse(st, ib, jx, jy, jz, b[0], b[1], b[2], 1.0);
+            apply_impulse(st, ia, jx, jy, jz, a[0], a[1], a[2], -1.0);
+        }
+    }
+    if (with_friction && mu > 0.0 && ln > 0.0) {
+        const double lt1 = *plt1, lt2 = *plt2;
+        double d1 = 0.0, d2 = 0.0;
+        if (kt1 > 0.0) d1 = -kt1 * rel_vel(st, ia, ib, a, b, t1[0], t1[1], t1[2]);
+        if (kt2 > 0.0) d2 = -kt2 * rel_vel(st, ia, ib, a, b, t2[0], t2[1], t2[2]);
+        double new1 = lt1 + d1, new2 = lt2 + d2;
+        const double limit = mu * ln;
+        const double mag = sqrt(new1 * new1 + new2 * new2);
+        if (mag > limit) {
+            const double scale = limit / mag;
+            new1 *= scale;
+            new2 *= scale;
+        }
+        d1 = new1 - lt1;
+        d2 = new2 - lt2;
+        *plt1 = new1;
+        *plt2 = new2;
+        if (d1 != 0.0 || d2 != 0.0) {
+            const double jx = d1 * t1[0] + d2 * t2[0];
+            const double jy = d1 * t1[1] + d2 * t2[1];
+            const double jz = d1 * t1[2] + d2 * t2[2];
+            apply_impulse(st, ib, jx, jy, jz, b[0], b[1], b[2], 1.0);
+            apply_impulse(st, ia, jx, jy, jz, a[0], a[1], a[2], -1.0);
+        }
+    }
+}
+
 // The phases of one system, its rows in sweep order. FIX: every row has
 // body_a = 0, body_b = 1 (plan rows, scene.py:228-243), so body indices are
 // compile-time constants.
@@ -352,46 +401,7 @@ __device__ __forceinline__ void sweep_system(St &st, const SweepIO &io, const Sw
             double *pln = lam_sm ? lam + j * SW_T : ph.lam_n + c;
             double *plt1 = lam_sm ? lt1s + j * SW_T : io.lam_t1 + c;
             double *plt2 = lam_sm ? lt2s + j * SW_T : io.lam_t2 + c;
-            double ln = *pln;
-            if (kn > 0.0) {
-                const double vn = rel_vel(st, ia, ib, a, b, n[0], n[1], n[2]);
-                double dl = kn * (tg - vn);
-                double new_l = ln + dl;
-                if (new_l < 0.0) new_l = 0.0;
-                dl = new_l - ln;
-                ln = new_l;
-                *pln = new_l;
-                if (dl != 0.0) {
-                    const double jx = dl * n[0], jy = dl * n[1], jz = dl * n[2];
-                    apply_impulse(st, ib, jx, jy, jz, b[0], b[1], b[2], 1.0);
-                    apply_impulse(st, ia, jx, jy, jz, a[0], a[1], a[2], -1.0);
-                }
-            }
-            if (ph.with_friction && mu > 0.0 && ln > 0.0) {
-                const double lt1 = *plt1, lt2 = *plt2;
-                double d1 = 0.0, d2 = 0.0;
-                if (kt1 > 0.0) d1 = -kt1 * rel_vel(st, ia, ib, a, b, t1[0], t1[1], t1[2]);
-                if (kt2 > 0.0) d2 = -kt2 * rel_vel(st, ia, ib, a, b, t2[0], t2[1], t2[2]);
-                double new1 = lt1 + d1, new2 = lt2 + d2;
-                const double limit = mu * ln;
-                const double mag = sqrt(new1 * new1 + new2 * new2);
-                if (mag > limit) {
-                    const double scale = limit / mag;
-                    new1 *= scale;
-                    new2 *= scale;
-                }
-                d1 = new1 - lt1;
-                d2 = new2 - lt2;
-                *plt1 = new1;
-                *plt2 = new2;
-                if (d1 != 0.0 || d2 != 0.0) {
-                    const double jx = d1 * t1[0] + d2 * t2[0];
-                    const double jy = d1 * t1[1] + d2 * t2[1];
-                    const double jz = d1 * t1[2] + d2 * t2[2];
-                    apply_impulse(st, ib, jx, jy, jz, b[0], b[1], b[2], 1.0);
-                    apply_impulse(st, ia, jx, jy, jz, a[0], a[1], a[2], -1.0);
-                }
-            }
+            solve_row(st, ia, ib, a, b, n, t1, t2, kn, kt1, kt2, tg, mu, pln, plt1, plt2, ph.with_friction);
             if (++j == m) j = 0;
         }
         __pipeline_wait_prior(0);
@@ -473,6 +483,202 @@ __global__ void __launch_bounds__(SW_T) k_sweeps(int64_t S, int nb, SysRows rows
         for (int j = 0; j < nv; ++j) {
             io.vel[s * nv + j] = st.V[j * SW_T];
             io.imp[s * nv + j] = st.I[j * SW_T];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ packed rows + bulk copies
+//
+// The plan paths (cs_plan_solve, cs_multipair_solve) pack each row's sweep fields
+// into one 176-byte record after the build; the sweep then streams chunks of
+// PK_CH records of its system into a shared-memory double buffer with one TMA
+// bulk copy (cp.async.bulk, mbarrier completion) per chunk instead of 20 8-byte
+// asynchronous copies per row (LDGSTS: 8 issue cycles each).
+constexpr int PK_F = 22;  // a[3] b[3] n[3] t1[3] t2[3] kn kt1 kt2 target(pos) target(vel) mu ids(2 x i32)
+constexpr int PK_CH = 8;  // rows per bulk copy
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT%=;\n}" ::"r"(
+            smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// rows (interleaved) -> records packed[(s stride + j) PK_F + f]; a thread per row slot
+__global__ void k_pack_rows(int64_t S, SysRows rows, SweepIO io, const double *tg_pos, const double *tg_vel,
+                            double *__restrict__ packed) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= rows.planes) return;
+    const int64_t blk = (t >> 5) / rows.stride, j = (t >> 5) % rows.stride, s = blk * 32 + (t & 31);
+    if (s >= S || j >= rows.n(s)) return;
+    double *o = packed + (s * rows.stride + j) * PK_F;
+    for (int k = 0; k < 3; ++k) {
+        const int64_t v = rows.vec(t, k);
+        o[k] = io.ra[v]; o[3 + k] = io.rb[v]; o[6 + k] = io.nrm[v]; o[9 + k] = io.tan1[v]; o[12 + k] = io.tan2[v];
+    }
+    o[15] = io.kn[t]; o[16] = io.kt1[t]; o[17] = io.kt2[t];
+    o[18] = tg_pos[t]; o[19] = tg_vel[t]; o[20] = io.mu[t];
+    const int2 ids = make_int2((int)io.body_a[t], (int)io.body_b[t]);
+    o[21] = __longlong_as_double(((long long)(unsigned)ids.y << 32) | (unsigned)ids.x);
+}
+
+template <bool FIX, class St>
+__device__ __forceinline__ void sweep_packed(St &st, const SweepIO &io, const SweepPhase *phs, int n_phases,
+                                             const SysRows &rows, int64_t s, const double *packed, double *buf,
+                                             uint64_t *bar, double *lam) {
+    const int m = (int)rows.n(s);
+    if (m <= 0) return;
+    const int64_t base = rows.row(s, 0), step = 32;  // accumulators stay in the interleaved layout
+    const double *src = packed + s * rows.stride * PK_F;
+    const bool lam_sm = m <= LAM_CAP;
+    double *lt1s = lam + LAM_CAP * SW_T, *lt2s = lam + 2 * LAM_CAP * SW_T;
+    if (lam_sm)
+        for (int j = 0; j < m; ++j) {
+            __pipeline_memcpy_async(lt1s + j * SW_T, io.lam_t1 + base + step * j, 8);
+            __pipeline_memcpy_async(lt2s + j * SW_T, io.lam_t2 + base + step * j, 8);
+        }
+    const int nch = (m + PK_CH - 1) / PK_CH;
+    unsigned use0 = 0, use1 = 0;  // completed phases of each buffer's barrier
+    auto issue = [&](int k, int b) {
+        const int r0 = k * PK_CH, nr = min(PK_CH, m - r0);
+        fence_proxy_async();  // the buffer's previous rows were read through the generic proxy
+        bulk_load(buf + b * PK_CH * PK_F, src + (int64_t)r0 * PK_F, (unsigned)(nr * PK_F * sizeof(double)), bar + b);
+    };
+    for (int phi = 0; phi < n_phases; ++phi) {
+        const SweepPhase ph = phs[phi];
+        if (ph.iters <= 0) continue;
+        if (lam_sm) {
+            for (int j = 0; j < m; ++j) __pipeline_memcpy_async(lam + j * SW_T, ph.lam_n + base + step * j, 8);
+            __pipeline_commit();
+            __pipeline_wait_prior(0);
+        }
+        const bool pos = phi == 0;  // targets: phase 0 the bias, phase 1 the restitution (record fields 18 / 19)
+        const int64_t T = ph.iters * (int64_t)nch;
+        issue(0, 0);
+        for (int64_t q = 0; q < T; ++q) {
+            const int b = (int)(q & 1), k = (int)(q % nch);
+            if (q + 1 < T) issue((int)((q + 1) % nch), b ^ 1);
+            mbar_wait(bar + b, b ? (use1++ & 1) : (use0++ & 1));
+            const double *rb = buf + b * PK_CH * PK_F;
+            const int r0 = k * PK_CH, nr = min(PK_CH, m - r0);
+            for (int r = 0; r < nr; ++r) {
+                const double2 *w2 = reinterpret_cast<const double2 *>(rb + r * PK_F);
+                double f[PK_F];
+#pragma unroll
+                for (int i = 0; i < PK_F / 2; ++i) { const double2 x = w2[i]; f[2 * i] = x.x; f[2 * i + 1] = x.y; }
+                const double a[3] = {f[0], f[1], f[2]}, bb[3] = {f[3], f[4], f[5]}, n[3] = {f[6], f[7], f[8]};
+                const double t1[3] = {f[9], f[10], f[11]}, t2[3] = {f[12], f[13], f[14]};
+                const long long ids = __double_as_longlong(f[21]);
+                const int ia = FIX ? 0 : (int)(ids & 0xffffffff), ib = FIX ? 1 : (int)(ids >> 32);
+                const int j = r0 + r;
+                const int64_t c = base + step * j;
+                double *pln = lam_sm ? lam + j * SW_T : ph.lam_n + c;
+                double *plt1 = lam_sm ? lt1s + j * SW_T : io.lam_t1 + c;
+                double *plt2 = lam_sm ? lt2s + j * SW_T : io.lam_t2 + c;
+                solve_row(st, ia, ib, a, bb, n, t1, t2, f[15], f[16], f[17], pos ? f[18] : f[19], f[20], pln, plt1, plt2,
+                          ph.with_friction);
+            }
+        }
+        if (lam_sm)
+            for (int jj = 0; jj < m; ++jj) ph.lam_n[base + step * jj] = lam[jj * SW_T];
+    }
+    __pipeline_commit();
+    __pipeline_wait_prior(0);
+    if (lam_sm)
+        for (int jj = 0; jj < m; ++jj) {
+            io.lam_t1[base + step * jj] = lt1s[jj * SW_T];
+            io.lam_t2[base + step * jj] = lt2s[jj * SW_T];
+        }
+}
+
+__host__ __device__ inline size_t packed_smem_doubles(int nb, bool regs) {
+    return (size_t)36 * nb + (regs ? 0 : (size_t)12 * nb) + (size_t)2 * PK_CH * PK_F + 3 * (size_t)LAM_CAP;
+}
+
+// The plan paths' sweeps (interleaved rows, packed records): one system per
+// thread (SW_T == 1 block), MODE as k_sweeps.
+template <int MODE, bool FIX>
+__global__ void __launch_bounds__(SW_T) k_sweeps_packed(int64_t S, int nb, SysRows rows, SweepIO io,
+                                                        const double *__restrict__ packed, SweepPhase p0,
+                                                        SweepPhase p1, int n_phases) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ uint64_t bar[2];
+    const int64_t s = blockIdx.x * (int64_t)SW_T + threadIdx.x;
+    if (s >= S) return;
+    static_assert(SW_T == 1, "the packed sweep runs one system per block");
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    fence_proxy_async();
+    const int nv = 6 * nb;
+    double *Ws = sm;
+    for (int j = 0; j < 36 * nb; ++j) Ws[j] = __ldg(io.w_mat + s * 36 * nb + j);
+    double *after_w = sm + (size_t)36 * nb + (MODE ? 0 : (size_t)12 * nb);
+    double *buf = after_w;  // 16-byte aligned: 36 nb (+ 12 nb) doubles are a multiple of 2
+    double *lam = after_w + 2 * PK_CH * PK_F;
+    const SweepPhase phs[2] = {p0, p1};
+    if (MODE == 2) {
+        RegState2 st;
+        st.W = Ws;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            st.v0[k] = io.vel[s * 12 + k]; st.v1[k] = io.vel[s * 12 + 6 + k];
+            st.i0[k] = io.imp[s * 12 + k]; st.i1[k] = io.imp[s * 12 + 6 + k];
+        }
+        st.z0 = frozen_body(Ws, st.v0);
+        st.z1 = frozen_body(Ws + 36 * SW_T, st.v1);
+        sweep_packed<FIX>(st, io, phs, n_phases, rows, s, packed, buf, bar, lam);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            io.vel[s * 12 + k] = st.v0[k]; io.vel[s * 12 + 6 + k] = st.v1[k];
+            io.imp[s * 12 + k] = st.i0[k]; io.imp[s * 12 + 6 + k] = st.i1[k];
+        }
+    } else if (MODE == 4) {
+        RegStateN<4> st;
+        st.W = Ws;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                st.v_[b][k] = b < nb ? io.vel[s * nv + 6 * b + k] : 0.0;
+                st.i_[b][k] = b < nb ? io.imp[s * nv + 6 * b + k] : 0.0;
+            }
+            st.z_[b] = b < nb ? frozen_body(Ws + 36 * b * SW_T, st.v_[b]) : true;
+        }
+        sweep_packed<FIX>(st, io, phs, n_phases, rows, s, packed, buf, bar, lam);
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+            if (b < nb)
+#pragma unroll
+                for (int k = 0; k < 6; ++k) {
+                    io.vel[s * nv + 6 * b + k] = st.v_[b][k];
+                    io.imp[s * nv + 6 * b + k] = st.i_[b][k];
+                }
+    } else {
+        SmemState st;
+        st.W = Ws;
+        st.V = sm + 36 * nb;
+        st.I = st.V + nv;
+        for (int j = 0; j < nv; ++j) {
+            st.V[j] = io.vel[s * nv + j];
+            st.I[j] = io.imp[s * nv + j];
+        }
+        sweep_packed<FIX>(st, io, phs, n_phases, rows, s, packed, buf, bar, lam);
+        for (int j = 0; j < nv; ++j) {
+            io.vel[s * nv + j] = st.V[j];
+            io.imp[s * nv + j] = st.I[j];
         }
     }
 }
@@ -600,6 +806,27 @@ void launch_sweeps(int64_t n_sys, int nb, const SysRows &rows, const SweepIO &io
     else if (two) go(k_sweeps<2, false>);
     else if (regs) go(k_sweeps<4, false>);
     else go(k_sweeps<0, false>);
+}
+
+void launch_sweeps_packed(int64_t n_sys, int nb, const SysRows &rows, const SweepIO &io, const SweepPhase *phases,
+                          int n_phases, double *packed, cudaStream_t s, bool fixed_bodies) {
+    if (n_sys <= 0 || n_phases <= 0) return;
+    k_pack_rows<<<(unsigned)((rows.planes + 255) / 256), 256, 0, s>>>(n_sys, rows, io, phases[0].target,
+                                                                       n_phases > 1 ? phases[1].target
+                                                                                    : phases[0].target,
+                                                                       packed);
+    const unsigned grid = (unsigned)((n_sys + SW_T - 1) / SW_T);
+    const SweepPhase p1 = n_phases > 1 ? phases[1] : phases[0];
+    const bool two = nb == 2, regs = nb <= 4;
+    const size_t smem = packed_smem_doubles(nb, regs) * sizeof(double);
+    auto go = [&](auto kern) {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, SW_T, smem, s>>>(n_sys, nb, rows, io, packed, phases[0], p1, n_phases);
+    };
+    if (two && fixed_bodies) go(k_sweeps_packed<2, true>);
+    else if (two) go(k_sweeps_packed<2, false>);
+    else if (regs) go(k_sweeps_packed<4, false>);
+    else go(k_sweeps_packed<0, false>);
 }
 
 void launch_body_wrenches(int64_t n_sys, int nb, const SysRows &rows, const WrenchIO &io, cudaStream_t s) {

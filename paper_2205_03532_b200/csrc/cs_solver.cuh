@@ -64,6 +64,11 @@ void launch_constraints_build(int64_t n_sys, int nb, const SysRows &rows, const 
 // fixed_bodies: every row has body_a = 0, body_b = 1 (plan rows)
 void launch_sweeps(int64_t n_sys, int nb, const SysRows &rows, const SweepIO &io, const SweepPhase *phases,
                    int n_phases, cudaStream_t s, bool fixed_bodies = false);
+// Interleaved plan rows only: packs the sweep fields of every row (phase 0's and
+// phase 1's targets included) into `packed` [n_sys * stride * 22] and sweeps from
+// the records with bulk copies.
+void launch_sweeps_packed(int64_t n_sys, int nb, const SysRows &rows, const SweepIO &io, const SweepPhase *phases,
+                          int n_phases, double *packed, cudaStream_t s, bool fixed_bodies = false);
 void launch_body_wrenches(int64_t n_sys, int nb, const SysRows &rows, const WrenchIO &io, cudaStream_t s);
 
 // Plan rows: system s's rows are the kept contacts of its pair slots (plan envs)
