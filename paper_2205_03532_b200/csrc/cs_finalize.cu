@@ -533,7 +533,11 @@ __global__ void __launch_bounds__(FL_WARPS * 32) k_fin_fold_large(ReduceIO io, R
 
 
 constexpr int CH_WARPS = 4;   // warps per k_fin_chain CTA
-constexpr int CG = 8;         // lanes per half chain: pops tested per round
+#ifndef CH_CG
+#define CH_CG 8  // measured best: 4 lanes (8 chains per warp) is 3% slower
+#endif
+constexpr int CG = CH_CG;     // lanes per half chain: pops tested per round
+constexpr int NG = 32 / CG;   // half chains per warp
 constexpr int CS = 64;        // stack entries per half chain in shared memory
 
 // One half of _monotone_hull (reduction.py:214-223) by one thread with its stack in
@@ -574,14 +578,14 @@ __device__ int half_chain_global(const double2 *kuv, const int32_t *kpos, int L,
 // rows, each lane prefetching every 8th key one octet ahead. The stack is the half
 // hull.
 __global__ void __launch_bounds__(CH_WARPS * 32) k_fin_chain(ReduceIO io, ReduceParams p) {
-    __shared__ double2 s_st[CH_WARPS * 4][CS];
-    __shared__ int32_t s_stp[CH_WARPS * 4][CS];
+    __shared__ double2 s_st[CH_WARPS * NG][CS];
+    __shared__ int32_t s_stp[CH_WARPS * NG][CS];
     __shared__ int bstart[CH_BUCKETS + 1];
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int g = lane >> 3, li = lane & 7, gb = g * CG;
-    double2 *st = s_st[wib * 4 + g];
-    int32_t *stp = s_stp[wib * 4 + g];
+    const int g = lane / CG, li = lane & (CG - 1), gb = g * CG;
+    double2 *st = s_st[wib * NG + g];
+    int32_t *stp = s_stp[wib * NG + g];
     if (threadIdx.x == 0) {
         int r = 0;
         for (int k = 0; k < CH_BUCKETS; ++k) { bstart[k] = r; r += io.njob[k]; }
@@ -592,7 +596,7 @@ __global__ void __launch_bounds__(CH_WARPS * 32) k_fin_chain(ReduceIO io, Reduce
     const int64_t bcap = 4 * io.E * (int64_t)p.N;
     while (true) {
         int base = 0;
-        if (lane == 0) base = atomicAdd(io.njob + CH_BUCKETS, 4);
+        if (lane == 0) base = atomicAdd(io.njob + CH_BUCKETS, NG);
         base = __shfl_sync(FULL, base, 0);
         if (base >= ntot) break;
         // this group's chain: job base + g (4 consecutive jobs: similar lengths)
@@ -617,8 +621,9 @@ __global__ void __launch_bounds__(CH_WARPS * 32) k_fin_chain(ReduceIO io, Reduce
         const int dir = (kind & 1) ? -1 : 1;
         const double2 *kuv = kind < 2 ? io.suv + row0 : io.tuv + row0;
         const int32_t *kpos = kind < 2 ? nullptr : io.tpos + row0;
-        int Lmax = max(__shfl_sync(FULL, L, 0), __shfl_sync(FULL, L, 8));
-        Lmax = max(Lmax, max(__shfl_sync(FULL, L, 16), __shfl_sync(FULL, L, 24)));
+        int Lmax = 0;
+#pragma unroll
+        for (int gg = 0; gg < NG; ++gg) Lmax = max(Lmax, __shfl_sync(FULL, L, gg * CG));
         // key x of the chain (index clamped into the list: no branch around the loads)
         auto key = [&](int x, double &u, double &v, int &ps) {
             const int c = min(x, L - 1);
@@ -651,7 +656,7 @@ __global__ void __launch_bounds__(CH_WARPS * 32) k_fin_chain(ReduceIO io, Reduce
                     const double2 a = st[top - 1 - li], o = st[top - 2 - li];
                     popi = !((a.x - o.x) * (vb - o.y) - (a.y - o.y) * (ub - o.x) > 0.0);
                 }
-                const unsigned stop = (__ballot_sync(FULL, !popi) >> gb) & 0xffu;
+                const unsigned stop = (__ballot_sync(FULL, !popi) >> gb) & ((1u << CG) - 1u);
                 const int npop = more ? (stop ? __ffs(stop) - 1 : CG) : 0;
                 top -= npop;
                 more = npop == CG;
