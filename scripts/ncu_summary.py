@@ -104,6 +104,10 @@ def main():
                   "dram_bytes_per_launch": mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum"),
                   "duration_ms_ncu": float(d["gpu__time_duration.sum"][0].replace(",", "")) *
                   (1e-3 if d["gpu__time_duration.sum"][1] == "usecond" else 1.0),
+                  "fp64_pipe_pct": float(d["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"][0]),
+                  "issue_active_pct": float(d["smsp__issue_active.avg.pct_of_peak_sustained_active"][0]),
+                  "warps_active_pct": float(d["sm__warps_active.avg.pct_of_peak_sustained_active"][0]),
+                  "l2_hit_pct": float(d["lts__t_sector_hit_rate.pct"][0]),
                   "note": "ncu --set full, cold-cache serialized replay; traffic = dram read + write bytes"}
             with open(os.path.join(prof, f"{kern}_ncu.json"), "w") as fh:
                 json.dump(js, fh, indent=1)
