@@ -64,6 +64,16 @@ def _destroy_plan(ptr: int) -> None:
         pass
 
 
+class _PlanHandle:
+    """Owns a cs_plan's device memory. The plan's tensor views keep this handle (not
+    the Plan) alive, so dropping a Plan frees its buffers at once unless a view of
+    them is still held (no Plan <-> view reference cycle waiting for the GC)."""
+
+    def __init__(self, ptr: int):
+        self.ptr = ptr
+        weakref.finalize(self, _destroy_plan, ptr)
+
+
 class Plan:
     """Owns the device buffers of one env configuration (cs_plan_create)."""
 
@@ -87,12 +97,12 @@ class Plan:
                                              stages, ctypes.byref(ptr)))
         self.ptr = int(ptr.value)
         self.stages = stages
-        weakref.finalize(self, _destroy_plan, self.ptr)
+        self._handle = _PlanHandle(self.ptr)
         o = _native.OutputsC()
         _native.check(lib.cs_plan_outputs(self.ptr, ctypes.byref(o)))
         self.c = o
         E, N, K, cap = o.n_envs, o.max_patches, o.per_patch_cap, o.total_capacity
-        v = lambda name, shape, dt: _native.device_view(getattr(o, name), shape, dt, self)  # noqa: E731
+        v = lambda name, shape, dt: _native.device_view(getattr(o, name), shape, dt, self._handle)  # noqa: E731
         self.cand_base = v("cand_base", (E,), "i8")
         self.env_status = v("env_status", (E,), "i4")
         self.n_cand = v("n_cand", (E,), "i4")
@@ -190,12 +200,12 @@ class Plan:
         out = {"stride": int(r.stride), "planes": int(R)}
         vec = ("point", "normal", "ra", "rb", "tan1", "tan2")
         for k in ("body_a", "body_b"):
-            out[k] = _native.device_view(getattr(r, k), (R,), "i8", self)
+            out[k] = _native.device_view(getattr(r, k), (R,), "i8", self._handle)
         for k in vec:
-            out[k] = _native.device_view(getattr(r, k), (3, R), "f8", self)
+            out[k] = _native.device_view(getattr(r, k), (3, R), "f8", self._handle)
         for k in ("depth", "mu", "restitution", "slop", "kn", "kt1", "kt2", "bias_target", "restitution_target",
                   "lam_n", "lam_vel", "lam_t1", "lam_t2"):
-            out[k] = _native.device_view(getattr(r, k), (R,), "f8", self)
+            out[k] = _native.device_view(getattr(r, k), (R,), "f8", self._handle)
         if e is None:
             return out
         m = int(self.n_kept[e].item())
@@ -282,6 +292,12 @@ class ReducedContacts:
 
 
 _plan_cache: dict = {}
+
+
+def clear_plan_cache() -> None:
+    """Drop the plans collide() keeps per (handles, params) key (their device memory
+    is freed once no result view of them is held)."""
+    _plan_cache.clear()
 
 
 def get_plan(sdf_handles, mesh_handles, params: ReductionParams | None) -> Plan:

@@ -67,8 +67,8 @@ def main():
                               "ms_per_step": t, "face_queries_per_s": E * F / (t * 1e-3),
                               "candidates_per_env": float(nc.mean()),
                               "phase_ms": {n: float(ph[:, i].mean()) for i, n in enumerate(plan.PHASES)}}), flush=True)
-            del plan, sp, mp, cd
-            gc.collect()  # plan <-> device-view cycles
+            del plan, sp, mp, cd  # frees the plan's buffers (collide._PlanHandle)
+            gc.collect()
             torch.cuda.empty_cache()
 
 

@@ -410,3 +410,19 @@ def test_collide_cuda_graph_replay(P, grid64, nut, gen64):
     eager = snap()
     for k in keys:
         assert torch.equal(got[k], eager[k]), k
+
+
+def test_plan_memory_released_without_gc(P, grid64, nut):
+    """Dropping a Plan frees its device buffers at once (views keep a small handle,
+    not the Plan, so there is no reference cycle); a held view keeps them alive."""
+    E = 256
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    plan = P.Plan([P.register_sdf(grid64)] * E, [P.register_mesh(nut)] * E, P.ReductionParams())
+    used = free0 - torch.cuda.mem_get_info()[0]
+    assert used > 100e6
+    view = plan.n_cand
+    del plan
+    assert free0 - torch.cuda.mem_get_info()[0] > 0.9 * used  # still owned through the view
+    del view
+    assert free0 - torch.cuda.mem_get_info()[0] < 0.1 * used
