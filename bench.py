@@ -339,16 +339,23 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    outer = []
     for _ in range(args.steps):
         if not args.no_flush:
             flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
         plan.collide(sp, mp, cd)
+        if world > 1:  # the step's one collective: the per-env stats all-gather
+            gather_env_stats(plan.stats, E * world)
+        b.record(stream)
+        outer.append((a, b))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
     phases = plan.read_timing(args.steps)
-    total_ms = float(phases[:, plan.PHASES.index("total")].sum())
+    total_ms = float(sum(a.elapsed_time(b) for a, b in outer))
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -356,33 +363,31 @@ def main():
     ms_per_step = total_ms / args.steps
     value = world * E * F * args.steps / (total_ms * 1e-3)
 
-    # the same step replayed from a CUDA graph (launch gaps removed), flush between
-    gs = torch.cuda.Stream()
-    gs.wait_stream(stream)
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph, stream=gs):
-        plan.collide(sp, mp, cd, stream=gs)
-    graph.replay()
-    torch.cuda.synchronize()
-    g_ms = []
-    for _ in range(args.steps):
-        if not args.no_flush:
-            flush.fill_(1)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        graph.replay()
-        b.record(stream)
-        b.synchronize()
-        g_ms.append(a.elapsed_time(b))
-    gt = torch.tensor([float(np.sum(g_ms))], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(gt, op=dist.ReduceOp.MAX)
-    graph_ms_total = float(gt.item())
-    del graph
-    # the headline is the graph replay; eager launches with phase events beside it
+    # N == 1: the same step replayed from a CUDA graph (launch gaps removed),
+    # flush between; the headline. N > 1 keeps the eager steps (each with its all-gather).
     eager = {"ms_per_step": ms_per_step, "value": value, "phase_ms": "see phase_ms"}
-    ms_per_step = graph_ms_total / args.steps
-    value = world * E * F * args.steps / (graph_ms_total * 1e-3)
+    if world == 1:
+        gs = torch.cuda.Stream()
+        gs.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gs):
+            plan.collide(sp, mp, cd, stream=gs)
+        graph.replay()
+        torch.cuda.synchronize()
+        g_ms = []
+        for _ in range(args.steps):
+            if not args.no_flush:
+                flush.fill_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            graph.replay()
+            b.record(stream)
+            b.synchronize()
+            g_ms.append(a.elapsed_time(b))
+        graph_ms_total = float(np.sum(g_ms))
+        del graph
+        ms_per_step = graph_ms_total / args.steps
+        value = world * E * F * args.steps / (graph_ms_total * 1e-3)
 
     solver = solver_leg(P, plan, w, lo, hi, E, min(args.steps, 50), args.quick)
 
@@ -455,7 +460,8 @@ def main():
                                        "achieved_gbs": pgd_bytes / (pgd_ms * 1e-3) / 1e9,
                                        "basis": "32 B per trilinear sample"}},
             "clocks": clk,
-            "timing": "CUDA-graph replay of the step, CUDA events per step, max over ranks (SURVEY §8(d))",
+            "timing": ("CUDA-graph replay of the step, CUDA events per step (SURVEY §8(d))" if world == 1 else
+                       "eager steps incl. the stats all-gather, CUDA events per step, max over ranks"),
             "eager": eager,
             "solver": solver,
             "stats": {"candidates_per_env": float(stats[:, 0].double().mean()),
