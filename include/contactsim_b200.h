@@ -55,6 +55,8 @@ int cs_device_info(int32_t *sm_count, int64_t *l2_bytes, int64_t *persist_l2_max
 int cs_sdf_register(const float *values, int values_on_device, int32_t nx, int32_t ny, int32_t nz,
                     const double origin[3], double voxel, const double aabb_lo[3], const double aabb_hi[3],
                     int32_t *handle);
+/* Freeing a grid (or mesh) that live plans sample defers the release to the
+ * destruction of the last such plan; the handle is invalid for new plans at once. */
 int cs_sdf_free(int32_t handle);
 /* [dev] pointer to the stored values (for the per-pair drop-ins below). */
 int cs_sdf_values(int32_t handle, const float **values);

@@ -58,6 +58,8 @@ struct SdfEntry {
     float *bwin = nullptr;  // brick-window minima (GridT::bwin)
     size_t bytes = 0;
     SdfDesc desc{};
+    int users = 0;        // live plans naming this grid
+    bool doomed = false;  // freed by the caller while in use: released with the last plan
 };
 struct MeshEntry {
     bool live = false;
@@ -66,6 +68,8 @@ struct MeshEntry {
     int32_t *chunk_voff = nullptr, *chunk_verts = nullptr;
     uint2 *face_loc = nullptr;
     MeshDesc desc{};
+    int users = 0;
+    bool doomed = false;
 };
 
 std::mutex g_mu;
@@ -97,6 +101,32 @@ int dalloc(T **p, size_t n) {
     if (n == 0) n = 1;
     CS_CUDA(cudaMalloc(reinterpret_cast<void **>(p), n * sizeof(T)));
     return CS_OK;
+}
+
+// (g_mu held) device memory of a store entry
+int free_sdf_entry(SdfEntry &s) {
+    CS_CUDA(cudaFree(s.values));
+    CS_CUDA(cudaFree(s.cwin));
+    CS_CUDA(cudaFree(s.bwin));
+    s = SdfEntry{};
+    return CS_OK;
+}
+int free_mesh_entry(MeshEntry &m) {
+    CS_CUDA(cudaFree(m.verts));
+    CS_CUDA(cudaFree(m.tris));
+    CS_CUDA(cudaFree(m.chunk_voff));
+    CS_CUDA(cudaFree(m.chunk_verts));
+    CS_CUDA(cudaFree(m.face_loc));
+    m = MeshEntry{};
+    return CS_OK;
+}
+// a plan stops using its assets: entries freed by the caller meanwhile go now
+void release_assets(const std::vector<int32_t> &sdfs, const std::vector<int32_t> &meshes) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (int32_t h : sdfs)
+        if (--g_sdf[h].users == 0 && g_sdf[h].doomed) free_sdf_entry(g_sdf[h]);
+    for (int32_t h : meshes)
+        if (--g_mesh[h].users == 0 && g_mesh[h].doomed) free_mesh_entry(g_mesh[h]);
 }
 
 }  // namespace
@@ -144,9 +174,12 @@ struct cs_plan {
         if (r == CS_OK) allocs.push_back(*p);
         return r;
     }
+    // assets this plan samples (their store entries outlive it, cs_sdf_free / cs_mesh_free)
+    std::vector<int32_t> sdf_used, mesh_used;
     ~cs_plan() {
         for (cudaEvent_t e : events) cudaEventDestroy(e);
         for (void *p : allocs) cudaFree(p);
+        release_assets(sdf_used, mesh_used);
     }
 };
 
@@ -259,13 +292,14 @@ int cs_sdf_register(const float *values, int values_on_device, int32_t nx, int32
 
 int cs_sdf_free(int32_t handle) {
     std::lock_guard<std::mutex> lk(g_mu);
-    if (handle < 0 || handle >= (int)g_sdf.size() || !g_sdf[handle].live) return fail(CS_ERR_HANDLE, "bad SDF handle %d", handle);
+    if (handle < 0 || handle >= (int)g_sdf.size() || !g_sdf[handle].live || g_sdf[handle].doomed)
+        return fail(CS_ERR_HANDLE, "bad SDF handle %d", handle);
     SdfEntry &s = g_sdf[handle];
-    CS_CUDA(cudaFree(s.values));
-    CS_CUDA(cudaFree(s.cwin));
-    CS_CUDA(cudaFree(s.bwin));
-    s = SdfEntry{};
-    return CS_OK;
+    if (s.users > 0) {  // a live plan samples it: freed when the last such plan is destroyed
+        s.doomed = true;
+        return CS_OK;
+    }
+    return free_sdf_entry(s);
 }
 
 int cs_sdf_values(int32_t handle, const float **values) {
@@ -384,15 +418,14 @@ int cs_mesh_register(const double *vertices, int64_t nv, const int32_t *triangle
 
 int cs_mesh_free(int32_t handle) {
     std::lock_guard<std::mutex> lk(g_mu);
-    if (handle < 0 || handle >= (int)g_mesh.size() || !g_mesh[handle].live) return fail(CS_ERR_HANDLE, "bad mesh handle %d", handle);
+    if (handle < 0 || handle >= (int)g_mesh.size() || !g_mesh[handle].live || g_mesh[handle].doomed)
+        return fail(CS_ERR_HANDLE, "bad mesh handle %d", handle);
     MeshEntry &m = g_mesh[handle];
-    CS_CUDA(cudaFree(m.verts));
-    CS_CUDA(cudaFree(m.tris));
-    CS_CUDA(cudaFree(m.chunk_voff));
-    CS_CUDA(cudaFree(m.chunk_verts));
-    CS_CUDA(cudaFree(m.face_loc));
-    m = MeshEntry{};
-    return CS_OK;
+    if (m.users > 0) {
+        m.doomed = true;
+        return CS_OK;
+    }
+    return free_mesh_entry(m);
 }
 
 // ---------------------------------------------------------------- per-pair drop-ins
@@ -536,6 +569,7 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
     bool uniform = true;
     PlanGrid ugrid{};
     int32_t maxcv = 1;
+    std::vector<int32_t> used_s, used_m;
     {
         std::lock_guard<std::mutex> lk(g_mu);
         int r = ensure_tables();
@@ -543,8 +577,10 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
         for (int64_t e = 0; e < n_envs; ++e) {
             uniform &= sdf_handles[e] == sdf_handles[0];
             int s = sdf_handles[e], m = mesh_handles[e];
-            if (s < 0 || s >= MAX_HANDLES || !g_sdf[s].live) return fail(CS_ERR_HANDLE, "env %lld: bad SDF handle %d", (long long)e, s);
-            if (m < 0 || m >= MAX_HANDLES || !g_mesh[m].live) return fail(CS_ERR_HANDLE, "env %lld: bad mesh handle %d", (long long)e, m);
+            if (s < 0 || s >= MAX_HANDLES || !g_sdf[s].live || g_sdf[s].doomed)
+                return fail(CS_ERR_HANDLE, "env %lld: bad SDF handle %d", (long long)e, s);
+            if (m < 0 || m >= MAX_HANDLES || !g_mesh[m].live || g_mesh[m].doomed)
+                return fail(CS_ERR_HANDLE, "env %lld: bad mesh handle %d", (long long)e, m);
             int64_t nt = g_mesh[m].desc.nt;
             cap[(size_t)e] = nt;
             maxcv = std::max(maxcv, g_mesh[m].desc.max_chunk_verts);
@@ -553,8 +589,18 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
         }
         if (uniform) ugrid = g_sdf[sdf_handles[0]].desc.gp;
         chunk_first.push_back((int32_t)bmap.size());
+        used_s.assign(sdf_handles, sdf_handles + n_envs);
+        used_m.assign(mesh_handles, mesh_handles + n_envs);
+        for (auto *u : {&used_s, &used_m}) {
+            std::sort(u->begin(), u->end());
+            u->erase(std::unique(u->begin(), u->end()), u->end());
+        }
+        for (int32_t h : used_s) ++g_sdf[h].users;
+        for (int32_t h : used_m) ++g_mesh[h].users;
     }
     cs_plan *P = new cs_plan();
+    P->sdf_used = std::move(used_s);  // released by ~cs_plan (also on the failure paths below)
+    P->mesh_used = std::move(used_m);
     P->E = n_envs;
     P->stages = stages;
     P->uniform_sdf = uniform;

@@ -426,3 +426,34 @@ def test_plan_memory_released_without_gc(P, grid64, nut):
     assert free0 - torch.cuda.mem_get_info()[0] > 0.9 * used  # still owned through the view
     del view
     assert free0 - torch.cuda.mem_get_info()[0] < 0.1 * used
+
+
+def test_asset_free_deferred_while_plans_use_it(P, grid64, gen64, meshes):
+    """cs_sdf_free / cs_mesh_free on an asset a live plan samples defer the release to
+    the last such plan's destruction (no use-after-free); a freed handle cannot start
+    a new plan."""
+    import ctypes
+
+    from paper_2205_03532_b200 import _native
+
+    lib = _native.lib()
+    v, t = np.ascontiguousarray(meshes["nut_v"], np.float64), np.ascontiguousarray(meshes["nut_t"], np.int32)
+    hm = ctypes.c_int32(-1)
+    _native.check(lib.cs_mesh_register(v.ctypes.data, len(v), t.ctypes.data, len(t), ctypes.byref(hm)))
+    hs = P.register_sdf(grid64)
+    envs = list(gen64["envs"])[:2]
+    sp = torch.from_numpy(np.stack([gen64[f"e{e}_sdf_pose"] for e in envs])).cuda()
+    mp = torch.from_numpy(np.stack([gen64[f"e{e}_mesh_pose"] for e in envs])).cuda()
+    cd = torch.full((2,), float(gen64["cd"]), dtype=torch.float64, device="cuda")
+    plan = P.Plan([hs, hs], [hm.value, hm.value], P.ReductionParams())
+    plan.collide(sp, mp, cd)
+    before = plan.cand_face.clone()
+    _native.check(lib.cs_mesh_free(hm.value))  # deferred: the plan still samples it
+    plan.collide(sp, mp, cd)
+    torch.cuda.synchronize()
+    assert torch.equal(plan.cand_face, before)
+    assert lib.cs_mesh_free(hm.value) == _native.CS_ERR_HANDLE  # already freed by the caller
+    with pytest.raises(RuntimeError):
+        P.Plan([hs], [hm.value], P.ReductionParams())
+    del plan  # releases the mesh now
+    assert lib.cs_mesh_free(hm.value) == _native.CS_ERR_HANDLE
