@@ -64,7 +64,18 @@ __device__ double warp_hull_area_label(const int32_t *lab, int C, int L, const d
     return area;
 }
 
+#ifdef RED_PROF
+__device__ unsigned long long g_red_prof[8];
+#define RED_MARK(i) do { if (threadIdx.x == 0) { const long long t_ = clock64(); atomicAdd(&g_red_prof[i], (unsigned long long)(t_ - t_red)); t_red = t_; } } while (0)
+extern "C" int cs_debug_red_prof(unsigned long long *out) { return (int)cudaMemcpyFromSymbol(out, g_red_prof, sizeof(g_red_prof)); }
+#else
+#define RED_MARK(i) do {} while (0)
+#endif
+
 __global__ void __launch_bounds__(RED_T) k_reduce(ReduceIO io, ReduceParams p, int SB) {
+#ifdef RED_PROF
+    long long t_red = clock64();
+#endif
     extern __shared__ __align__(16) unsigned char dyn[];
     __shared__ int s_P;
     __shared__ int s_ws[WS_INTS];
@@ -115,6 +126,7 @@ __global__ void __launch_bounds__(RED_T) k_reduce(ReduceIO io, ReduceParams p, i
     }
 
     int P = 0;  // builders; uniform across the CTA at every barrier
+    RED_MARK(0);
     for (int start = 0; start < n_order; start += p.batch_size) {
         const int bsz = min(p.batch_size, n_order - start);
         // stage the batch: candidate index, normal and depth per position (read many times below)
@@ -154,6 +166,7 @@ __global__ void __launch_bounds__(RED_T) k_reduce(ReduceIO io, ReduceParams p, i
         // patch, each step spread over the CTA: the unassigned batch positions are kept
         // as an ascending list (ordered block-scan compaction), so "first argmax" is
         // numpy's, and the next seed comes out of the same pass as the bin.
+        RED_MARK(1);
         int nu, dp;
         {
             int run = 0;
@@ -335,7 +348,9 @@ __global__ void __launch_bounds__(RED_T) k_reduce(ReduceIO io, ReduceParams p, i
             dp = nx.i;
         }
         __syncthreads();
+        RED_MARK(3);
     }
+    RED_MARK(2);
     // builders -> outputs
     for (int q = tid; q < N; q += RED_T) {
         double *o = io.patch_normal + 3 * (e * N + q);
@@ -352,6 +367,7 @@ __global__ void __launch_bounds__(RED_T) k_reduce(ReduceIO io, ReduceParams p, i
         if (l >= 0) atomicAdd(&hcnt[l], 1);
     }
     __syncthreads();
+    RED_MARK(4);
     if (wid != 0) return;
     int32_t *moff = io.member_offsets + e * (N + 1);
     if (lane == 0) {
@@ -386,6 +402,7 @@ __global__ void __launch_bounds__(RED_T) k_reduce(ReduceIO io, ReduceParams p, i
             __syncwarp();
         }
     }
+    RED_MARK(5);
 }
 
 size_t reduce_smem_bytes(int N, int SB) { return red_smem_bytes(N, SB); }
