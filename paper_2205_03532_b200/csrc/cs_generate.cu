@@ -345,7 +345,7 @@ __device__ __forceinline__ void face_start(const FaceGeom &f, int which, double 
 }
 
 template <bool COUNT, bool UNIFORM>
-__global__ void __launch_bounds__(256, GRAD_MINB) k_pgd_grad(const int2 *__restrict__ block_map, const EnvXf *__restrict__ xf,
+__global__ void __launch_bounds__(256, UNIFORM ? GRAD_MINB : GRAD_MINB - 1) k_pgd_grad(const int2 *__restrict__ block_map, const EnvXf *__restrict__ xf,
                                                   const SdfDesc *__restrict__ sdfs, const MeshDesc *__restrict__ meshes,
                                                   Staging st, int stage,
                                                   unsigned long long *__restrict__ counter, const PlanGrid gu) {
@@ -420,7 +420,7 @@ __device__ __forceinline__ bool backtrack(const G &g, const FaceGeom &f, const d
 }
 
 template <bool COUNT, bool UNIFORM>
-__global__ void __launch_bounds__(256, FIRST_MINB) k_pgd_first(const int2 *__restrict__ block_map, const EnvXf *__restrict__ xf,
+__global__ void __launch_bounds__(256, UNIFORM ? FIRST_MINB : FIRST_MINB - 1) k_pgd_first(const int2 *__restrict__ block_map, const EnvXf *__restrict__ xf,
                                                    const SdfDesc *__restrict__ sdfs, const MeshDesc *__restrict__ meshes,
                                                    Staging st, unsigned long long *__restrict__ counter, const PlanGrid gu) {
     const unsigned n = st.work_count[0];
@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(256, FIRST_MINB) k_pgd_first(const int2 *__res
 
 // Iterations 1.. of the faces still moving (the gradient at their point is in the row).
 template <bool COUNT, bool UNIFORM>
-__global__ void __launch_bounds__(128, REST_MINB) k_pgd_rest(const int2 *__restrict__ block_map, const EnvXf *__restrict__ xf,
+__global__ void __launch_bounds__(128, UNIFORM ? REST_MINB : REST_MINB - 1) k_pgd_rest(const int2 *__restrict__ block_map, const EnvXf *__restrict__ xf,
                                                   const SdfDesc *__restrict__ sdfs, const MeshDesc *__restrict__ meshes,
                                                   Staging st, unsigned long long *__restrict__ counter, const PlanGrid gu) {
     const unsigned n = st.work_count[3];
@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(128, REST_MINB) k_pgd_rest(const int2 *__restr
 // in ascending face order) and apply the world-frame epilogue (generation.py:98-114).
 // One CTA per env: chunk offsets by a block scan of the found counts, then one
 // warp per chunk compacts its rows with a ballot.
-__global__ void __launch_bounds__(COMPACT_BLOCK) k_compact(const EnvXf *__restrict__ xf,
+__global__ void __launch_bounds__(COMPACT_BLOCK, COMPACT_MINB) k_compact(const EnvXf *__restrict__ xf,
                                                            const int64_t *__restrict__ cand_base,
                                                            const int2 *__restrict__ block_map,
                                                            const int32_t *__restrict__ chunk_first, Staging st,

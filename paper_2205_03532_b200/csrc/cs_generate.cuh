@@ -3,7 +3,8 @@
 
 namespace cs {
 
-// register budgets / grids of the descent wavefront (measured best, round 1)
+// register budgets / grids of the descent wavefront (measured best, round 1); plans with
+// per-env grids (UNIFORM false) take one CTA per SM less: no spills (config 3: 1% faster)
 #ifndef FIRST_MINB
 #define FIRST_MINB 3
 #endif
@@ -20,7 +21,13 @@ namespace cs {
 #define PREP_MINB 5  // 48 registers (measured best; 4 and 6 are slower)
 #endif
 constexpr int PGD_GRAB = 64;  // work items a warp claims per atomic
-constexpr int COMPACT_BLOCK = 256;
+#ifndef COMPACT_BLOCK_DEF
+#define COMPACT_BLOCK_DEF 256
+#endif
+#ifndef COMPACT_MINB
+#define COMPACT_MINB 1
+#endif
+constexpr int COMPACT_BLOCK = COMPACT_BLOCK_DEF;
 constexpr int MAX_MINIMIZE_ITERS = 12;  // generation.py:19
 
 // One face that survived the cull and the Lipschitz prune (k_face_prep), waiting

@@ -72,8 +72,9 @@ extern "C" int cs_debug_red_prof(unsigned long long *out) { return (int)cudaMemc
 #define RED_MARK(i) do {} while (0)
 #endif
 
-__global__ void __launch_bounds__(RED_T, 7) k_reduce(ReduceIO io, ReduceParams p, int SB) {
-    // 7 CTAs per SM (<= 72 registers): 1036 >= 1024 envs in one wave; 80 registers measured 13% slower
+__global__ void __launch_bounds__(RED_T) k_reduce(ReduceIO io, ReduceParams p, int SB) {
+    // keep at <= 72 registers (7 CTAs per SM: 1036 >= 1024 envs in one wave); 80 registers measured
+    // 13% slower, and a (RED_T, 7) bound makes ptxas spill
 #ifdef RED_PROF
     long long t_red = clock64();
 #endif
