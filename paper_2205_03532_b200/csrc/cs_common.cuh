@@ -103,6 +103,15 @@ struct GridT {
 };
 
 constexpr int BRICK = 2;  // cells per brick edge
+#ifdef PREP_STATS
+static __device__ unsigned long long g_bound_stat[4];  // brick passes, brick settled, cell passes, cell skipped
+#define BOUND_STAT(i) atomicAdd(&g_bound_stat[i], 1ull)
+#else
+#define BOUND_STAT(i) ((void)0)
+#endif
+#ifndef CELL_SKIP
+#define CELL_SKIP 1.5  // voxels (sample_lower_bound)
+#endif
 #ifndef CWIN_MAX_LOOKUPS
 #define CWIN_MAX_LOOKUPS 16  // face boxes needing more window lookups skip the bound (measured best)
 #endif
@@ -328,7 +337,12 @@ __device__ __forceinline__ double sample_lower_bound(const GridT<T> &g, const do
         }
         const double md = (double)m;
         const double lb = md - fabs(md) * 0x1p-40 - 1e-300;
-        if (lb > cd_hint) return lb;
+        BOUND_STAT(0);
+        if (lb > cd_hint) { BOUND_STAT(1); return lb; }
+        // the cell pass lifts the bound by about a brick at most: it is skipped when the
+        // brick bound is far below cd (a missed cull at worst, never a wrong one; measured
+        // best at 1.5 voxels: faster prep, no extra descents)
+        if (lb < cd_hint - CELL_SKIP * g.voxel) return lb;
     }
 #endif
     const int rmin = min(c1[0] - c0[0], min(c1[1] - c0[1], c1[2] - c0[2])) + 1;
@@ -339,7 +353,8 @@ __device__ __forceinline__ double sample_lower_bound(const GridT<T> &g, const do
         last[k] = c1[k] - w + 1;  // start of the last window
         n *= (last[k] - c0[k] + w - 1) / w + 1;
     }
-    if (n > CWIN_MAX_LOOKUPS) return -INFINITY;
+    if (n > CWIN_MAX_LOOKUPS) { BOUND_STAT(3); return -INFINITY; }
+    BOUND_STAT(2);
     const float *tab = g.cwin + (size_t)lvl * ntab;
     float m = INFINITY;
     const int nxw = (last[0] - c0[0] + w - 1) / w + 1;  // windows per row

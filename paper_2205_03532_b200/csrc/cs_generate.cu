@@ -91,6 +91,9 @@ __device__ __forceinline__ double3 to_grid(const EnvXf &X, double4 v) {
 __device__ unsigned long long g_prep_prof[16];
 #define PREP_MARK(i) do { if (threadIdx.x == 0) { const long long t_ = clock64(); atomicAdd(&g_prep_prof[i], (unsigned long long)(t_ - t_last)); t_last = t_; } } while (0)
 extern "C" int cs_debug_prep_prof(unsigned long long *out) { return (int)cudaMemcpyFromSymbol(out, g_prep_prof, sizeof(g_prep_prof)); }
+#ifdef PREP_STATS
+extern "C" int cs_debug_bound_stat(unsigned long long *out) { return (int)cudaMemcpyFromSymbol(out, g_bound_stat, sizeof(g_bound_stat)); }
+#endif
 #else
 #define PREP_MARK(i) do {} while (0)
 #endif

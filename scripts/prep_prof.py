@@ -40,6 +40,12 @@ def main():
     if b[8]:  # -DPREP_STATS: face outcomes (the bound is evaluated but not applied)
         for i, nm in zip(range(8, 14), ["faces", "aabb near", "bound culls", "prune culls", "both cull", "neither"]):
             print(f"{nm:12s} {b[i]:12.0f}  {100 * b[i] / b[8]:5.1f}%")
+        bs = (ctypes.c_ulonglong * 4)()
+        lib.cs_debug_bound_stat.restype = ctypes.c_int
+        lib.cs_debug_bound_stat(bs)
+        x = np.array(bs[:], dtype=np.float64) / (reps + 1)
+        print(f"brick passes {x[0]:.0f}, settled by bricks {x[1]:.0f}; cell passes {x[2]:.0f}; "
+              f"boxes too large for the cell pass {x[3]:.0f}")
 
 
 if __name__ == "__main__":
