@@ -457,3 +457,54 @@ def test_asset_free_deferred_while_plans_use_it(P, grid64, gen64, meshes):
         P.Plan([hs], [hm.value], P.ReductionParams())
     del plan  # releases the mesh now
     assert lib.cs_mesh_free(hm.value) == _native.CS_ERR_HANDLE
+
+
+_GRIDS = {}  # GPU-generated grids shared by the tests below
+
+
+@pytest.mark.parametrize("seed", [11, 12])
+def test_random_frames_vs_oracle(P, seed):
+    """Fresh pose seeds at res 256 with the SDF body itself moved and rotated per env
+    (the nut follows it rigidly, so the pair stays engaged): every env's stats
+    against the oracle and four envs field by field."""
+    from oracle import oracle as O
+    from paper_2205_03532_b200.math3d import quat_multiply, quat_to_matrix
+    from paper_2205_03532_b200.scenes import m16_meshes, m16_workload
+    from paper_2205_03532_b200.sdf.grid import SdfResolutionSpec, generate_sdf
+
+    nut, bolt, _ = m16_meshes()
+    if 256 not in _GRIDS:
+        _GRIDS[256] = generate_sdf(bolt, SdfResolutionSpec(256, 4))
+    grid = _GRIDS[256]
+    E = 128
+    w = m16_workload(E, seed=seed, grid=grid)
+    rng = np.random.default_rng(seed)
+    sp = np.zeros((E, 7))
+    mp = np.zeros((E, 7))
+    for e in range(E):
+        q = rng.standard_normal(4)
+        q /= np.linalg.norm(q)
+        t = rng.uniform(-0.05, 0.05, 3)
+        sp[e, :3], sp[e, 3:] = t, q
+        # nut pose relative to the bolt as drawn, composed with the bolt's world pose
+        mp[e, :3] = t + quat_to_matrix(q) @ w["mesh_pose"][e, :3]
+        mp[e, 3:] = quat_multiply(q, w["mesh_pose"][e, 3:])
+    res = P.collide([P.register_sdf(grid)] * E, [P.register_mesh(nut)] * E, sp, mp, w["cd"])
+    og = O.Grid(grid.values, grid.dims, grid.origin, grid.voxel_size, *grid.mesh_aabb)
+    ost = O.collide_batched(og, nut.vertices, nut.triangles, sp, mp, w["cd"])
+    assert np.array_equal(res.n_cand.cpu().numpy(), ost[:, 0].astype(np.int64))
+    assert np.array_equal(res.n_patch.cpu().numpy(), ost[:, 1].astype(np.int64))
+    st = res.stats.cpu().numpy()
+    assert np.array_equal(st[:, 2], ost[:, 2].astype(np.float32)) and np.array_equal(st[:, 3], ost[:, 3].astype(np.float32))
+    assert (ost[:, 0] > 0).mean() > 0.9
+    for e in rng.choice(E, size=4, replace=False):
+        e = int(e)
+        cd = float(w["cd"][e])
+        ref = O.generate_contacts(og, nut.vertices, nut.triangles, sp[e], mp[e], cd)
+        cs = res.contact_set(e)
+        assert np.array_equal(cs.points, ref["points"]) and np.array_equal(cs.normals, ref["normals"]), e
+        assert np.array_equal(cs.depths, ref["depths"]) and np.array_equal(cs.face_indices, ref["faces"]), e
+        r = O.reduce_contacts(ref["points"], ref["normals"], ref["depths"], ref["faces"], min_depth=-cd)
+        got = pack_patch_list(res.patches(e), 6)
+        for key in ("rep", "nkept", "members", "kept_faces", "wsum", "wp", "wn", "wt", "area", "maxd"):
+            assert np.array_equal(np.asarray(got[key]), np.asarray(r[key])), (e, key)
