@@ -363,34 +363,73 @@ __global__ void __launch_bounds__(RED_T) k_reduce(ReduceIO io, ReduceParams p, i
     }
     if (tid == 0) io.n_patch[e] = P;
     __syncthreads();
-    // CSR: stable counting sort of candidate indices by patch
-    for (int i = tid; i < C; i += RED_T) {
-        const int l = lab[i];
-        if (l >= 0) atomicAdd(&hcnt[l], 1);
+    // CSR: stable counting sort of candidate indices by patch. With room in the (now
+    // idle) batch staging, the four warps take contiguous quarters of the candidates:
+    // per-warp label counts give every (warp, patch) its base, so each patch's members
+    // stay in ascending candidate order; else warp 0 alone.
+    int32_t *moff = io.member_offsets + e * (N + 1);
+    int32_t *mem = io.members + base;
+    const bool par = (size_t)25 * SB >= (size_t)16 * N;
+    int *hw = par ? reinterpret_cast<int *>(bdep) : hcnt;  // [4][N] counts, then bases (par)
+    if (par) {
+        for (int q = tid; q < 4 * N; q += RED_T) hw[q] = 0;
+        __syncthreads();
+    }
+    const int qlen = par ? (C + 3) / 4 : C;
+    const int i0 = par ? min(C, wid * qlen) : 0, i1 = par ? min(C, i0 + qlen) : C;
+    if (par) {
+        for (int i = i0 + lane; i < i1; i += 32) {
+            const int l = lab[i];
+            if (l >= 0) atomicAdd(&hw[wid * N + l], 1);
+        }
+    } else {
+        for (int i = tid; i < C; i += RED_T) {
+            const int l = lab[i];
+            if (l >= 0) atomicAdd(&hcnt[l], 1);
+        }
     }
     __syncthreads();
     RED_MARK(4);
-    if (wid != 0) return;
-    int32_t *moff = io.member_offsets + e * (N + 1);
-    if (lane == 0) {
+    if (par) {
         int run = 0;
-        for (int q = 0; q < N; ++q) {
-            moff[q] = run;
-            const int c = q < P ? hcnt[q] : 0;
-            hcnt[q] = run;  // running base
-            run += c;
+        for (int q0 = 0; q0 < N; q0 += RED_T) {
+            const int q = q0 + tid;
+            int c[4] = {0, 0, 0, 0};
+            if (q < P)
+                for (int w = 0; w < 4; ++w) c[w] = hw[w * N + q];
+            int tot;
+            const int x = run + block_excl_scan(c[0] + c[1] + c[2] + c[3], s_ws, &tot);
+            if (q < N) {
+                moff[q] = x;
+                int b = x;
+                for (int w = 0; w < 4; ++w) { hw[w * N + q] = b; b += c[w]; }
+            }
+            run += tot;
         }
-        moff[N] = run;
+        if (tid == 0) moff[N] = run;
+        __syncthreads();
+    } else {
+        if (wid != 0) return;
+        if (lane == 0) {
+            int run = 0;
+            for (int q = 0; q < N; ++q) {
+                moff[q] = run;
+                const int c = q < P ? hcnt[q] : 0;
+                hcnt[q] = run;  // running base
+                run += c;
+            }
+            moff[N] = run;
+        }
+        __syncwarp();
     }
-    __syncwarp();
-    int32_t *mem = io.members + base;
+    int *cnt = par ? hw + wid * N : hcnt;  // this warp's running bases
     constexpr int PF = 8;  // labels prefetched per lane: keeps 8 loads in flight per round
-    for (int c0 = 0; c0 < C; c0 += 32 * PF) {
+    for (int c0 = i0; c0 < i1; c0 += 32 * PF) {
         int lb[PF];
 #pragma unroll
         for (int u = 0; u < PF; ++u) {
             const int i = c0 + 32 * u + lane;
-            lb[u] = (i < C) ? lab[i] : -1;
+            lb[u] = (i < i1) ? lab[i] : -1;
         }
 #pragma unroll
         for (int u = 0; u < PF; ++u) {
@@ -398,9 +437,9 @@ __global__ void __launch_bounds__(RED_T) k_reduce(ReduceIO io, ReduceParams p, i
             const int l = lb[u];
             const unsigned peers = __match_any_sync(FULL, l);
             const int rank = __popc(peers & lt);
-            if (l >= 0) mem[hcnt[l] + rank] = i;
+            if (l >= 0) mem[cnt[l] + rank] = i;
             __syncwarp();
-            if (l >= 0 && rank == 0) hcnt[l] += __popc(peers);
+            if (l >= 0 && rank == 0) cnt[l] += __popc(peers);
             __syncwarp();
         }
     }
