@@ -330,7 +330,9 @@ __device__ void sort_patch(const Team &t, const ReduceIO &io, const ReduceParams
             if (hull) {
                 A.u[k] = V3(px, py, pz, t1[0], t1[1], t1[2]);  // _project_2d: (n,3) @ (3,), n >= 2
                 A.v[k] = V3(px, py, pz, t2[0], t2[1], t2[2]);
-                A.k[k] = k;
+                // tie key 2k + touching: orders like k (k distinct) and carries the flag
+                // through the sort, so the rows below need no second gather of the depth
+                A.k[k] = 2 * k + (d >= 0.0 ? 1 : 0);
             }
         }
         if (FOLD) {
@@ -382,9 +384,9 @@ __device__ void sort_patch(const Team &t, const ReduceIO &io, const ReduceParams
         bool touch = false;
         double2 uv = make_double2(0.0, 0.0);
         if (j < m) {
-            const int k = R.k[j];
+            const int kk = R.k[j], k = kk >> 1;
             uv = make_double2(R.u[j], R.v[j]);
-            touch = __ldg(D + mem[k]) >= 0.0;
+            touch = kk & 1;
             io.suv[row0 + j] = uv;
             io.sp[row0 + j] = touch ? k : ~k;
         }
