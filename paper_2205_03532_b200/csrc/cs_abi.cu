@@ -496,6 +496,7 @@ static int plan_buffers(cs_plan *P, const std::vector<int64_t> &cap) {
         tot += cap[(size_t)e];
         maxcap = std::max(maxcap, cap[(size_t)e]);
     }
+    if (tot >= ((int64_t)1 << 31)) return fail(CS_ERR_VALUE, "plan of %lld face rows exceeds the 2^31 row index range", (long long)tot);
     P->total_cap = tot;
     const int N = P->rp.N, K = P->rp.K;
     int r;

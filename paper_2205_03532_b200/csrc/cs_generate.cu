@@ -281,10 +281,11 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int2 
     __syncthreads();
     if (survive) {
         FaceWork *w = st.work + sbase + pos;
-        w->row = cand_base[e] + f0 + pos;
-        w->blk = (int32_t)blockIdx.x;
-        w->face = (int32_t)f | (which << 30);
-        w->phi[0] = pa; w->phi[1] = pb; w->phi[2] = pc; w->phi[3] = ps;
+        // the record as three 16-byte stores
+        reinterpret_cast<int4 *>(w)[0] =
+            make_int4((int32_t)(cand_base[e] + f0 + pos), (int32_t)blockIdx.x, (int32_t)f | (which << 30), e);
+        reinterpret_cast<double2 *>(w)[1] = make_double2(pa, pb);
+        reinterpret_cast<double2 *>(w)[2] = make_double2(pc, ps);
     }
     PREP_MARK(5);
 }
@@ -358,13 +359,14 @@ __global__ void __launch_bounds__(256, UNIFORM ? GRAD_MINB : GRAD_MINB - 1) k_pg
         unsigned idx = i, flag = 0;
         if (stage == 1) { const unsigned a = st.acc[i]; idx = a & ~ACC_FINAL; flag = a & ACC_FINAL; }
         const FaceWork *w = st.work + idx;
-        const int64_t row = w->row;
-        const int blk = w->blk;
-        const int e = __ldg(&block_map[blk].x);
+        const int4 hd = __ldg(reinterpret_cast<const int4 *>(w));  // row, blk, face, env in one load
+        const int64_t row = hd.x;
+        const int blk = hd.y;
+        const int e = hd.w;
         const PlanGrid &g = grid_of<UNIFORM>(gu, sdfs, xf, e);
         double px, py, pz;
         if (stage == 0) {  // the start point, from the corners (not staged: recomputing is cheaper than the traffic)
-            face_start(face_geom(xf[e], meshes, w->face & 0x3fffffff), (int)((unsigned)w->face >> 30), px, py, pz);
+            face_start(face_geom(xf[e], meshes, hd.z & 0x3fffffff), (int)((unsigned)hd.z >> 30), px, py, pz);
         } else {
             px = st.point[3 * row]; py = st.point[3 * row + 1]; pz = st.point[3 * row + 2];
         }
@@ -373,7 +375,7 @@ __global__ void __launch_bounds__(256, UNIFORM ? GRAD_MINB : GRAD_MINB - 1) k_pg
         if (COUNT) ns += 6;
         st.grad[3 * row] = gx; st.grad[3 * row + 1] = gy; st.grad[3 * row + 2] = gz;
         if (stage == 1) {
-            if (flag) finish_face(st, row, blk, w->face & 0x3fffffff, st.phi[row], xf[e].cd);
+            if (flag) finish_face(st, row, blk, hd.z & 0x3fffffff, st.phi[row], xf[e].cd);
             else st.slow[atomicAdd(st.work_count + 3, 1u)] = idx;
         }
     }
@@ -430,16 +432,17 @@ __global__ void __launch_bounds__(256, UNIFORM ? FIRST_MINB : FIRST_MINB - 1) k_
     unsigned long long ns = 0;
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const FaceWork *w = st.work + i;
-        const int64_t row = w->row;
-        const int blk = w->blk;
-        const int face = w->face & 0x3fffffff;
-        const int e = __ldg(&block_map[blk].x);
+        const int4 hd = __ldg(reinterpret_cast<const int4 *>(w));  // row, blk, face, env in one load
+        const int64_t row = hd.x;
+        const int blk = hd.y;
+        const int face = hd.z & 0x3fffffff;
+        const int e = hd.w;
         const EnvXf &X = xf[e];
         const double gx = st.grad[3 * row], gy = st.grad[3 * row + 1], gz = st.grad[3 * row + 2];
         double phi = w->phi[3];
         const FaceGeom f = face_geom(X, meshes, face);
         double px, py, pz;
-        face_start(f, (int)((unsigned)w->face >> 30), px, py, pz);
+        face_start(f, (int)((unsigned)hd.z >> 30), px, py, pz);
         // a face that does not move ends here with this gradient: its point and phi go to
         // the staging row only when it is found (the only rows k_compact reads)
         auto done_here = [&]() {
@@ -479,10 +482,11 @@ __global__ void __launch_bounds__(128, UNIFORM ? REST_MINB : REST_MINB - 1) k_pg
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const unsigned idx = st.slow[i];
         const FaceWork *w = st.work + idx;
-        const int64_t row = w->row;
-        const int blk = w->blk;
-        const int face = w->face & 0x3fffffff;
-        const int e = __ldg(&block_map[blk].x);
+        const int4 hd = __ldg(reinterpret_cast<const int4 *>(w));  // row, blk, face, env in one load
+        const int64_t row = hd.x;
+        const int blk = hd.y;
+        const int face = hd.z & 0x3fffffff;
+        const int e = hd.w;
         const EnvXf &X = xf[e];
         const PlanGrid &g = grid_of<UNIFORM>(gu, sdfs, xf, e);
         const FaceGeom f = face_geom(X, meshes, face);

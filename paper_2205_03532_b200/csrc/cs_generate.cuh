@@ -33,11 +33,13 @@ constexpr int MAX_MINIMIZE_ITERS = 12;  // generation.py:19
 // One face that survived the cull and the Lipschitz prune (k_face_prep), waiting
 // for its projected-gradient descent (the k_pgd_* wavefront).
 struct FaceWork {
-    int64_t row;        // staging row: cand_base[e] + f0 + rank among the chunk's survivors
+    int32_t row;        // staging row: cand_base[e] + f0 + rank among the chunk's survivors (< 2^31)
     int32_t blk;        // k_face_prep block (env, chunk)
     int32_t face;       // face index | start corner << 30 (0 centroid, 1..3 = a, b, c)
+    int32_t env;        // the block's env (saves the descent a dependent block_map lookup)
     double phi[4];      // phi at a, b, c and at the start point
 };
+static_assert(sizeof(FaceWork) == 48, "FaceWork is three 16-byte words");
 
 // Per-face staging. k_face_prep block b covers faces [f0, f0 + FACE_CHUNK) of one
 // env; its survivors own rows cand_base[e] + f0 + [0, chunk_count[b]) in face order.
