@@ -626,6 +626,7 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
     if (!r) r = P->alloc(&P->st.work_count, 4);
     if (!r) r = P->alloc(&P->st.alpha, (size_t)P->total_cap);
     if (!r) r = P->alloc(&P->st.acc, (size_t)P->total_cap);
+    if (!r) r = P->alloc(&P->st.acc_hd, (size_t)P->total_cap);
     if (!r) r = P->alloc(&P->st.slow, (size_t)P->total_cap);
     if (!r) r = P->alloc(&P->chunk_first, chunk_first.size());
     if (!r) r = P->alloc(&P->st.point, 3 * (size_t)P->total_cap);

@@ -357,9 +357,15 @@ __global__ void __launch_bounds__(256, UNIFORM ? GRAD_MINB : GRAD_MINB - 1) k_pg
     unsigned long long ns = 0;
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         unsigned idx = i, flag = 0;
-        if (stage == 1) { const unsigned a = st.acc[i]; idx = a & ~ACC_FINAL; flag = a & ACC_FINAL; }
-        const FaceWork *w = st.work + idx;
-        const int4 hd = __ldg(reinterpret_cast<const int4 *>(w));  // row, blk, face, env in one load
+        int4 hd;  // row, blk, face, env: from the record, or (moved faces) beside the index
+        if (stage == 1) {
+            const unsigned a = st.acc[i];
+            hd = st.acc_hd[i];
+            idx = a & ~ACC_FINAL;
+            flag = a & ACC_FINAL;
+        } else {
+            hd = __ldg(reinterpret_cast<const int4 *>(st.work + idx));
+        }
         const int64_t row = hd.x;
         const int blk = hd.y;
         const int e = hd.w;
@@ -464,7 +470,9 @@ __global__ void __launch_bounds__(256, UNIFORM ? FIRST_MINB : FIRST_MINB - 1) k_
         st.phi[row] = phi;
         st.alpha[row] = alpha;
         // moved < tol ends the descent (its final gradient is at the new point); 1 < max_iters
-        st.acc[atomicAdd(st.work_count + 2, 1u)] = i | (moved < X.tol ? ACC_FINAL : 0u);
+        const unsigned slot = atomicAdd(st.work_count + 2, 1u);
+        st.acc[slot] = i | (moved < X.tol ? ACC_FINAL : 0u);
+        st.acc_hd[slot] = hd;
     }
     if (COUNT) {
         for (int o = 16; o; o >>= 1) ns += __shfl_xor_sync(0xffffffffu, ns, o);

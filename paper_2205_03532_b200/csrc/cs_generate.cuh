@@ -54,6 +54,7 @@ struct Staging {
     FaceWork *work;        // [capacity] survivors, dense
     double *alpha;         // [row] descent step of a moved face
     uint32_t *acc;         // [capacity] work indices moved by k_pgd_first (| ACC_FINAL)
+    int4 *acc_hd;          // [capacity] ... and their work-record headers (row, blk, face, env)
     uint32_t *slow;        // [capacity] work indices still moving after iteration 0
     unsigned *work_count;  // [0] survivors, [1] (unused), [2] accepted, [3] slow
 };
