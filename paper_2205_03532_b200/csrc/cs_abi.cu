@@ -68,6 +68,7 @@ struct MeshEntry {
     int32_t *chunk_voff = nullptr, *chunk_verts = nullptr;
     uint2 *face_loc = nullptr;
     MeshDesc desc{};
+    std::vector<int32_t> chunk_voff_h;  // host copy (k_face_prep block map)
     int users = 0;
     bool doomed = false;
 };
@@ -145,6 +146,7 @@ struct cs_plan {
     int32_t *env_sdf = nullptr, *env_mesh = nullptr;
     int64_t *cand_base = nullptr;
     int2 *block_map = nullptr;       // k_face_prep block -> (env, first face of the chunk)
+    int4 *prep_map = nullptr;        // ... and (env, first face, chunk vertex offset, vertex count | mesh << 16)
     int32_t *chunk_first = nullptr;  // [E+1] first k_face_prep block of each env
     int32_t max_chunk_verts = 1;     // largest chunk vertex list over the plan's meshes
     EnvXf *xf = nullptr;
@@ -399,6 +401,7 @@ int cs_mesh_register(const double *vertices, int64_t nv, const int32_t *triangle
     CS_CUDA(cudaMalloc(&m.chunk_verts, sizeof(int32_t) * std::max<size_t>(1, cverts.size())));
     CS_CUDA(cudaMalloc(&m.face_loc, sizeof(uint2) * floc.size()));
     CS_CUDA(cudaMemcpy(m.chunk_voff, voff.data(), sizeof(int32_t) * voff.size(), cudaMemcpyHostToDevice));
+    m.chunk_voff_h.assign(voff.begin(), voff.end());
     CS_CUDA(cudaMemcpy(m.chunk_verts, cverts.data(), sizeof(int32_t) * cverts.size(), cudaMemcpyHostToDevice));
     CS_CUDA(cudaMemcpy(m.face_loc, floc.data(), sizeof(uint2) * floc.size(), cudaMemcpyHostToDevice));
     m.desc.verts = m.verts;
@@ -566,6 +569,7 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
     }
     std::vector<int64_t> cap((size_t)n_envs);
     std::vector<int2> bmap;
+    std::vector<int4> pmap;
     std::vector<int32_t> chunk_first;
     bool uniform = true;
     PlanGrid ugrid{};
@@ -586,7 +590,12 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
             cap[(size_t)e] = nt;
             maxcv = std::max(maxcv, g_mesh[m].desc.max_chunk_verts);
             chunk_first.push_back((int32_t)bmap.size());
-            for (int64_t f = 0; f < nt; f += FACE_CHUNK) bmap.push_back(make_int2((int)e, (int)f));
+            const std::vector<int32_t> &vo = g_mesh[m].chunk_voff_h;
+            for (int64_t f = 0; f < nt; f += FACE_CHUNK) {
+                bmap.push_back(make_int2((int)e, (int)f));
+                const int c = (int)(f / FACE_CHUNK);
+                pmap.push_back(make_int4((int)e, (int)f, vo[c], (vo[c + 1] - vo[c]) | (m << 16)));
+            }
         }
         if (uniform) ugrid = g_sdf[sdf_handles[0]].desc.gp;
         chunk_first.push_back((int32_t)bmap.size());
@@ -617,6 +626,7 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
     if (!r) r = P->alloc(&P->env_sdf, (size_t)n_envs);
     if (!r) r = P->alloc(&P->env_mesh, (size_t)n_envs);
     if (!r) r = P->alloc(&P->block_map, bmap.size());
+    if (!r) r = P->alloc(&P->prep_map, pmap.size());
     if (!r) r = P->alloc(&P->xf, (size_t)n_envs);
     if (!r) r = P->alloc(&P->st.face, (size_t)P->total_cap);
     if (!r) r = P->alloc(&P->st.chunk_count, bmap.size());
@@ -642,6 +652,7 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
     cudaError_t ce = cudaMemcpy(P->env_sdf, sdf_handles, sizeof(int32_t) * (size_t)n_envs, cudaMemcpyHostToDevice);
     if (ce == cudaSuccess) ce = cudaMemcpy(P->env_mesh, mesh_handles, sizeof(int32_t) * (size_t)n_envs, cudaMemcpyHostToDevice);
     if (ce == cudaSuccess) ce = cudaMemcpy(P->block_map, bmap.data(), sizeof(int2) * bmap.size(), cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess) ce = cudaMemcpy(P->prep_map, pmap.data(), sizeof(int4) * pmap.size(), cudaMemcpyHostToDevice);
     if (ce == cudaSuccess)
         ce = cudaMemcpy(P->chunk_first, chunk_first.data(), sizeof(int32_t) * chunk_first.size(), cudaMemcpyHostToDevice);
     if (ce != cudaSuccess) { delete P; return fail(CS_ERR_CUDA, "plan upload: %s", cudaGetErrorString(ce)); }
@@ -717,7 +728,7 @@ int cs_collide_active(cs_plan *P, const double *sdf_pose, const double *mesh_pos
     CS_LAUNCHED();
     mark(1);
     const PlanGrid *ug = P->uniform_sdf ? &P->uniform_grid : nullptr;
-    launch_face_prep(P->nblocks, P->block_map, P->xf, d_sdfs, d_meshes, P->cand_base, P->st, P->max_chunk_verts,
+    launch_face_prep(P->nblocks, P->prep_map, P->xf, d_sdfs, d_meshes, P->cand_base, P->st, P->max_chunk_verts,
                      P->sample_counter, ug, s);
     CS_LAUNCHED();
     mark(2);

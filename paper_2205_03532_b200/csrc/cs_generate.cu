@@ -108,7 +108,7 @@ constexpr int FACE_ITEM = 1 << 30;  // sample-list code of a face centre (else a
 // scalars are constant-bank operands; otherwise the env's grid view is staged in
 // shared memory.
 template <bool COUNT, bool UNIFORM>
-__global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int2 *__restrict__ block_map,
+__global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int4 *__restrict__ prep_map,
                                                           const EnvXf *__restrict__ xf,
                                                           const SdfDesc *__restrict__ sdfs,
                                                           const MeshDesc *__restrict__ meshes,
@@ -123,8 +123,13 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int2 
 #ifdef PREP_PROF
     long long t_last = clock64();
 #endif
-    const int2 bm = block_map[blockIdx.x];
-    const int e = bm.x, f0 = bm.y;
+    // (env, first face, chunk vertex offset, vertex count | mesh << 16): the mesh and
+    // chunk loads below need not wait for the env's transform
+    const int4 bm = prep_map[blockIdx.x];
+    const int e = bm.x, f0 = bm.y, v0 = bm.z, ncv = bm.w & 0xffff, mesh = bm.w >> 16;
+    const double4 *verts = meshes[mesh].verts;
+    const int32_t *cverts = meshes[mesh].chunk_verts;
+    const int64_t nt = meshes[mesh].nt;
     if (threadIdx.x < sizeof(EnvXf) / 8)
         reinterpret_cast<double *>(&sx)[threadIdx.x] = reinterpret_cast<const double *>(xf + e)[threadIdx.x];
     __syncthreads();
@@ -139,12 +144,6 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int2 
             reinterpret_cast<double *>(&sg)[threadIdx.x] = reinterpret_cast<const double *>(&sdfs[sx.sdf].gp)[threadIdx.x];
     }
     const PlanGrid &grid = UNIFORM ? gu : sg;
-    const double4 *verts = meshes[sx.mesh].verts;
-    const int32_t *cverts = meshes[sx.mesh].chunk_verts;
-    const int64_t nt = meshes[sx.mesh].nt;
-    const int chunk = f0 / FACE_CHUNK;
-    const int v0 = __ldg(meshes[sx.mesh].chunk_voff + chunk);
-    const int ncv = __ldg(meshes[sx.mesh].chunk_voff + chunk + 1) - v0;
     // shared: vertex x/y/z/phi [maxcv], centre phi [FACE_CHUNK], face corner slots
     // [FACE_CHUNK], the sample list [maxcv + FACE_CHUNK], vertex flags [maxcv]
     double *vx = dsm, *vy = dsm + maxcv, *vz = dsm + 2 * maxcv, *vphi = dsm + 3 * maxcv, *cphi = dsm + 4 * maxcv;
@@ -153,7 +152,7 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int2 
     unsigned char *need = reinterpret_cast<unsigned char *>(list + maxcv + FACE_CHUNK);
     __shared__ int s_nl;
     const int64_t f = (int64_t)f0 + threadIdx.x;
-    const uint2 loc = f < nt ? __ldg(meshes[sx.mesh].face_loc + f) : make_uint2(0, 0);  // in flight during the transform
+    const uint2 loc = f < nt ? __ldg(meshes[mesh].face_loc + f) : make_uint2(0, 0);  // in flight during the transform
     // verts_grid = to_grid.apply(vertices) (generation.py:70), per distinct vertex
     for (int j = threadIdx.x; j < ncv; j += FACE_CHUNK) {
         const double3 p = to_grid(sx, ld_vert(verts + __ldg(cverts + v0 + j)));
@@ -647,7 +646,7 @@ size_t face_prep_smem(int maxcv) {
     return (size_t)maxcv * (4 * sizeof(double) + sizeof(int) + 1) + (size_t)FACE_CHUNK * (sizeof(double) + sizeof(uint2) + sizeof(int));
 }
 
-void launch_face_prep(int64_t nblocks, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs,
+void launch_face_prep(int64_t nblocks, const int4 *block_map, const EnvXf *xf, const SdfDesc *sdfs,
                       const MeshDesc *meshes, const int64_t *cand_base, const Staging &st, int maxcv,
                       unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s) {
     if (nblocks <= 0) return;

@@ -71,7 +71,7 @@ void launch_env_xf(int64_t E, const int32_t *env_sdf, const int32_t *env_mesh, c
                    const double *sdf_pose, const double *mesh_pose, int pose_format, const double *cd, EnvXf *xf,
                    int32_t *env_status, double *env_min_depth, unsigned *work_count, cudaStream_t s,
                    const int32_t *active = nullptr);
-void launch_face_prep(int64_t nblocks, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs,
+void launch_face_prep(int64_t nblocks, const int4 *block_map, const EnvXf *xf, const SdfDesc *sdfs,
                       const MeshDesc *meshes, const int64_t *cand_base, const Staging &st, int max_chunk_verts,
                       unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s);
 void launch_pgd_wave(int sm_count, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs, const MeshDesc *meshes,
