@@ -36,7 +36,7 @@ UNIT = "queries/s"
 PAPER_QPS = 1024 * 17798 / 11e-3  # PAPER.md:227,584 (A5000, whole contact-handling step), derived
 # k_env_xf, k_face_prep, k_pgd_grad x2, k_pgd_first, k_pgd_rest, k_compact, k_reduce, k_patch_off,
 # k_fin_sort_warp, k_fin_sort_block, k_fin_chain, k_fin_kept, k_stats
-LAUNCHES_PER_STEP = 14
+LAUNCHES_PER_STEP = 15
 
 
 def parse():

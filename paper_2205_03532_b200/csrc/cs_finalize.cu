@@ -61,6 +61,16 @@ __global__ void k_patch_off(int64_t E, const int32_t *__restrict__ n_patch, int3
     if (threadIdx.x == 0) off[E] = running;
 }
 
+// patch (work index) -> env, so stage 1 finds a patch's env with one load
+__global__ void k_patch_env(int64_t E, const int32_t *__restrict__ n_patch, const int32_t *__restrict__ off,
+                            int32_t *__restrict__ wenv) {
+    const int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (e >= E) return;
+    const int o = off[e], n = n_patch[e];
+    for (int q = lane; q < n; q += 32) wenv[o + q] = (int32_t)e;
+}
+
 // numpy stable argsort(-depths) order: depth descending, ties by index, NaN last.
 __device__ __forceinline__ bool depth_before(double da, int a, double db, int b) {
     bool an = isnan(da), bnn = isnan(db);
@@ -257,15 +267,6 @@ __device__ __forceinline__ bool needs_touch_hull(int m, int nt, int K) { return 
 
 // ------------------------------------------------------------------ stage 1: per patch
 
-__device__ __forceinline__ int64_t env_of(const int32_t *patch_off, int64_t E, int w) {
-    int64_t lo = 0, hi = E - 1;  // last e with patch_off[e] <= w
-    while (lo < hi) {
-        int64_t mid = (lo + hi + 1) >> 1;
-        if (patch_off[mid] <= w) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-}
-
 // Patch w = (e, q), by a team (warp or CTA). A/B: the team's sort buffers (shared
 // memory, or the patch's global rows when it is very large); B holds the member
 // weights until the sort. tile: 9 x T doubles of shared memory.
@@ -360,7 +361,6 @@ __device__ void sort_patch(const Team &t, const ReduceIO &io, const ReduceParams
         io.max_depth[pq] = anynan ? (double)NAN : mx;  // deps.max() propagates NaN
         io.pdeep[w] = am.i;
         io.pnt[w] = nt;
-        io.wenv[w] = (int32_t)e;
         if (hull) {  // chain jobs (4w + kind), bucketed by chain length (k_fin_chain: longest first)
             const int64_t cap = 4 * io.E * N;
             int k = job_bucket(m);
@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(FW_WARPS * 32) k_fin_sort_warp(ReduceIO io, Re
     const int64_t E = io.E;
     const int total = io.patch_off[E];
     for (int w = blockIdx.x * FW_WARPS + wib; w < total; w += gridDim.x * FW_WARPS) {
-        const int64_t e = env_of(io.patch_off, E, w);
+        const int64_t e = io.wenv[w];
         const int q = w - io.patch_off[e];
         const int32_t *mo = io.member_offsets + e * (p.N + 1);
         if (mo[q + 1] - mo[q] > FW_SMEM) {  // handed to the CTA path (order-free: patches are independent)
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(FB_THREADS) k_fin_sort_block(ReduceIO io, Redu
     const int total = *io.large_count;
     for (int li = blockIdx.x; li < total; li += gridDim.x) {
         const int w = io.large_list[li];
-        const int64_t e = env_of(io.patch_off, E, w);
+        const int64_t e = io.wenv[w];
         const int q = w - io.patch_off[e];
         const int32_t *mo = io.member_offsets + e * (p.N + 1);
         Keys A, B;
@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(FL_WARPS * 32) k_fin_fold_large(ReduceIO io, R
     const int total = *io.large_count;
     for (int li = blockIdx.x * FL_WARPS + wib; li < total; li += gridDim.x * FL_WARPS) {
         const int w = io.large_list[li];
-        const int64_t e = env_of(io.patch_off, E, w);
+        const int64_t e = io.wenv[w];
         const int q = w - io.patch_off[e];
         const int64_t base = io.cand_base[e];
         const int32_t *mo = io.member_offsets + e * (p.N + 1);
@@ -880,6 +880,7 @@ __global__ void k_stats(ReduceIO io, ReduceParams p) {
 void launch_finalize(const ReduceIO &io, const ReduceParams &p, int sm_count, cudaStream_t s) {
     if (io.E <= 0) return;
     k_patch_off<<<1, 1024, 0, s>>>(io.E, io.n_patch, io.patch_off, io.large_count, io.njob);
+    k_patch_env<<<(unsigned)((io.E * 32 + 255) / 256), 256, 0, s>>>(io.E, io.n_patch, io.patch_off, io.wenv);
     const int64_t maxw = io.E * (int64_t)p.N;
     const size_t wsm = FW_BYTES_PER_WARP * FW_WARPS;
     static bool configured = false;
