@@ -141,6 +141,8 @@ struct cs_plan {
     int64_t nblocks = 0;
     bool uniform_sdf = false;      // every env samples the same grid
     PlanGrid uniform_grid{};  // ...whose view then travels as a kernel parameter
+    bool uniform_mesh = false;     // every env uses the same mesh
+    MeshDesc uniform_mesh_desc{};  // ...whose descriptor travels as a kernel parameter
     std::vector<void *> allocs;
     // inputs / tables
     int32_t *env_sdf = nullptr, *env_mesh = nullptr;
@@ -575,6 +577,8 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
     PlanGrid ugrid{};
     int32_t maxcv = 1;
     std::vector<int32_t> used_s, used_m;
+    bool umesh = false;
+    MeshDesc umdesc{};
     {
         std::lock_guard<std::mutex> lk(g_mu);
         int r = ensure_tables();
@@ -598,6 +602,9 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
             }
         }
         if (uniform) ugrid = g_sdf[sdf_handles[0]].desc.gp;
+        umesh = true;
+        for (int64_t e = 0; e < n_envs; ++e) umesh &= mesh_handles[e] == mesh_handles[0];
+        if (umesh) umdesc = g_mesh[mesh_handles[0]].desc;
         chunk_first.push_back((int32_t)bmap.size());
         used_s.assign(sdf_handles, sdf_handles + n_envs);
         used_m.assign(mesh_handles, mesh_handles + n_envs);
@@ -615,6 +622,8 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
     P->stages = stages;
     P->uniform_sdf = uniform;
     P->uniform_grid = ugrid;
+    P->uniform_mesh = umesh;
+    P->uniform_mesh_desc = umdesc;
     P->max_chunk_verts = maxcv;
     if (stages & CS_STAGE_REDUCE) {
         P->rp.N = params->max_patches; P->rp.K = params->per_patch_cap; P->rp.batch_size = params->batch_size;
@@ -733,7 +742,8 @@ int cs_collide_active(cs_plan *P, const double *sdf_pose, const double *mesh_pos
     CS_LAUNCHED();
     mark(2);
     launch_pgd_wave(g_sms > 0 ? g_sms : 148, P->block_map, P->xf, d_sdfs, d_meshes, P->st,
-                    P->sample_counter ? P->sample_counter + 1 : nullptr, ug, s);
+                    P->sample_counter ? P->sample_counter + 1 : nullptr, ug, s,
+                    P->uniform_mesh ? &P->uniform_mesh_desc : nullptr);
     CS_LAUNCHED();
     mark(3);
     launch_compact(P->E, P->xf, P->cand_base, P->block_map, P->chunk_first, P->st, P->cands, P->io.n_cand, s);

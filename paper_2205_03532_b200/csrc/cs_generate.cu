@@ -325,12 +325,18 @@ struct FaceGeom {
     double ax, ay, az, bx, by, bz, cx, cy, cz;
 };
 
-__device__ __forceinline__ FaceGeom face_geom(const EnvXf &X, const MeshDesc *meshes, int face) {
-    const MeshDesc &M = meshes[X.mesh];
-    const int4 tri = __ldg(M.tris + face);
-    const double3 a = to_grid(X, ld_vert(M.verts + tri.x));
-    const double3 b = to_grid(X, ld_vert(M.verts + tri.y));
-    const double3 c = to_grid(X, ld_vert(M.verts + tri.z));
+// um: every env of the plan uses mesh mu (a kernel parameter): the triangle and
+// vertex loads then do not wait for the env's descriptor
+__device__ __forceinline__ FaceGeom face_geom(const EnvXf &X, const MeshDesc *meshes, const MeshDesc &mu, int um,
+                                              int face) {
+    const int4 *tris;
+    const double4 *verts;
+    if (um) { tris = mu.tris; verts = mu.verts; }
+    else { tris = meshes[X.mesh].tris; verts = meshes[X.mesh].verts; }
+    const int4 tri = __ldg(tris + face);
+    const double3 a = to_grid(X, ld_vert(verts + tri.x));
+    const double3 b = to_grid(X, ld_vert(verts + tri.y));
+    const double3 c = to_grid(X, ld_vert(verts + tri.z));
     return FaceGeom{a.x, a.y, a.z, b.x, b.y, b.z, c.x, c.y, c.z};
 }
 
@@ -351,7 +357,8 @@ template <bool COUNT, bool UNIFORM>
 __global__ void __launch_bounds__(256, UNIFORM ? GRAD_MINB : GRAD_MINB - 1) k_pgd_grad(const int2 *__restrict__ block_map, const EnvXf *__restrict__ xf,
                                                   const SdfDesc *__restrict__ sdfs, const MeshDesc *__restrict__ meshes,
                                                   Staging st, int stage,
-                                                  unsigned long long *__restrict__ counter, const PlanGrid gu) {
+                                                  unsigned long long *__restrict__ counter, const PlanGrid gu,
+                                                  const MeshDesc mu, int um) {
     const unsigned n = stage == 0 ? st.work_count[0] : st.work_count[2];
     unsigned long long ns = 0;
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -371,7 +378,7 @@ __global__ void __launch_bounds__(256, UNIFORM ? GRAD_MINB : GRAD_MINB - 1) k_pg
         const PlanGrid &g = grid_of<UNIFORM>(gu, sdfs, xf, e);
         double px, py, pz;
         if (stage == 0) {  // the start point, from the corners (not staged: recomputing is cheaper than the traffic)
-            face_start(face_geom(xf[e], meshes, hd.z & 0x3fffffff), (int)((unsigned)hd.z >> 30), px, py, pz);
+            face_start(face_geom(xf[e], meshes, mu, um, hd.z & 0x3fffffff), (int)((unsigned)hd.z >> 30), px, py, pz);
         } else {
             px = st.point[3 * row]; py = st.point[3 * row + 1]; pz = st.point[3 * row + 2];
         }
@@ -432,7 +439,8 @@ __device__ __forceinline__ bool backtrack(const G &g, const FaceGeom &f, const d
 template <bool COUNT, bool UNIFORM>
 __global__ void __launch_bounds__(256, UNIFORM ? FIRST_MINB : FIRST_MINB - 1) k_pgd_first(const int2 *__restrict__ block_map, const EnvXf *__restrict__ xf,
                                                    const SdfDesc *__restrict__ sdfs, const MeshDesc *__restrict__ meshes,
-                                                   Staging st, unsigned long long *__restrict__ counter, const PlanGrid gu) {
+                                                   Staging st, unsigned long long *__restrict__ counter, const PlanGrid gu,
+                                                  const MeshDesc mu, int um) {
     const unsigned n = st.work_count[0];
     unsigned long long ns = 0;
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -445,7 +453,7 @@ __global__ void __launch_bounds__(256, UNIFORM ? FIRST_MINB : FIRST_MINB - 1) k_
         const EnvXf &X = xf[e];
         const double gx = st.grad[3 * row], gy = st.grad[3 * row + 1], gz = st.grad[3 * row + 2];
         double phi = w->phi[3];
-        const FaceGeom f = face_geom(X, meshes, face);
+        const FaceGeom f = face_geom(X, meshes, mu, um, face);
         double px, py, pz;
         face_start(f, (int)((unsigned)hd.z >> 30), px, py, pz);
         // a face that does not move ends here with this gradient: its point and phi go to
@@ -483,7 +491,8 @@ __global__ void __launch_bounds__(256, UNIFORM ? FIRST_MINB : FIRST_MINB - 1) k_
 template <bool COUNT, bool UNIFORM>
 __global__ void __launch_bounds__(128, UNIFORM ? REST_MINB : REST_MINB - 1) k_pgd_rest(const int2 *__restrict__ block_map, const EnvXf *__restrict__ xf,
                                                   const SdfDesc *__restrict__ sdfs, const MeshDesc *__restrict__ meshes,
-                                                  Staging st, unsigned long long *__restrict__ counter, const PlanGrid gu) {
+                                                  Staging st, unsigned long long *__restrict__ counter, const PlanGrid gu,
+                                                  const MeshDesc mu, int um) {
     const unsigned n = st.work_count[3];
     unsigned long long ns = 0;
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -496,7 +505,7 @@ __global__ void __launch_bounds__(128, UNIFORM ? REST_MINB : REST_MINB - 1) k_pg
         const int e = hd.w;
         const EnvXf &X = xf[e];
         const PlanGrid &g = grid_of<UNIFORM>(gu, sdfs, xf, e);
-        const FaceGeom f = face_geom(X, meshes, face);
+        const FaceGeom f = face_geom(X, meshes, mu, um, face);
         const double vphi[3] = {w->phi[0], w->phi[1], w->phi[2]};
         double px = st.point[3 * row], py = st.point[3 * row + 1], pz = st.point[3 * row + 2];
         double phi = st.phi[row], alpha = st.alpha[row];
@@ -663,15 +672,18 @@ void launch_face_prep(int64_t nblocks, const int4 *block_map, const EnvXf *xf, c
 }
 
 void launch_pgd_wave(int sm_count, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs, const MeshDesc *meshes,
-                     const Staging &st, unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s) {
+                     const Staging &st, unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s,
+                     const MeshDesc *umesh) {
     const PlanGrid gu = uniform ? *uniform : PlanGrid{};
+    const MeshDesc mu = umesh ? *umesh : MeshDesc{};
+    const int um = umesh ? 1 : 0;
     const unsigned g = (unsigned)sm_count * 8, gr = (unsigned)sm_count * REST_GRID;
 #define CS_WAVE(C, U)                                                                                 \
     do {                                                                                              \
-        k_pgd_grad<C, U><<<g, 256, 0, s>>>(block_map, xf, sdfs, meshes, st, 0, counter, gu);         \
-        k_pgd_first<C, U><<<g, 256, 0, s>>>(block_map, xf, sdfs, meshes, st, counter, gu);           \
-        k_pgd_grad<C, U><<<g, 256, 0, s>>>(block_map, xf, sdfs, meshes, st, 1, counter, gu);         \
-        k_pgd_rest<C, U><<<gr, 128, 0, s>>>(block_map, xf, sdfs, meshes, st, counter, gu);           \
+        k_pgd_grad<C, U><<<g, 256, 0, s>>>(block_map, xf, sdfs, meshes, st, 0, counter, gu, mu, um); \
+        k_pgd_first<C, U><<<g, 256, 0, s>>>(block_map, xf, sdfs, meshes, st, counter, gu, mu, um);   \
+        k_pgd_grad<C, U><<<g, 256, 0, s>>>(block_map, xf, sdfs, meshes, st, 1, counter, gu, mu, um); \
+        k_pgd_rest<C, U><<<gr, 128, 0, s>>>(block_map, xf, sdfs, meshes, st, counter, gu, mu, um);   \
     } while (0)
     if (uniform) {
         if (counter) CS_WAVE(true, true); else CS_WAVE(false, true);

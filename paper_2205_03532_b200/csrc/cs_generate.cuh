@@ -75,7 +75,8 @@ void launch_face_prep(int64_t nblocks, const int4 *block_map, const EnvXf *xf, c
                       const MeshDesc *meshes, const int64_t *cand_base, const Staging &st, int max_chunk_verts,
                       unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s);
 void launch_pgd_wave(int sm_count, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs, const MeshDesc *meshes,
-                     const Staging &st, unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s);
+                     const Staging &st, unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s,
+                     const MeshDesc *umesh = nullptr);
 size_t face_prep_smem(int max_chunk_verts);
 void launch_compact(int64_t E, const EnvXf *xf, const int64_t *cand_base, const int2 *block_map,
                     const int32_t *chunk_first, const Staging &st, const Candidates &cs, int32_t *n_cand,
