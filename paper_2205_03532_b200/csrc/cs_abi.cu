@@ -738,7 +738,7 @@ int cs_collide_active(cs_plan *P, const double *sdf_pose, const double *mesh_pos
     mark(1);
     const PlanGrid *ug = P->uniform_sdf ? &P->uniform_grid : nullptr;
     launch_face_prep(P->nblocks, P->prep_map, P->xf, d_sdfs, d_meshes, P->cand_base, P->st, P->max_chunk_verts,
-                     P->sample_counter, ug, s);
+                     P->sample_counter, ug, s, P->uniform_mesh ? &P->uniform_mesh_desc : nullptr);
     CS_LAUNCHED();
     mark(2);
     launch_pgd_wave(g_sms > 0 ? g_sms : 148, P->block_map, P->xf, d_sdfs, d_meshes, P->st,

@@ -114,7 +114,8 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int4 
                                                           const MeshDesc *__restrict__ meshes,
                                                           const int64_t *__restrict__ cand_base, Staging st, int maxcv,
                                                           unsigned long long *__restrict__ counter,
-                                                          const PlanGrid gu) {
+                                                          const PlanGrid gu,
+                                                          const MeshDesc mu, int um) {
     extern __shared__ double dsm[];
     __shared__ EnvXf sx;
     __shared__ PlanGrid sg;
@@ -127,9 +128,11 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int4 
     // chunk loads below need not wait for the env's transform
     const int4 bm = prep_map[blockIdx.x];
     const int e = bm.x, f0 = bm.y, v0 = bm.z, ncv = bm.w & 0xffff, mesh = bm.w >> 16;
-    const double4 *verts = meshes[mesh].verts;
-    const int32_t *cverts = meshes[mesh].chunk_verts;
-    const int64_t nt = meshes[mesh].nt;
+    const MeshDesc &M = um ? mu : meshes[mesh];  // uniform-mesh plans: a kernel parameter
+    const double4 *verts = M.verts;
+    const int32_t *cverts = M.chunk_verts;
+    const int64_t nt = M.nt;
+    const uint2 *face_loc = M.face_loc;
     if (threadIdx.x < sizeof(EnvXf) / 8)
         reinterpret_cast<double *>(&sx)[threadIdx.x] = reinterpret_cast<const double *>(xf + e)[threadIdx.x];
     __syncthreads();
@@ -152,7 +155,7 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int4 
     unsigned char *need = reinterpret_cast<unsigned char *>(list + maxcv + FACE_CHUNK);
     __shared__ int s_nl;
     const int64_t f = (int64_t)f0 + threadIdx.x;
-    const uint2 loc = f < nt ? __ldg(meshes[mesh].face_loc + f) : make_uint2(0, 0);  // in flight during the transform
+    const uint2 loc = f < nt ? __ldg(face_loc + f) : make_uint2(0, 0);  // in flight during the transform
     // verts_grid = to_grid.apply(vertices) (generation.py:70), per distinct vertex
     for (int j = threadIdx.x; j < ncv; j += FACE_CHUNK) {
         const double3 p = to_grid(sx, ld_vert(verts + __ldg(cverts + v0 + j)));
@@ -657,17 +660,20 @@ size_t face_prep_smem(int maxcv) {
 
 void launch_face_prep(int64_t nblocks, const int4 *block_map, const EnvXf *xf, const SdfDesc *sdfs,
                       const MeshDesc *meshes, const int64_t *cand_base, const Staging &st, int maxcv,
-                      unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s) {
+                      unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s,
+                      const MeshDesc *umesh) {
+    const MeshDesc mu = umesh ? *umesh : MeshDesc{};
+    const int um = umesh ? 1 : 0;
     if (nblocks <= 0) return;
     const PlanGrid gu = uniform ? *uniform : PlanGrid{};
     const unsigned nb = (unsigned)nblocks;
     const size_t sm = face_prep_smem(maxcv);
     if (uniform) {
-        if (counter) k_face_prep<true, true><<<nb, FACE_CHUNK, sm, s>>>(block_map, xf, sdfs, meshes, cand_base, st, maxcv, counter, gu);
-        else k_face_prep<false, true><<<nb, FACE_CHUNK, sm, s>>>(block_map, xf, sdfs, meshes, cand_base, st, maxcv, nullptr, gu);
+        if (counter) k_face_prep<true, true><<<nb, FACE_CHUNK, sm, s>>>(block_map, xf, sdfs, meshes, cand_base, st, maxcv, counter, gu, mu, um);
+        else k_face_prep<false, true><<<nb, FACE_CHUNK, sm, s>>>(block_map, xf, sdfs, meshes, cand_base, st, maxcv, nullptr, gu, mu, um);
     } else {
-        if (counter) k_face_prep<true, false><<<nb, FACE_CHUNK, sm, s>>>(block_map, xf, sdfs, meshes, cand_base, st, maxcv, counter, gu);
-        else k_face_prep<false, false><<<nb, FACE_CHUNK, sm, s>>>(block_map, xf, sdfs, meshes, cand_base, st, maxcv, nullptr, gu);
+        if (counter) k_face_prep<true, false><<<nb, FACE_CHUNK, sm, s>>>(block_map, xf, sdfs, meshes, cand_base, st, maxcv, counter, gu, mu, um);
+        else k_face_prep<false, false><<<nb, FACE_CHUNK, sm, s>>>(block_map, xf, sdfs, meshes, cand_base, st, maxcv, nullptr, gu, mu, um);
     }
 }
 

@@ -73,7 +73,8 @@ void launch_env_xf(int64_t E, const int32_t *env_sdf, const int32_t *env_mesh, c
                    const int32_t *active = nullptr);
 void launch_face_prep(int64_t nblocks, const int4 *block_map, const EnvXf *xf, const SdfDesc *sdfs,
                       const MeshDesc *meshes, const int64_t *cand_base, const Staging &st, int max_chunk_verts,
-                      unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s);
+                      unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s,
+                      const MeshDesc *umesh = nullptr);
 void launch_pgd_wave(int sm_count, const int2 *block_map, const EnvXf *xf, const SdfDesc *sdfs, const MeshDesc *meshes,
                      const Staging &st, unsigned long long *counter, const PlanGrid *uniform, cudaStream_t s,
                      const MeshDesc *umesh = nullptr);
