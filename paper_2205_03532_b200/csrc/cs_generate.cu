@@ -683,7 +683,7 @@ void launch_pgd_wave(int sm_count, const int2 *block_map, const EnvXf *xf, const
     const PlanGrid gu = uniform ? *uniform : PlanGrid{};
     const MeshDesc mu = umesh ? *umesh : MeshDesc{};
     const int um = umesh ? 1 : 0;
-    const unsigned g = (unsigned)sm_count * 8, gr = (unsigned)sm_count * REST_GRID;
+    const unsigned g = (unsigned)sm_count * WAVE_GRID, gr = (unsigned)sm_count * REST_GRID;
 #define CS_WAVE(C, U)                                                                                 \
     do {                                                                                              \
         k_pgd_grad<C, U><<<g, 256, 0, s>>>(block_map, xf, sdfs, meshes, st, 0, counter, gu, mu, um); \

@@ -14,6 +14,10 @@ namespace cs {
 #ifndef REST_MINB
 #define REST_MINB 4
 #endif
+#ifndef WAVE_GRID
+#define WAVE_GRID 32  // CTAs per SM of the grad / first wave kernels (grid-stride loops): measured best
+                      // (8: +0.05 ms, 64: +0.02 ms; many small CTAs balance the tail)
+#endif
 #ifndef REST_GRID
 #define REST_GRID 8
 #endif
