@@ -37,6 +37,13 @@ namespace cs {
 #ifndef FW_SMEM
 #define FW_SMEM 128     // members per warp-path patch (all in shared memory)
 #endif
+#ifndef FIN_GRID
+#define FIN_GRID 16  // scale of the finalize grids (patches assigned by grid stride): patch sizes vary
+                     // widely, so many CTAs balance the tail (x1: +0.10 ms; x8..x64 alike)
+#endif
+#ifndef FIN_GRID_CHAIN
+#define FIN_GRID_CHAIN 1  // k_fin_chain claims jobs dynamically: x4 is no faster
+#endif
 #ifndef FB_THREADS
 #define FB_THREADS 128  // k_fin_sort_block
 #endif
@@ -890,11 +897,11 @@ void launch_finalize(const ReduceIO &io, const ReduceParams &p, int sm_count, cu
         configured = true;
     }
     auto cap = [&](int64_t want, int64_t limit) { return (unsigned)(want < limit ? want : limit); };
-    k_fin_sort_warp<<<cap((int64_t)sm_count * 8, (maxw + FW_WARPS - 1) / FW_WARPS), FW_WARPS * 32, wsm, s>>>(io, p);
-    k_fin_sort_block<<<cap((int64_t)sm_count * 4, maxw), FB_THREADS, FB_BYTES, s>>>(io, p);
-    k_fin_fold_large<<<cap((int64_t)sm_count * 4, (maxw + FL_WARPS - 1) / FL_WARPS), FL_WARPS * 32, 0, s>>>(io, p);
-    k_fin_chain<<<cap((int64_t)sm_count * 8, (maxw + CH_WARPS - 1) / CH_WARPS), CH_WARPS * 32, 0, s>>>(io, p);
-    k_fin_kept<<<cap((int64_t)sm_count * 8, (maxw + FK_WARPS - 1) / FK_WARPS), FK_WARPS * 32, 0, s>>>(io, p);
+    k_fin_sort_warp<<<cap((int64_t)sm_count * 8 * FIN_GRID, (maxw + FW_WARPS - 1) / FW_WARPS), FW_WARPS * 32, wsm, s>>>(io, p);
+    k_fin_sort_block<<<cap((int64_t)sm_count * 4 * FIN_GRID, maxw), FB_THREADS, FB_BYTES, s>>>(io, p);
+    k_fin_fold_large<<<cap((int64_t)sm_count * 4 * FIN_GRID, (maxw + FL_WARPS - 1) / FL_WARPS), FL_WARPS * 32, 0, s>>>(io, p);
+    k_fin_chain<<<cap((int64_t)sm_count * 8 * FIN_GRID_CHAIN, (maxw + CH_WARPS - 1) / CH_WARPS), CH_WARPS * 32, 0, s>>>(io, p);
+    k_fin_kept<<<cap((int64_t)sm_count * 8 * FIN_GRID, (maxw + FK_WARPS - 1) / FK_WARPS), FK_WARPS * 32, 0, s>>>(io, p);
     k_stats<<<(unsigned)((io.E * 32 + 255) / 256), 256, 0, s>>>(io, p);
 }
 
