@@ -212,3 +212,48 @@ def test_solver_errors(P):
         SolverParams(dt=0.0)
     with pytest.raises(ValueError):
         SolverParams(vel_iterations=-1)
+
+
+def test_solver_six_body_system_vs_oracle(P):
+    """Systems above four bodies take the shared-memory state path: a 6-body system
+    (three dynamic bodies, random rows between all of them) against the oracle."""
+    from oracle import oracle as O
+    from paper_2205_03532_b200.dynamics import ContactConstraints, SolverState
+
+    rng = np.random.default_rng(21)
+    nb, m = 6, 90
+    st = SolverState(nb)
+    for b in (0, 2, 5):
+        mass = rng.uniform(0.01, 0.05)
+        st.ref[b] = rng.standard_normal(3) * 0.01
+        st.w_mat[b, :3, :3] = np.eye(3) / mass
+        A = rng.standard_normal((3, 3))
+        st.w_mat[b, 3:, 3:] = np.linalg.inv(A @ A.T * 1e-6 + np.eye(3) * 1e-7)
+        st.vel[b] = rng.standard_normal(6) * 0.1
+    rows = []
+    for c in range(m):
+        a, b = rng.choice(nb, size=2, replace=False)
+        n = rng.standard_normal(3)
+        n /= np.linalg.norm(n)
+        rows.append({"body_a": int(a), "body_b": int(b), "point": rng.standard_normal(3) * 0.01, "normal": n,
+                     "depth": float(rng.uniform(-2e-4, 4e-4)), "mu": 0.5, "restitution": 0.3, "slop": 5e-5})
+    vel0 = st.vel.copy()
+    con = ContactConstraints.build(rows, st, 1 / 240, 0.2)
+    con.position_sweeps(st, 10)
+    con.velocity_sweeps(st, 2)
+    wr = con.body_wrenches(nb, 1 / 240)
+    ba = np.array([r["body_a"] for r in rows]); bb = np.array([r["body_b"] for r in rows])
+    pts = np.array([r["point"] for r in rows]); nrm = np.array([r["normal"] for r in rows])
+    dep = np.array([r["depth"] for r in rows])
+    oc = O.constraints_build(ba, bb, pts, nrm, dep, 0.3, 5e-5, st.ref, st.w_mat, vel0, 1 / 240, 0.2)
+    for k in ("kn", "kt1", "kt2", "bias_target", "restitution_target"):
+        assert np.array_equal(getattr(con, k), oc[k]), k
+    v, imp = np.array(vel0), np.zeros((nb, 6))
+    ln, l1, l2, lv = (np.zeros(m) for _ in range(4))
+    geo = (ba, bb, oc["ra"], oc["rb"], nrm, oc["tan1"], oc["tan2"], oc["kn"], oc["kt1"], oc["kt2"])
+    O.gauss_seidel_sweeps(10, st.w_mat, v, imp, *geo, oc["bias_target"], 0.5, ln, l1, l2, True)
+    O.gauss_seidel_sweeps(2, st.w_mat, v, imp, *geo, oc["restitution_target"], 0.5, lv, l1, l2, False)
+    assert np.array_equal(st.vel, v) and np.array_equal(st.impulse, imp)
+    assert np.array_equal(con.lam_n, ln) and np.array_equal(con.lam_vel, lv)
+    owr = O.body_wrenches(nb, ba, bb, oc["ra"], oc["rb"], nrm, oc["tan1"], oc["tan2"], ln, lv, l1, l2, 1 / 240)
+    assert np.array_equal(wr, owr)
