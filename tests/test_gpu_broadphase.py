@@ -185,3 +185,32 @@ def test_multipair_scenes_match_oracle(P, grid64_npz, meshes):
         wr = O.body_wrenches(4, a, b, con["ra"], con["rb"], nrm, con["tan1"], con["tan2"], ln, lv, l1, l2, h)
         assert np.array_equal(gv[i], v), i
         assert np.array_equal(wrench[i], wr), i
+
+
+def test_broadphase_max_scene_and_status_codes(P):
+    """The per-scene cap (2048 bodies, sweep semantics, inverted boxes included)
+    against the oracle, and the batched status codes for the scenes it refuses."""
+    from oracle import oracle as O
+    from paper_2205_03532_b200.geometry import broadphase_batched, broadphase_pairs
+    from paper_2205_03532_b200.geometry.broadphase import MAX_BODIES
+
+    rng = np.random.default_rng(33)
+    n = MAX_BODIES
+    c = rng.uniform(-0.5, 0.5, (n, 3))
+    ext = rng.uniform(0.002, 0.02, (n, 3))
+    lo, hi = c - ext, c + ext
+    lo[10, 0], hi[10, 0] = hi[10, 0], lo[10, 0]
+    lo[11, 0] = lo[12, 0] = lo[13, 0]
+    ids = rng.permutation(n * 2)[:n]
+    got = broadphase_pairs([((lo[i], hi[i]), int(ids[i])) for i in range(n)], 1e-3)
+    ref = [tuple(int(x) for x in p) for p in O.broadphase_pairs(lo, hi, ids, 1e-3)]
+    assert got == ref and len(ref) > 100
+    # scene 0 fine, scene 1 over the cap (3), scene 2 duplicate ids (4), scene 3 NaN (1)
+    m = n + 1
+    lo2 = np.concatenate([lo[:5], rng.uniform(-1, 1, (m, 3)), lo[:3], lo[:3]])
+    hi2 = lo2 + 0.01
+    hi2[-1, 1] = np.nan
+    ids2 = np.concatenate([np.arange(5), np.arange(m), [1, 2, 1], [0, 1, 2]])
+    off = np.array([0, 5, 5 + m, 8 + m, 11 + m])
+    _, _, n_pairs, status = broadphase_batched(lo2, hi2, off, np.zeros(4), ids2)
+    assert status.cpu().tolist() == [0, 3, 4, 1]
