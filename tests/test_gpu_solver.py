@@ -223,13 +223,15 @@ def test_solver_six_body_system_vs_oracle(P):
     rng = np.random.default_rng(21)
     nb, m = 6, 90
     st = SolverState(nb)
-    for b in (0, 2, 5):
+    for b in (0, 2, 5):  # bodies 0, 2: the rigid-body mobility layout; 5: a full 6x6
         mass = rng.uniform(0.01, 0.05)
         st.ref[b] = rng.standard_normal(3) * 0.01
         st.w_mat[b, :3, :3] = np.eye(3) / mass
         A = rng.standard_normal((3, 3))
         st.w_mat[b, 3:, 3:] = np.linalg.inv(A @ A.T * 1e-6 + np.eye(3) * 1e-7)
         st.vel[b] = rng.standard_normal(6) * 0.1
+    B = rng.standard_normal((6, 6))
+    st.w_mat[5] = B @ B.T * 10.0
     rows = []
     for c in range(m):
         a, b = rng.choice(nb, size=2, replace=False)
@@ -253,7 +255,7 @@ def test_solver_six_body_system_vs_oracle(P):
     geo = (ba, bb, oc["ra"], oc["rb"], nrm, oc["tan1"], oc["tan2"], oc["kn"], oc["kt1"], oc["kt2"])
     O.gauss_seidel_sweeps(10, st.w_mat, v, imp, *geo, oc["bias_target"], 0.5, ln, l1, l2, True)
     O.gauss_seidel_sweeps(2, st.w_mat, v, imp, *geo, oc["restitution_target"], 0.5, lv, l1, l2, False)
-    assert np.array_equal(st.vel, v) and np.array_equal(st.impulse, imp)
-    assert np.array_equal(con.lam_n, ln) and np.array_equal(con.lam_vel, lv)
+    assert st.vel.tobytes() == v.tobytes() and st.impulse.tobytes() == imp.tobytes()
+    assert con.lam_n.tobytes() == ln.tobytes() and con.lam_vel.tobytes() == lv.tobytes()
     owr = O.body_wrenches(nb, ba, bb, oc["ra"], oc["rb"], nrm, oc["tan1"], oc["tan2"], ln, lv, l1, l2, 1 / 240)
     assert np.array_equal(wr, owr)
