@@ -11,6 +11,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "cs_reduce.cuh"
@@ -138,6 +139,7 @@ struct cs_plan {
     ReduceParams rp{};
     int64_t max_batch = 1;
     int64_t total_cap = 0;
+    unsigned char *row_arena = nullptr;  // per-row buffers of the descent and of the reduction (aliased)
     int64_t nblocks = 0;
     bool uniform_sdf = false;      // every env samples the same grid
     PlanGrid uniform_grid{};  // ...whose view then travels as a kernel parameter
@@ -511,6 +513,36 @@ static int plan_buffers(cs_plan *P, const std::vector<int64_t> &cap) {
     A(P->status, E);
     A(P->io.n_cand, E);
     A(P->cands.point, 3 * tot); A(P->cands.normal, 3 * tot); A(P->cands.depth, tot); A(P->cands.face, tot);
+    // The descent's per-row staging is dead once k_compact has written the candidates,
+    // and the reduction's per-row scratch is live only after it (both stream-ordered
+    // within one collide; neither carries state across calls): one arena holds either.
+    {
+        const bool red = (P->stages & CS_STAGE_REDUCE) != 0;
+        auto carve = [&](uintptr_t base, bool gen_side) {
+            uintptr_t off = 0;
+            auto take = [&](auto *&ptr, size_t n) {
+                off = (off + 255) & ~(uintptr_t)255;
+                ptr = reinterpret_cast<std::remove_reference_t<decltype(ptr)>>(base + off);
+                off += n * sizeof(*ptr);
+            };
+            const size_t t = (size_t)tot;
+            if (gen_side) {
+                Staging &st = P->st;
+                take(st.point, 3 * t); take(st.phi, t); take(st.grad, 3 * t); take(st.face, t); take(st.work, t);
+                take(st.alpha, t); take(st.acc, t); take(st.acc_hd, t); take(st.slow, t);
+            } else {
+                ReduceIO &q = P->io;
+                take(q.order, t); take(q.label, t); take(q.su, t); take(q.sv, t); take(q.sp, t); take(q.suv, t);
+                take(q.tuv, t); take(q.tpos, t); take(q.tu, t); take(q.tv, t); take(q.tk, t); take(q.hj, 4 * t);
+                take(q.hu, 4 * t); take(q.hv, 4 * t);
+            }
+            return (size_t)off;
+        };
+        const size_t gen_bytes = carve(0, true), red_bytes = red ? carve(0, false) : 0;
+        A(P->row_arena, std::max(gen_bytes, red_bytes));
+        carve(reinterpret_cast<uintptr_t>(P->row_arena), true);
+        if (red) carve(reinterpret_cast<uintptr_t>(P->row_arena), false);
+    }
     CS_CUDA(cudaMemset(P->status, 0, sizeof(int32_t) * (size_t)E));
     CS_CUDA(cudaMemset(P->io.n_cand, 0, sizeof(int32_t) * (size_t)E));
     ReduceIO &io = P->io;
@@ -518,10 +550,7 @@ static int plan_buffers(cs_plan *P, const std::vector<int64_t> &cap) {
     io.cand_base = P->cand_base;
     io.point = P->cands.point; io.normal = P->cands.normal; io.depth = P->cands.depth; io.face = P->cands.face;
     if (P->stages & CS_STAGE_REDUCE) {
-        A(io.order, tot); A(io.label, tot); A(io.su, tot); A(io.sv, tot); A(io.sp, tot);
         A(io.sh, 2 * tot + E * (4 * (int64_t)N + 4));
-        A(io.suv, tot); A(io.tuv, tot); A(io.tpos, tot); A(io.tu, tot); A(io.tv, tot); A(io.tk, tot);
-        A(io.hj, 4 * tot); A(io.hu, 4 * tot); A(io.hv, 4 * tot);
         A(io.hlen, 4 * E * N); A(io.pdeep, E * N); A(io.pnt, E * N); A(io.wenv, E * N);
         A(io.jobs, 64 * 4 * E * N); A(io.njob, 65);
         A(io.patch_off, E + 1);
@@ -637,20 +666,11 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
     if (!r) r = P->alloc(&P->block_map, bmap.size());
     if (!r) r = P->alloc(&P->prep_map, pmap.size());
     if (!r) r = P->alloc(&P->xf, (size_t)n_envs);
-    if (!r) r = P->alloc(&P->st.face, (size_t)P->total_cap);
     if (!r) r = P->alloc(&P->st.chunk_count, bmap.size());
     if (!r) r = P->alloc(&P->st.chunk_off, bmap.size());
     if (!r) r = P->alloc(&P->st.chunk_found, bmap.size());
-    if (!r) r = P->alloc(&P->st.work, (size_t)P->total_cap);
     if (!r) r = P->alloc(&P->st.work_count, 4);
-    if (!r) r = P->alloc(&P->st.alpha, (size_t)P->total_cap);
-    if (!r) r = P->alloc(&P->st.acc, (size_t)P->total_cap);
-    if (!r) r = P->alloc(&P->st.acc_hd, (size_t)P->total_cap);
-    if (!r) r = P->alloc(&P->st.slow, (size_t)P->total_cap);
     if (!r) r = P->alloc(&P->chunk_first, chunk_first.size());
-    if (!r) r = P->alloc(&P->st.point, 3 * (size_t)P->total_cap);
-    if (!r) r = P->alloc(&P->st.phi, (size_t)P->total_cap);
-    if (!r) r = P->alloc(&P->st.grad, 3 * (size_t)P->total_cap);
     if (!r && (stages & CS_STAGE_REDUCE) && !params->has_min_depth) {
         r = P->alloc(&P->env_min_depth, (size_t)n_envs);
         P->io.env_min_depth = P->env_min_depth;

@@ -3,8 +3,8 @@
 
     python scripts/bench_sweep.py [--res 64 128 256 512] [--envs 1024 4096 16384]
 
-Prints one JSON line per (res, envs). Envs above 16384 need > 60 GB of plan
-buffers (3.7 MB per env) and are left to multi-GPU sharding (bench.py --gpus N).
+Prints one JSON line per (res, envs). A plan takes 4.3 MB per env (scripts/plan_memory.py),
+so one B200 holds about 43 k envs; beyond that, shard envs over GPUs (bench.py --gpus N).
 """
 import argparse
 import gc
