@@ -158,6 +158,9 @@ int cs_plan_create_reduce(int64_t n_envs, const int64_t *capacity, const cs_redu
                           cs_plan **plan);
 int cs_plan_destroy(cs_plan *plan);
 int cs_plan_outputs(cs_plan *plan, cs_outputs *out);
+/* Device bytes the plan holds (its buffers, including solver rows once allocated);
+ * for sizing env counts per GPU. Not in the reference (its arrays are per call). */
+int cs_plan_device_bytes(cs_plan *plan, int64_t *bytes);
 
 /* One collide step: sdf_pose/mesh_pose [dev] (E,7) or (E,12) per pose_format,
  * contact_distance [dev] (E). Stream-ordered; no host synchronisation. */

@@ -68,6 +68,7 @@ _SIGS = {
     "cs_plan_create": ([_i64, _vp, _vp, ctypes.POINTER(ReductionParamsC), _i32, ctypes.POINTER(_vp)], ctypes.c_int),
     "cs_plan_create_reduce": ([_i64, _vp, ctypes.POINTER(ReductionParamsC), ctypes.POINTER(_vp)], ctypes.c_int),
     "cs_plan_destroy": ([_vp], ctypes.c_int),
+    "cs_plan_device_bytes": ([_vp, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
     "cs_plan_outputs": ([_vp, ctypes.POINTER(OutputsC)], ctypes.c_int),
     "cs_collide": ([_vp, _vp, _vp, _i32, _vp, _vp], ctypes.c_int),
     "cs_reduce": ([_vp, _vp], ctypes.c_int),

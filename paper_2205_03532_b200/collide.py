@@ -157,6 +157,14 @@ class Plan:
         """Record CUDA events around each phase of the next `slots` collide calls (0 disables)."""
         _native.call("cs_plan_timing", self.ptr, int(slots))
 
+    @property
+    def device_bytes(self) -> int:
+        """Device memory the plan holds (cs_plan_device_bytes): about 4.3 MB per env
+        of the M16 nut (17 304 faces), for sizing env counts per GPU."""
+        n = ctypes.c_int64(0)
+        _native.call("cs_plan_device_bytes", self.ptr, ctypes.byref(n))
+        return int(n.value)
+
     def read_timing(self, max_steps: int) -> np.ndarray:
         """(steps, 7) ms per phase (Plan.PHASES), oldest first."""
         out = np.zeros((max_steps, len(self.PHASES)), np.float32)

@@ -146,6 +146,7 @@ struct cs_plan {
     bool uniform_mesh = false;     // every env uses the same mesh
     MeshDesc uniform_mesh_desc{};  // ...whose descriptor travels as a kernel parameter
     std::vector<void *> allocs;
+    int64_t device_bytes = 0;
     // inputs / tables
     int32_t *env_sdf = nullptr, *env_mesh = nullptr;
     int64_t *cand_base = nullptr;
@@ -177,7 +178,7 @@ struct cs_plan {
     template <class T>
     int alloc(T **p, size_t n) {
         int r = dalloc(p, n);
-        if (r == CS_OK) allocs.push_back(*p);
+        if (r == CS_OK) { allocs.push_back(*p); device_bytes += n * sizeof(T); }
         return r;
     }
     // assets this plan samples (their store entries outlive it, cs_sdf_free / cs_mesh_free)
@@ -718,6 +719,12 @@ int cs_plan_create_reduce(int64_t n_envs, const int64_t *capacity, const cs_redu
 
 int cs_plan_destroy(cs_plan *plan) {
     delete plan;
+    return CS_OK;
+}
+
+int cs_plan_device_bytes(cs_plan *plan, int64_t *bytes) {
+    if (!plan || !bytes) return fail(CS_ERR_VALUE, "null argument");
+    *bytes = plan->device_bytes;
     return CS_OK;
 }
 

@@ -428,6 +428,28 @@ def test_plan_memory_released_without_gc(P, grid64, nut):
     assert free0 - torch.cuda.mem_get_info()[0] < 0.1 * used
 
 
+def test_plan_device_bytes(P, grid64, nut):
+    """Plan.device_bytes (cs_plan_device_bytes) accounts for what the plan allocates,
+    linear in the env count, and the descent staging shares the reduction's per-row
+    arena (at most 200 B of the two per face row, not their 312 B sum)."""
+    hs, hm = P.register_sdf(grid64), P.register_mesh(nut)
+    F = len(nut.triangles)
+    sizes = []
+    for E in (256, 512):
+        torch.cuda.synchronize()
+        free0 = torch.cuda.mem_get_info()[0]
+        plan = P.Plan([hs] * E, [hm] * E, P.ReductionParams())
+        used = free0 - torch.cuda.mem_get_info()[0]
+        b = plan.device_bytes
+        assert 0.9 * used <= b <= used + (64 << 20), (b, used)  # cudaMalloc granularity on top
+        sizes.append(b)
+        del plan
+    per_env = (sizes[1] - sizes[0]) / 256
+    assert abs(sizes[1] - 2 * sizes[0]) < 0.02 * sizes[1]
+    # candidates 60 B + members 4 B + arena <= 200 B per row, plus per-env/patch outputs
+    assert per_env < F * 270 + 200_000, per_env
+
+
 def test_asset_free_deferred_while_plans_use_it(P, grid64, gen64, meshes):
     """cs_sdf_free / cs_mesh_free on an asset a live plan samples defer the release to
     the last such plan's destruction (no use-after-free); a freed handle cannot start
