@@ -57,6 +57,8 @@ struct SdfEntry {
     float *values = nullptr;
     float *cwin = nullptr;  // cell-window minima (GridT::cwin)
     float *bwin = nullptr;  // brick-window minima (GridT::bwin)
+    cudaArray_t arr = nullptr;       // the values as a 2D layered texture (GridT::tex)
+    cudaTextureObject_t tex = 0;
     size_t bytes = 0;
     SdfDesc desc{};
     int users = 0;        // live plans naming this grid
@@ -110,6 +112,8 @@ int free_sdf_entry(SdfEntry &s) {
     CS_CUDA(cudaFree(s.values));
     CS_CUDA(cudaFree(s.cwin));
     CS_CUDA(cudaFree(s.bwin));
+    if (s.tex) CS_CUDA(cudaDestroyTextureObject(s.tex));
+    if (s.arr) CS_CUDA(cudaFreeArray(s.arr));
     s = SdfEntry{};
     return CS_OK;
 }
@@ -282,6 +286,28 @@ int cs_sdf_register(const float *values, int values_on_device, int32_t nx, int32
         CS_CUDA(cudaDeviceSynchronize());
         CS_CUDA(cudaFree(tmp));
     }
+#ifndef CS_NO_TEX
+    {   // the values as a 2D layered texture (x, y, layer z): tld4 returns a cell face's
+        // 2 x 2 corners in one fetch (cs_common.cuh: sample_axes)
+        cudaChannelFormatDesc cf = cudaCreateChannelDesc<float>();
+        CS_CUDA(cudaMalloc3DArray(&s.arr, &cf, make_cudaExtent(nx, ny, nz), cudaArrayLayered));
+        cudaMemcpy3DParms cp{};
+        cp.srcPtr = make_cudaPitchedPtr(s.values, (size_t)nx * sizeof(float), nx, ny);
+        cp.dstArray = s.arr;
+        cp.extent = make_cudaExtent(nx, ny, nz);
+        cp.kind = cudaMemcpyDeviceToDevice;
+        CS_CUDA(cudaMemcpy3D(&cp));
+        cudaResourceDesc rd{};
+        rd.resType = cudaResourceTypeArray;
+        rd.res.array.array = s.arr;
+        cudaTextureDesc td{};
+        td.addressMode[0] = td.addressMode[1] = td.addressMode[2] = cudaAddressModeClamp;
+        td.filterMode = cudaFilterModePoint;
+        td.readMode = cudaReadModeElementType;
+        td.normalizedCoords = 0;
+        CS_CUDA(cudaCreateTextureObject(&s.tex, &rd, &td, nullptr));
+    }
+#endif
     SdfDesc &d = s.desc;
     d.values = s.values;
     d.nx = nx; d.ny = ny; d.nz = nz; d.pad = 0;
@@ -291,6 +317,7 @@ int cs_sdf_register(const float *values, int values_on_device, int32_t nx, int32
     d.gp = cs::make_grid<float>(s.values, nx, ny, nz, origin[0], origin[1], origin[2], voxel);
     d.gp.cwin = s.cwin;
     d.gp.bwin = s.bwin;
+    d.gp.tex = 0;  // the texture is used by uniform-grid plans only (a warp-uniform handle: cs_plan_create)
     CS_CUDA(cudaMemcpy(d_sdfs + h, &d, sizeof(SdfDesc), cudaMemcpyHostToDevice));
     s.live = true;
     *handle = h;
@@ -631,7 +658,12 @@ int cs_plan_create(int64_t n_envs, const int32_t *sdf_handles, const int32_t *me
                 pmap.push_back(make_int4((int)e, (int)f, vo[c], (vo[c + 1] - vo[c]) | (m << 16)));
             }
         }
-        if (uniform) ugrid = g_sdf[sdf_handles[0]].desc.gp;
+        if (uniform) {
+            ugrid = g_sdf[sdf_handles[0]].desc.gp;
+            // tld4 takes its texture handle in a uniform register: only plans whose envs
+            // all sample one grid (the handle a kernel parameter) gather through it
+            ugrid.tex = (unsigned long long)g_sdf[sdf_handles[0]].tex;
+        }
         umesh = true;
         for (int64_t e = 0; e < n_envs; ++e) umesh &= mesh_handles[e] == mesh_handles[0];
         if (umesh) umdesc = g_mesh[mesh_handles[0]].desc;
