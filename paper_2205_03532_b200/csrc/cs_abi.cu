@@ -187,7 +187,25 @@ struct cs_plan {
     }
     // assets this plan samples (their store entries outlive it, cs_sdf_free / cs_mesh_free)
     std::vector<int32_t> sdf_used, mesh_used;
+    FinFork fork{};        // side streams of the finalize's concurrent branches (created lazily)
+    bool fork_ready = false;
+    const FinFork *get_fork() {
+        if (!fork_ready) {
+            if (cudaStreamCreateWithFlags(&fork.s_block, cudaStreamNonBlocking) != cudaSuccess ||
+                cudaStreamCreateWithFlags(&fork.s_fold, cudaStreamNonBlocking) != cudaSuccess ||
+                cudaEventCreateWithFlags(&fork.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&fork.ev_block, cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&fork.ev_fold, cudaEventDisableTiming) != cudaSuccess)
+                return nullptr;  // no fork: the finalize runs in stream order
+            fork_ready = true;
+        }
+        return &fork;
+    }
     ~cs_plan() {
+        if (fork_ready) {
+            cudaStreamDestroy(fork.s_block); cudaStreamDestroy(fork.s_fold);
+            cudaEventDestroy(fork.ev_fork); cudaEventDestroy(fork.ev_block); cudaEventDestroy(fork.ev_fold);
+        }
         for (cudaEvent_t e : events) cudaEventDestroy(e);
         for (void *p : allocs) cudaFree(p);
         release_assets(sdf_used, mesh_used);
@@ -561,7 +579,7 @@ static int plan_buffers(cs_plan *P, const std::vector<int64_t> &cap) {
             } else {
                 ReduceIO &q = P->io;
                 take(q.order, t); take(q.label, t); take(q.su, t); take(q.sv, t); take(q.sp, t); take(q.suv, t);
-                take(q.tuv, t); take(q.tpos, t); take(q.tu, t); take(q.tv, t); take(q.tk, t); take(q.hj, 4 * t);
+                take(q.tuv, t); take(q.tpos, t); take(q.tu, t); take(q.tv, t); take(q.tk, t); take(q.fw, t); take(q.hj, 4 * t);
                 take(q.hu, 4 * t); take(q.hv, 4 * t);
             }
             return (size_t)off;
@@ -769,7 +787,7 @@ int cs_plan_outputs(cs_plan *plan, cs_outputs *out) {
 static int run_reduce(cs_plan *P, cudaStream_t s) {
     launch_reduce(P->io, P->rp, P->max_batch, s);
     CS_LAUNCHED();
-    launch_finalize(P->io, P->rp, g_sms > 0 ? g_sms : 148, s);
+    launch_finalize(P->io, P->rp, g_sms > 0 ? g_sms : 148, s, P->get_fork());
     CS_LAUNCHED();
     return CS_OK;
 }
@@ -812,7 +830,7 @@ int cs_collide_active(cs_plan *P, const double *sdf_pose, const double *mesh_pos
         launch_reduce(P->io, P->rp, P->max_batch, s);
         CS_LAUNCHED();
         mark(5);
-        launch_finalize(P->io, P->rp, g_sms > 0 ? g_sms : 148, s);
+        launch_finalize(P->io, P->rp, g_sms > 0 ? g_sms : 148, s, P->get_fork());
         CS_LAUNCHED();
     } else {
         mark(5);

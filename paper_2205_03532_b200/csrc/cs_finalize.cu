@@ -68,14 +68,20 @@ __global__ void k_patch_off(int64_t E, const int32_t *__restrict__ n_patch, int3
     if (threadIdx.x == 0) off[E] = running;
 }
 
-// patch (work index) -> env, so stage 1 finds a patch's env with one load
-__global__ void k_patch_env(int64_t E, const int32_t *__restrict__ n_patch, const int32_t *__restrict__ off,
-                            int32_t *__restrict__ wenv) {
+// patch (work index) -> env, so stage 1 finds a patch's env with one load; patches
+// above FW_SMEM members go to the list of the CTA-per-patch kernels
+__global__ void k_patch_env(int64_t E, int N, const int32_t *__restrict__ n_patch, const int32_t *__restrict__ off,
+                            const int32_t *__restrict__ member_offsets, int32_t *__restrict__ wenv,
+                            int32_t *__restrict__ large_list, int32_t *__restrict__ large_count) {
     const int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (e >= E) return;
     const int o = off[e], n = n_patch[e];
-    for (int q = lane; q < n; q += 32) wenv[o + q] = (int32_t)e;
+    const int32_t *mo = member_offsets + e * (N + 1);
+    for (int q = lane; q < n; q += 32) {
+        wenv[o + q] = (int32_t)e;
+        if (mo[q + 1] - mo[q] > FW_SMEM) large_list[atomicAdd(large_count, 1)] = o + q;
+    }
 }
 
 // numpy stable argsort(-depths) order: depth descending, ties by index, NaN last.
@@ -432,10 +438,7 @@ __global__ void __launch_bounds__(FW_WARPS * 32) k_fin_sort_warp(ReduceIO io, Re
         const int64_t e = io.wenv[w];
         const int q = w - io.patch_off[e];
         const int32_t *mo = io.member_offsets + e * (p.N + 1);
-        if (mo[q + 1] - mo[q] > FW_SMEM) {  // handed to the CTA path (order-free: patches are independent)
-            if ((threadIdx.x & 31) == 0) io.large_list[atomicAdd(io.large_count, 1)] = w;
-            continue;
-        }
+        if (mo[q + 1] - mo[q] > FW_SMEM) continue;  // the CTA path's (k_patch_env listed it)
         sort_patch<true>(t, io, p, w, e, q, A, B, tile);
     }
 }
@@ -494,7 +497,7 @@ __global__ void __launch_bounds__(FL_WARPS * 32) k_fin_fold_large(ReduceIO io, R
         const int32_t *mem = io.members + base + moff;
         const double *P = io.point + 3 * base, *Nn = io.normal + 3 * base, *D = io.depth + base;
         const int64_t pq = e * p.N + q;
-        double *wb = m <= FL_W ? s_w[wib] : io.tu + base + moff;
+        double *wb = m <= FL_W ? s_w[wib] : io.fw + base + moff;
         double fd = 0.0, fpx = 0.0, fpy = 0.0, fpz = 0.0, fnx = 0.0, fny = 0.0, fnz = 0.0;
         auto fetch = [&](int k) {
             if (k < m) {
@@ -884,10 +887,12 @@ __global__ void k_stats(ReduceIO io, ReduceParams p) {
     }
 }
 
-void launch_finalize(const ReduceIO &io, const ReduceParams &p, int sm_count, cudaStream_t s) {
+void launch_finalize(const ReduceIO &io, const ReduceParams &p, int sm_count, cudaStream_t s, const FinFork *fk) {
     if (io.E <= 0) return;
     k_patch_off<<<1, 1024, 0, s>>>(io.E, io.n_patch, io.patch_off, io.large_count, io.njob);
-    k_patch_env<<<(unsigned)((io.E * 32 + 255) / 256), 256, 0, s>>>(io.E, io.n_patch, io.patch_off, io.wenv);
+    k_patch_env<<<(unsigned)((io.E * 32 + 255) / 256), 256, 0, s>>>(io.E, p.N, io.n_patch, io.patch_off,
+                                                                     io.member_offsets, io.wenv, io.large_list,
+                                                                     io.large_count);
     const int64_t maxw = io.E * (int64_t)p.N;
     const size_t wsm = FW_BYTES_PER_WARP * FW_WARPS;
     static bool configured = false;
@@ -897,11 +902,31 @@ void launch_finalize(const ReduceIO &io, const ReduceParams &p, int sm_count, cu
         configured = true;
     }
     auto cap = [&](int64_t want, int64_t limit) { return (unsigned)(want < limit ? want : limit); };
+    // The three stage-1 kernels are independent (k_patch_env wrote the work lists): with
+    // a fork they run as concurrent branches (graph branches when captured), so the
+    // CTA-per-patch sort and the sequential sums fill each other's tails. The chains
+    // need both sorts; the sums join before the stats.
+    cudaStream_t sb = s, sf = s;
+    if (fk) {
+        cudaEventRecord(fk->ev_fork, s);
+        cudaStreamWaitEvent(fk->s_block, fk->ev_fork, 0);
+        cudaStreamWaitEvent(fk->s_fold, fk->ev_fork, 0);
+        sb = fk->s_block;
+        sf = fk->s_fold;
+    }
+    k_fin_fold_large<<<cap((int64_t)sm_count * 4 * FIN_GRID, (maxw + FL_WARPS - 1) / FL_WARPS), FL_WARPS * 32, 0, sf>>>(io, p);
+    k_fin_sort_block<<<cap((int64_t)sm_count * 4 * FIN_GRID, maxw), FB_THREADS, FB_BYTES, sb>>>(io, p);
     k_fin_sort_warp<<<cap((int64_t)sm_count * 8 * FIN_GRID, (maxw + FW_WARPS - 1) / FW_WARPS), FW_WARPS * 32, wsm, s>>>(io, p);
-    k_fin_sort_block<<<cap((int64_t)sm_count * 4 * FIN_GRID, maxw), FB_THREADS, FB_BYTES, s>>>(io, p);
-    k_fin_fold_large<<<cap((int64_t)sm_count * 4 * FIN_GRID, (maxw + FL_WARPS - 1) / FL_WARPS), FL_WARPS * 32, 0, s>>>(io, p);
+    if (fk) {
+        cudaEventRecord(fk->ev_block, sb);
+        cudaStreamWaitEvent(s, fk->ev_block, 0);
+    }
     k_fin_chain<<<cap((int64_t)sm_count * 8 * FIN_GRID_CHAIN, (maxw + CH_WARPS - 1) / CH_WARPS), CH_WARPS * 32, 0, s>>>(io, p);
     k_fin_kept<<<cap((int64_t)sm_count * 8 * FIN_GRID, (maxw + FK_WARPS - 1) / FK_WARPS), FK_WARPS * 32, 0, s>>>(io, p);
+    if (fk) {
+        cudaEventRecord(fk->ev_fold, sf);
+        cudaStreamWaitEvent(s, fk->ev_fold, 0);
+    }
     k_stats<<<(unsigned)((io.E * 32 + 255) / 256), 256, 0, s>>>(io, p);
 }
 

@@ -31,6 +31,7 @@ struct ReduceIO {
     double2 *tuv;        // the touching members' sorted (u, v), compacted (rows) ...
     int32_t *tpos;       // ... and their positions in the sorted rows
     double *tu, *tv;     // second sort buffer of patches too large for shared memory
+    double *fw;          // member weights of k_fin_fold_large's patches above FL_W (it runs beside the sort)
     int32_t *tk;
     int32_t *hj;         // [4 rows] chain stacks: sorted positions (the hull output) ...
     double *hu, *hv;     // ... and their (u, v) (backing store of the shared-memory window)
@@ -53,6 +54,13 @@ struct ReduceIO {
 };
 
 void launch_reduce(const ReduceIO &io, const ReduceParams &p, int64_t max_batch, cudaStream_t s);
-void launch_finalize(const ReduceIO &io, const ReduceParams &p, int sm_count, cudaStream_t s);
+// Side streams and events of a plan: launch_finalize forks its independent kernels
+// onto them (concurrent graph branches when the collide is captured).
+struct FinFork {
+    cudaStream_t s_block, s_fold;
+    cudaEvent_t ev_fork, ev_block, ev_fold;
+};
+void launch_finalize(const ReduceIO &io, const ReduceParams &p, int sm_count, cudaStream_t s,
+                     const FinFork *fk = nullptr);
 
 }  // namespace cs
