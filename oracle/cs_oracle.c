@@ -643,7 +643,7 @@ static int og_reduce_labels(const og_cands *c, const og_params *p, int32_t *labe
 }
 
 /* numpy stable argsort of -depths (NaN last). */
-static const double *og_sort_depths;
+static _Thread_local const double *og_sort_depths; /* per thread: envs run in parallel (OpenMP) */
 static int og_negdepth_cmp(const void *pa, const void *pb) {
     int64_t a = *(const int64_t *)pa, b = *(const int64_t *)pb;
     double x = -og_sort_depths[a], y = -og_sort_depths[b];
@@ -834,4 +834,78 @@ int og_num_threads(void) {
 #else
     return 1;
 #endif
+}
+
+/* Per-env digest of EVERY output of generate + reduce (test infrastructure: the GPU
+ * suite compares the batched collide's outputs of all envs against it). The stream
+ * of 64-bit words of an env, in order:
+ *   n_cand; points[3c], normals[3c], depths[c] (double bits), faces[c];
+ *   n_patch; per patch: rep[3], nkept, kept candidate indices[nkept], n_members,
+ *   members[n_members], wsum, wp[3], wn[3], wt[3], area, max_depth
+ * and digest = sum_i (w_i ^ 0x9e3779b97f4a7c15) * (2 i + 1) mod 2^64 (tests/conftest.py:
+ * env_digest computes the same from the GPU outputs). */
+typedef struct {
+    uint64_t h, i;
+} og_dig;
+static inline void og_dig_u(og_dig *d, uint64_t w) {
+    d->h += (w ^ 0x9e3779b97f4a7c15ull) * (2 * d->i + 1);
+    d->i++;
+}
+static inline void og_dig_d(og_dig *d, double x) {
+    uint64_t w;
+    memcpy(&w, &x, 8);
+    og_dig_u(d, w);
+}
+
+void og_collide_digest(int64_t E, const float *values, int64_t nx, int64_t ny, int64_t nz, double ox, double oy,
+                       double oz, double voxel, const double *aabb_lo, const double *aabb_hi, const double *verts,
+                       int64_t nv, const int32_t *tris, int64_t nt, const double *sdf7, const double *mesh7,
+                       const double *cd, int max_patches, int per_patch_cap, double cone, int batch_size,
+                       uint64_t *digest) {
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t e = 0; e < E; ++e) {
+        size_t cap = (size_t)(nt > 0 ? nt : 1);
+        double *P = (double *)malloc(sizeof(double) * 3 * cap), *Nn = (double *)malloc(sizeof(double) * 3 * cap);
+        double *D = (double *)malloc(sizeof(double) * cap);
+        int64_t *F = (int64_t *)malloc(sizeof(int64_t) * cap);
+        int64_t c = og_generate_contacts(values, nx, ny, nz, ox, oy, oz, voxel, aabb_lo, aabb_hi, verts, nv, tris, nt,
+                                         sdf7 + 7 * e, mesh7 + 7 * e, cd[e], P, Nn, D, F, 0);
+        if (c < 0) c = 0;
+        og_dig d = {0, 0};
+        og_dig_u(&d, (uint64_t)c);
+        for (int64_t i = 0; i < 3 * c; ++i) og_dig_d(&d, P[i]);
+        for (int64_t i = 0; i < 3 * c; ++i) og_dig_d(&d, Nn[i]);
+        for (int64_t i = 0; i < c; ++i) og_dig_d(&d, D[i]);
+        for (int64_t i = 0; i < c; ++i) og_dig_u(&d, (uint64_t)F[i]);
+        int64_t np_ = 0;
+        if (c > 0) {
+            size_t N = (size_t)max_patches, K = (size_t)per_patch_cap;
+            double *rep = malloc(sizeof(double) * 3 * N), *ws = malloc(sizeof(double) * N), *wp = malloc(sizeof(double) * 3 * N);
+            double *wn = malloc(sizeof(double) * 3 * N), *wt = malloc(sizeof(double) * 3 * N), *ar = malloc(sizeof(double) * N);
+            double *md = malloc(sizeof(double) * N);
+            int64_t *nkp = malloc(sizeof(int64_t) * N), *kept = malloc(sizeof(int64_t) * N * K);
+            int64_t *moff = malloc(sizeof(int64_t) * (N + 1)), *mem = malloc(sizeof(int64_t) * (size_t)c);
+            np_ = og_reduce_contacts(c, P, Nn, D, max_patches, per_patch_cap, cone, -cd[e], 1, batch_size, rep, nkp,
+                                     kept, moff, mem, ws, wp, wn, wt, ar, md);
+            og_dig_u(&d, (uint64_t)np_);
+            for (int64_t q = 0; q < np_; ++q) {
+                for (int k = 0; k < 3; ++k) og_dig_d(&d, rep[3 * q + k]);
+                og_dig_u(&d, (uint64_t)nkp[q]);
+                for (int64_t k = 0; k < nkp[q]; ++k) og_dig_u(&d, (uint64_t)kept[q * K + k]);
+                og_dig_u(&d, (uint64_t)(moff[q + 1] - moff[q]));
+                for (int64_t k = moff[q]; k < moff[q + 1]; ++k) og_dig_u(&d, (uint64_t)mem[k]);
+                og_dig_d(&d, ws[q]);
+                for (int k = 0; k < 3; ++k) og_dig_d(&d, wp[3 * q + k]);
+                for (int k = 0; k < 3; ++k) og_dig_d(&d, wn[3 * q + k]);
+                for (int k = 0; k < 3; ++k) og_dig_d(&d, wt[3 * q + k]);
+                og_dig_d(&d, ar[q]);
+                og_dig_d(&d, md[q]);
+            }
+            free(rep); free(ws); free(wp); free(wn); free(wt); free(ar); free(md); free(nkp); free(kept); free(moff); free(mem);
+        } else {
+            og_dig_u(&d, 0);
+        }
+        digest[e] = d.h;
+        free(P); free(Nn); free(D); free(F);
+    }
 }

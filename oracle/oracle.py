@@ -217,6 +217,24 @@ def collide_batched(grid: Grid, vertices, triangles, sdf_pose7, mesh_pose7, cont
     return np.array([[s.n_cand, s.n_patch, s.n_kept, s.max_depth] for s in stats], dtype=np.float64)
 
 
+def collide_digest(grid: Grid, vertices, triangles, sdf_pose7, mesh_pose7, contact_distance, max_patches=128,
+                   per_patch_cap=6, normal_cone_cos=float(np.cos(np.radians(20.0))), batch_size=1024) -> np.ndarray:
+    """Per env digest (uint64) of every output of generate_contacts + reduce_contacts
+    (og_collide_digest; the word stream is documented there), OpenMP over envs."""
+    s7 = _f64(sdf_pose7).reshape(-1, 7)
+    m7 = _f64(mesh_pose7).reshape(-1, 7)
+    E = len(m7)
+    cd = _f64(np.broadcast_to(np.asarray(contact_distance, dtype=np.float64), (E,)))
+    v = _f64(vertices)
+    t = np.ascontiguousarray(triangles, dtype=np.int32)
+    out = np.zeros(E, np.uint64)
+    lib().og_collide_digest(ctypes.c_int64(E), *grid._args(), _p(grid.aabb_lo), _p(grid.aabb_hi), _p(v),
+                            ctypes.c_int64(len(v)), _p(t), ctypes.c_int64(len(t)), _p(s7), _p(m7), _p(cd),
+                            ctypes.c_int(max_patches), ctypes.c_int(per_patch_cap), ctypes.c_double(normal_cone_cos),
+                            ctypes.c_int(batch_size), _p(out))
+    return out
+
+
 def num_threads() -> int:
     return int(lib().og_num_threads())
 

@@ -190,6 +190,9 @@ struct cs_plan {
     FinFork fork{};        // side streams of the finalize's concurrent branches (created lazily)
     bool fork_ready = false;
     const FinFork *get_fork() {
+#ifdef CS_NO_FORK
+        return nullptr;
+#endif
         if (!fork_ready) {
             if (cudaStreamCreateWithFlags(&fork.s_block, cudaStreamNonBlocking) != cudaSuccess ||
                 cudaStreamCreateWithFlags(&fork.s_fold, cudaStreamNonBlocking) != cudaSuccess ||

@@ -3,7 +3,7 @@
 cd $GRAFT_REPO_ROOT
 export PATH=/usr/local/cuda/bin:$PATH
 rm -f gpurun_out/variants.txt
-timeout 900 python -m pytest tests -m gpu -q -x --timeout 600 -p no:cacheprovider ${TESTS:-} > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
+timeout 900 python -m pytest tests -m gpu -q -x --timeout 600 -p no:cacheprovider -k "${KEXPR:-}" > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
 timeout 600 python bench.py --steps 20 --warmup 5 --quick > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 echo "main $(grep -o '"ms_per_step": [0-9.]*' gpurun_out/bench.log | head -1) $(grep -o '"phase_ms": {[^}]*}' gpurun_out/bench.log)" >> gpurun_out/variants.txt
 for d in _variants/*/; do

@@ -45,6 +45,12 @@ def synth():
 
 
 @pytest.fixture(scope="session")
+def merge():
+    """Reduction cases that take _add_patch's merge branch (tests/golden/make_merge_golden.py)."""
+    return golden("red_merge.npz")
+
+
+@pytest.fixture(scope="session")
 def kat():
     return golden("kat.npz")
 
@@ -109,3 +115,53 @@ def assert_same(got: dict, ref, prefix: str, keys, label: str = "") -> None:
             bad = np.argwhere(~same)
             raise AssertionError(f"{label}{k}: {len(bad)} mismatches, first at {bad[:3].tolist()}: "
                                  f"{a[tuple(bad[0])]!r} vs {b[tuple(bad[0])]!r}")
+
+
+_DIG_K = np.uint64(0x9E3779B97F4A7C15)
+
+
+def _digest_words(words: np.ndarray) -> int:
+    w = np.ascontiguousarray(words).view(np.uint64)
+    i = np.arange(len(w), dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        return int(np.sum((w ^ _DIG_K) * (np.uint64(2) * i + np.uint64(1)), dtype=np.uint64))
+
+
+def digest_env(P, Nn, D, F, rep, nk, kept, moff, mem, ws, wp, wn, wt, ar, md) -> int:
+    """One env's digest from its candidate arrays (C rows) and patch arrays (q patches;
+    kept/members as candidate indices): the word stream of og_collide_digest."""
+    u = lambda a: np.asarray(a, dtype=np.int64).view(np.uint64).ravel()  # noqa: E731
+    f = lambda a: np.asarray(a, dtype=np.float64).view(np.uint64).ravel()  # noqa: E731
+    c = len(D)
+    parts = [u([c]), f(P), f(Nn), f(D), u(F)]
+    q = len(nk) if c > 0 else 0
+    parts.append(u([q]))
+    for j in range(q):
+        m0, m1 = int(moff[j]), int(moff[j + 1])
+        parts += [f(rep[j]), u([nk[j]]), u(kept[j][: nk[j]]), u([m1 - m0]), u(mem[m0:m1]), f([ws[j]]), f(wp[j]),
+                  f(wn[j]), f(wt[j]), f([ar[j]]), f([md[j]])]
+    return _digest_words(np.concatenate(parts))
+
+
+def env_digests(plan) -> np.ndarray:
+    """Per env digest of every output of a collide (the word stream of the oracle's
+    og_collide_digest, oracle/cs_oracle.c): candidates, then per patch the normal,
+    kept candidates, members, aggregates, area and max depth."""
+    E = plan.n_envs
+    base = plan.cand_base.cpu().numpy()
+    nc = plan.n_cand.cpu().numpy().astype(np.int64)
+    npch = plan.n_patch.cpu().numpy().astype(np.int64)
+    P, Nn, D = plan.cand_point.cpu().numpy(), plan.cand_normal.cpu().numpy(), plan.cand_depth.cpu().numpy()
+    F = plan.cand_face.cpu().numpy()
+    rep, nk, kc = plan.patch_normal.cpu().numpy(), plan.patch_nkept.cpu().numpy(), plan.kept_cand.cpu().numpy()
+    mo, mem = plan.member_offsets.cpu().numpy(), plan.members.cpu().numpy()
+    ws, wp, wn, wt = (plan.w_sum.cpu().numpy(), plan.wp_sum.cpu().numpy(), plan.wn_sum.cpu().numpy(),
+                      plan.wt_sum.cpu().numpy())
+    ar, md = plan.area.cpu().numpy(), plan.max_depth.cpu().numpy()
+    out = np.zeros(E, np.uint64)
+    for e in range(E):
+        b, c, q = int(base[e]), int(nc[e]), int(npch[e])
+        out[e] = digest_env(P[b:b + c], Nn[b:b + c], D[b:b + c], F[b:b + c], rep[e, :q], nk[e, :q], kc[e, :q],
+                            mo[e, : q + 1], mem[b:b + c], ws[e, :q], wp[e, :q], wn[e, :q], wt[e, :q], ar[e, :q],
+                            md[e, :q])
+    return out

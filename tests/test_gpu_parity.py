@@ -10,7 +10,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import CS_KEYS, GOLDEN, PATCH_KEYS, assert_same, pack_patch_list
+from conftest import CS_KEYS, GOLDEN, PATCH_KEYS, assert_same, env_digests, pack_patch_list
 
 pytestmark = pytest.mark.gpu
 
@@ -115,6 +115,18 @@ def test_reduce_contacts_synthetic(P, synth):
         assert_same(pack_patch_list(patches, int(K)), synth, pre + "pt_", PATCH_KEYS, f"case {c} ")
 
 
+def test_reduce_contacts_merge_branch(P, merge):
+    """The merge branch of _add_patch (reduction.py:99-105): gemm/gemv cosines one ulp apart at the cone."""
+    for c in merge["cases"]:
+        pre = f"c{c}_"
+        N, K, cone, md, bs = merge[pre + "params"]
+        cs = P.ContactSet(merge[pre + "cs_points"], merge[pre + "cs_normals"], merge[pre + "cs_depths"],
+                          merge[pre + "cs_faces"], 0, 1)
+        rp = P.ReductionParams(int(N), int(K), float(cone), None if np.isnan(md) else float(md), int(bs))
+        patches = P.reduce_contacts(cs, rp)
+        assert_same(pack_patch_list(patches, int(K)), merge, pre + "pt_", PATCH_KEYS, f"case {c} ")
+
+
 def test_batched_collide_r64(P, grid64, nut, gen64):
     """All six golden envs (two with a moved SDF pose) in one collide call."""
     envs = list(gen64["envs"])
@@ -173,8 +185,9 @@ def test_batched_collide_r256_vs_golden(P, bolt, nut, gen256):
 
 
 def test_full_size_1024_envs_vs_oracle(P):
-    """Config 2 at full size: every env's stats against the oracle, a sample of
-    envs field by field, determinism across runs, and Algorithm-1 invariants."""
+    """Config 2 at full size: every output field of all 1024 envs against the oracle
+    (per-env digests), a sample of envs field by field, determinism across runs, and
+    Algorithm-1 invariants."""
     from oracle import oracle as O
     from paper_2205_03532_b200.scenes import m16_workload
 
@@ -191,8 +204,14 @@ def test_full_size_1024_envs_vs_oracle(P):
     assert np.array_equal(n_patch, ost[:, 1].astype(np.int64))
     assert np.array_equal(stats[:, 2], ost[:, 2].astype(np.float32))
     assert np.array_equal(stats[:, 3], ost[:, 3].astype(np.float32))
+    # EVERY output field of EVERY env, bit for bit: per-env digests of the candidates,
+    # patch normals, kept candidates, members, aggregates, areas and max depths
+    dig = env_digests(res.plan)
+    odig = O.collide_digest(og, nut.vertices, nut.triangles, w["sdf_pose"], w["mesh_pose"], w["cd"])
+    bad = np.nonzero(dig != odig)[0]
+    assert len(bad) == 0, f"{len(bad)} of {E} envs differ, first {bad[:8].tolist()}"
     rng = np.random.default_rng(7)
-    for e in rng.choice(E, size=12, replace=False):
+    for e in rng.choice(E, size=4, replace=False):
         cs = res.contact_set(int(e))
         ref = O.generate_contacts(og, nut.vertices, nut.triangles, w["sdf_pose"][e], w["mesh_pose"][e], float(w["cd"][e]))
         assert np.array_equal(cs.points, ref["points"]) and np.array_equal(cs.normals, ref["normals"])
@@ -307,8 +326,8 @@ def test_reduce_deep_hull_stacks(P):
 def test_config3_suite_4096_envs_vs_oracle(P):
     """Config 3 at full size: 4096 envs over pegs 4/8/12/16 mm in
     tight holes and M4..M20 nuts on bolts (9 assets, res-256 grids), one collide
-    call with per-env handles; every env's stats against the oracle, two envs per
-    asset field by field."""
+    call with per-env handles; every output field of all 4096 envs against the oracle
+    (per-env digests), two envs per asset field by field."""
     from oracle import oracle as O
     from paper_2205_03532_b200.scenes import suite_workload
 
@@ -321,6 +340,7 @@ def test_config3_suite_4096_envs_vs_oracle(P):
     n_cand = res.n_cand.cpu().numpy()
     n_patch = res.n_patch.cpu().numpy()
     stats = res.stats.cpu().numpy()
+    dig = env_digests(res.plan)
     rng = np.random.default_rng(5)
     for k, a in enumerate(A):
         idx = np.nonzero(asset == k)[0]
@@ -333,6 +353,10 @@ def test_config3_suite_4096_envs_vs_oracle(P):
         assert np.array_equal(stats[idx, 2], ost[:, 2].astype(np.float32)), a["name"]
         assert np.array_equal(stats[idx, 3], ost[:, 3].astype(np.float32)), a["name"]
         assert (n_cand[idx] > 0).mean() > 0.5, a["name"]  # the poses engage the parts
+        # every output field of every env of the asset, bit for bit (per-env digests)
+        odig = O.collide_digest(og, m.vertices, m.triangles, w["sdf_pose"][idx], w["mesh_pose"][idx], w["cd"][idx])
+        bad = np.nonzero(dig[idx] != odig)[0]
+        assert len(bad) == 0, f"{a['name']}: {len(bad)} of {len(idx)} envs differ, first {idx[bad[:8]].tolist()}"
         for e in rng.choice(idx, size=2, replace=False):
             e = int(e)
             ref = O.generate_contacts(og, m.vertices, m.triangles, w["sdf_pose"][e], w["mesh_pose"][e],

@@ -59,6 +59,18 @@ def test_reduce_contacts_synthetic(synth):
         assert_same(r, synth, pre + "pt_", PATCH_KEYS, f"case {c} ")
 
 
+def test_reduce_contacts_merge_branch(merge):
+    """The merge branch of _add_patch (reduction.py:99-105): the reference took it in every case."""
+    for c in merge["cases"]:
+        assert int(merge[f"c{c}_merges"]) >= 1
+        pre = f"c{c}_"
+        N, K, cone, md, bs = merge[pre + "params"]
+        r = O.reduce_contacts(merge[pre + "cs_points"], merge[pre + "cs_normals"], merge[pre + "cs_depths"],
+                              merge[pre + "cs_faces"], max_patches=int(N), per_patch_cap=int(K), normal_cone_cos=cone,
+                              min_depth=None if np.isnan(md) else md, batch_size=int(bs))
+        assert_same(r, merge, pre + "pt_", PATCH_KEYS, f"case {c} ")
+
+
 def test_sphere_plane_known_answers(kat):
     g = O.Grid(kat["sphere_values"], kat["sphere_dims"], kat["sphere_origin"], float(kat["sphere_voxel"]),
                kat["sphere_aabb_lo"], kat["sphere_aabb_hi"])
@@ -96,3 +108,22 @@ def test_batched_collide_stats(meshes, grid64_npz, gen64):
         assert row[0] == len(gen64[f"e{e}_cs_depths"])
         assert row[1] == len(gen64[f"e{e}_pt_nkept"])
         assert row[2] == gen64[f"e{e}_pt_nkept"].sum()
+
+
+def test_env_digest_matches_oracle_word_stream(meshes, grid64_npz, gen64):
+    """tests/conftest.py:digest_env (applied to the GPU outputs by the full-size parity
+    tests) and the oracle's og_collide_digest hash the same word stream."""
+    from conftest import digest_env
+
+    og = O.Grid.from_npz(grid64_npz)
+    cd = float(gen64["cd"])
+    envs = list(gen64["envs"])
+    sp = np.stack([gen64[f"e{e}_sdf_pose"] for e in envs])
+    mp = np.stack([gen64[f"e{e}_mesh_pose"] for e in envs])
+    ref = O.collide_digest(og, meshes["nut_v"], meshes["nut_t"], sp, mp, cd)
+    for i in range(len(envs)):
+        g = O.generate_contacts(og, meshes["nut_v"], meshes["nut_t"], sp[i], mp[i], cd)
+        r = O.reduce_contacts(g["points"], g["normals"], g["depths"], g["faces"], min_depth=-cd)
+        d = digest_env(g["points"], g["normals"], g["depths"], g["faces"], r["rep"], r["nkept"], r["kept"],
+                       r["member_offsets"], r["members"], r["wsum"], r["wp"], r["wn"], r["wt"], r["area"], r["maxd"])
+        assert d == int(ref[i]), i
