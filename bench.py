@@ -34,9 +34,10 @@ sys.path.insert(0, ROOT)
 METRIC = "SDF contact queries/s & collide-step ms, 1024 nut-bolt envs, 1/2/4/8 B200"
 UNIT = "queries/s"
 PAPER_QPS = 1024 * 17798 / 11e-3  # PAPER.md:227,584 (A5000, whole contact-handling step), derived
-# k_env_xf, k_face_prep, k_pgd_grad x2, k_pgd_first, k_pgd_rest, k_compact, k_reduce, k_patch_off,
-# k_fin_sort_warp, k_fin_sort_block, k_fin_chain, k_fin_kept, k_stats
-LAUNCHES_PER_STEP = 15
+# per collide step: k_env_xf, k_face_prep, k_pgd_grad x2, k_pgd_first,
+# k_pgd_rest, k_compact, k_reduce, k_patch_off, k_patch_env, k_fin_fold_large, k_fin_sort_block,
+# k_fin_sort_warp, k_fin_chain, k_fin_kept, k_stats
+LAUNCHES_PER_STEP = 16
 
 
 def parse():
@@ -45,16 +46,17 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--envs", type=int, default=1024, help="envs per GPU")
+    ap.add_argument("--envs", type=int, default=1024, help="envs per GPU (weak scaling)")
+    ap.add_argument("--envs-total", type=int, default=0,
+                    help="envs over all GPUs (strong scaling, e.g. 1024 over 8 = 128 per GPU); overrides --envs")
     ap.add_argument("--res", type=int, default=256)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--l2-pin", action="store_true",
                     help="pin the grid in L2 (persisting window); measured slower: the carve-out costs the step's "
                          "staging traffic more than the grid gathers gain")
     ap.add_argument("--no-flush", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=256, help="envs in the CPU-baseline sample")
-    ap.add_argument("--ref-sample", type=int, default=32, help="envs per reference-arm step")
     ap.add_argument("--quick", action="store_true", help="skip e2e / cpu baseline (profiling runs)")
+    ap.add_argument("--dry-run", action="store_true", help="launcher + sharding + stats all-gather only (no GPU)")
     return ap.parse_args()
 
 
@@ -126,14 +128,21 @@ def ncu_traffic():
     return ncu_summary().get("dram_bytes_per_launch")
 
 
-def cpu_baseline(w, sample: int, repeats: int = 2) -> dict:
-    from oracle import oracle as O  # the checker, timed here as the reported CPU baseline
+def cpu_baseline(w, repeats: int = 2, ref_envs_b: int = 0, ref_envs_a: int = 8) -> dict:
+    """The CPU baselines on this box's host cores, in the same run (reported, not targets):
+    * the oracle port (oracle/cs_oracle.c: the reference restated in C, OpenMP over
+      envs on every host thread) over the WHOLE workload, best of `repeats`;
+    * the reference itself (baseline/_ref: the unmodified reference package, numba +
+      numpy), Modes A and B of BASELINE.md §2 on bounded env samples.
+    The headline value is the reference's better mode when it is installed (kind
+    "reference"), else the port's."""
+    from oracle import oracle as O  # the checker, timed here as a reported CPU baseline
 
     grid = w["grid"]
     og = O.Grid(grid.values, grid.dims, grid.origin, grid.voxel_size, *grid.mesh_aabb)
     nut = w["nut"]
-    n = min(sample, len(w["mesh_pose"]))
-    sp, mp, cd = w["sdf_pose"][:n], w["mesh_pose"][:n], w["cd"][:n]
+    E, F = len(w["mesh_pose"]), len(nut.triangles)
+    sp, mp, cd = w["sdf_pose"], w["mesh_pose"], w["cd"]
     O.collide_batched(og, nut.vertices, nut.triangles, sp[:2], mp[:2], cd[:2])  # warm
     best = None
     for _ in range(repeats):
@@ -141,78 +150,159 @@ def cpu_baseline(w, sample: int, repeats: int = 2) -> dict:
         O.collide_batched(og, nut.vertices, nut.triangles, sp, mp, cd)
         dt = time.perf_counter() - t0
         best = dt if best is None else min(best, dt)
-    return {"value": n * len(nut.triangles) / best, "unit": UNIT, "cores": O.num_threads(), "kind": "port",
-            "sample": f"{n} envs of the same workload (generate + reduce per env, OpenMP over envs), best of {repeats}",
-            "ms_per_1024_envs": best / n * 1024 * 1e3}
+    port = {"value": E * F / best, "unit": UNIT, "cores": O.num_threads(), "kind": "port",
+            "sample": f"the whole {E}-env workload per run (generate + reduce per env, OpenMP over envs), best of "
+                      f"{repeats}", "ms_per_1024_envs": best / E * 1024 * 1e3}
+    sys.path.insert(0, os.path.join(ROOT, "baseline"))
+    import reference_cpu as R
+
+    why = R.available()
+    if why is not None:
+        return dict(port, reference_unavailable=why)
+    lo, hi = grid.mesh_aabb
+    assets = R.assets_from_arrays(grid.values, grid.dims, grid.origin, grid.voxel_size, lo, hi, nut.vertices,
+                                  nut.triangles, len(w["bolt"].triangles))
+    nb = ref_envs_b or 4 * R.cores()
+    ref = R.measure(assets, sp, mp, F, min(nb, E), min(ref_envs_a, E))
+    return {"value": ref["value"], "unit": UNIT, "cores": ref["cores"], "kind": "reference",
+            "sample": f"the reference package (baseline/_ref, numba + numpy) called per env as Scene._collect_contacts "
+                      f"does; better of Mode A ({ref['mode_a']['envs']} envs, serial loop, numba threads = cores) and "
+                      f"Mode B ({ref['mode_b']['envs']} envs, {ref['mode_b']['procs']} processes x 1 thread), "
+                      f"BASELINE.md §2; first call per process discarded",
+            "cpu_model": ref["cpu_model"], "best_mode": ref["best_mode"], "ms_per_1024_envs": ref["ms_per_1024_envs"],
+            "mode_a": ref["mode_a"], "mode_b": ref["mode_b"], "port": port}
 
 
 def run_reference(args):
+    """`--impl reference`: the reference's CPU path on this box's host cores, rank 0 only.
+    The timed steps are WHOLE steps of the workload (every env of every rank: N x --envs),
+    each one oracle-port call over all envs on all host threads (oracle/cs_oracle.c, the
+    reference restated in C and pinned to it bit for bit; the reference itself is Python +
+    numba, so there is no compiled reference to build). Beside it, the reference package
+    itself (baseline/_ref) in BASELINE.md §2's Modes A and B on bounded samples. Nothing
+    here loads this repo's CUDA library: the assets come from the reference's own
+    generators (baseline/_ref)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     from oracle import oracle as O
-    from paper_2205_03532_b200.geometry.mesh import TriMesh
-    from paper_2205_03532_b200.scenes import m16_meshes, nut_poses
-    from paper_2205_03532_b200.geometry.fasteners import bolt_thread_base_z
 
-    # Asset preparation is outside the timed region: the bolt grid comes from the
-    # GPU arm's cache on this box, else from the GPU SDF generator (bit-identical to
-    # the reference's generate_sdf, tests/test_gpu_parity.py). Only generate +
-    # reduce per env is timed, on the host cores.
-    nut, bolt, bolt_spec = m16_meshes(80)
-    grid = _reference_grid(bolt, args.res)
-    E = args.envs * world
-    poses = nut_poses(E, args.seed, bolt_spec.pitch, float(bolt_thread_base_z(bolt_spec)))
-    og = O.Grid(grid["values"], grid["dims"], grid["origin"], grid["voxel"], grid["lo"], grid["hi"])
-    S = min(args.ref_sample, E)
+    sys.path.insert(0, os.path.join(ROOT, "baseline"))
+    import reference_cpu as R
+
+    why = R.available()
+    E = args.envs_total if args.envs_total else args.envs * args.gpus
+    t_setup = time.perf_counter()
+    if why is None:
+        assets = R.build_assets(args.res)
+        grid, nut = assets["grid"], assets["nut"]
+        poses = R.nut_poses(E, args.seed, assets["pitch"], assets["z0"])
+        g = {"values": grid.values, "dims": np.array(grid.dims), "origin": grid.origin, "voxel": grid.voxel_size,
+             "lo": grid.mesh_aabb[0], "hi": grid.mesh_aabb[1]}
+        nut_v, nut_t = nut.vertices, nut.triangles
+        grid_source = "the reference's generate_sdf (baseline/_ref), outside the timed region"
+    else:
+        print(json.dumps({"impl": "reference", "unavailable": f"the reference package is not installed: {why}"}))
+        return
+    setup_s = time.perf_counter() - t_setup
+    og = O.Grid(g["values"], g["dims"], g["origin"], g["voxel"], g["lo"], g["hi"])
     sp = np.tile([0, 0, 0, 1.0, 0, 0, 0], (E, 1))
-    cd = np.full(E, 2.0 * grid["voxel"])
+    cd = np.full(E, 2.0 * g["voxel"])
+    F = len(nut_t)
     times = []
-    rng = np.random.default_rng(1)
     for k in range(args.warmup + args.steps):
-        idx = rng.choice(E, size=S, replace=False)
         t0 = time.perf_counter()
-        O.collide_batched(og, nut.vertices, nut.triangles, sp[idx], poses[idx], cd[idx])
+        O.collide_batched(og, nut_v, nut_t, sp, poses, cd)
         if k >= args.warmup:
             times.append(time.perf_counter() - t0)
     step = float(np.mean(times))
-    value = S * len(nut.triangles) / step
+    value = E * F / step
+    ref = R.measure(assets, sp, poses, F, min(4 * R.cores(), E), min(8, E))
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": step * 1e3 * E / S, "higher_is_better": True, "scaling": "weak",
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": value / PAPER_QPS, "dtype": "f64", "data": "synthetic (seeded SURVEY §8(d) poses)",
-        "config": _config(args, E, len(nut.triangles), grid["dims"]),
+        "config": _config(args, E, F, g["dims"]),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": O.num_threads(), "kind": "port",
-                         "sample": f"{S} random envs per step of the {E}-env workload; ms_per_step scaled to {E} envs"},
+                         "sample": f"whole {E}-env steps (every env of the workload each step), oracle port "
+                                   f"(OpenMP over envs)", "cpu_model": R.cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_package": {"value": ref["value"], "unit": UNIT, "cores": ref["cores"], "cpu_model": ref["cpu_model"],
+                              "best_mode": ref["best_mode"], "ms_per_1024_envs": ref["ms_per_1024_envs"],
+                              "mode_a": ref["mode_a"], "mode_b": ref["mode_b"],
+                              "note": "the unmodified reference package (baseline/_ref), BASELINE.md §2 modes, bounded "
+                                      "env samples"},
+        "grid_source": grid_source, "setup_s": setup_s,
     }
     print(json.dumps(line), flush=True)
 
 
-def _reference_grid(bolt, res):
-    """Bolt grid for the CPU arm: cached next to the repo by the GPU arm when it ran
-    on this box; otherwise generated by the GPU generator if a GPU is present."""
-    cache = os.path.join(ROOT, ".bench_cache", f"bolt_r{res}.npz")
-    if os.path.exists(cache):
-        d = np.load(cache)
-        return {k: d[k] for k in d.files}
-    from paper_2205_03532_b200.sdf.grid import SdfResolutionSpec, generate_sdf
+def _config(args, E, F, dims, world=None):
+    world = world or args.gpus
+    per = f"{args.envs} M16 nut-on-bolt envs per GPU" if not args.envs_total else \
+        f"{E} M16 nut-on-bolt envs over {world} GPU(s) ({E // world} per GPU)"
+    return {
+        "workload": f"{per} (config 2), bolt SDF res {args.res} "
+                    f"{tuple(int(d) for d in dims)}, nut mesh {F} faces, seeded poses (seed {args.seed})",
+        "envs_total": int(E), "envs_per_gpu": int(E // world), "mesh_faces": int(F), "sdf_dims": [int(d) for d in dims],
+        "reduction": "ReductionParams() defaults, min_depth = -cd (Scene semantics)",
+        "l2": "flushed between timed steps (256 MiB write, untimed)" if not args.no_flush else "not flushed",
+        "l2_pin": bool(args.l2_pin), "parallelism": f"env shards, {world} rank(s) (one process per GPU, NCCL)",
+    }
 
-    g = generate_sdf(bolt, SdfResolutionSpec(res, 4))
-    out = {"values": g.values, "dims": np.array(g.dims), "origin": g.origin, "voxel": g.voxel_size,
-           "lo": g.mesh_aabb[0], "hi": g.mesh_aabb[1]}
+
+def device_peaks() -> dict:
+    """Roofline denominators measured live on this GPU (cs_bench_gather): random 32-byte
+    sector gathers from a 32 MiB L2-resident buffer through L2 only, through __ldg and
+    through tld4 on a layered texture, and a streaming read of 4 GiB (HBM)."""
+    import ctypes
+
+    from paper_2205_03532_b200 import _native
+
+    lib = _native.lib()
+    out = {}
+    for mode, name, nbytes, iters in ((0, "l2_gather_gbs", 32 << 20, 20), (1, "ldg_gather_gbs", 32 << 20, 20),
+                                      (2, "tex_gather_gbs", 32 << 20, 20), (3, "hbm_stream_gbs", 4 << 30, 10)):
+        v = ctypes.c_double(0.0)
+        rc = lib.cs_bench_gather(mode, nbytes, iters, ctypes.byref(v))
+        out[name] = float(v.value) if rc == 0 else None
+    out["how"] = ("cs_bench_gather (csrc/cs_bench.cu): every SM full, 64 random sector loads per thread; L2 peaks over a "
+                  "32 MiB buffer (L2-resident), HBM over 4 GiB")
     return out
 
 
-def _config(args, E, F, dims):
-    return {
-        "workload": f"{args.envs} M16 nut-on-bolt envs per GPU (config 2), bolt SDF res {args.res} "
-                    f"{tuple(int(d) for d in dims)}, nut mesh {F} faces, seeded poses (seed {args.seed})",
-        "envs_total": int(E), "envs_per_gpu": args.envs, "mesh_faces": int(F), "sdf_dims": [int(d) for d in dims],
-        "reduction": "ReductionParams() defaults, min_depth = -cd (Scene semantics)",
-        "l2": "flushed between timed steps (256 MiB write, untimed)" if not args.no_flush else "not flushed",
-        "l2_pin": bool(args.l2_pin), "parallelism": f"env shards, {args.gpus} rank(s)",
-    }
+def roofline(E, F, prep_ms, samples_prep, pgd_ms, samples_pgd, peaks, live) -> dict:
+    """k_face_prep (the step's largest launch) against HBM and L2: SURVEY §8(d) algorithmic
+    bytes (48 B per face query + 32 B per trilinear sample) over its live event time, and
+    the ncu capture's L2 / DRAM bytes over the capture's duration (profiles/k_face_prep_ncu.json)."""
+    alg = 48.0 * E * F + 32.0 * samples_prep
+    achieved = alg / (prep_ms * 1e-3) / 1e9
+    ncu = ncu_summary()
+    l2p = live.get("l2_gather_gbs")
+    out = {"kernel": "k_face_prep", "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+           "frac": achieved / peaks["hbm_gbs"], "traffic": ncu.get("dram_bytes_per_launch"),
+           "peak_source": peaks["source"], "alg_bytes_per_launch": alg, "samples_per_launch": samples_prep,
+           "basis": "48 B per face query (E x F) + 32 B per trilinear sample (8 float32 corners, SURVEY §8(d)); "
+                    "samples counted exactly by the counting build of k_face_prep",
+           "l2": {"peak_gather_gbs": l2p, "peak_ldg_gather_gbs": live.get("ldg_gather_gbs"),
+                  "peak_tex_gather_gbs": live.get("tex_gather_gbs"),
+                  "frac_alg": achieved / l2p if l2p else None,
+                  "ncu_lts_bytes_per_launch": ncu.get("lts_bytes_per_launch"), "ncu_lts_gbs": ncu.get("lts_gbs_ncu"),
+                  "frac_ncu": (ncu["lts_gbs_ncu"] / l2p) if (l2p and ncu.get("lts_gbs_ncu")) else None,
+                  "ncu_l1_hit_pct": ncu.get("l1_hit_pct"), "ncu_l2_hit_pct": ncu.get("l2_hit_pct")},
+           "hbm": {"peak_copy_gbs": peaks["hbm_gbs"], "peak_stream_gbs": live.get("hbm_stream_gbs"),
+                   "ncu_dram_gbs": ncu.get("dram_gbs_ncu"),
+                   "frac_ncu": (ncu["dram_gbs_ncu"] / peaks["hbm_gbs"]) if ncu.get("dram_gbs_ncu") else None},
+           "peaks_how": live.get("how"),
+           "limiter": {k: ncu.get(k) for k in ("fp64_pipe_pct", "issue_active_pct", "warps_active_pct", "l2_hit_pct")},
+           "limiter_note": "ncu: neither HBM, L2 nor the FP64 pipe saturates; the kernel is bound by dependent "
+                           "gather and barrier latency at the occupancy its float64 register footprint allows "
+                           "(DESIGN.md §4)",
+           "pgd_phase": {"kernels": "k_pgd_grad x2 + k_pgd_first + k_pgd_rest", "ms": pgd_ms,
+                         "alg_bytes": 32.0 * samples_pgd, "samples": samples_pgd,
+                         "achieved_gbs": 32.0 * samples_pgd / (pgd_ms * 1e-3) / 1e9,
+                         "basis": "32 B per trilinear sample"}}
+    return out
 
 
 def solver_leg(P, plan, w, lo, hi, E, steps, quick, cpu_sample=64):
@@ -294,30 +384,76 @@ def solver_leg(P, plan, w, lo, hi, E, steps, quick, cpu_sample=64):
     return out
 
 
+def launch_ranks(args) -> int:
+    """`python bench.py --gpus N` outside torchrun: re-launch this command as N ranks
+    (torch.distributed.run, one process per GPU, rendezvous on 127.0.0.1)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def dry_run(args, rank: int, world: int) -> None:
+    """`--dry-run`: the multi-GPU plumbing without a GPU (the CPU test of the launcher):
+    one rank per process (gloo), the env shards, and the per-step stats all-gather of
+    every rank's envs (StatsGather) with synthetic stats; rank 0 prints one JSON line."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2205_03532_b200.distributed import StatsGather
+    from paper_2205_03532_b200.scenes import shard_range
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    E_total = args.envs_total if args.envs_total else args.envs * world
+    lo, hi = shard_range(E_total, rank, world)
+    local = torch.stack([torch.arange(lo, hi, dtype=torch.float32) + c for c in (0, 1e4, 2e4, 0.5)], dim=1)
+    g = StatsGather(E_total)
+    for _ in range(args.steps):
+        g.launch(local)
+    got = g.result().numpy()
+    want = np.stack([np.arange(E_total) + c for c in (0, 1e4, 2e4, 0.5)], axis=1).astype(np.float32)
+    shards = [list(shard_range(E_total, r, world)) for r in range(world)]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "envs_total": E_total, "shards": shards,
+                          "scaling": "strong" if args.envs_total else "weak",
+                          "gather_ok": bool(np.array_equal(got, want))}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
+    rank, world, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(launch_ranks(args))
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     if args.impl == "reference":
         return run_reference(args)
+    if args.dry_run:
+        return dry_run(args, rank, world)
     import torch
     import torch.distributed as dist
 
     import paper_2205_03532_b200 as P
-    from paper_2205_03532_b200.distributed import gather_env_stats
-    from paper_2205_03532_b200.scenes import m16_workload
+    from paper_2205_03532_b200.distributed import StatsGather
+    from paper_2205_03532_b200.scenes import m16_workload, shard_range
 
-    rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    E = args.envs
-    w = m16_workload(E * world, seed=args.seed, resolution=args.res)
-    lo, hi = rank * E, (rank + 1) * E
+    # weak scaling: --envs per GPU; strong scaling: --envs-total over all GPUs
+    E_total = args.envs_total if args.envs_total else args.envs * world
+    lo, hi = shard_range(E_total, rank, world)
+    E = hi - lo
+    w = m16_workload(E_total, seed=args.seed, resolution=args.res)
     grid, nut = w["grid"], w["nut"]
     F = len(nut.triangles)
-    if rank == 0:
-        os.makedirs(os.path.join(ROOT, ".bench_cache"), exist_ok=True)
-        np.savez(os.path.join(ROOT, ".bench_cache", f"bolt_r{args.res}.npz"), values=grid.values, dims=np.array(grid.dims),
-                 origin=grid.origin, voxel=grid.voxel_size, lo=grid.mesh_aabb[0], hi=grid.mesh_aabb[1])
     h_sdf, h_mesh = P.register_sdf(grid), P.register_mesh(nut)
     plan = P.Plan([h_sdf] * E, [h_mesh] * E, P.ReductionParams())
     sp = torch.from_numpy(np.ascontiguousarray(w["sdf_pose"][lo:hi])).cuda()
@@ -327,15 +463,18 @@ def main():
     if args.l2_pin:
         P.pin_sdf_in_l2(grid, 1.0, stream)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    gather = StatsGather(E_total, device=torch.device("cuda", local))
 
     # exact sample count of one step (counting build, outside the timed region)
     samples_prep, samples_pgd = plan.count_samples(sp, mp, cd)
     for _ in range(max(3, args.warmup)):
         plan.collide(sp, mp, cd)
+        gather.launch(plan.stats, after=stream)
+    gather.wait(stream)
     torch.cuda.synchronize()
 
+    # eager steps (phase timing): collide, then the stats all-gather on its side stream
     plan.enable_timing(args.steps)
-    clocks = ClockSampler(local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -346,55 +485,62 @@ def main():
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         plan.collide(sp, mp, cd)
-        if world > 1:  # the step's one collective: the per-env stats all-gather
-            gather_env_stats(plan.stats, E * world)
         b.record(stream)
+        gather.launch(plan.stats, after=stream)
         outer.append((a, b))
+    gather.wait(stream)
     torch.cuda.synchronize()
+    phases = plan.read_timing(args.steps)
+    eager_ms = float(sum(a.elapsed_time(b) for a, b in outer)) / args.steps
+    eager = {"ms_per_step": eager_ms, "value": E_total * F / (eager_ms * 1e-3), "phase_ms": "see phase_ms"}
+
+    # the headline: the step replayed from a CUDA graph (launch gaps removed),
+    # L2 flushed between steps; the stats all-gather (N > 1: NCCL) is issued after each
+    # replay on its side stream, overlapping the next step, and the last one's tail is
+    # timed (it ends the job)
+    gs = torch.cuda.Stream()
+    gs.wait_stream(stream)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=gs):
+        plan.collide(sp, mp, cd, stream=gs)
+    graph.replay()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
     if world > 1:
         dist.barrier()
+    torch.cuda.synchronize()
+    g_ev = []
+    for _ in range(args.steps):
+        if not args.no_flush:
+            flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        graph.replay()
+        b.record(stream)
+        gather.launch(plan.stats, after=stream)
+        g_ev.append((a, b))
+    gather.wait(stream)
+    tail = torch.cuda.Event(enable_timing=True)
+    tail.record(stream)
+    torch.cuda.synchronize()
     clk = clocks.stop()
-    phases = plan.read_timing(args.steps)
-    total_ms = float(sum(a.elapsed_time(b) for a, b in outer))
+    total_ms = float(sum(a.elapsed_time(b) for a, b in g_ev)) + g_ev[-1][1].elapsed_time(tail)
+    del graph
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max over ranks
     total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = world * E * F * args.steps / (total_ms * 1e-3)
-
-    # N == 1: the same step replayed from a CUDA graph (launch gaps removed),
-    # flush between; the headline. N > 1 keeps the eager steps (each with its all-gather).
-    eager = {"ms_per_step": ms_per_step, "value": value, "phase_ms": "see phase_ms"}
-    if world == 1:
-        gs = torch.cuda.Stream()
-        gs.wait_stream(stream)
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=gs):
-            plan.collide(sp, mp, cd, stream=gs)
-        graph.replay()
-        torch.cuda.synchronize()
-        g_ms = []
-        for _ in range(args.steps):
-            if not args.no_flush:
-                flush.fill_(1)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            graph.replay()
-            b.record(stream)
-            b.synchronize()
-            g_ms.append(a.elapsed_time(b))
-        graph_ms_total = float(np.sum(g_ms))
-        del graph
-        ms_per_step = graph_ms_total / args.steps
-        value = world * E * F * args.steps / (graph_ms_total * 1e-3)
+    value = E_total * F * args.steps / (total_ms * 1e-3)
 
     # its CPU baseline only at N = 1 (like the headline's)
     solver = solver_leg(P, plan, w, lo, hi, E, min(args.steps, 50), args.quick or world > 1)
 
-    # stats all-gather (the only collective), once after the timed region
-    stats = gather_env_stats(plan.stats.clone(), E * world)
+    # the gathered stats of the last step (every rank's envs)
+    stats = gather.result().clone()
     plan.enable_timing(0)
+    peaks_live = device_peaks()
 
     # roofline of the dominant kernel (k_face_prep, the largest single launch of the
     # step): SURVEY §8(d) bytes / its live event time. Per face query 48 B (3 corners
@@ -430,39 +576,29 @@ def main():
         et = torch.tensor([float(np.sum(e_ms))], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * E * F * args.steps / (float(et.item()) * 1e-3), "unit": UNIT,
+        e2e = {"value": E_total * F * args.steps / (float(et.item()) * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(hsp.nbytes + hmp.nbytes + hcd.nbytes), "d2h_bytes_per_step": int(hst.nbytes),
                "ms_per_step": float(et.item()) / args.steps}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if args.envs_total else "weak",
             "vs_baseline": value / PAPER_QPS,
             "vs_baseline_ref": "derived 1.66e9 face queries/s: 1024 envs x 17798 faces / 11 ms (PAPER.md:227,584, A5000)",
             "dtype": "f64", "data": "synthetic (seeded SURVEY §8(d) poses, procedural M16 assets)",
-            "config": _config(args, E * world, F, grid.dims),
+            "config": _config(args, E_total, F, grid.dims, world),
             "e2e": e2e,
             "gpu_launches": LAUNCHES_PER_STEP * args.steps,
             "phase_ms": mean_phase,
-            "roofline": {"kernel": "k_face_prep", "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
-                         "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic(),
-                         "peak_source": peaks["source"], "alg_bytes_per_launch": alg_bytes,
-                         "samples_per_launch": samples_prep,
-                         "limiter": {k: ncu_summary().get(k) for k in ("fp64_pipe_pct", "issue_active_pct",
-                                                                        "warps_active_pct", "l2_hit_pct")},
-                         "limiter_note": "ncu: neither HBM nor the FP64 pipe saturates; the kernel is bound by "
-                                         "dependent gather / barrier latency at the occupancy its float64 "
-                                         "register footprint allows (DESIGN.md §4)",
-                         "basis": "48 B per face query (E x F) + 32 B per trilinear sample (8 float32 corners, "
-                                  "SURVEY §8(d)); samples counted exactly by the counting build of k_face_prep",
-                         "pgd_phase": {"kernels": "k_pgd_grad x2 + k_pgd_first + k_pgd_rest", "ms": pgd_ms,
-                                       "alg_bytes": pgd_bytes, "samples": samples_pgd,
-                                       "achieved_gbs": pgd_bytes / (pgd_ms * 1e-3) / 1e9,
-                                       "basis": "32 B per trilinear sample"}},
+            "roofline": roofline(E, F, prep_ms, samples_prep, pgd_ms, samples_pgd, peaks, peaks_live),
             "clocks": clk,
-            "timing": ("CUDA-graph replay of the step, CUDA events per step (SURVEY §8(d))" if world == 1 else
-                       "eager steps incl. the stats all-gather, CUDA events per step, max over ranks"),
+            "timing": "CUDA-graph replay of the collide step, CUDA events per step (SURVEY §8(d)), L2 flushed between "
+                      "steps (untimed); the per-step stats all-gather on a side stream overlaps the next step and "
+                      "the last one's tail is timed; max over ranks",
+            "allgather": {"bytes_per_step": int(16 * E_total), "stream": "side (overlapped)",
+                          "backend": "nccl" if world > 1 else "local copy (N = 1)"},
             "eager": eager,
             "solver": solver,
             "stats": {"candidates_per_env": float(stats[:, 0].double().mean()),
@@ -470,7 +606,7 @@ def main():
                       "kept_per_env": float(stats[:, 2].double().mean())},
         }
         if world == 1 and not args.quick:
-            line["cpu_baseline"] = cpu_baseline(w, args.cpu_sample)
+            line["cpu_baseline"] = cpu_baseline(w)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

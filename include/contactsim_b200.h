@@ -45,6 +45,13 @@ int cs_abi_version(void);
 /* SM count, L2 bytes and max persisting-L2 bytes of the current device. */
 int cs_device_info(int32_t *sm_count, int64_t *l2_bytes, int64_t *persist_l2_max);
 
+/* Roofline denominator measured on this device (no reference counterpart: bench.py
+ * support). Random 32-byte-sector gathers from an L2-resident buffer of `bytes`
+ * (mode 0: ld.global.cg, L2 only; 1: __ldg, L1 + L2; 2: tld4 on a 2D layered texture,
+ * 16 B per fetch) or a streaming read of a buffer above L2 (mode 3: the HBM read peak);
+ * `iters` timed launches after two warm ones. *gbs: achieved GB/s. */
+int cs_bench_gather(int32_t mode, int64_t bytes, int32_t iters, double *gbs);
+
 /* ------------------------------------------------------------------------
  * Device-resident SDF store.
  * Replaces holding SignedDistanceGrid.values per call (sdf/grid.py:48-68):

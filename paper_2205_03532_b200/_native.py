@@ -55,6 +55,7 @@ _SIGS = {
     "cs_last_error": ([], ctypes.c_char_p),
     "cs_abi_version": ([], ctypes.c_int),
     "cs_device_info": ([ctypes.POINTER(_i32), ctypes.POINTER(_i64), ctypes.POINTER(_i64)], ctypes.c_int),
+    "cs_bench_gather": ([_i32, _i64, _i32, ctypes.POINTER(_f64)], ctypes.c_int),
     "cs_sdf_register": ([_vp, ctypes.c_int, _i32, _i32, _i32, _vp, _f64, _vp, _vp, ctypes.POINTER(_i32)], ctypes.c_int),
     "cs_sdf_free": ([_i32], ctypes.c_int),
     "cs_sdf_values": ([_i32, ctypes.POINTER(_vp)], ctypes.c_int),

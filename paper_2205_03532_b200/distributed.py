@@ -42,6 +42,59 @@ def gather_env_stats(local_stats: torch.Tensor, n_envs: int, group=None) -> torc
     return torch.cat(parts, dim=0)
 
 
+class StatsGather:
+    """The per-step stats all-gather with its buffers allocated once (the step loop
+    allocates nothing) and, on CUDA, issued on a side stream so it stays off the
+    collide's critical path: `launch(stats, after=stream)` makes the side stream wait
+    for the step (an event), copies the local stats into the padded send buffer and
+    all-gathers into a persistent (world * width, 4) buffer; `wait(stream)` orders a
+    consumer after it; `result()` is the (n_envs, 4) view in env order."""
+
+    def __init__(self, n_envs: int, cols: int = 4, device=None, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.n_envs = n_envs
+        self.sizes = [shard_range(n_envs, r, self.world) for r in range(self.world)]
+        self.width = max(hi - lo for lo, hi in self.sizes)
+        dev = torch.device(device) if device is not None else torch.device("cpu")
+        self.send = torch.zeros((self.width, cols), dtype=torch.float32, device=dev)
+        self.out = torch.zeros((self.world * self.width, cols), dtype=torch.float32, device=dev)
+        contiguous = all(hi - lo == self.width for lo, hi in self.sizes)
+        self._view = self.out if contiguous else None
+        self.side = torch.cuda.Stream(device=dev) if dev.type == "cuda" else None
+        self._done = None
+
+    def launch(self, local_stats: torch.Tensor, after=None) -> None:
+        if self.side is not None:
+            ev = torch.cuda.Event()
+            ev.record(after if after is not None else torch.cuda.current_stream(self.send.device))
+            self.side.wait_event(ev)
+            ctx = torch.cuda.stream(self.side)
+        else:
+            import contextlib
+
+            ctx = contextlib.nullcontext()
+        with ctx:
+            self.send[: local_stats.shape[0]].copy_(local_stats, non_blocking=True)
+            if self.world > 1:
+                dist.all_gather_into_tensor(self.out, self.send, group=self.group)
+            else:
+                self.out[: local_stats.shape[0]].copy_(self.send[: local_stats.shape[0]])
+            if self.side is not None:
+                self._done = torch.cuda.Event()
+                self._done.record(self.side)
+
+    def wait(self, stream=None) -> None:
+        if self._done is not None:
+            (stream if stream is not None else torch.cuda.current_stream(self.send.device)).wait_event(self._done)
+
+    def result(self) -> torch.Tensor:
+        if self._view is not None:
+            return self._view[: self.n_envs]
+        return torch.cat([self.out[r * self.width: r * self.width + (hi - lo)] for r, (lo, hi) in
+                          enumerate(self.sizes)], dim=0)
+
+
 def step_report(stats: torch.Tensor) -> dict:
     """Scene-level totals from gathered stats (StepReport fields, scene.py:155-161)."""
     s = stats.double()

@@ -15,7 +15,9 @@ import sys
 from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sectors.sum",
+        "lts__t_sectors_lookup_hit.sum", "lts__t_sectors_lookup_miss.sum", "l1tex__t_sectors.sum",
+        "l1tex__t_sector_hit_rate.pct", "l1tex__texin_requests.sum", "smsp__inst_executed_op_texture.sum",
         "l1tex__t_bytes.sum", "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct",
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
@@ -103,12 +105,19 @@ def main():
             js = {"kernel": kern, "tag": tag,
                   "dram_bytes_per_launch": mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum"),
                   "duration_ms_ncu": float(d["gpu__time_duration.sum"][0].replace(",", "")) *
-                  (1e-3 if d["gpu__time_duration.sum"][1] == "usecond" else 1.0),
+                  {"usecond": 1e-3, "us": 1e-3, "nsecond": 1e-6, "ns": 1e-6}.get(d["gpu__time_duration.sum"][1], 1.0),
                   "fp64_pipe_pct": float(d["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"][0]),
                   "issue_active_pct": float(d["smsp__issue_active.avg.pct_of_peak_sustained_active"][0]),
                   "warps_active_pct": float(d["sm__warps_active.avg.pct_of_peak_sustained_active"][0]),
                   "l2_hit_pct": float(d["lts__t_sector_hit_rate.pct"][0]),
-                  "note": "ncu --set full, cold-cache serialized replay; traffic = dram read + write bytes"}
+                  "note": "ncu --set full, cold-cache serialized replay; traffic = dram read + write bytes; "
+                          "l2 bytes = lts__t_sectors x 32"}
+            if "lts__t_sectors.sum" in d:
+                js["lts_bytes_per_launch"] = 32.0 * float(d["lts__t_sectors.sum"][0].replace(",", ""))
+                js["lts_gbs_ncu"] = js["lts_bytes_per_launch"] / (js["duration_ms_ncu"] * 1e-3) / 1e9
+            js["dram_gbs_ncu"] = js["dram_bytes_per_launch"] / (js["duration_ms_ncu"] * 1e-3) / 1e9
+            if "l1tex__t_sector_hit_rate.pct" in d:
+                js["l1_hit_pct"] = float(d["l1tex__t_sector_hit_rate.pct"][0])
             with open(os.path.join(prof, f"{kern}_ncu.json"), "w") as fh:
                 json.dump(js, fh, indent=1)
         print("wrote", kern)

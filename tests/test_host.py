@@ -118,3 +118,38 @@ def test_stats_allgather_gloo_world2():
     for rank, arr, rep in outs:
         assert np.array_equal(arr, expect)
         assert rep["contacts_before"] == int(expect[:, 0].sum())
+
+
+def _bench(*args, env=None):
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ, **(env or {}))
+    e.pop("WORLD_SIZE", None) if env is None or "WORLD_SIZE" not in env else None
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), *args], capture_output=True, text=True,
+                       timeout=300, env=e, cwd=root)
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    return r.returncode, (json.loads(lines[-1]) if lines else None), r.stderr
+
+
+def test_bench_launcher_two_ranks():
+    """`bench.py --gpus 2` outside torchrun launches two ranks (torch.distributed.run on
+    127.0.0.1); they shard the envs and all-gather every env's stats in order (gloo)."""
+    rc, out, err = _bench("--gpus", "2", "--dry-run", "--steps", "2", "--envs", "7")
+    assert rc == 0, err[-2000:]
+    assert out["n_gpus"] == 2 and out["envs_total"] == 14 and out["shards"] == [[0, 7], [7, 14]]
+    assert out["gather_ok"] and out["scaling"] == "weak"
+
+
+def test_bench_strong_scaling_shards():
+    """--envs-total: the same total work split over the ranks (uneven shards padded in the gather)."""
+    rc, out, err = _bench("--gpus", "2", "--dry-run", "--steps", "1", "--envs-total", "1023")
+    assert rc == 0, err[-2000:]
+    assert out["shards"] == [[0, 512], [512, 1023]] and out["scaling"] == "strong" and out["gather_ok"]
+
+
+def test_bench_rejects_world_size_mismatch():
+    rc, out, err = _bench("--gpus", "4", "--dry-run", env={"WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": "0"})
+    assert rc != 0 and "WORLD_SIZE" in err
