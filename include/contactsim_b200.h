@@ -12,6 +12,7 @@
  *   CS_ERR_NONFINITE -> NonFiniteStateError       (generation.py:66-68, errors.py:19)
  *   CS_ERR_MESH      -> MeshValidationError       (grid.py:169,189-192, errors.py:8)
  *   CS_ERR_HANDLE / CS_ERR_CUDA / CS_ERR_OOM -> RuntimeError
+ *   CS_ERR_IO        -> OSError                  (open() in grid.py:154)
  *
  * Numerics: IEEE double arithmetic in the reference's operation order (numba
  * kernels: no FMA contraction), and the reference's BLAS 3-term dot products
@@ -34,7 +35,8 @@ typedef enum {
     CS_ERR_MESH = 3,
     CS_ERR_HANDLE = 4,
     CS_ERR_CUDA = 5,
-    CS_ERR_OOM = 6
+    CS_ERR_OOM = 6,
+    CS_ERR_IO = 7
 } cs_status;
 
 #define CS_ABI_VERSION 1
@@ -62,6 +64,19 @@ int cs_bench_gather(int32_t mode, int64_t bytes, int32_t iters, double *gbs);
 int cs_sdf_register(const float *values, int values_on_device, int32_t nx, int32_t ny, int32_t nz,
                     const double origin[3], double voxel, const double aabb_lo[3], const double aabb_hi[3],
                     int32_t *handle);
+/* SignedDistanceGrid.load (sdf/grid.py:151-160) straight into the device store:
+ * the CSIMSDF1 header ("<8s3i d 3d 6d") is parsed here and the float32 values are
+ * streamed from the file to the device through pinned staging buffers (no host
+ * array). Errors: CS_ERR_IO (cannot open), CS_ERR_VALUE (bad magic -> the
+ * reference's "not an SDF grid file", short file, bad dims). `info` (optional)
+ * receives the grid metadata. */
+typedef struct {
+    int32_t dims[3];
+    double origin[3];
+    double voxel;
+    double aabb_lo[3], aabb_hi[3];
+} cs_sdf_file_info;
+int cs_sdf_register_file(const char *path, int32_t *handle, cs_sdf_file_info *info);
 /* Freeing a grid (or mesh) that live plans sample defers the release to the
  * destruction of the last such plan; the handle is invalid for new plans at once. */
 int cs_sdf_free(int32_t handle);

@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CS_LIB_PATH") or os.path.join(_HERE, "_lib", "libcontactsim_b200.so")
 CSRC = os.path.join(_HERE, "csrc")
 
-CS_OK, CS_ERR_VALUE, CS_ERR_NONFINITE, CS_ERR_MESH, CS_ERR_HANDLE, CS_ERR_CUDA, CS_ERR_OOM = range(7)
+CS_OK, CS_ERR_VALUE, CS_ERR_NONFINITE, CS_ERR_MESH, CS_ERR_HANDLE, CS_ERR_CUDA, CS_ERR_OOM, CS_ERR_IO = range(8)
 CS_POSE7, CS_POSE12 = 0, 1
 CS_STAGE_GENERATE, CS_STAGE_REDUCE, CS_STAGE_ALL = 1, 2, 3
 
@@ -41,6 +41,10 @@ class OutputsC(ctypes.Structure):
     ]
 
 
+class SdfFileInfoC(ctypes.Structure):
+    _fields_ = [("dims", _i32 * 3), ("origin", _f64 * 3), ("voxel", _f64), ("aabb_lo", _f64 * 3), ("aabb_hi", _f64 * 3)]
+
+
 class SolverParamsC(ctypes.Structure):
     _fields_ = [("h", _f64), ("bias_factor", _f64), ("pos_iterations", _i32), ("vel_iterations", _i32)]
 
@@ -57,6 +61,7 @@ _SIGS = {
     "cs_device_info": ([ctypes.POINTER(_i32), ctypes.POINTER(_i64), ctypes.POINTER(_i64)], ctypes.c_int),
     "cs_bench_gather": ([_i32, _i64, _i32, ctypes.POINTER(_f64)], ctypes.c_int),
     "cs_sdf_register": ([_vp, ctypes.c_int, _i32, _i32, _i32, _vp, _f64, _vp, _vp, ctypes.POINTER(_i32)], ctypes.c_int),
+    "cs_sdf_register_file": ([ctypes.c_char_p, ctypes.POINTER(_i32), ctypes.POINTER(SdfFileInfoC)], ctypes.c_int),
     "cs_sdf_free": ([_i32], ctypes.c_int),
     "cs_sdf_values": ([_i32, ctypes.POINTER(_vp)], ctypes.c_int),
     "cs_sdf_l2_persist": ([_i32, _vp, _f32], ctypes.c_int),
@@ -152,6 +157,8 @@ def check(status: int) -> None:
         raise MeshValidationError(msg)
     if status == CS_ERR_OOM:
         raise MemoryError(msg)
+    if status == CS_ERR_IO:
+        raise OSError(msg)
     raise RuntimeError(msg)
 
 
@@ -164,6 +171,31 @@ def stream_handle(stream=None) -> int:
 
     s = stream if stream is not None else torch.cuda.current_stream()
     return int(s.cuda_stream)
+
+
+def hand_to_stream(stream, *tensors) -> None:
+    """Make tensors staged on the current stream safe to read on `stream`: `stream`
+    waits for the current stream's work so far, and the caching allocator is told the
+    tensors are in use there (record_stream), so their memory is not reused until
+    `stream`'s kernels are done. No-op when `stream` is None or the current stream."""
+    import torch
+
+    if stream is None:
+        return
+    cur = torch.cuda.current_stream()
+    if int(stream.cuda_stream) == int(cur.cuda_stream):
+        return
+    stream.wait_stream(cur)
+    for t in tensors:
+        if t is not None:
+            t.record_stream(stream)
+
+
+def sync_stream(stream=None) -> None:
+    """Block until `stream` (default: the current stream) has finished."""
+    import torch
+
+    (stream if stream is not None else torch.cuda.current_stream()).synchronize()
 
 
 class DevArray:

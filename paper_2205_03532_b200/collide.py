@@ -16,7 +16,9 @@ reference's list[ContactPatch] for one env.
 from __future__ import annotations
 
 import ctypes
+import threading
 import weakref
+from collections import OrderedDict
 
 import numpy as np
 
@@ -28,8 +30,66 @@ from .sdf.grid import SignedDistanceGrid
 
 
 
+class PlanCache:
+    """Bounded, thread-safe LRU of plans keyed by (thread, assets, params).
+
+    The per-pair drop-ins and collide() reuse one plan per configuration instead of
+    allocating device buffers on every call. Keys carry the calling thread's id, so
+    two threads never share a plan's buffers (a plan is re-entrant per stream, not
+    across concurrent callers). At most `maxsize` plans are kept; when an SDF or mesh
+    asset is finalised its plans are dropped first, so the deferred free of its device
+    copy completes and its handle is reused."""
+
+    _all: "weakref.WeakSet[PlanCache]" = weakref.WeakSet()
+
+    def __init__(self, maxsize: int = 8):
+        self.maxsize = maxsize
+        self._d: OrderedDict = OrderedDict()
+        self._assets: dict = {}
+        self._lock = threading.Lock()
+        PlanCache._all.add(self)
+
+    def get(self, key, make, sdf_handles=(), mesh_handles=()):
+        key = (threading.get_ident(),) + tuple(key)
+        with self._lock:
+            plan = self._d.get(key)
+            if plan is not None:
+                self._d.move_to_end(key)
+                return plan
+        plan = make()
+        with self._lock:
+            self._d[key] = plan
+            self._assets[key] = (frozenset(int(h) for h in sdf_handles), frozenset(int(h) for h in mesh_handles))
+            while len(self._d) > self.maxsize:
+                old, _ = self._d.popitem(last=False)
+                self._assets.pop(old, None)
+        return plan
+
+    def evict(self, sdf: int | None = None, mesh: int | None = None) -> None:
+        with self._lock:
+            for k in [k for k, (s, m) in self._assets.items() if (sdf is not None and sdf in s) or
+                      (mesh is not None and mesh in m)]:
+                self._d.pop(k, None)
+                self._assets.pop(k, None)
+
+    def clear(self) -> None:
+        with self._lock:
+            self._d.clear()
+            self._assets.clear()
+
+    def __len__(self) -> int:
+        return len(self._d)
+
+
+def evict_asset_plans(sdf: int | None = None, mesh: int | None = None) -> None:
+    """Drop every cached plan that uses SDF handle `sdf` / mesh handle `mesh`."""
+    for c in list(PlanCache._all):
+        c.evict(sdf, mesh)
+
+
 def _free_mesh(h: int) -> None:
     try:
+        evict_asset_plans(mesh=h)
         _native.lib().cs_mesh_free(h)
     except Exception:
         pass
@@ -137,13 +197,36 @@ class Plan:
         for t in (sdf_pose, mesh_pose, contact_distance):
             if not (t.is_cuda and t.dtype.is_floating_point and t.element_size() == 8 and t.is_contiguous()):
                 raise ValueError("poses and contact_distance must be contiguous float64 CUDA tensors")
+        self._check_pose_shapes(sdf_pose, mesh_pose, contact_distance, pose_format)
+        _native.hand_to_stream(stream, sdf_pose, mesh_pose, contact_distance)
         _native.call("cs_collide", self.ptr, sdf_pose.data_ptr(), mesh_pose.data_ptr(), pose_format,
                      contact_distance.data_ptr(), _native.stream_handle(stream))
+
+    def _check_pose_shapes(self, sdf_pose, mesh_pose, contact_distance, pose_format) -> None:
+        """The C side reads E poses of 7 (or 12) doubles and E contact distances."""
+        if not (self.stages & _native.CS_STAGE_GENERATE):
+            raise ValueError("plan has no generate stage")
+        width = 7 if pose_format == _native.CS_POSE7 else 12 if pose_format == _native.CS_POSE12 else None
+        if width is None:
+            raise ValueError(f"unknown pose format {pose_format}")
+        E = self.n_envs
+        for name, t in (("sdf_pose", sdf_pose), ("mesh_pose", mesh_pose)):
+            if tuple(t.shape) not in ((E, width), (E * width,)):
+                raise ValueError(f"{name} must have shape ({E}, {width}), got {tuple(t.shape)}")
+        if contact_distance.numel() != E:
+            raise ValueError(f"contact_distance must hold {E} values, got {contact_distance.numel()}")
 
     def collide_host(self, sdf_pose: np.ndarray, mesh_pose: np.ndarray, contact_distance: np.ndarray,
                      pose_format: int = _native.CS_POSE7, stats_out: np.ndarray | None = None, stream=None):
         """End-to-end call with host buffers: H2D poses, collide, D2H stats [E,4], synchronise."""
         st = stats_out if stats_out is not None else np.empty((self.n_envs, 4), np.float32)
+        for a in (sdf_pose, mesh_pose, contact_distance, st):
+            if not (isinstance(a, np.ndarray) and a.flags.c_contiguous):
+                raise ValueError("collide_host takes C-contiguous numpy arrays")
+        if sdf_pose.dtype != np.float64 or mesh_pose.dtype != np.float64 or contact_distance.dtype != np.float64 \
+                or st.dtype != np.float32 or st.size != 4 * self.n_envs:
+            raise ValueError("collide_host: float64 poses / contact_distance and a float32 (E, 4) stats buffer")
+        self._check_pose_shapes(sdf_pose, mesh_pose, contact_distance, pose_format)
         _native.call("cs_collide_host", self.ptr, sdf_pose.ctypes.data, mesh_pose.ctypes.data, pose_format,
                      contact_distance.ctypes.data, st.ctypes.data, _native.stream_handle(stream))
         return st
@@ -190,6 +273,19 @@ class Plan:
         for t in (state.ref, state.w_mat, state.vel, state.impulse, mu, restitution, slop):
             if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
                 raise ValueError("solver state and per-env parameters must be contiguous float64 CUDA tensors")
+        E = self.n_envs
+        want = {"ref": (E, 2, 3), "w_mat": (E, 2, 6, 6), "vel": (E, 2, 6), "impulse": (E, 2, 6)}
+        for name, shape in want.items():
+            got = tuple(getattr(state, name).shape)
+            if got != shape:
+                raise ValueError(f"state.{name} must have shape {shape} (one two-body system per env), got {got}")
+        for name, t in (("mu", mu), ("restitution", restitution), ("slop", slop)):
+            if t.numel() != E:
+                raise ValueError(f"{name} must hold {E} values, got {t.numel()}")
+        if wrench is not None and not (wrench.is_cuda and wrench.dtype == torch.float64 and wrench.is_contiguous()
+                                       and tuple(wrench.shape) == (E, 2, 6)):
+            raise ValueError(f"wrench must be a contiguous float64 CUDA tensor of shape ({E}, 2, 6)")
+        _native.hand_to_stream(stream, state.ref, state.w_mat, state.vel, state.impulse, mu, restitution, slop, wrench)
         if wrench is None:
             wrench = torch.empty((self.n_envs, 2, 6), dtype=torch.float64, device="cuda")
         cp = params.to_c()
@@ -236,9 +332,10 @@ class ReducedContacts:
     """Device-resident result of one collide step (views into the plan's buffers;
     valid until the plan runs again)."""
 
-    def __init__(self, plan: Plan, body_ids=None):
+    def __init__(self, plan: Plan, body_ids=None, stream=None):
         self.plan = plan
         self.body_ids = body_ids
+        self.stream = stream  # the stream the step ran on (check() waits for it)
 
     def __getattr__(self, name):
         return getattr(self.plan, name)
@@ -248,7 +345,8 @@ class ReducedContacts:
         return self.plan.n_envs
 
     def check(self) -> None:
-        """Raise the reference's errors for envs flagged on device (syncs)."""
+        """Raise the reference's errors for envs flagged on device (waits for the step's stream)."""
+        _native.sync_stream(self.stream)
         st = self.plan.env_status.cpu().numpy()
         if (st == 1).any():
             raise NonFiniteStateError(f"non-finite pose in contact generation (envs {np.nonzero(st == 1)[0][:8].tolist()})")
@@ -299,23 +397,23 @@ class ReducedContacts:
         return out
 
 
-_plan_cache: dict = {}
+_plan_cache = PlanCache(maxsize=4)
 
 
 def clear_plan_cache() -> None:
-    """Drop the plans collide() keeps per (handles, params) key (their device memory
-    is freed once no result view of them is held)."""
-    _plan_cache.clear()
+    """Drop every cached plan: collide()'s and the per-pair drop-ins' (their device
+    memory is freed once no result view of them is held)."""
+    for c in list(PlanCache._all):
+        c.clear()
 
 
 def get_plan(sdf_handles, mesh_handles, params: ReductionParams | None) -> Plan:
     params = params or ReductionParams()
-    key = (tuple(np.asarray(sdf_handles).tolist()), tuple(np.asarray(mesh_handles).tolist()),
-           params.max_patches, params.per_patch_cap, params.normal_cone_cos, params.min_depth, params.batch_size)
-    plan = _plan_cache.get(key)
-    if plan is None:
-        plan = _plan_cache[key] = Plan(sdf_handles, mesh_handles, params)
-    return plan
+    s = tuple(np.asarray(sdf_handles).tolist())
+    m = tuple(np.asarray(mesh_handles).tolist())
+    key = (s, m, params.max_patches, params.per_patch_cap, params.normal_cone_cos, params.min_depth,
+           params.batch_size)
+    return _plan_cache.get(key, lambda: Plan(sdf_handles, mesh_handles, params), set(s), set(m))
 
 
 def collide(sdf_handles, mesh_handles, sdf_pose, mesh_pose, contact_distance, params: ReductionParams | None = None,
@@ -339,8 +437,8 @@ def collide(sdf_handles, mesh_handles, sdf_pose, mesh_pose, contact_distance, pa
     cd = dev(contact_distance).reshape(-1)
     if cd.numel() == 1:
         cd = cd.expand(E).contiguous()
-    plan.collide(sp, mp, cd, _native.CS_POSE7, stream)
-    res = ReducedContacts(plan)
+    plan.collide(sp, mp, cd, _native.CS_POSE7, stream)  # hands the staged inputs to `stream`
+    res = ReducedContacts(plan, stream=stream)
     if check:
         res.check()
     return res

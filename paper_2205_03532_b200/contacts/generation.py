@@ -48,17 +48,26 @@ def assign_roles(body_a: BodyShape, body_b: BodyShape) -> CollisionPairing:
     return CollisionPairing(sdf.body_id, mesh.body_id, not (body_a.sdf_enabled or body_b.sdf_enabled))
 
 
-_gen_plans: dict = {}
+def _gen_plans():
+    global _GEN_PLANS
+    if _GEN_PLANS is None:
+        from ..collide import PlanCache
+
+        _GEN_PLANS = PlanCache(maxsize=8)
+    return _GEN_PLANS
+
+
+_GEN_PLANS = None
 
 
 def _plan_for(sdf_handle: int, mesh_handle: int):
+    """One-env generate plan per (thread, grid, mesh): bounded LRU, dropped when the
+    grid or mesh is finalised (collide.PlanCache)."""
     from ..collide import Plan
 
-    key = (sdf_handle, mesh_handle)
-    plan = _gen_plans.get(key)
-    if plan is None:
-        plan = _gen_plans[key] = Plan([sdf_handle], [mesh_handle], None, stages=_native.CS_STAGE_GENERATE)
-    return plan
+    return _gen_plans().get((sdf_handle, mesh_handle),
+                            lambda: Plan([sdf_handle], [mesh_handle], None, stages=_native.CS_STAGE_GENERATE),
+                            (sdf_handle,), (mesh_handle,))
 
 
 def generate_contacts(pairing: CollisionPairing, grid: SignedDistanceGrid, mesh: TriMesh, sdf_pose: Transform,

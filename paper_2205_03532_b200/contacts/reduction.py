@@ -16,19 +16,21 @@ from .types import ContactPatch, ContactSet, ReductionParams
 
 MERGE_COS = float(np.cos(np.radians(5.0)))
 
-_red_plans: dict = {}
+_RED_PLANS = None
 
 
 def _plan_for(capacity: int, params: ReductionParams):
-    from ..collide import Plan
+    """One-env reduce plan per (thread, capacity class, params): bounded LRU
+    (collide.PlanCache), so concurrent callers never share buffers."""
+    global _RED_PLANS
+    from ..collide import Plan, PlanCache
     from .. import _native
 
+    if _RED_PLANS is None:
+        _RED_PLANS = PlanCache(maxsize=8)
     cap = 1 << max(10, int(capacity - 1).bit_length())
     key = (cap, params.max_patches, params.per_patch_cap, params.normal_cone_cos, params.min_depth, params.batch_size)
-    plan = _red_plans.get(key)
-    if plan is None:
-        plan = _red_plans[key] = Plan(None, None, params, stages=_native.CS_STAGE_REDUCE, capacity=[cap])
-    return plan
+    return _RED_PLANS.get(key, lambda: Plan(None, None, params, stages=_native.CS_STAGE_REDUCE, capacity=[cap]))
 
 
 def reduce_contacts(candidates: ContactSet, params: ReductionParams | None = None) -> list[ContactPatch]:

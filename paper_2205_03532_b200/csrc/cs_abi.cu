@@ -235,67 +235,140 @@ int cs_device_info(int32_t *sm_count, int64_t *l2_bytes, int64_t *persist_l2_max
 
 // ---------------------------------------------------------------- SDF store
 
-int cs_sdf_register(const float *values, int values_on_device, int32_t nx, int32_t ny, int32_t nz,
-                    const double origin[3], double voxel, const double aabb_lo[3], const double aabb_hi[3],
-                    int32_t *handle) {
+static int check_grid_args(int32_t nx, int32_t ny, int32_t nz, double voxel) {
     if (nx < 2 || ny < 2 || nz < 2) return fail(CS_ERR_VALUE, "grid dims must be at least 2 per axis");
     if (!(voxel > 0.0)) return fail(CS_ERR_VALUE, "voxel_size must be positive");
     const int64_t n = (int64_t)nx * ny * nz;
     if (n >= (int64_t)1 << 31) return fail(CS_ERR_VALUE, "grid of %lld voxels exceeds the 2^31 device index range", (long long)n);
+    return CS_OK;
+}
+
+// A free SDF slot (g_mu held); -1 when the table is full.
+static int free_sdf_slot() {
+    for (int i = 0; i < MAX_HANDLES; ++i)
+        if (!g_sdf[i].live) return i;
+    return -1;
+}
+
+static int finish_sdf_register(int h, int32_t nx, int32_t ny, int32_t nz, const double origin[3], double voxel,
+                               const double aabb_lo[3], const double aabb_hi[3], int32_t *handle);
+
+int cs_sdf_register(const float *values, int values_on_device, int32_t nx, int32_t ny, int32_t nz,
+                    const double origin[3], double voxel, const double aabb_lo[3], const double aabb_hi[3],
+                    int32_t *handle) {
+    int r = check_grid_args(nx, ny, nz, voxel);
+    if (r) return r;
+    const int64_t n = (int64_t)nx * ny * nz;
     if (!values || !handle || !origin || !aabb_lo || !aabb_hi) return fail(CS_ERR_VALUE, "null argument");
     std::lock_guard<std::mutex> lk(g_mu);
-    int r = ensure_tables();
+    r = ensure_tables();
     if (r) return r;
-    int h = -1;
-    for (int i = 0; i < MAX_HANDLES; ++i)
-        if (!g_sdf[i].live) { h = i; break; }
+    const int h = free_sdf_slot();
     if (h < 0) return fail(CS_ERR_HANDLE, "SDF handle table full (%d)", MAX_HANDLES);
     SdfEntry &s = g_sdf[h];
     s.bytes = (size_t)n * sizeof(float);
     CS_CUDA(cudaMalloc(&s.values, s.bytes));
     CS_CUDA(cudaMemcpy(s.values, values, s.bytes, values_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
-    GridT<float> probe = cs::make_grid<float>(nullptr, nx, ny, nz, origin[0], origin[1], origin[2], voxel);
-    {   // brick-window minima: the first pass of the face lower bound (cs_common.cuh: sample_lower_bound)
-        std::vector<float> h32((size_t)n);
-        CS_CUDA(cudaMemcpy(h32.data(), s.values, s.bytes, cudaMemcpyDeviceToHost));
-        const int bx = probe.bnx, by = probe.bny, bz = probe.bnz;
-        std::vector<float> bm((size_t)bx * by * bz, INFINITY);
-        for (int z = 0; z < nz; ++z)
-            for (int y = 0; y < ny; ++y)
-                for (int x = 0; x < nx; ++x) {
-                    const float v = h32[(size_t)x + (size_t)nx * ((size_t)y + (size_t)ny * z)];
-                    // node x belongs to bricks (x - 1) / BRICK .. x / BRICK (a brick's node range is closed)
-                    for (int kz = std::max(0, (z - 1) / BRICK); kz <= std::min(bz - 1, z / BRICK); ++kz)
-                        for (int ky = std::max(0, (y - 1) / BRICK); ky <= std::min(by - 1, y / BRICK); ++ky)
-                            for (int kx = std::max(0, (x - 1) / BRICK); kx <= std::min(bx - 1, x / BRICK); ++kx) {
-                                if (kx * BRICK > x || kx * BRICK + BRICK < x || ky * BRICK > y || ky * BRICK + BRICK < y ||
-                                    kz * BRICK > z || kz * BRICK + BRICK < z)
-                                    continue;
-                                float &o = bm[(size_t)kx + (size_t)bx * ((size_t)ky + (size_t)by * kz)];
-                                o = std::fmin(o, v);
-                            }
-                }
-        // window tables: widths {1, 2} per axis, window [b, b + w - 1] clamped to the last brick
-        const size_t nb = bm.size();
-        std::vector<float> bw(8 * nb);
-        for (int t = 0; t < 8; ++t) {
-            const int wx = 1 + (t & 1), wy = 1 + ((t >> 1) & 1), wz = 1 + ((t >> 2) & 1);
-            for (int z = 0; z < bz; ++z)
-                for (int y = 0; y < by; ++y)
-                    for (int x = 0; x < bx; ++x) {
-                        float m = INFINITY;
-                        for (int dz = 0; dz < wz; ++dz)
-                            for (int dy = 0; dy < wy; ++dy)
-                                for (int dx = 0; dx < wx; ++dx) {
-                                    const int xx = std::min(x + dx, bx - 1), yy = std::min(y + dy, by - 1),
-                                              zz = std::min(z + dz, bz - 1);
-                                    m = std::fmin(m, bm[(size_t)xx + (size_t)bx * ((size_t)yy + (size_t)by * zz)]);
-                                }
-                        bw[(size_t)t * nb + (size_t)x + (size_t)bx * ((size_t)y + (size_t)by * z)] = m;
-                    }
+    return finish_sdf_register(h, nx, ny, nz, origin, voxel, aabb_lo, aabb_hi, handle);
+}
+
+// The CSIMSDF1 file (sdf/grid.py:138-160: "<8s3i d 3d 6d" header, then float32
+// values) straight into the device store: the values stream from the file through two
+// pinned staging buffers (a read overlaps the previous chunk's copy), never as a host array.
+int cs_sdf_register_file(const char *path, int32_t *handle, cs_sdf_file_info *info) {
+    if (!path || !handle) return fail(CS_ERR_VALUE, "null argument");
+    FILE *fh = std::fopen(path, "rb");
+    if (!fh) return fail(CS_ERR_IO, "cannot open %s", path);
+    unsigned char head[100];
+    if (std::fread(head, 1, sizeof(head), fh) != sizeof(head)) { std::fclose(fh); return fail(CS_ERR_VALUE, "not an SDF grid file: %s", path); }
+    if (std::memcmp(head, "CSIMSDF1", 8) != 0) { std::fclose(fh); return fail(CS_ERR_VALUE, "not an SDF grid file: %s", path); }
+    int32_t dims[3];
+    double voxel, origin[3], aabb[6];
+    std::memcpy(dims, head + 8, 12);
+    std::memcpy(&voxel, head + 20, 8);
+    std::memcpy(origin, head + 28, 24);
+    std::memcpy(aabb, head + 52, 48);
+    int r = check_grid_args(dims[0], dims[1], dims[2], voxel);
+    if (r) { std::fclose(fh); return r; }
+    const int64_t n = (int64_t)dims[0] * dims[1] * dims[2];
+    std::lock_guard<std::mutex> lk(g_mu);
+    r = ensure_tables();
+    if (r) { std::fclose(fh); return r; }
+    const int h = free_sdf_slot();
+    if (h < 0) { std::fclose(fh); return fail(CS_ERR_HANDLE, "SDF handle table full (%d)", MAX_HANDLES); }
+    SdfEntry &s = g_sdf[h];
+    s.bytes = (size_t)n * sizeof(float);
+    constexpr size_t CHUNK = (size_t)8 << 20;
+    unsigned char *stage = nullptr;
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    auto cleanup = [&]() {
+        if (stage) cudaFreeHost(stage);
+        for (auto e : ev) if (e) cudaEventDestroy(e);
+        if (cs) cudaStreamDestroy(cs);
+        std::fclose(fh);
+    };
+    cudaError_t ce = cudaMalloc(&s.values, s.bytes);
+    if (ce == cudaSuccess) ce = cudaHostAlloc(&stage, 2 * CHUNK, cudaHostAllocDefault);
+    if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
+    if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
+    size_t done = 0;
+    int k = 0;
+    bool truncated = false;
+    while (ce == cudaSuccess && done < s.bytes) {
+        const size_t want = std::min(CHUNK, s.bytes - done);
+        unsigned char *buf = stage + (size_t)k * CHUNK;
+        ce = cudaEventSynchronize(ev[k]);  // the copy that last used this buffer is done
+        if (ce != cudaSuccess) break;
+        if (std::fread(buf, 1, want, fh) != want) { truncated = true; break; }
+        ce = cudaMemcpyAsync(reinterpret_cast<unsigned char *>(s.values) + done, buf, want, cudaMemcpyHostToDevice, cs);
+        if (ce == cudaSuccess) ce = cudaEventRecord(ev[k], cs);
+        done += want;
+        k ^= 1;
+    }
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(cs);
+    cleanup();
+    if (ce != cudaSuccess || truncated) {
+        cudaFree(s.values);
+        s.values = nullptr;
+        if (truncated) return fail(CS_ERR_VALUE, "values length does not match dims: %s", path);
+        return fail(CS_ERR_CUDA, "%s: %s", path, cudaGetErrorString(ce));
+    }
+    if (info) {
+        for (int a = 0; a < 3; ++a) {
+            info->dims[a] = dims[a];
+            info->origin[a] = origin[a];
+            info->aabb_lo[a] = aabb[a];
+            info->aabb_hi[a] = aabb[3 + a];
         }
-        CS_CUDA(cudaMalloc(&s.bwin, bw.size() * sizeof(float)));
-        CS_CUDA(cudaMemcpy(s.bwin, bw.data(), bw.size() * sizeof(float), cudaMemcpyHostToDevice));
+        info->voxel = voxel;
+    }
+    return finish_sdf_register(h, dims[0], dims[1], dims[2], origin, voxel, aabb, aabb + 3, handle);
+}
+
+// The device-side tables of a grid whose values are in g_sdf[h].values (g_mu held).
+static int finish_sdf_register(int h, int32_t nx, int32_t ny, int32_t nz, const double origin[3], double voxel,
+                               const double aabb_lo[3], const double aabb_hi[3], int32_t *handle) {
+    SdfEntry &s = g_sdf[h];
+    GridT<float> probe = cs::make_grid<float>(nullptr, nx, ny, nz, origin[0], origin[1], origin[2], voxel);
+    // brick-window minima (the first pass of the face lower bound, cs_common.cuh:
+    // sample_lower_bound), built on the device, and a scan of the values: non-finite
+    // values disable the bound; the largest |value| sets its absolute rounding margin
+    unsigned scan_h[2] = {0, 0};
+    {
+        const int bx = probe.bnx, by = probe.bny, bz = probe.bnz;
+        const size_t nb = (size_t)bx * by * bz;
+        float *bm = nullptr;
+        unsigned *scan = nullptr;
+        CS_CUDA(cudaMalloc(&s.bwin, 8 * nb * sizeof(float)));
+        CS_CUDA(cudaMalloc(&bm, nb * sizeof(float)));
+        CS_CUDA(cudaMalloc(&scan, 2 * sizeof(unsigned)));
+        build_brick_windows(s.values, nx, ny, nz, bx, by, bz, bm, s.bwin, scan, 0);
+        CS_CUDA(cudaGetLastError());
+        CS_CUDA(cudaMemcpy(scan_h, scan, sizeof(scan_h), cudaMemcpyDeviceToHost));
+        CS_CUDA(cudaFree(bm));
+        CS_CUDA(cudaFree(scan));
     }
     {   // cell-window minima of the exact face bound (cs_common.cuh: sample_lower_bound)
         const int64_t nc = (int64_t)(nx - 1) * (ny - 1) * (nz - 1);
@@ -338,6 +411,15 @@ int cs_sdf_register(const float *values, int values_on_device, int32_t nx, int32
     d.gp = cs::make_grid<float>(s.values, nx, ny, nz, origin[0], origin[1], origin[2], voxel);
     d.gp.cwin = s.cwin;
     d.gp.bwin = s.bwin;
+    if (scan_h[0]) {  // NaN / inf values: no bound (fminf would skip a NaN corner)
+        d.gp.cwin = nullptr;
+        d.gp.bwin = nullptr;
+    }
+    {
+        float vmax;
+        std::memcpy(&vmax, &scan_h[1], sizeof(float));
+        d.gp.lbm = (double)vmax * 0x1p-40;  // see sample_lower_bound
+    }
     d.gp.tex = 0;  // the texture is used by uniform-grid plans only (a warp-uniform handle: cs_plan_create)
     CS_CUDA(cudaMemcpy(d_sdfs + h, &d, sizeof(SdfDesc), cudaMemcpyHostToDevice));
     s.live = true;
@@ -617,6 +699,17 @@ static int plan_buffers(cs_plan *P, const std::vector<int64_t> &cap) {
     }
 #undef A
     P->max_batch = std::min<int64_t>(P->rp.batch_size, maxcap);
+    if (P->stages & CS_STAGE_REDUCE) {
+        // k_reduce stages one batch and the builders in shared memory: refuse plans whose
+        // (max_patches, batch_size) need more than the device's opt-in limit per block
+        int dev = 0, optin = 0;
+        CS_CUDA(cudaGetDevice(&dev));
+        CS_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        const size_t need = reduce_smem_bytes(N, (int)P->max_batch);
+        if (need > (size_t)optin)
+            return fail(CS_ERR_VALUE, "max_patches %d with batch_size %lld needs %zu bytes of shared memory per env "
+                        "(device limit %d): lower batch_size or max_patches", N, (long long)P->max_batch, need, optin);
+    }
     cs_outputs &o = P->out;
     o.n_envs = E;
     o.max_patches = N;

@@ -100,6 +100,8 @@ struct GridT {
     // corners of the cells of bricks [b, b + w - 1] per axis (BRICK cells per brick edge).
     const float *__restrict__ bwin;
     int bnx, bny, bnz;
+    // Absolute rounding margin of the bound: (max |value| over the grid) * 2^-40.
+    double lbm;
     // The values as a 2D layered texture object (x, y, layer z), or 0: sample_axes then
     // gathers each z face of the cell's corners with one tld4 (CS_NO_TEX builds: __ldg).
     unsigned long long tex;
@@ -138,6 +140,7 @@ __host__ __device__ inline GridT<T> make_grid(const T *v, int nx, int ny, int nz
     g.cwin = nullptr;
     g.bwin = nullptr;
     g.tex = 0;
+    g.lbm = 0.0;
     g.bnx = (nx - 2) / BRICK + 1; g.bny = (ny - 2) / BRICK + 1; g.bnz = (nz - 2) / BRICK + 1;
     return g;
 }
@@ -305,8 +308,13 @@ __device__ __forceinline__ void gradient(const GridT<T> &g, double px, double py
 // cell's 8 corners (weights f and 1 - f, evaluated in float64) plus a non-negative
 // outside term, and points outside the grid sample a clamped boundary cell, so no
 // sample in the box's cells is below the minimum corner value over those cells,
-// less the lerps' rounding (a few ulps; margin 2^-40 relative). The box is widened
-// by 1e-6 voxel so roundings of the points themselves stay inside. cd_hint: a
+// less the lerps' rounding. That rounding is relative to the LARGEST corner
+// magnitude M, not to the minimum: each lerp c0 RN(1 - f) + c1 f rounds the weight,
+// both products and the sum (<= 4 u M, u = 2^-53) and the three lerp levels compound
+// to < 16 u M = 2^-49 M. The margin is |min| 2^-40 plus lbm = (max |value| over the
+// grid) 2^-40, at least 2^9 times that, so the bound holds for any cd, including
+// cd -> 0 where the minimum corner is near zero and others are not (grids holding
+// NaN / inf get no bound at all: cs_sdf_register). The box is widened by 1e-6 voxel so roundings of the points themselves stay inside. cd_hint: a
 // looser bound above it is returned early. The minimum over
 // the box's cells is read from the window tables: with w = the largest power of two
 // (<= 8) not above any axis' cell count, each axis is covered by windows of w cells
@@ -362,7 +370,7 @@ __device__ __forceinline__ double sample_lower_bound(const GridT<T> &g, const do
             }
         }
         const double md = (double)m;
-        const double lb = md - fabs(md) * 0x1p-40 - 1e-300;
+        const double lb = md - fabs(md) * 0x1p-40 - g.lbm - 1e-300;
         BOUND_STAT(0);
         if (lb > cd_hint) { BOUND_STAT(1); return lb; }
         // the cell pass lifts the bound by about a brick at most: it is skipped when the
@@ -397,7 +405,7 @@ __device__ __forceinline__ double sample_lower_bound(const GridT<T> &g, const do
 #pragma unroll
     for (int i = 0; i < CWIN_MAX_LOOKUPS; ++i) m = fminf(m, r[i]);
     const double md = (double)m;
-    return md - fabs(md) * 0x1p-40 - 1e-300;
+    return md - fabs(md) * 0x1p-40 - g.lbm - 1e-300;
 }
 
 // sdf/_kernels.py:20-61

@@ -744,6 +744,72 @@ void build_cell_windows(const float *values, int nx, int ny, int nz, float *tabl
     }
 }
 
+// ---------------------------------------------------------------- brick-window minima
+// (GridT::bwin; built once at SDF registration, on the device)
+
+// bm[b] = min over the nodes of brick b: nodes k B .. k B + B per axis (closed, clamped
+// to the last node); bricks per axis (n - 2) / B + 1
+__global__ void k_brick_min(const float *__restrict__ v, int nx, int ny, int nz, int bx, int by, int bz,
+                            float *__restrict__ bm) {
+    const int64_t nb = (int64_t)bx * by * bz;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+        const int kx = (int)(b % bx), ky = (int)((b / bx) % by), kz = (int)(b / ((int64_t)bx * by));
+        const int x1 = min(kx * BRICK + BRICK, nx - 1), y1 = min(ky * BRICK + BRICK, ny - 1),
+                  z1 = min(kz * BRICK + BRICK, nz - 1);
+        float m = INFINITY;
+        for (int z = kz * BRICK; z <= z1; ++z)
+            for (int y = ky * BRICK; y <= y1; ++y) {
+                const float *row = v + (int64_t)nx * (y + (int64_t)ny * z);
+                for (int x = kx * BRICK; x <= x1; ++x) m = fminf(m, row[x]);
+            }
+        bm[b] = m;
+    }
+}
+
+// the 8 window tables: widths {1, 2} per axis, window [b, b + w - 1] clamped to the last brick
+__global__ void k_brick_windows(const float *__restrict__ bm, int bx, int by, int bz, float *__restrict__ bw) {
+    const int64_t nb = (int64_t)bx * by * bz;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+        const int x = (int)(b % bx), y = (int)((b / bx) % by), z = (int)(b / ((int64_t)bx * by));
+        const int x2 = min(x + 1, bx - 1), y2 = min(y + 1, by - 1), z2 = min(z + 1, bz - 1);
+        auto at = [&](int xx, int yy, int zz) { return bm[xx + (int64_t)bx * (yy + (int64_t)by * zz)]; };
+        const float m000 = at(x, y, z), m100 = at(x2, y, z), m010 = at(x, y2, z), m110 = at(x2, y2, z);
+        const float m001 = at(x, y, z2), m101 = at(x2, y, z2), m011 = at(x, y2, z2), m111 = at(x2, y2, z2);
+        const float w1 = m000, w2 = fminf(m000, m100);                       // (wx, 1, 1)
+        const float w3 = fminf(m000, m010), w4 = fminf(w2, fminf(m010, m110));  // (1, 2, 1), (2, 2, 1)
+        const float z0[4] = {w1, w2, w3, w4};
+        const float z1[4] = {m001, fminf(m001, m101), fminf(m001, m011), fminf(fminf(m001, m101), fminf(m011, m111))};
+        for (int t = 0; t < 8; ++t) bw[(int64_t)t * nb + b] = t < 4 ? z0[t] : fminf(z0[t - 4], z1[t - 4]);
+    }
+}
+
+// scan[0] |= 1 if a value is not finite; scan[1] = max |value| (float bits, finite values)
+__global__ void k_grid_scan(const float *__restrict__ v, int64_t n, unsigned *__restrict__ scan) {
+    unsigned bad = 0, mx = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float a = fabsf(v[i]);
+        if (!(a <= 3.402823466e38f)) bad = 1;
+        else mx = max(mx, __float_as_uint(a));
+    }
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if ((threadIdx.x & 31) == 0) {
+        if (bad) atomicOr(scan, 1u);
+        atomicMax(scan + 1, mx);
+    }
+}
+
+void build_brick_windows(const float *values, int nx, int ny, int nz, int bx, int by, int bz, float *bm, float *bw,
+                         unsigned *scan, cudaStream_t s) {
+    const int64_t nb = (int64_t)bx * by * bz, n = (int64_t)nx * ny * nz;
+    const unsigned gb = (unsigned)std::min<int64_t>((nb + 255) / 256, 148 * 32);
+    const unsigned gn = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
+    k_brick_min<<<gb, 256, 0, s>>>(values, nx, ny, nz, bx, by, bz, bm);
+    k_brick_windows<<<gb, 256, 0, s>>>(bm, bx, by, bz, bw);
+    cudaMemsetAsync(scan, 0, 2 * sizeof(unsigned), s);
+    k_grid_scan<<<gn, 256, 0, s>>>(values, n, scan);
+}
+
 void launch_compact(int64_t E, const EnvXf *xf, const int64_t *cand_base, const int2 *block_map,
                     const int32_t *chunk_first, const Staging &st, const Candidates &cs, int32_t *n_cand,
                     cudaStream_t s) {

@@ -87,6 +87,10 @@ void launch_compact(int64_t E, const EnvXf *xf, const int64_t *cand_base, const 
                     const int32_t *chunk_first, const Staging &st, const Candidates &cs, int32_t *n_cand,
                     cudaStream_t s);
 void build_cell_windows(const float *values, int nx, int ny, int nz, float *tables, float *tmp, cudaStream_t s);
+// brick minima bm [bx by bz], the 8 brick-window tables bw [8][bx by bz], and the grid
+// scan (scan[0]: a value is not finite; scan[1]: max |value| as float bits)
+void build_brick_windows(const float *values, int nx, int ny, int nz, int bx, int by, int bz, float *bm, float *bw,
+                         unsigned *scan, cudaStream_t s);
 void launch_face_contacts(const GridView &g, const double *tv, int64_t m, double cd, int max_iters, double tol,
                           double *op, double *ophi, double *og, uint8_t *ofd, cudaStream_t s);
 void launch_sdf_sample(const GridView &g, const double *p, int64_t n, double *out, cudaStream_t s);

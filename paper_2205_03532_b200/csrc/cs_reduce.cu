@@ -452,11 +452,15 @@ void launch_reduce(const ReduceIO &io, const ReduceParams &p, int64_t max_batch,
     if (io.E <= 0) return;
     const int SB = (int)max_batch;
     const size_t smem = reduce_smem_bytes(p.N, SB);
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        cudaFuncSetAttribute(k_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = smem;
-    }
+    // per device: the attribute is raised only when the call succeeds (a failed raise
+    // leaves the launch to report the error)
+    static size_t configured[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    size_t &cfg = configured[dev & 63];
+    if (smem > 48 * 1024 && smem > cfg &&
+        cudaFuncSetAttribute(k_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess)
+        cfg = smem;
     k_reduce<<<(unsigned)io.E, RED_T, smem, s>>>(io, p, SB);
 }
 

@@ -54,6 +54,7 @@ struct ReduceIO {
 };
 
 void launch_reduce(const ReduceIO &io, const ReduceParams &p, int64_t max_batch, cudaStream_t s);
+size_t reduce_smem_bytes(int N, int SB);  // k_reduce dynamic shared memory per env
 // Side streams and events of a plan: launch_finalize forks its independent kernels
 // onto them (concurrent graph branches when the collide is captured).
 struct FinFork {

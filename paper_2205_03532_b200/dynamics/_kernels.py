@@ -40,6 +40,9 @@ def gauss_seidel_sweeps(iters, w_mat, vel, imp, body_a, body_b, ra, rb, nrm, tan
     nb = int(d["vel"].shape[0])
     if m == 0 or iters <= 0:
         return
+    from .solver import check_solver_bodies
+
+    check_solver_bodies(nb)
     off = torch.tensor([0, m], dtype=i64, device="cuda")
     p = lambda k: d[k].data_ptr()  # noqa: E731
     _native.call("cs_gauss_seidel_sweeps", 1, nb, off.data_ptr(), int(iters), p("w_mat"), p("vel"), p("imp"),

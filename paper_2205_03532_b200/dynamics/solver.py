@@ -47,6 +47,18 @@ class SolverParams:
                                      self.vel_iterations)
 
 
+SOLVER_MAX_BODIES = 8  # cs_solver.cuh SOLVER_MAX_BODIES
+
+
+def check_solver_bodies(nb: int) -> None:
+    """The device solver keeps a system's bodies (velocities, impulses, 6x6 mobility
+    blocks) on chip, which bounds a system to SOLVER_MAX_BODIES bodies. The reference
+    has no limit; scenes above it must be split into independent systems."""
+    if not 1 <= int(nb) <= SOLVER_MAX_BODIES:
+        raise ValueError(f"the device contact solver handles systems of 1..{SOLVER_MAX_BODIES} bodies per call "
+                         f"(got {int(nb)}); split larger scenes into independent systems")
+
+
 class SolverState:
     """Twist (at a reference point) + 6x6 inverse mobility per body (solver.py:46-77)."""
 
@@ -123,6 +135,7 @@ class ContactConstraints:
         con.restitution[:] = [r["restitution"] for r in rows]
         slop = np.array([r["slop"] for r in rows], dtype=np.float64)
         nb = len(state.vel)
+        check_solver_bodies(nb)
         d_in = [_t(con.body_a, np.int64), _t(con.body_b, np.int64), _t(con.point), _t(con.normal), _t(con.depth),
                 _t(con.restitution), _t(slop), _t(state.ref), _t(state.w_mat), _t(state.vel)]
         names = ("ra", "rb", "tan1", "tan2", "kn", "kt1", "kt2", "bias_target", "restitution_target")
@@ -159,6 +172,7 @@ class ContactConstraints:
         m = len(self)
         if m == 0:
             return np.zeros((n_bodies, 6))
+        check_solver_bodies(n_bodies)
         out = torch.zeros((n_bodies, 6), dtype=torch.float64, device="cuda")
         off = torch.tensor([0, m], dtype=torch.int64, device="cuda")
         d = [_t(self.body_a, np.int64), _t(self.body_b, np.int64)] + [

@@ -153,6 +153,9 @@ class MultiPairScenes:
 
         p = poses7 if isinstance(poses7, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(poses7))
         p = p.to(device="cuda", dtype=torch.float64).contiguous().reshape(self.n_bodies, 7)
+        sp = p.index_select(0, self.d_sdf_idx).contiguous()
+        mp = p.index_select(0, self.d_mesh_idx).contiguous()
+        _native.hand_to_stream(stream, p, sp, mp)  # staged on the current stream, read on `stream`
         st = _native.stream_handle(stream)
         _native.call("cs_world_aabb", self.n_bodies, self.d_mesh_lo.data_ptr(), self.d_mesh_hi.data_ptr(),
                      p.data_ptr(), self.world_lo.data_ptr(), self.world_hi.data_ptr(), st)
@@ -163,12 +166,11 @@ class MultiPairScenes:
         _native.call("cs_pair_slots_active", self.n_slots, self.d_slot_scene.data_ptr(), self.d_slot_pair.data_ptr(),
                      self.d_pair_off.data_ptr(), self.pairs.data_ptr(), self.n_pairs.data_ptr(),
                      self.active.data_ptr(), st)
-        sp = p.index_select(0, self.d_sdf_idx).contiguous()
-        mp = p.index_select(0, self.d_mesh_idx).contiguous()
         _native.call("cs_collide_active", self.plan.ptr, sp.data_ptr(), mp.data_ptr(), _native.CS_POSE7,
                      self.d_cd.data_ptr(), self.active.data_ptr(), st)
-        res = ReducedContacts(self.plan)
+        res = ReducedContacts(self.plan, stream=stream)
         if check:
+            _native.sync_stream(stream)
             bs = self.bp_status.cpu().numpy()
             if (bs == 1).any():
                 raise ValueError("non-finite AABB in broadphase input")
@@ -191,12 +193,16 @@ class MultiPairScenes:
         S, nb = len(self.scenes), state.vel.shape[1]
         if state.vel.shape[0] != S or nb < self.max_bodies:
             raise ValueError("state must hold (n_scenes, >= bodies per scene) systems")
+        from .dynamics.solver import check_solver_bodies
+
+        check_solver_bodies(nb)
         slop = np.full(self.n_slots, params.penetration_slop) if params.penetration_slop is not None \
             else 0.5 * self.slot_voxel
         d_slop = torch.from_numpy(slop.astype(np.float64)).cuda()
         if wrench is None:
             wrench = torch.empty((S, nb, 6), dtype=torch.float64, device="cuda")
         cp = params.to_c()
+        _native.hand_to_stream(stream, d_slop, wrench)
         _native.call("cs_multipair_solve", self.plan.ptr, S, nb, self.d_slot_off.data_ptr(), self.d_slot_a.data_ptr(),
                      self.d_slot_b.data_ptr(), self.max_slots, state.ref.data_ptr(), state.w_mat.data_ptr(),
                      state.vel.data_ptr(), state.impulse.data_ptr(), self.d_slot_mu.data_ptr(),
