@@ -213,8 +213,9 @@ class Plan:
         for name, t in (("sdf_pose", sdf_pose), ("mesh_pose", mesh_pose)):
             if tuple(t.shape) not in ((E, width), (E * width,)):
                 raise ValueError(f"{name} must have shape ({E}, {width}), got {tuple(t.shape)}")
-        if contact_distance.numel() != E:
-            raise ValueError(f"contact_distance must hold {E} values, got {contact_distance.numel()}")
+        n_cd = contact_distance.numel() if hasattr(contact_distance, "numel") else contact_distance.size
+        if n_cd != E:
+            raise ValueError(f"contact_distance must hold {E} values, got {n_cd}")
 
     def collide_host(self, sdf_pose: np.ndarray, mesh_pose: np.ndarray, contact_distance: np.ndarray,
                      pose_format: int = _native.CS_POSE7, stats_out: np.ndarray | None = None, stream=None):

@@ -684,7 +684,7 @@ static int plan_buffers(cs_plan *P, const std::vector<int64_t> &cap) {
         A(io.sh, 2 * tot + E * (4 * (int64_t)N + 4));
         A(io.hlen, 4 * E * N); A(io.pdeep, E * N); A(io.pnt, E * N); A(io.wenv, E * N);
         A(io.jobs, 64 * 4 * E * N); A(io.njob, 65);
-        A(io.patch_off, E + 1);
+        A(io.patch_off, E + 1); A(io.red_slow, E);
         A(io.large_list, E * N); A(io.large_count, 1);
         A(io.n_patch, E); A(io.n_kept, E);
         A(io.patch_normal, 3 * E * N); A(io.builder_maxd, E * N);

@@ -15,6 +15,7 @@
 //   shared memory; candidates are read through the read-only path.
 // Per-patch finalisation lives in cs_finalize.cu.
 #include <float.h>
+#include <climits>
 
 #include "cs_reduce_util.cuh"
 
@@ -72,6 +73,104 @@ extern "C" int cs_debug_red_prof(unsigned long long *out) { return (int)cudaMemc
 #define RED_MARK(i) do {} while (0)
 #endif
 
+// Builders -> outputs, then the members CSR: a stable counting sort of candidate
+// indices by patch label. With room in the (now idle) batch staging `scratch`, the four
+// warps take contiguous quarters of the candidates: per-warp label counts give every
+// (warp, patch) its base, so each patch's members stay in ascending candidate order;
+// else warp 0 alone. Called by all RED_T threads after a barrier.
+__device__ void write_patches_csr(const ReduceIO &io, int N, int P, const double *bn, const unsigned long long *bmx,
+                                  int *hcnt, int *scratch, int SB, const int32_t *lab, int C) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
+    __shared__ int s_ws2[WS_INTS];
+    const int64_t e = blockIdx.x;
+    const int64_t base = io.cand_base[e];
+    for (int q = tid; q < N; q += RED_T) {
+        double *o = io.patch_normal + 3 * (e * N + q);
+        if (q < P) { o[0] = bn[3 * q]; o[1] = bn[3 * q + 1]; o[2] = bn[3 * q + 2]; }
+        else { o[0] = 0.0; o[1] = 0.0; o[2] = 0.0; }
+        io.builder_maxd[e * N + q] = q < P ? dec_d(bmx[q]) : 0.0;
+        hcnt[q] = 0;
+    }
+    if (tid == 0) io.n_patch[e] = P;
+    __syncthreads();
+    int32_t *moff = io.member_offsets + e * (N + 1);
+    int32_t *mem = io.members + base;
+    const bool par = (size_t)25 * SB >= (size_t)16 * N;
+    int *hw = par ? scratch : hcnt;  // [4][N] counts, then bases (par)
+    if (par) {
+        for (int q = tid; q < 4 * N; q += RED_T) hw[q] = 0;
+        __syncthreads();
+    }
+    const int qlen = par ? (C + 3) / 4 : C;
+    const int i0 = par ? min(C, wid * qlen) : 0, i1 = par ? min(C, i0 + qlen) : C;
+    if (par) {
+        for (int i = i0 + lane; i < i1; i += 32) {
+            const int l = lab[i];
+            if (l >= 0) atomicAdd(&hw[wid * N + l], 1);
+        }
+    } else {
+        for (int i = tid; i < C; i += RED_T) {
+            const int l = lab[i];
+            if (l >= 0) atomicAdd(&hcnt[l], 1);
+        }
+    }
+    __syncthreads();
+    if (par) {
+        int run = 0;
+        for (int q0 = 0; q0 < N; q0 += RED_T) {
+            const int q = q0 + tid;
+            int c[4] = {0, 0, 0, 0};
+            if (q < P)
+                for (int w = 0; w < 4; ++w) c[w] = hw[w * N + q];
+            int tot;
+            const int x = run + block_excl_scan(c[0] + c[1] + c[2] + c[3], s_ws2, &tot);
+            if (q < N) {
+                moff[q] = x;
+                int b = x;
+                for (int w = 0; w < 4; ++w) { hw[w * N + q] = b; b += c[w]; }
+            }
+            run += tot;
+        }
+        if (tid == 0) moff[N] = run;
+        __syncthreads();
+    } else {
+        if (wid != 0) return;
+        if (lane == 0) {
+            int run = 0;
+            for (int q = 0; q < N; ++q) {
+                moff[q] = run;
+                const int c = q < P ? hcnt[q] : 0;
+                hcnt[q] = run;  // running base
+                run += c;
+            }
+            moff[N] = run;
+        }
+        __syncwarp();
+    }
+    int *cnt = par ? hw + wid * N : hcnt;  // this warp's running bases
+    constexpr int PF = 8;  // labels prefetched per lane: keeps 8 loads in flight per round
+    for (int c0 = i0; c0 < i1; c0 += 32 * PF) {
+        int lb[PF];
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+            const int i = c0 + 32 * u + lane;
+            lb[u] = (i < i1) ? lab[i] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+            const int i = c0 + 32 * u + lane;
+            const int l = lb[u];
+            const unsigned peers = __match_any_sync(FULL, l);
+            const int rank = __popc(peers & lt);
+            if (l >= 0) mem[cnt[l] + rank] = i;
+            __syncwarp();
+            if (l >= 0 && rank == 0) cnt[l] += __popc(peers);
+            __syncwarp();
+        }
+    }
+}
+
 __global__ void __launch_bounds__(RED_T) k_reduce(ReduceIO io, ReduceParams p, int SB) {
     // keep at <= 72 registers (7 CTAs per SM: 1036 >= 1024 envs in one wave); 80 registers measured
     // 13% slower, and a (RED_T, 7) bound makes ptxas spill
@@ -97,6 +196,7 @@ __global__ void __launch_bounds__(RED_T) k_reduce(ReduceIO io, ReduceParams p, i
     uint8_t *st = reinterpret_cast<uint8_t *>(ul2 + SB);                           // [SB]
 
     const int64_t e = blockIdx.x;
+    if (io.red_slow && io.red_slow[e] == 0) return;  // k_reduce_fast finished this env
     const int64_t base = io.cand_base[e];
     const int C = io.n_cand[e];
     const double *nrm = io.normal + 3 * base;
@@ -353,97 +453,219 @@ __global__ void __launch_bounds__(RED_T) k_reduce(ReduceIO io, ReduceParams p, i
         RED_MARK(3);
     }
     RED_MARK(2);
-    // builders -> outputs
-    for (int q = tid; q < N; q += RED_T) {
-        double *o = io.patch_normal + 3 * (e * N + q);
-        if (q < P) { o[0] = bn[3 * q]; o[1] = bn[3 * q + 1]; o[2] = bn[3 * q + 2]; }
-        else { o[0] = 0.0; o[1] = 0.0; o[2] = 0.0; }
-        io.builder_maxd[e * N + q] = q < P ? dec_d(bmx[q]) : 0.0;
-        hcnt[q] = 0;
-    }
-    if (tid == 0) io.n_patch[e] = P;
-    __syncthreads();
-    // CSR: stable counting sort of candidate indices by patch. With room in the (now
-    // idle) batch staging, the four warps take contiguous quarters of the candidates:
-    // per-warp label counts give every (warp, patch) its base, so each patch's members
-    // stay in ascending candidate order; else warp 0 alone.
-    int32_t *moff = io.member_offsets + e * (N + 1);
-    int32_t *mem = io.members + base;
-    const bool par = (size_t)25 * SB >= (size_t)16 * N;
-    int *hw = par ? reinterpret_cast<int *>(bdep) : hcnt;  // [4][N] counts, then bases (par)
-    if (par) {
-        for (int q = tid; q < 4 * N; q += RED_T) hw[q] = 0;
-        __syncthreads();
-    }
-    const int qlen = par ? (C + 3) / 4 : C;
-    const int i0 = par ? min(C, wid * qlen) : 0, i1 = par ? min(C, i0 + qlen) : C;
-    if (par) {
-        for (int i = i0 + lane; i < i1; i += 32) {
-            const int l = lab[i];
-            if (l >= 0) atomicAdd(&hw[wid * N + l], 1);
-        }
-    } else {
-        for (int i = tid; i < C; i += RED_T) {
-            const int l = lab[i];
-            if (l >= 0) atomicAdd(&hcnt[l], 1);
-        }
-    }
-    __syncthreads();
-    RED_MARK(4);
-    if (par) {
-        int run = 0;
-        for (int q0 = 0; q0 < N; q0 += RED_T) {
-            const int q = q0 + tid;
-            int c[4] = {0, 0, 0, 0};
-            if (q < P)
-                for (int w = 0; w < 4; ++w) c[w] = hw[w * N + q];
-            int tot;
-            const int x = run + block_excl_scan(c[0] + c[1] + c[2] + c[3], s_ws, &tot);
-            if (q < N) {
-                moff[q] = x;
-                int b = x;
-                for (int w = 0; w < 4; ++w) { hw[w * N + q] = b; b += c[w]; }
-            }
-            run += tot;
-        }
-        if (tid == 0) moff[N] = run;
-        __syncthreads();
-    } else {
-        if (wid != 0) return;
-        if (lane == 0) {
-            int run = 0;
-            for (int q = 0; q < N; ++q) {
-                moff[q] = run;
-                const int c = q < P ? hcnt[q] : 0;
-                hcnt[q] = run;  // running base
-                run += c;
-            }
-            moff[N] = run;
-        }
-        __syncwarp();
-    }
-    int *cnt = par ? hw + wid * N : hcnt;  // this warp's running bases
-    constexpr int PF = 8;  // labels prefetched per lane: keeps 8 loads in flight per round
-    for (int c0 = i0; c0 < i1; c0 += 32 * PF) {
-        int lb[PF];
-#pragma unroll
-        for (int u = 0; u < PF; ++u) {
-            const int i = c0 + 32 * u + lane;
-            lb[u] = (i < i1) ? lab[i] : -1;
-        }
-#pragma unroll
-        for (int u = 0; u < PF; ++u) {
-            const int i = c0 + 32 * u + lane;
-            const int l = lb[u];
-            const unsigned peers = __match_any_sync(FULL, l);
-            const int rank = __popc(peers & lt);
-            if (l >= 0) mem[cnt[l] + rank] = i;
-            __syncwarp();
-            if (l >= 0 && rank == 0) cnt[l] += __popc(peers);
-            __syncwarp();
-        }
-    }
+    write_patches_csr(io, N, P, bn, bmx, hcnt, reinterpret_cast<int *>(bdep), SB, lab, C);
     RED_MARK(5);
+}
+
+
+// ------------------------------------------------------------------ fast path
+//
+// k_reduce_fast: the same Algorithm 1 for envs whose candidates all pass min_depth
+// and carry no NaN depth or normal (every generated candidate), as long as no patch
+// has to be evicted; any other env is flagged (red_slow[e] = 1) and redone from
+// scratch by k_reduce. Differences from k_reduce are in the schedule only:
+//   * the batch positions stay in place (no ordered compaction of the unassigned
+//     list): with no NaN, numpy's first argmax over the unassigned list in position
+//     order is the (depth, -position) maximum over the unassigned positions, so
+//     each seed comes out of an order-independent block argmax;
+//   * the _add_patch decision for a seed is known before its bin is formed (it
+//     depends only on the seed normal and the builders): every warp computes it
+//     redundantly (no barrier), so bin members get their final label in the binning
+//     pass itself, and a bin's max depth is the seed's depth (bin members are
+//     unassigned, hence not deeper than the seed);
+//   * one step = one pass over the batch + one block argmax: two barriers.
+// The assign pass is specialised on its BLAS pattern (G3 / V3) and, without NaN,
+// numpy's argmax is a strict > scan.
+
+// Block argmax over (v, i) without NaN: larger v, ties -> lower i; plus the count of
+// contributing entries. Each thread brings its local best (i < 0: none). A warp finds
+// its max v by shuffles, then the lowest index holding it and the count by one
+// reduction each; lane 0 of every warp posts to `part`, and after the barrier every
+// thread combines the RED_T / 32 posts the same way.
+struct BestD {
+    double v;
+    int i, cnt;
+};
+
+__device__ __forceinline__ BestD warp_best(double v, int i, int cnt) {
+    const unsigned FULL = 0xffffffffu;
+    double m = i >= 0 ? v : -INFINITY;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(FULL, m, o));
+    const bool has = __any_sync(FULL, i >= 0);
+    const int bi = __reduce_min_sync(FULL, (i >= 0 && v == m) ? i : INT_MAX);
+    const int c = __reduce_add_sync(FULL, cnt);
+    return BestD{m, has ? bi : -1, c};
+}
+
+__device__ __forceinline__ BestD block_best(BestD w, BestD *part) {
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = w;
+    __syncthreads();
+    BestD r = part[0];
+#pragma unroll
+    for (int k = 1; k < RED_T / 32; ++k) {
+        const BestD b = part[k];
+        r.cnt += b.cnt;
+        if (b.i >= 0 && (r.i < 0 || b.v > r.v || (b.v == r.v && b.i < r.i))) { r.v = b.v; r.i = b.i; }
+    }
+    return r;
+}
+
+// first argmax over q < P of cos(reps[q], n) (reps @ n: gemv, V3 when P >= 2), per warp
+__device__ __forceinline__ BestD warp_best_builder(const double *bn, int P, double n0, double n1, double n2) {
+    const int lane = threadIdx.x & 31;
+    double bv = -INFINITY;
+    int bi = -1;
+    for (int q = lane; q < P; q += 32) {  // ascending q per lane: strict > keeps the first
+        const double *b = bn + 3 * q;
+        const double c = P >= 2 ? V3(b[0], b[1], b[2], n0, n1, n2) : G3(b[0], b[1], b[2], n0, n1, n2);
+        if (bi < 0 || c > bv) { bv = c; bi = q; }
+    }
+    return warp_best(bv, bi, 0);
+}
+
+// normals[batch] @ reps.T for U entries at once: first argmax over the builders
+// (strict >, no NaN), each builder normal loaded once for the U entries
+template <bool GEMM, int U>
+__device__ __forceinline__ void assign_best(const double *bn, int P, const double (&a)[U][3], double (&bc)[U],
+                                            int (&best)[U]) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        bc[u] = GEMM ? G3(a[u][0], a[u][1], a[u][2], bn[0], bn[1], bn[2]) : V3(a[u][0], a[u][1], a[u][2], bn[0], bn[1], bn[2]);
+        best[u] = 0;
+    }
+    for (int q = 1; q < P; ++q) {
+        const double b0 = bn[3 * q], b1 = bn[3 * q + 1], b2 = bn[3 * q + 2];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const double c = GEMM ? G3(a[u][0], a[u][1], a[u][2], b0, b1, b2) : V3(a[u][0], a[u][1], a[u][2], b0, b1, b2);
+            if (c > bc[u]) { bc[u] = c; best[u] = q; }
+        }
+    }
+}
+
+constexpr int AU = 2;  // assign-pass entries per thread per builder sweep
+
+__global__ void __launch_bounds__(RED_T, 7) k_reduce_fast(ReduceIO io, ReduceParams p, int SB) {
+    extern __shared__ __align__(16) unsigned char dyn[];
+    __shared__ BestD s_part[RED_T / 32];
+    const int N = p.N;
+    const int tid = threadIdx.x;
+    double *bn = reinterpret_cast<double *>(dyn);                                  // [N][3]
+    unsigned long long *bmx = reinterpret_cast<unsigned long long *>(bn + 3 * N);  // [N]
+    int *hcnt = reinterpret_cast<int *>(bmx + N);                                  // [N]
+    double *bdep = reinterpret_cast<double *>(dyn + (((size_t)N * 36 + 15) & ~(size_t)15));  // [SB]
+    uint8_t *st = reinterpret_cast<uint8_t *>(bdep + SB);                          // [SB] 1: assigned
+
+    const int64_t e = blockIdx.x;
+    const int64_t base = io.cand_base[e];
+    const int C = io.n_cand[e];
+    const double *nrm = io.normal + 3 * base;
+    const double *dep = io.depth + base;
+    int32_t *lab = io.label + base;
+    const bool has_md = io.env_min_depth ? true : (p.has_min_depth != 0);
+    const double md = io.env_min_depth ? io.env_min_depth[e] : p.min_depth;
+    int P = 0;  // builders; uniform across the CTA
+    for (int start = 0; start < C; start += p.batch_size) {
+        const int bsz = min(p.batch_size, C - start);
+        // stage depths; eligibility (every candidate passes min_depth, no NaN); the assign
+        // pass (_assign_to_existing); the first seed
+        const bool gemm = (bsz >= 2 && P >= 2) || (bsz == 1 && P == 1);
+        bool bad = false;
+        double lv = 0.0;
+        int li = -1, lc = 0;
+        for (int k0 = 0; k0 < bsz; k0 += AU * RED_T) {
+            double a[AU][3], d[AU], bc[AU];
+            int best[AU];
+#pragma unroll
+            for (int u = 0; u < AU; ++u) {
+                const int k = k0 + u * RED_T + tid;
+                const int64_t i = start + min(k, bsz - 1);
+                d[u] = __ldg(dep + i);
+                a[u][0] = __ldg(nrm + 3 * i); a[u][1] = __ldg(nrm + 3 * i + 1); a[u][2] = __ldg(nrm + 3 * i + 2);
+                bad |= isnan(d[u]) || isnan(a[u][0]) || isnan(a[u][1]) || isnan(a[u][2]) || (has_md && !(d[u] >= md));
+            }
+            if (P > 0) {
+                if (gemm) assign_best<true, AU>(bn, P, a, bc, best);
+                else assign_best<false, AU>(bn, P, a, bc, best);
+            }
+#pragma unroll
+            for (int u = 0; u < AU; ++u) {
+                const int k = k0 + u * RED_T + tid;
+                if (k >= bsz) continue;
+                bdep[k] = d[u];
+                const bool s = P > 0 && bc[u] >= p.cone;
+                st[k] = s ? 1 : 0;
+                if (s) {
+                    lab[start + k] = best[u];
+                    atomicMax(&bmx[best[u]], enc_d(d[u]));
+                } else {
+                    lab[start + k] = -1;
+                    if (li < 0 || d[u] > lv) { lv = d[u]; li = k; }  // ascending k: first max
+                    ++lc;
+                }
+            }
+        }
+        if (__syncthreads_or(bad)) {  // the general kernel redoes this env
+            if (tid == 0) io.red_slow[e] = 1;
+            return;
+        }
+        BestD nx = block_best(warp_best(lv, li, lc), s_part);
+        int nu = nx.cnt, sk = nx.i;
+        __syncthreads();
+        // seed / bin / add-patch steps (reduction.py:63-73, 91-110)
+        while (nu > 0) {
+            const int64_t si = start + sk;
+            const double s0 = __ldg(nrm + 3 * si), s1 = __ldg(nrm + 3 * si + 1), s2 = __ldg(nrm + 3 * si + 2);
+            const double sd = bdep[sk];
+            int label;
+            bool merge = false;
+            {
+                const BestD bq = P > 0 ? warp_best_builder(bn, P, s0, s1, s2) : BestD{0.0, -1, 0};
+                const bool similar = P > 0 && bq.v >= p.cone;
+                merge = similar && (bq.v >= MERGE_COS || P >= N);
+                if (!merge && P >= N) {  // eviction: the general kernel redoes this env
+                    if (tid == 0) io.red_slow[e] = 1;
+                    return;
+                }
+                label = merge ? bq.i : P;
+            }
+            // BinReduce: cos = normals[unassigned] @ seed_normal (V3: the list holds the seed
+            // and, when it has other entries, >= 2 rows), the seed forced in
+            lv = 0.0; li = -1; lc = 0;
+            for (int k = tid; k < bsz; k += RED_T) {
+                if (st[k]) continue;
+                const int64_t i = start + k;
+                const double c = V3(__ldg(nrm + 3 * i), __ldg(nrm + 3 * i + 1), __ldg(nrm + 3 * i + 2), s0, s1, s2);
+                if (c >= p.cone || k == sk) {
+                    st[k] = 1;
+                    lab[i] = label;
+                } else {
+                    const double d = bdep[k];
+                    if (li < 0 || d > lv) { lv = d; li = k; }
+                    ++lc;
+                }
+            }
+            nx = block_best(warp_best(lv, li, lc), s_part);
+            if (tid == 0) {
+                if (merge) {  // the deeper patch's normal; max depth over the union
+                    const unsigned long long ed = enc_d(sd);
+                    if (sd > dec_d(bmx[label])) { bn[3 * label] = s0; bn[3 * label + 1] = s1; bn[3 * label + 2] = s2; }
+                    if (ed > bmx[label]) bmx[label] = ed;
+                } else {
+                    bn[3 * label] = s0; bn[3 * label + 1] = s1; bn[3 * label + 2] = s2;
+                    bmx[label] = enc_d(sd);
+                }
+            }
+            P += merge ? 0 : 1;
+            nu = nx.cnt;
+            sk = nx.i;
+            __syncthreads();
+        }
+    }
+    if (tid == 0) io.red_slow[e] = 0;
+    __syncthreads();
+    write_patches_csr(io, N, P, bn, bmx, hcnt, reinterpret_cast<int *>(bdep), SB, lab, C);
 }
 
 size_t reduce_smem_bytes(int N, int SB) { return red_smem_bytes(N, SB); }
@@ -457,10 +679,15 @@ void launch_reduce(const ReduceIO &io, const ReduceParams &p, int64_t max_batch,
     static size_t configured[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
-    size_t &cfg = configured[dev & 63];
+    static size_t configured_fast[64] = {};
+    size_t &cfg = configured[dev & 63], &cfg_fast = configured_fast[dev & 63];
     if (smem > 48 * 1024 && smem > cfg &&
         cudaFuncSetAttribute(k_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess)
         cfg = smem;
+    if (smem > 48 * 1024 && smem > cfg_fast &&
+        cudaFuncSetAttribute(k_reduce_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess)
+        cfg_fast = smem;
+    if (io.red_slow) k_reduce_fast<<<(unsigned)io.E, RED_T, smem, s>>>(io, p, SB);
     k_reduce<<<(unsigned)io.E, RED_T, smem, s>>>(io, p, SB);
 }
 

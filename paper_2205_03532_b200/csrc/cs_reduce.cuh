@@ -42,6 +42,7 @@ struct ReduceIO {
     int32_t *jobs;       // [64][4 E N] chain jobs (4 w + kind) bucketed by chain length
     int32_t *njob;       // [65] per-bucket counts, claimed
     int32_t *patch_off;  // [E+1]
+    int32_t *red_slow;   // [E] k_reduce_fast left env e to k_reduce (NaN, min_depth cull, eviction)
     int32_t *large_list, *large_count;  // patches above the warp path's size limit
     // outputs
     int32_t *n_patch, *n_kept;

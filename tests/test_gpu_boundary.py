@@ -195,7 +195,7 @@ def test_argument_checks(P, grid64, nut):
         plan.collide(d(4, 7), d(4, 7), d(5))
     with pytest.raises(ValueError):
         plan.collide_host(np.zeros((4, 7)), np.zeros((4, 7)), np.zeros(2))
-    with pytest.raises(ValueError, match="state.vel"):
+    with pytest.raises(ValueError, match="state.ref"):
         plan.solve(BatchedSolverState(4, 3), d(4), d(4), d(4))
     with pytest.raises(ValueError, match="mu"):
         plan.solve(BatchedSolverState(4, 2), d(3), d(4), d(4))
