@@ -164,25 +164,30 @@ struct SdfDesc {
 __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
 __device__ __forceinline__ double dmax(double a, double b) { return b > a ? b : a; }
 
-// RN(a / b) for b > 0 normal, given rb = RN(1 / b): one reciprocal multiply and
-// a Markstein correction, then the exact remainder r2 = a - q b proves q is the
-// correctly rounded quotient (|r2| below b times half the spacing of q); if the
-// proof fails the IEEE division is used. Bit-identical to a / b. The threshold is
-// assembled on the high word only (32-bit integer ops).
+// RN(a / b) for b >= 2^-900, given rb = RN(1 / b): one reciprocal multiply and a
+// Markstein correction give a faithful q; the exact remainder r2 = a - q b (one FMA)
+// then proves q is the correctly rounded quotient: for q normal and not a power of
+// two, with 2^k <= |q| < 2^(k+1), q = RN(a / b) iff |a / b - q| < 2^(k-53) (division
+// has no ties), i.e. |r2| < 2^k (b 2^-53). That threshold is a power of two times
+// b 2^-53, exact whenever it is >= 2^-1000. Anything else (a power-of-two q, tiny or
+// zero quotients, a failed proof) takes the IEEE division. Bit-identical to a / b.
+// The IEEE division out of line: inlined, the compiler evaluates its fast path on
+// every call and selects (if-conversion), which costs as much as the proof saves.
+static __device__ __noinline__ double div_ieee(double a, double b) { return a / b; }
+
 __device__ __forceinline__ double div_rn(double a, double b, double rb) {
     double q = a * rb;
-    double r = __fma_rn(-q, b, a);
+    const double r = __fma_rn(-q, b, a);
     q = __fma_rn(r, rb, q);
-    double r2 = __fma_rn(-q, b, a);
+    const double r2 = __fma_rn(-q, b, a);
     const int qh = __double2hiint(q);
-    const int E = (qh >> 20) & 0x7ff;
-    // b * 2^(E - 1023 - 53), halved when q is a power of two and the quotient lies below it
-    int sh = E - 1076;
-    if (((qh & 0xfffff) | __double2loint(q)) == 0 && ((r2 < 0.0) != (q < 0.0))) sh -= 1;
-    const double thr = __hiloint2double(__double2hiint(b) + (sh << 20), __double2loint(b));
-    if (E >= 120 && E <= 2000 && fabs(r2) < thr) return q;
-    return a / b;  // zero, tiny/huge quotients, and unproven roundings (never seen in practice)
+    const double thr = __hiloint2double(qh & 0x7ff00000, 0) * (b * 0x1p-53);
+    if (((qh & 0xfffff) | __double2loint(q)) != 0 && thr >= 0x1p-1000 && fabs(r2) < thr) return q;
+    return div_ieee(a, b);
 }
+
+// x / 3.0 (the centroid, contacts/_kernels.py:40), correctly rounded via div_rn
+__device__ __forceinline__ double div3(double x) { return div_rn(x, 3.0, 0x1.5555555555555p-2); }
 
 // One axis of a sample (sdf/_kernels.py:299-308, 256-273): c = min(max(g, 0.0), n - 1.0)
 // (numba's max/min keep -0.0), d = g - c (the outside-distance component),
@@ -475,7 +480,7 @@ __device__ __forceinline__ bool face_body(const GridT<T> &g, double ax, double a
     double diam = dmax(e0, dmax(e1, e2));
     double phi_min = dmin(phi_a, dmin(phi_b, phi_c));
     if (phi_min - diam > cd) return false;
-    double sx = (ax + bx + cx) / 3.0, sy = (ay + by + cy) / 3.0, sz = (az + bz + cz) / 3.0;
+    double sx = div3(ax + bx + cx), sy = div3(ay + by + cy), sz = div3(az + bz + cz);
     double phi = sample(g, sx, sy, sz);
     if (COUNT) r.nsamp += 1;
     if (phi_a < phi) { sx = ax; sy = ay; sz = az; phi = phi_a; }

@@ -698,107 +698,6 @@ __global__ void __launch_bounds__(CH_WARPS * 32) k_fin_chain(ReduceIO io, Reduce
     }
 }
 
-// ONE LANE PER HALF CHAIN of _monotone_hull (reduction.py:214-223): the sequential
-// loop as written, 32 chains per warp. Job 4w + kind as for k_fin_chain. The chain is
-// issue-light (one cross product per test), so many independent chains per warp
-// beat cooperative pop tests; the top two stack entries live in registers, the
-// stack itself in shared memory (lane-interleaved rows), and the keys are prefetched
-// KP ahead in registers. Jobs are bucketed by chain length, longest first, and a warp
-// claims 32 consecutive ones (similar lengths). A stack that would outgrow CS1 is
-// redone by half_chain_global.
-constexpr int C1_WARPS = 2;  // warps per CTA
-constexpr int CS1 = 32;      // stack entries per chain in shared memory
-constexpr int KP = 4;        // keys in flight per lane
-
-__global__ void __launch_bounds__(C1_WARPS * 32) k_fin_chain_lane(ReduceIO io, ReduceParams p) {
-    __shared__ double2 s_st[C1_WARPS][CS1][32];
-    __shared__ int32_t s_stp[C1_WARPS][CS1][32];
-    __shared__ int bstart[CH_BUCKETS + 1];
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    if (threadIdx.x == 0) {
-        int r = 0;
-        for (int k = 0; k < CH_BUCKETS; ++k) { bstart[k] = r; r += io.njob[k]; }
-        bstart[CH_BUCKETS] = r;
-    }
-    __syncthreads();
-    const int ntot = bstart[CH_BUCKETS];
-    const int64_t bcap = 4 * io.E * (int64_t)p.N;
-    double2 (*st)[32] = s_st[wib];
-    int32_t (*stp)[32] = s_stp[wib];
-    while (true) {
-        int base = 0;
-        if (lane == 0) base = atomicAdd(io.njob + CH_BUCKETS, 32);
-        base = __shfl_sync(FULL, base, 0);
-        if (base >= ntot) break;
-        const int idx = base + lane;
-        if (idx >= ntot) continue;
-        int k = 0;
-        for (int sz = CH_BUCKETS / 2; sz > 0; sz >>= 1)  // last k with bstart[k] <= idx
-            if (bstart[k + sz] <= idx) k += sz;
-        const int jw = io.jobs[k * bcap + idx - bstart[k]];
-        const int w = jw >> 2, kind = jw & 3;
-        const int64_t e = io.wenv[w];
-        const int q = w - io.patch_off[e];
-        const int32_t *mo = io.member_offsets + e * (p.N + 1);
-        const int m = mo[q + 1] - mo[q];
-        const int64_t row0 = io.cand_base[e] + mo[q];
-        const int L = kind < 2 ? m : io.pnt[w];
-        const bool fwd = (kind & 1) == 0;
-        const double2 *kuv = kind < 2 ? io.suv + row0 : io.tuv + row0;
-        const int32_t *kpos = kind < 2 ? nullptr : io.tpos + row0;
-        auto sidx_of = [&](int x) { return max(fwd ? x : L - 1 - x, 0); };  // L == 0: row 0, unused
-        double2 pre[KP];
-        int prp[KP];
-#pragma unroll
-        for (int j = 0; j < KP; ++j) {
-            const int sx = sidx_of(min(j, L - 1));
-            pre[j] = __ldg(kuv + sx);
-            prp[j] = kpos ? __ldg(kpos + sx) : sx;
-        }
-        double ou = 0.0, ov = 0.0, au = 0.0, av = 0.0;  // h[top - 2], h[top - 1]
-        int top = 0;
-        bool ovf = false;
-        for (int x0 = 0; x0 < L && !ovf; x0 += KP) {
-#pragma unroll
-            for (int j = 0; j < KP; ++j) {
-                const int x = x0 + j;
-                if (x < L && !ovf) {
-                    const double ub = pre[j].x, vb = pre[j].y;
-                    const int pb = prp[j];
-                    {   // refill this slot with key x + KP
-                        const int sx = sidx_of(min(x + KP, L - 1));
-                        pre[j] = __ldg(kuv + sx);
-                        prp[j] = kpos ? __ldg(kpos + sx) : sx;
-                    }
-                    // pop while cross(h[-2], h[-1], b) <= 0 (or NaN)
-                    while (top >= 2 && !((au - ou) * (vb - ov) - (av - ov) * (ub - ou) > 0.0)) {
-                        --top;
-                        au = ou; av = ov;
-                        if (top >= 2) { const double2 o = st[top - 2][lane]; ou = o.x; ov = o.y; }
-                    }
-                    if (top < CS1) {
-                        st[top][lane] = make_double2(ub, vb);
-                        stp[top][lane] = pb;
-                        ou = au; ov = av; au = ub; av = vb;
-                        ++top;
-                    } else {
-                        ovf = true;
-                    }
-                }
-            }
-        }
-        const int64_t h0 = 4 * row0 + (int64_t)kind * m;
-        int32_t *hj = io.hj + h0;
-        if (!ovf) {
-            for (int j = 0; j < top; ++j) hj[j] = stp[j][lane];
-        } else {
-            top = half_chain_global(kuv, kpos, L, fwd ? 1 : -1, hj, io.hu + h0, io.hv + h0);
-        }
-        io.hlen[4 * (int64_t)w + kind] = top;
-    }
-}
-
 // ------------------------------------------------------------------ stage 4: kept selection
 
 __device__ __forceinline__ int dec_k(int k) { return k < 0 ? ~k : k; }
@@ -1022,11 +921,7 @@ void launch_finalize(const ReduceIO &io, const ReduceParams &p, int sm_count, cu
         cudaEventRecord(fk->ev_block, sb);
         cudaStreamWaitEvent(s, fk->ev_block, 0);
     }
-#ifdef CS_CHAIN_GROUPS
     k_fin_chain<<<cap((int64_t)sm_count * 8 * FIN_GRID_CHAIN, (maxw + CH_WARPS - 1) / CH_WARPS), CH_WARPS * 32, 0, s>>>(io, p);
-#else
-    k_fin_chain_lane<<<cap((int64_t)sm_count * 16, (4 * maxw + 32 * C1_WARPS - 1) / (32 * C1_WARPS)), C1_WARPS * 32, 0, s>>>(io, p);
-#endif
     k_fin_kept<<<cap((int64_t)sm_count * 8 * FIN_GRID, (maxw + FK_WARPS - 1) / FK_WARPS), FK_WARPS * 32, 0, s>>>(io, p);
     if (fk) {
         cudaEventRecord(fk->ev_fold, sf);

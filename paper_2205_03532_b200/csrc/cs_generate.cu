@@ -225,9 +225,9 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int4 
         if (code & FACE_ITEM) {
             const uint2 loc = sloc[code & 0xffff];
             const int a = (int)(loc.x & 0xffffu), b = (int)(loc.x >> 16), c = (int)loc.y;
-            px = (vx[a] + vx[b] + vx[c]) / 3.0;
-            py = (vy[a] + vy[b] + vy[c]) / 3.0;
-            pz = (vz[a] + vz[b] + vz[c]) / 3.0;
+            px = div3(vx[a] + vx[b] + vx[c]);
+            py = div3(vy[a] + vy[b] + vy[c]);
+            pz = div3(vz[a] + vz[b] + vz[c]);
         } else {
             px = vx[code]; py = vy[code]; pz = vz[code];
         }
@@ -310,6 +310,13 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int4 
 // Same operations in the same order as the sequential loop; only the schedule
 // differs (uniform work per kernel instead of one divergent state machine).
 
+#ifndef PGD_FUSE_REST
+#define PGD_FUSE_REST 0  // stage 1 and the rest of the descent in one kernel (k_pgd_grad1_rest)
+#endif
+#ifndef PGD_FUSE0
+#define PGD_FUSE0 0  // iteration 0's gradient inside k_pgd_first (no stage-0 k_pgd_grad launch)
+#endif
+
 constexpr unsigned ACC_FINAL = 0x80000000u;  // accepted-list flag: the move ended the descent
 
 __device__ __forceinline__ void finish_face(const Staging &st, int64_t row, int blk, int face, double phi, double cd) {
@@ -346,7 +353,7 @@ __device__ __forceinline__ FaceGeom face_geom(const EnvXf &X, const MeshDesc *me
 // The descent's start (contacts/_kernels.py:40-52): the centroid, or the corner k_face_prep chose.
 __device__ __forceinline__ void face_start(const FaceGeom &f, int which, double &px, double &py, double &pz) {
     if (which == 0) {
-        px = (f.ax + f.bx + f.cx) / 3.0; py = (f.ay + f.by + f.cy) / 3.0; pz = (f.az + f.bz + f.cz) / 3.0;
+        px = div3(f.ax + f.bx + f.cx); py = div3(f.ay + f.by + f.cy); pz = div3(f.az + f.bz + f.cz);
     } else if (which == 1) {
         px = f.ax; py = f.ay; pz = f.az;
     } else if (which == 2) {
@@ -454,15 +461,27 @@ __global__ void __launch_bounds__(256, UNIFORM ? FIRST_MINB : FIRST_MINB - 1) k_
         const int face = hd.z & 0x3fffffff;
         const int e = hd.w;
         const EnvXf &X = xf[e];
-        const double gx = st.grad[3 * row], gy = st.grad[3 * row + 1], gz = st.grad[3 * row + 2];
         double phi = w->phi[3];
         const FaceGeom f = face_geom(X, meshes, mu, um, face);
         double px, py, pz;
         face_start(f, (int)((unsigned)hd.z >> 30), px, py, pz);
-        // a face that does not move ends here with this gradient: its point and phi go to
-        // the staging row only when it is found (the only rows k_compact reads)
+#if PGD_FUSE0
+        // iteration 0's gradient at the start point, here (no k_pgd_grad stage 0)
+        double gx, gy, gz;
+        gradient(grid_of<UNIFORM>(gu, sdfs, xf, e), px, py, pz, gx, gy, gz);
+        if (COUNT) ns += 6;
+#else
+        const double gx = st.grad[3 * row], gy = st.grad[3 * row + 1], gz = st.grad[3 * row + 2];
+#endif
+        // a face that does not move ends here with this gradient: its point, phi (and
+        // gradient) go to the staging row only when it is found (the only rows k_compact reads)
         auto done_here = [&]() {
-            if (phi <= X.cd) { st.point[3 * row] = px; st.point[3 * row + 1] = py; st.point[3 * row + 2] = pz; st.phi[row] = phi; }
+            if (phi <= X.cd) {
+                st.point[3 * row] = px; st.point[3 * row + 1] = py; st.point[3 * row + 2] = pz; st.phi[row] = phi;
+#if PGD_FUSE0
+                st.grad[3 * row] = gx; st.grad[3 * row + 1] = gy; st.grad[3 * row + 2] = gz;
+#endif
+            }
             finish_face(st, row, blk, face, phi, X.cd);
         };
         if (sqrt(gx * gx + gy * gy + gz * gz) < 1e-12) {  // contacts/_kernels.py:61-62: break
@@ -483,6 +502,64 @@ __global__ void __launch_bounds__(256, UNIFORM ? FIRST_MINB : FIRST_MINB - 1) k_
         const unsigned slot = atomicAdd(st.work_count + 2, 1u);
         st.acc[slot] = i | (moved < X.tol ? ACC_FINAL : 0u);
         st.acc_hd[slot] = hd;
+    }
+    if (COUNT) {
+        for (int o = 16; o; o >>= 1) ns += __shfl_xor_sync(0xffffffffu, ns, o);
+        if ((threadIdx.x & 31) == 0 && ns) atomicAdd(counter, ns);
+    }
+}
+
+// Iterations 1.. of a face still moving: (gx, gy, gz) is the gradient at p; on return
+// (p, phi, g) are the descent's final point, value and gradient.
+template <bool COUNT, class G>
+__device__ __forceinline__ void descend_rest(const G &g, const EnvXf &X, const FaceGeom &f, const double *vphi,
+                                             double &px, double &py, double &pz, double &phi, double alpha,
+                                             double &gx, double &gy, double &gz, unsigned long long &ns) {
+    for (int it = 1; it < MAX_MINIMIZE_ITERS; ++it) {
+        if (sqrt(gx * gx + gy * gy + gz * gz) < 1e-12) break;
+        double moved;
+        const bool acc = backtrack<COUNT>(g, f, vphi, gx, gy, gz, px, py, pz, phi, alpha, moved, ns);
+        if (acc) {  // the gradient at the new point: the next iteration's, or the final one
+            gradient(g, px, py, pz, gx, gy, gz);
+            if (COUNT) ns += 6;
+        }
+        if (moved < X.tol) break;
+    }
+}
+
+// Stage 1 fused with the rest of the descent: the gradient at the moved point of every
+// accepted face; faces not yet done continue their descent in the same thread (no
+// k_pgd_rest launch, and the long descents start as soon as their gradient is known).
+template <bool COUNT, bool UNIFORM>
+__global__ void __launch_bounds__(256, UNIFORM ? FIRST_MINB : FIRST_MINB - 1) k_pgd_grad1_rest(const EnvXf *__restrict__ xf,
+                                                  const SdfDesc *__restrict__ sdfs, const MeshDesc *__restrict__ meshes,
+                                                  Staging st, unsigned long long *__restrict__ counter, const PlanGrid gu,
+                                                  const MeshDesc mu, int um) {
+    const unsigned n = st.work_count[2];
+    unsigned long long ns = 0;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const unsigned a = st.acc[i];
+        const int4 hd = st.acc_hd[i];
+        const unsigned idx = a & ~ACC_FINAL;
+        const int64_t row = hd.x;
+        const int blk = hd.y, face = hd.z & 0x3fffffff, e = hd.w;
+        const PlanGrid &g = grid_of<UNIFORM>(gu, sdfs, xf, e);
+        double px = st.point[3 * row], py = st.point[3 * row + 1], pz = st.point[3 * row + 2];
+        double gx, gy, gz;
+        gradient(g, px, py, pz, gx, gy, gz);
+        if (COUNT) ns += 6;
+        double phi = st.phi[row];
+        if (!(a & ACC_FINAL)) {
+            const EnvXf &X = xf[e];
+            const FaceWork *w = st.work + idx;
+            const FaceGeom f = face_geom(X, meshes, mu, um, face);
+            const double vphi[3] = {w->phi[0], w->phi[1], w->phi[2]};
+            descend_rest<COUNT>(g, X, f, vphi, px, py, pz, phi, st.alpha[row], gx, gy, gz, ns);
+            st.point[3 * row] = px; st.point[3 * row + 1] = py; st.point[3 * row + 2] = pz;
+            st.phi[row] = phi;
+        }
+        st.grad[3 * row] = gx; st.grad[3 * row + 1] = gy; st.grad[3 * row + 2] = gz;
+        finish_face(st, row, blk, face, phi, xf[e].cd);
     }
     if (COUNT) {
         for (int o = 16; o; o >>= 1) ns += __shfl_xor_sync(0xffffffffu, ns, o);
@@ -511,19 +588,9 @@ __global__ void __launch_bounds__(128, UNIFORM ? REST_MINB : REST_MINB - 1) k_pg
         const FaceGeom f = face_geom(X, meshes, mu, um, face);
         const double vphi[3] = {w->phi[0], w->phi[1], w->phi[2]};
         double px = st.point[3 * row], py = st.point[3 * row + 1], pz = st.point[3 * row + 2];
-        double phi = st.phi[row], alpha = st.alpha[row];
+        double phi = st.phi[row];
         double gx = st.grad[3 * row], gy = st.grad[3 * row + 1], gz = st.grad[3 * row + 2];
-        for (int it = 1; it < MAX_MINIMIZE_ITERS; ++it) {
-            // (gx, gy, gz) is the gradient at p for this iteration
-            if (sqrt(gx * gx + gy * gy + gz * gz) < 1e-12) break;
-            double moved;
-            const bool acc = backtrack<COUNT>(g, f, vphi, gx, gy, gz, px, py, pz, phi, alpha, moved, ns);
-            if (acc) {  // the gradient at the new point: the next iteration's, or the final one
-                gradient(g, px, py, pz, gx, gy, gz);
-                if (COUNT) ns += 6;
-            }
-            if (moved < X.tol) break;
-        }
+        descend_rest<COUNT>(g, X, f, vphi, px, py, pz, phi, st.alpha[row], gx, gy, gz, ns);
         st.point[3 * row] = px; st.point[3 * row + 1] = py; st.point[3 * row + 2] = pz;
         st.phi[row] = phi;
         st.grad[3 * row] = gx; st.grad[3 * row + 1] = gy; st.grad[3 * row + 2] = gz;
@@ -686,10 +753,14 @@ void launch_pgd_wave(int sm_count, const int2 *block_map, const EnvXf *xf, const
     const unsigned g = (unsigned)sm_count * WAVE_GRID, gr = (unsigned)sm_count * REST_GRID;
 #define CS_WAVE(C, U)                                                                                 \
     do {                                                                                              \
-        k_pgd_grad<C, U><<<g, 256, 0, s>>>(block_map, xf, sdfs, meshes, st, 0, counter, gu, mu, um); \
+        if (!PGD_FUSE0) k_pgd_grad<C, U><<<g, 256, 0, s>>>(block_map, xf, sdfs, meshes, st, 0, counter, gu, mu, um); \
         k_pgd_first<C, U><<<g, 256, 0, s>>>(block_map, xf, sdfs, meshes, st, counter, gu, mu, um);   \
-        k_pgd_grad<C, U><<<g, 256, 0, s>>>(block_map, xf, sdfs, meshes, st, 1, counter, gu, mu, um); \
-        k_pgd_rest<C, U><<<gr, 128, 0, s>>>(block_map, xf, sdfs, meshes, st, counter, gu, mu, um);   \
+        if (PGD_FUSE_REST) {                                                                          \
+            k_pgd_grad1_rest<C, U><<<g, 256, 0, s>>>(xf, sdfs, meshes, st, counter, gu, mu, um);         \
+        } else {                                                                                      \
+            k_pgd_grad<C, U><<<g, 256, 0, s>>>(block_map, xf, sdfs, meshes, st, 1, counter, gu, mu, um); \
+            k_pgd_rest<C, U><<<gr, 128, 0, s>>>(block_map, xf, sdfs, meshes, st, counter, gu, mu, um);   \
+        }                                                                                             \
     } while (0)
     if (uniform) {
         if (counter) CS_WAVE(true, true); else CS_WAVE(false, true);
