@@ -197,18 +197,20 @@ struct Axis {
     int i;
 };
 
+// For finite g (the contract: poses and vertices are validated finite):
+//   * the lower clamp keeps numba's max(-0.0, 0.0) == -0.0 (a select, not DMNMX);
+//   * the upper clamp is a select too (fmin costs four instructions on sm_100);
+//   * d = g - c is +0.0 exactly when not clamped (no select);
+//   * i = min(floor(c), n - 2) and f = c - i: only c == n - 1 is clamped, where the
+//     reference's base cell n - 2 gives f = 1 (sdf/_kernels.py:261-270).
 __device__ __forceinline__ Axis make_axis(double g, double nm1, double nm2, int n2) {
     Axis a;
-    const bool lo = g < 0.0;
-    double c = lo ? 0.0 : g;
-    const bool hi = nm1 < c;
-    c = hi ? nm1 : c;
-    a.d = (lo || hi) ? g - c : 0.0;  // g - c is exactly 0 when not clamped
-    int ip = __double2int_rd(c);      // floor (c >= 0)
-    double fl = __int2double_rn(ip);
-    if (ip > n2) { ip = n2; fl = nm2; }
-    a.i = ip;
-    a.f = c - fl;
+    double c = g < 0.0 ? 0.0 : g;
+    c = nm1 < c ? nm1 : c;
+    a.d = g - c;
+    a.i = min(__double2int_rd(c), n2);  // floor (c >= 0)
+    a.f = c - __int2double_rn(a.i);
+    (void)nm2;
     return a;
 }
 
