@@ -420,7 +420,10 @@ __device__ __forceinline__ void carve(unsigned char *p, int cap, Keys &A, Keys &
 }
 
 constexpr size_t FW_BYTES_PER_WARP = (size_t)FW_SMEM * 2 * (8 + 8 + 4) + 9 * 32 * 8;
-constexpr int FB_SMEM = 1024;  // members a k_fin_sort_block CTA sorts in shared memory
+#ifndef FB_SMEM_DEF
+#define FB_SMEM_DEF 1024
+#endif
+constexpr int FB_SMEM = FB_SMEM_DEF;  // members a k_fin_sort_block CTA sorts in shared memory
 constexpr size_t FB_BYTES = (size_t)FB_SMEM * 2 * (8 + 8 + 4);
 
 // Patches of <= FW_SMEM members: one warp each.
