@@ -79,7 +79,7 @@ extern "C" int cs_debug_red_prof(unsigned long long *out) { return (int)cudaMemc
 // (warp, patch) its base, so each patch's members stay in ascending candidate order;
 // else warp 0 alone. Called by all RED_T threads after a barrier.
 __device__ void write_patches_csr(const ReduceIO &io, int N, int P, const double *bn, const unsigned long long *bmx,
-                                  int *hcnt, int *scratch, int SB, const int32_t *lab, int C) {
+                                  int *hcnt, int *scratch, size_t scratch_bytes, const int32_t *lab, int C) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
     __shared__ int s_ws2[WS_INTS];
@@ -96,7 +96,7 @@ __device__ void write_patches_csr(const ReduceIO &io, int N, int P, const double
     __syncthreads();
     int32_t *moff = io.member_offsets + e * (N + 1);
     int32_t *mem = io.members + base;
-    const bool par = (size_t)25 * SB >= (size_t)16 * N;
+    const bool par = scratch_bytes >= (size_t)16 * N;
     int *hw = par ? scratch : hcnt;  // [4][N] counts, then bases (par)
     if (par) {
         for (int q = tid; q < 4 * N; q += RED_T) hw[q] = 0;
@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(RED_T) k_reduce(ReduceIO io, ReduceParams p, i
         RED_MARK(3);
     }
     RED_MARK(2);
-    write_patches_csr(io, N, P, bn, bmx, hcnt, reinterpret_cast<int *>(bdep), SB, lab, C);
+    write_patches_csr(io, N, P, bn, bmx, hcnt, reinterpret_cast<int *>(bdep), (size_t)25 * SB, lab, C);
     RED_MARK(5);
 }
 
@@ -488,14 +488,17 @@ struct BestD {
 };
 
 __device__ __forceinline__ BestD warp_best(double v, int i, int cnt) {
+    // the max by 32-bit reductions over the order-preserving encoding (hi word, then
+    // lo word among the hi-word maxima); v + 0.0 maps -0.0 to +0.0 (numpy: equal)
     const unsigned FULL = 0xffffffffu;
-    double m = i >= 0 ? v : -INFINITY;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(FULL, m, o));
-    const bool has = __any_sync(FULL, i >= 0);
-    const int bi = __reduce_min_sync(FULL, (i >= 0 && v == m) ? i : INT_MAX);
+    const unsigned long long enc = i >= 0 ? enc_d(v + 0.0) : 0ull;  // 0: below every encoding
+    const unsigned hi = (unsigned)(enc >> 32), lo = (unsigned)enc;
+    const unsigned mh = __reduce_max_sync(FULL, hi);
+    const unsigned ml = __reduce_max_sync(FULL, hi == mh ? lo : 0u);
+    const bool top = i >= 0 && hi == mh && lo == ml;
+    const int bi = (int)__reduce_min_sync(FULL, top ? (unsigned)i : 0xffffffffu);
     const int c = __reduce_add_sync(FULL, cnt);
-    return BestD{m, has ? bi : -1, c};
+    return BestD{dec_d(((unsigned long long)mh << 32) | ml), bi, c};
 }
 
 __device__ __forceinline__ BestD block_best(BestD w, BestD *part) {
@@ -665,10 +668,15 @@ __global__ void __launch_bounds__(RED_T, 7) k_reduce_fast(ReduceIO io, ReducePar
     }
     if (tid == 0) io.red_slow[e] = 0;
     __syncthreads();
-    write_patches_csr(io, N, P, bn, bmx, hcnt, reinterpret_cast<int *>(bdep), SB, lab, C);
+    write_patches_csr(io, N, P, bn, bmx, hcnt, reinterpret_cast<int *>(bdep), (size_t)9 * SB, lab, C);
 }
 
 size_t reduce_smem_bytes(int N, int SB) { return red_smem_bytes(N, SB); }
+
+// k_reduce_fast's layout: builders [N] (36 B each), batch depths [SB] f64, flags [SB] u8.
+// Less than k_reduce's, so the L1 left beside 7 CTAs per SM holds the batch normals
+// the seed steps re-read.
+static size_t red_fast_smem_bytes(int N, int SB) { return (((size_t)N * 36 + 15) & ~(size_t)15) + (size_t)SB * 9; }
 
 void launch_reduce(const ReduceIO &io, const ReduceParams &p, int64_t max_batch, cudaStream_t s) {
     if (io.E <= 0) return;
@@ -684,10 +692,11 @@ void launch_reduce(const ReduceIO &io, const ReduceParams &p, int64_t max_batch,
     if (smem > 48 * 1024 && smem > cfg &&
         cudaFuncSetAttribute(k_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess)
         cfg = smem;
-    if (smem > 48 * 1024 && smem > cfg_fast &&
-        cudaFuncSetAttribute(k_reduce_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess)
-        cfg_fast = smem;
-    if (io.red_slow) k_reduce_fast<<<(unsigned)io.E, RED_T, smem, s>>>(io, p, SB);
+    const size_t fsmem = red_fast_smem_bytes(p.N, SB);
+    if (fsmem > 48 * 1024 && fsmem > cfg_fast &&
+        cudaFuncSetAttribute(k_reduce_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem) == cudaSuccess)
+        cfg_fast = fsmem;
+    if (io.red_slow) k_reduce_fast<<<(unsigned)io.E, RED_T, fsmem, s>>>(io, p, SB);
     k_reduce<<<(unsigned)io.E, RED_T, smem, s>>>(io, p, SB);
 }
 
