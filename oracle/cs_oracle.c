@@ -391,12 +391,21 @@ static void og_tangent_basis(const double *n, double *t1, double *t2) {
 }
 
 typedef struct { double u, v; int64_t pos; } og_uv;
+static int og_nan_last_cmp(double x, double y) {
+    const int xn = isnan(x), yn = isnan(y);
+    if (xn || yn) return xn - yn;
+    return (x < y) ? -1 : (x > y);
+}
+
 static int og_uv_cmp(const void *pa, const void *pb) {
+    /* numpy's sort order per key: NaN after every number, NaNs equal to each other
+     * (npy_sort's LT: a < b || (b != b && a == a)); lexsort is stable, so ties keep
+     * their positions */
     const og_uv *a = (const og_uv *)pa, *b = (const og_uv *)pb;
-    if (a->u < b->u) return -1;
-    if (a->u > b->u) return 1;
-    if (a->v < b->v) return -1;
-    if (a->v > b->v) return 1;
+    const int c = og_nan_last_cmp(a->u, b->u);
+    if (c) return c;
+    const int d = og_nan_last_cmp(a->v, b->v);
+    if (d) return d;
     return (a->pos < b->pos) ? -1 : (a->pos > b->pos);
 }
 

@@ -181,14 +181,14 @@ struct BlockTeam {
     __device__ void stats(ArgMax &am, double &mx, int &nan, int &cnt) const {
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
         WarpTeam{nullptr}.stats(am, mx, nan, cnt);
-        if (lane == 0) { this->am[wid] = am; dred[wid] = mx; ired[wid] = cnt | (nan ? (1 << 30) : 0); }
+        if (lane == 0) { this->am[wid] = am; dred[wid] = mx; ired[wid] = cnt | (nan << 29); }  // nan: 2 flag bits
         __syncthreads();
-        am = this->am[0]; mx = dred[0]; cnt = ired[0] & ~(1 << 30); nan = ired[0] >> 30;
+        am = this->am[0]; mx = dred[0]; cnt = ired[0] & ((1 << 29) - 1); nan = ired[0] >> 29;
         for (int i = 1; i < nw; ++i) {
             am = argmax_combine(am, this->am[i]);
             mx = fmax(mx, dred[i]);
-            cnt += ired[i] & ~(1 << 30);
-            nan |= ired[i] >> 30;
+            cnt += ired[i] & ((1 << 29) - 1);
+            nan |= ired[i] >> 29;
         }
         __syncthreads();
     }
@@ -221,7 +221,7 @@ struct Keys {
 // segment, then in every round binary-searches its split of the merge path of the
 // two runs it falls in and merges c outputs into the other buffer. log2(T) rounds.
 // Returns the buffer holding the result (0: a, 1: b).
-template <class Team>
+template <bool NANS, class Team>
 __device__ int team_merge_sort(const Team &t, Keys a, Keys b, int m) {
     const int T = t.size(), r = t.rank();
     const int c = (m + T - 1) / T;
@@ -233,7 +233,7 @@ __device__ int team_merge_sort(const Team &t, Keys a, Keys b, int m) {
         while (j >= s0) {
             const double uj = a.u[j], vj = a.v[j];
             const int kj = a.k[j];
-            if (!key_less(u, v, k, uj, vj, kj)) break;
+            if (!key_less<NANS>(u, v, k, uj, vj, kj)) break;
             a.u[j + 1] = uj; a.v[j + 1] = vj; a.k[j + 1] = kj;
             --j;
         }
@@ -250,7 +250,7 @@ __device__ int team_merge_sort(const Team &t, Keys a, Keys b, int m) {
             int lo = max(0, d - (b1 - a1)), hi = min(d, a1 - a0);
             while (lo < hi) {  // first A element that is not among the first d outputs
                 const int mid = (lo + hi) >> 1, bj = a1 + d - 1 - mid;
-                if (key_less(S.u[a0 + mid], S.v[a0 + mid], S.k[a0 + mid], S.u[bj], S.v[bj], S.k[bj])) lo = mid + 1;
+                if (key_less<NANS>(S.u[a0 + mid], S.v[a0 + mid], S.k[a0 + mid], S.u[bj], S.v[bj], S.k[bj])) lo = mid + 1;
                 else hi = mid;
             }
             int i = a0 + lo, j = a1 + (d - lo);
@@ -259,7 +259,7 @@ __device__ int team_merge_sort(const Team &t, Keys a, Keys b, int m) {
             if (i < a1) { ua = S.u[i]; va = S.v[i]; ka = S.k[i]; }
             if (j < b1) { ub = S.u[j]; vb = S.v[j]; kb = S.k[j]; }
             for (int o = s0; o < s1; ++o) {
-                if (j >= b1 || (i < a1 && key_less(ua, va, ka, ub, vb, kb))) {
+                if (j >= b1 || (i < a1 && key_less<NANS>(ua, va, ka, ub, vb, kb))) {
                     D.u[o] = ua; D.v[o] = va; D.k[o] = ka;
                     if (++i < a1) { ua = S.u[i]; va = S.v[i]; ka = S.k[i]; }
                 } else {
@@ -309,7 +309,7 @@ __device__ void sort_patch(const Team &t, const ReduceIO &io, const ReduceParams
     const int r = t.rank(), T = t.size();
     ArgMax am = {0.0, -1, 0};
     double mx = -INFINITY, s = 0.0;
-    bool anynan = false;
+    bool anynan = false, uvnan = false;
     int nt = 0;
     // member data of this rank's next member, loaded one chunk ahead (the loads are
     // DRAM latency: the candidate rows outgrow L2)
@@ -347,6 +347,7 @@ __device__ void sort_patch(const Team &t, const ReduceIO &io, const ReduceParams
                 // tie key 2k + touching: orders like k (k distinct) and carries the flag
                 // through the sort, so the rows below need no second gather of the depth
                 A.k[k] = 2 * k + (d >= 0.0 ? 1 : 0);
+                uvnan |= isnan(A.u[k]) || isnan(A.v[k]);
             }
         }
         if (FOLD) {
@@ -360,9 +361,10 @@ __device__ void sort_patch(const Team &t, const ReduceIO &io, const ReduceParams
         }
     }
     {
-        int nan = anynan ? 1 : 0;
+        int nan = (anynan ? 1 : 0) | (uvnan ? 2 : 0);
         t.stats(am, mx, nan, nt);
-        anynan = nan != 0;
+        anynan = (nan & 1) != 0;
+        uvnan = (nan & 2) != 0;
     }
     if (FOLD && r < 9) {
         const int kind = r / 3, c = r % 3;
@@ -388,7 +390,8 @@ __device__ void sort_patch(const Team &t, const ReduceIO &io, const ReduceParams
     }
     t.sync();
     if (!hull) return;
-    const Keys R = team_merge_sort(t, A, B, m) ? B : A;
+    // numpy's NaN order only where a projection is NaN (the comparisons stay plain otherwise)
+    const Keys R = (uvnan ? team_merge_sort<true>(t, A, B, m) : team_merge_sort<false>(t, A, B, m)) ? B : A;
     // sorted keys -> rows (non-touching members as ~k), and the touching keys alone,
     // in the same order, with their sorted positions (the touching chains' input)
     int run = 0;
@@ -565,7 +568,7 @@ __device__ int half_chain_global(const double2 *kuv, const int32_t *kpos, int L,
         const double2 b = kuv[s];
         while (top >= 2) {
             const double ou = hu[top - 2], ov = hv[top - 2], au = hu[top - 1], av = hv[top - 1];
-            if ((au - ou) * (b.y - ov) - (av - ov) * (b.x - ou) > 0.0) break;
+            if (!((au - ou) * (b.y - ov) - (av - ov) * (b.x - ou) <= 0.0)) break;  // NaN: no pop (Python)
             --top;
         }
         hu[top] = b.x; hv[top] = b.y; hj[top] = kpos ? kpos[s] : s;
@@ -669,7 +672,7 @@ __global__ void __launch_bounds__(CH_WARPS * 32) k_fin_chain(ReduceIO io, Reduce
                 bool popi = false;
                 if (more && top - li >= 2) {
                     const double2 a = st[top - 1 - li], o = st[top - 2 - li];
-                    popi = !((a.x - o.x) * (vb - o.y) - (a.y - o.y) * (ub - o.x) > 0.0);
+                    popi = (a.x - o.x) * (vb - o.y) - (a.y - o.y) * (ub - o.x) <= 0.0;  // NaN: no pop (Python)
                 }
                 const unsigned stop = (__ballot_sync(FULL, !popi) >> gb) & ((1u << CG) - 1u);
                 const int npop = more ? (stop ? __ffs(stop) - 1 : CG) : 0;

@@ -86,10 +86,26 @@ __device__ __forceinline__ void tangent_basis(const double *n, double *t1, doubl
 }
 
 // lexsort((v, u)) is a stable sort by (u, v); with the original position as the
-// last key it is a total order, so the bitonic network reproduces it exactly.
+// last key it is a total order, so the bitonic network reproduces it exactly. Per
+// key numpy orders NaN after every number and NaNs as equal (npy_sort's
+// LT(a, b) = a < b || (b != b && a == a)). NANS = false: keys known to be free of NaN.
+template <bool NANS = true>
 __device__ __forceinline__ bool key_less(double ua, double va, int pa, double ub, double vb, int pb) {
-    if (ua != ub) return ua < ub;
-    if (va != vb) return va < vb;
+    if (!NANS) {
+        if (ua != ub) return ua < ub;
+        if (va != vb) return va < vb;
+        return pa < pb;
+    }
+    if (ua != ub) {
+        if (ua < ub) return true;
+        if (ub < ua) return false;
+        if (isnan(ua) != isnan(ub)) return isnan(ub);  // one NaN: the number first
+    }
+    if (va != vb) {
+        if (va < vb) return true;
+        if (vb < va) return false;
+        if (isnan(va) != isnan(vb)) return isnan(vb);
+    }
     return pa < pb;
 }
 

@@ -51,6 +51,12 @@ def merge():
 
 
 @pytest.fixture(scope="session")
+def nan_cases():
+    """Reduction cases with NaN points, normals and depths (tests/golden/make_nan_golden.py)."""
+    return golden("red_nan.npz")
+
+
+@pytest.fixture(scope="session")
 def kat():
     return golden("kat.npz")
 

@@ -127,6 +127,18 @@ def test_reduce_contacts_merge_branch(P, merge):
         assert_same(pack_patch_list(patches, int(K)), merge, pre + "pt_", PATCH_KEYS, f"case {c} ")
 
 
+def test_reduce_contacts_nan_inputs(P, nan_cases):
+    """NaN points, normals and depths: numpy's NaN rules, as the reference ran them."""
+    for c in nan_cases["cases"]:
+        pre = f"c{c}_"
+        N, K, cone, md, bs = nan_cases[pre + "params"]
+        cs = P.ContactSet(nan_cases[pre + "cs_points"], nan_cases[pre + "cs_normals"], nan_cases[pre + "cs_depths"],
+                          nan_cases[pre + "cs_faces"], 0, 1)
+        rp = P.ReductionParams(int(N), int(K), float(cone), None if np.isnan(md) else float(md), int(bs))
+        patches = P.reduce_contacts(cs, rp)
+        assert_same(pack_patch_list(patches, int(K)), nan_cases, pre + "pt_", PATCH_KEYS, f"case {c} ")
+
+
 def test_batched_collide_r64(P, grid64, nut, gen64):
     """All six golden envs (two with a moved SDF pose) in one collide call."""
     envs = list(gen64["envs"])

@@ -71,6 +71,18 @@ def test_reduce_contacts_merge_branch(merge):
         assert_same(r, merge, pre + "pt_", PATCH_KEYS, f"case {c} ")
 
 
+def test_reduce_contacts_nan_inputs(nan_cases):
+    """NaN coordinates, normals and depths follow numpy's rules (NaN last in lexsort,
+    `cross <= 0` false on NaN, first-NaN argmax, NaN sums) as the reference ran them."""
+    for c in nan_cases["cases"]:
+        pre = f"c{c}_"
+        N, K, cone, md, bs = nan_cases[pre + "params"]
+        r = O.reduce_contacts(nan_cases[pre + "cs_points"], nan_cases[pre + "cs_normals"], nan_cases[pre + "cs_depths"],
+                              nan_cases[pre + "cs_faces"], max_patches=int(N), per_patch_cap=int(K),
+                              normal_cone_cos=cone, min_depth=None if np.isnan(md) else md, batch_size=int(bs))
+        assert_same(r, nan_cases, pre + "pt_", PATCH_KEYS, f"case {c} ")
+
+
 def test_sphere_plane_known_answers(kat):
     g = O.Grid(kat["sphere_values"], kat["sphere_dims"], kat["sphere_origin"], float(kat["sphere_voxel"]),
                kat["sphere_aabb_lo"], kat["sphere_aabb_hi"])
