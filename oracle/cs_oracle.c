@@ -732,7 +732,7 @@ int og_reduce_contacts(int64_t n, const double *points, const double *normals, c
     w.stack = (int64_t *)malloc(sizeof(int64_t) * 2 * nn);
     w.hull = (int64_t *)malloc(sizeof(int64_t) * 2 * nn);
     w.idx = (int64_t *)malloc(sizeof(int64_t) * 2 * nn);
-    w.x = (double *)malloc(sizeof(double) * 2 * nn);
+    w.x = (double *)malloc(sizeof(double) * 4 * nn);  /* the hull polygon (u, v): up to 2n - 2 vertices (NaN keys never pop) */
     w.y = (double *)malloc(sizeof(double) * 2 * nn);
     double *mp = (double *)malloc(sizeof(double) * 3 * nn);
     double *mn = (double *)malloc(sizeof(double) * 3 * nn);

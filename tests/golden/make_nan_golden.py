@@ -12,6 +12,12 @@ a point on the hull chain, reduction.py:215), lexsort orders NaN after every num
 coordinates: the projections u and/or v), in normals and in depths, alone and
 together, with and without min_depth, at several batch sizes, and are written to
 red_nan.npz in red_synth.npz's layout.
+
+Generation on a grid holding NaN nodes: the r64 bolt grid (grid_bolt_r64.npz) with
+40 nodes near the surface set to NaN (their flat indices are stored as g_bad), three
+of gen_r64's envs through generate_contacts + reduce_contacts as Scene calls them
+(ReductionParams(min_depth=-cd)); NaN samples never make a contact (phi <= cd is
+False) but NaN gradients give NaN normals, which reach the reduction.
 """
 
 from __future__ import annotations
@@ -25,8 +31,12 @@ REF = "/root/reference/pkg/src"
 if REF not in sys.path:
     sys.path.insert(0, REF)
 
+from contactsim.contacts.generation import generate_contacts  # noqa: E402
 from contactsim.contacts.reduction import reduce_contacts  # noqa: E402
-from contactsim.contacts.types import ContactSet, ReductionParams  # noqa: E402
+from contactsim.contacts.types import CollisionPairing, ContactSet, ReductionParams  # noqa: E402
+from contactsim.geometry.mesh import TriMesh  # noqa: E402
+from contactsim.math3d import Transform  # noqa: E402
+from contactsim.sdf.grid import SignedDistanceGrid  # noqa: E402
 
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from make_golden import flatten, pack_contactset, pack_patches  # noqa: E402
@@ -87,6 +97,33 @@ def main() -> None:
         cases.append(ci)
         print(f"nan case {ci}: n={n} {sorted(nans)} -> {len(patches)} patches")
     out["cases"] = np.array(cases)
+
+    g = np.load(os.path.join(OUT, "grid_bolt_r64.npz"))
+    m = np.load(os.path.join(OUT, "meshes.npz"))
+    gen = np.load(os.path.join(OUT, "gen_r64.npz"))
+    vals = g["values"].astype(np.float32).copy()
+    near = np.nonzero(np.abs(vals) < 2.0 * float(g["voxel"]))[0]
+    bad = np.sort(rng.choice(near, 40, replace=False))
+    vals[bad] = np.nan
+    grid = SignedDistanceGrid(g["origin"], float(g["voxel"]), g["dims"], vals, (g["aabb_lo"], g["aabb_hi"]))
+    nut = TriMesh(m["nut_v"], m["nut_t"])
+    cd = float(gen["cd"])
+    envs = [int(e) for e in gen["envs"][:3]]
+    out["g_bad"] = bad
+    out["g_envs"] = np.array(envs)
+    out["g_cd"] = np.array(cd)
+    for e in envs:
+        sp, mp = gen[f"e{e}_sdf_pose"], gen[f"e{e}_mesh_pose"]
+        cs = generate_contacts(CollisionPairing(0, 1), grid, nut, Transform.from_pose(sp[:3], sp[3:]),
+                               Transform.from_pose(mp[:3], mp[3:]), cd)
+        patches = reduce_contacts(cs, ReductionParams(min_depth=-cd))
+        pre = f"ge{e}_"
+        out[pre + "sdf_pose"] = sp
+        out[pre + "mesh_pose"] = mp
+        flatten(pre + "cs_", pack_contactset(cs), out)
+        flatten(pre + "pt_", pack_patches(patches, 6), out)
+        print(f"nan grid env {e}: {len(cs)} candidates ({int(np.isnan(cs.normals).any(axis=1).sum())} NaN normals) "
+              f"-> {len(patches)} patches")
     np.savez_compressed(os.path.join(OUT, "red_nan.npz"), **out)
 
 

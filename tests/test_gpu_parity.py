@@ -139,6 +139,26 @@ def test_reduce_contacts_nan_inputs(P, nan_cases):
         assert_same(pack_patch_list(patches, int(K)), nan_cases, pre + "pt_", PATCH_KEYS, f"case {c} ")
 
 
+def test_collide_on_nan_grid(P, nan_cases, grid64_npz, nut):
+    """A grid holding NaN nodes (no face bound for it; NaN normals reach the reduction
+    and seed patches up to the cap): batched collide against the reference's outputs."""
+    d = grid64_npz
+    vals = d["values"].astype(np.float32).copy()
+    vals[nan_cases["g_bad"]] = np.nan
+    grid = P.SignedDistanceGrid(d["origin"], float(d["voxel"]), d["dims"], vals, (d["aabb_lo"], d["aabb_hi"]))
+    envs = list(nan_cases["g_envs"])
+    E = len(envs)
+    cd = float(nan_cases["g_cd"])
+    sp = np.stack([nan_cases[f"ge{e}_sdf_pose"] for e in envs])
+    mp = np.stack([nan_cases[f"ge{e}_mesh_pose"] for e in envs])
+    res = P.collide([P.register_sdf(grid)] * E, [P.register_mesh(nut)] * E, sp, mp, np.full(E, cd))
+    for i, e in enumerate(envs):
+        cs = res.contact_set(i)
+        got = {"points": cs.points, "normals": cs.normals, "depths": cs.depths, "faces": cs.face_indices}
+        assert_same(got, nan_cases, f"ge{e}_cs_", CS_KEYS, f"env {e} ")
+        assert_same(pack_patch_list(res.patches(i), 6), nan_cases, f"ge{e}_pt_", PATCH_KEYS, f"env {e} ")
+
+
 def test_batched_collide_r64(P, grid64, nut, gen64):
     """All six golden envs (two with a moved SDF pose) in one collide call."""
     envs = list(gen64["envs"])

@@ -83,6 +83,23 @@ def test_reduce_contacts_nan_inputs(nan_cases):
         assert_same(r, nan_cases, pre + "pt_", PATCH_KEYS, f"case {c} ")
 
 
+def test_generate_reduce_on_nan_grid(nan_cases, meshes, grid64_npz):
+    """A grid with NaN nodes: NaN samples make no contact, NaN gradients make NaN normals
+    that seed patches up to the cap (eviction), as the reference ran it."""
+    g = O.Grid.from_npz(grid64_npz)
+    vals = g.values.copy()
+    vals[nan_cases["g_bad"]] = np.nan
+    g.values = vals
+    cd = float(nan_cases["g_cd"])
+    for e in nan_cases["g_envs"]:
+        pre = f"ge{e}_"
+        cs = O.generate_contacts(g, meshes["nut_v"], meshes["nut_t"], nan_cases[pre + "sdf_pose"],
+                                 nan_cases[pre + "mesh_pose"], cd)
+        assert_same(cs, nan_cases, pre + "cs_", CS_KEYS, f"env {e} ")
+        r = O.reduce_contacts(cs["points"], cs["normals"], cs["depths"], cs["faces"], min_depth=-cd)
+        assert_same(r, nan_cases, pre + "pt_", PATCH_KEYS, f"env {e} ")
+
+
 def test_sphere_plane_known_answers(kat):
     g = O.Grid(kat["sphere_values"], kat["sphere_dims"], kat["sphere_origin"], float(kat["sphere_voxel"]),
                kat["sphere_aabb_lo"], kat["sphere_aabb_hi"])
