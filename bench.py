@@ -305,6 +305,34 @@ def roofline(E, F, prep_ms, samples_prep, pgd_ms, samples_pgd, peaks, live) -> d
     return out
 
 
+def per_pair_leg(P, w, envs: int = 64) -> dict:
+    """The per-pair drop-in a reference user gets by swapping imports: one env at a time
+    through generate_contacts + reduce_contacts (contacts/generation.py, reduction.py),
+    called as Scene._collect_contacts does (scene.py:206-226: cd = 2 voxel,
+    ReductionParams(min_depth=-cd)), host arrays in and out of every call (the
+    ContactSet and the list[ContactPatch] are numpy). Timed on the host clock around
+    each synchronous call; the first call per plan (plan creation) is untimed."""
+    grid, nut = w["grid"], w["nut"]
+    pairing = P.CollisionPairing(0, 1)
+    cd = float(w["cd"][0])
+    rp = P.ReductionParams(min_depth=-cd)
+    sp = P.Transform()
+    tf = [P.Transform.from_pose(m[:3], m[3:]) for m in w["mesh_pose"][: envs + 1]]
+    P.reduce_contacts(P.generate_contacts(pairing, grid, nut, sp, tf[0], cd), rp)  # plans, JIT-free warm-up
+    tg, tr, nc = [], [], []
+    for k in range(1, envs + 1):
+        t0 = time.perf_counter()
+        cs = P.generate_contacts(pairing, grid, nut, sp, tf[k], cd)
+        t1 = time.perf_counter()
+        P.reduce_contacts(cs, rp)
+        t2 = time.perf_counter()
+        tg.append(t1 - t0); tr.append(t2 - t1); nc.append(len(cs))
+    return {"call": "generate_contacts + reduce_contacts, one env per call (host arrays in/out)", "envs": envs,
+            "ms_per_env": 1e3 * float(np.mean(np.add(tg, tr))), "gen_ms": 1e3 * float(np.mean(tg)),
+            "red_ms": 1e3 * float(np.mean(tr)), "candidates_per_env": float(np.mean(nc)),
+            "timing": "host clock around each synchronous drop-in call"}
+
+
 def solver_leg(P, plan, w, lo, hi, E, steps, quick, cpu_sample=64):
     """SURVEY §8(f) row 1, measured beside the headline: the contact solve of one
     substep (Plan.solve: rows from the reduced contacts, 16 position sweeps with
@@ -580,6 +608,8 @@ def main():
                "h2d_bytes_per_step": int(hsp.nbytes + hmp.nbytes + hcd.nbytes), "d2h_bytes_per_step": int(hst.nbytes),
                "ms_per_step": float(et.item()) / args.steps}
 
+    per_pair = per_pair_leg(P, w) if (world == 1 and not args.quick) else None
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -601,6 +631,7 @@ def main():
                           "backend": "nccl" if world > 1 else "local copy (N = 1)"},
             "eager": eager,
             "solver": solver,
+            "per_pair": per_pair,
             "stats": {"candidates_per_env": float(stats[:, 0].double().mean()),
                       "patches_per_env": float(stats[:, 1].double().mean()),
                       "kept_per_env": float(stats[:, 2].double().mean())},

@@ -901,12 +901,15 @@ void launch_finalize(const ReduceIO &io, const ReduceParams &p, int sm_count, cu
                                                                      io.large_count);
     const int64_t maxw = io.E * (int64_t)p.N;
     const size_t wsm = FW_BYTES_PER_WARP * FW_WARPS;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_fin_sort_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
-        cudaFuncSetAttribute(k_fin_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FB_BYTES);
-        configured = true;
-    }
+    // per device, and only once both raises succeeded (a failed raise leaves the launch
+    // to report the error)
+    static bool configured[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!configured[dev & 63] &&
+        cudaFuncSetAttribute(k_fin_sort_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm) == cudaSuccess &&
+        cudaFuncSetAttribute(k_fin_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FB_BYTES) == cudaSuccess)
+        configured[dev & 63] = true;
     auto cap = [&](int64_t want, int64_t limit) { return (unsigned)(want < limit ? want : limit); };
     // The three stage-1 kernels are independent (k_patch_env wrote the work lists): with
     // a fork they run as concurrent branches (graph branches when captured), so the
