@@ -11,6 +11,7 @@ import sys
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from bench import ClockSampler  # noqa: E402  (nvidia-smi clocks during the timed steps)
 
 
 def main():
@@ -36,9 +37,11 @@ def main():
         plan.collide(sp, mp, cd)
     torch.cuda.synchronize()
     plan.enable_timing(args.steps)
+    clocks = ClockSampler(torch.cuda.current_device())
     for _ in range(args.steps):
         plan.collide(sp, mp, cd)
     torch.cuda.synchronize()
+    clk = clocks.stop()
     ph = plan.read_timing(args.steps)
     t = float(ph[:, plan.PHASES.index("total")].mean())
     faces = int(sum(len(A[k]["mesh"].triangles) for k in asset))
@@ -48,7 +51,8 @@ def main():
             "phase_ms": {n: float(ph[:, i].mean()) for i, n in enumerate(plan.PHASES)},
             "candidates_per_env": {a["name"]: float(nc[asset == k].mean()) for k, a in enumerate(A)},
             "grids": {a["name"]: list(a["grid"].dims) for a in A},
-            "steps": args.steps, "warmup": args.warmup, "dtype": "f64",
+            "steps": args.steps, "warmup": args.warmup, "dtype": "f64", "clocks": clk,
+            "timing": "CUDA events around each eager collide (Plan.enable_timing)",
             "data": "synthetic (seeded poses, procedural assets)"}
     print(json.dumps(line), flush=True)
 

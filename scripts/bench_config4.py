@@ -16,6 +16,7 @@ import sys
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from bench import ClockSampler  # noqa: E402  (nvidia-smi clocks during the timed steps)
 
 
 def main():
@@ -60,6 +61,7 @@ def main():
         mps.step(dp, check=False)
     torch.cuda.synchronize()
     ms = []
+    clocks = ClockSampler(torch.cuda.current_device())
     for _ in range(args.steps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
@@ -67,6 +69,7 @@ def main():
         b.record()
         b.synchronize()
         ms.append(a.elapsed_time(b))
+    clk = clocks.stop()
     # the substep's contact solve of every scene (4 bodies; nut dynamic, bolt static, pads chain-driven)
     from paper_2205_03532_b200.dynamics import BatchedSolverState, SolverParams
 
@@ -101,7 +104,8 @@ def main():
             "patches_per_pair": {k: float(res.n_patch.cpu().numpy()[(kind == k) & act].mean())
                                  for k in ("bolt-nut", "pad-nut")},
             "solve_ms": float(np.median(sms)), "solve": "MultiPairScenes.solve: 16 pos + 1 vel sweeps per scene",
-            "steps": args.steps, "warmup": args.warmup, "dtype": "f64",
+            "steps": args.steps, "warmup": args.warmup, "dtype": "f64", "clocks": clk,
+            "timing": "CUDA events around each eager MultiPairScenes.step / solve (median)",
             "data": "synthetic (seeded SURVEY §8(d) poses, procedural assets)"}
     print(json.dumps(line), flush=True)
 

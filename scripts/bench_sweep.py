@@ -15,6 +15,7 @@ import sys
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from bench import ClockSampler  # noqa: E402  (nvidia-smi clocks during the timed steps)
 
 
 def main():
@@ -57,16 +58,19 @@ def main():
                 plan.collide(sp, mp, cd)
             torch.cuda.synchronize()
             plan.enable_timing(args.steps)
+            clocks = ClockSampler(torch.cuda.current_device())
             for _ in range(args.steps):
                 plan.collide(sp, mp, cd)
             torch.cuda.synchronize()
+            clk = clocks.stop()
             ph = plan.read_timing(args.steps)
             t = float(ph[:, plan.PHASES.index("total")].mean())
             nc = plan.n_cand.cpu().numpy()
             print(json.dumps({"res": res, "dims": list(grid.dims), "grid_mb": grid.values.nbytes / 1e6, "envs": E,
                               "ms_per_step": t, "face_queries_per_s": E * F / (t * 1e-3),
                               "candidates_per_env": float(nc.mean()),
-                              "phase_ms": {n: float(ph[:, i].mean()) for i, n in enumerate(plan.PHASES)}}), flush=True)
+                              "phase_ms": {n: float(ph[:, i].mean()) for i, n in enumerate(plan.PHASES)},
+                              "clocks": clk, "timing": "CUDA events around each eager collide"}), flush=True)
             del plan, sp, mp, cd  # frees the plan's buffers (collide._PlanHandle)
             gc.collect()
             torch.cuda.empty_cache()

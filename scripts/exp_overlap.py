@@ -18,7 +18,8 @@ mp = torch.from_numpy(np.ascontiguousarray(w["mesh_pose"])).cuda()
 cd = torch.from_numpy(np.ascontiguousarray(w["cd"])).cuda()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 main = torch.cuda.current_stream()
-for K in (1, 2, 3, 4, 8):
+SEQ = len(sys.argv) > 2 and sys.argv[2] == "seq"  # sub-plans one after the other on one stream
+for K in (1, 2, 4, 8, 16):
     n = E // K
     plans = [P.Plan([hs] * n, [hm] * n, P.ReductionParams()) for _ in range(K)]
     sl = [(k * n, (k + 1) * n) for k in range(K)]
@@ -34,7 +35,7 @@ for K in (1, 2, 3, 4, 8):
         for s in streams:
             s.wait_stream(cap)
         for pl, s, a in zip(plans, streams, args):
-            pl.collide(*a, stream=s)
+            pl.collide(*a, stream=cap if SEQ else s)
         for s in streams:
             cap.wait_stream(s)
     for _ in range(5):
