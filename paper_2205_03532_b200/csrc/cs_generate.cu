@@ -409,6 +409,14 @@ __global__ void __launch_bounds__(256, UNIFORM ? GRAD_MINB : GRAD_MINB - 1) k_pg
 
 // One backtracking search (contacts/_kernels.py:64-75) from (p, phi) along -g/|g|.
 // Returns true on an accepted move (p, phi, alpha updated, moved set).
+#ifdef BT_STATS
+__device__ unsigned long long g_bt_stat[16];  // accepted at try 0..3, no move, known projections, sampled; [8..]: k_pgd_first by start
+extern "C" int cs_debug_bt_stat(unsigned long long *out) { return (int)cudaMemcpyFromSymbol(out, g_bt_stat, sizeof(g_bt_stat)); }
+#define BT_STAT(i) atomicAdd(&g_bt_stat[i], 1ull)
+#else
+#define BT_STAT(i) ((void)0)
+#endif
+
 template <bool COUNT, class G>
 __device__ __forceinline__ bool backtrack(const G &g, const FaceGeom &f, const double *vphi, double gx, double gy,
                                           double gz, double &px, double &py, double &pz, double &phi, double &alpha,
@@ -425,15 +433,17 @@ __device__ __forceinline__ bool backtrack(const G &g, const FaceGeom &f, const d
         // the projection often is the current point or a corner itself: identical
         // inputs, so the sample's value is already known
         double phi_new;
-        if (same3(qx, qy, qz, px, py, pz)) phi_new = phi;
-        else if (same3(qx, qy, qz, f.ax, f.ay, f.az)) phi_new = vphi[0];
-        else if (same3(qx, qy, qz, f.bx, f.by, f.bz)) phi_new = vphi[1];
-        else if (same3(qx, qy, qz, f.cx, f.cy, f.cz)) phi_new = vphi[2];
+        if (same3(qx, qy, qz, px, py, pz)) { phi_new = phi; BT_STAT(5); BT_STAT(12); }
+        else if (same3(qx, qy, qz, f.ax, f.ay, f.az)) { phi_new = vphi[0]; BT_STAT(5); }
+        else if (same3(qx, qy, qz, f.bx, f.by, f.bz)) { phi_new = vphi[1]; BT_STAT(5); }
+        else if (same3(qx, qy, qz, f.cx, f.cy, f.cz)) { phi_new = vphi[2]; BT_STAT(5); }
         else {
             phi_new = sample(g, qx, qy, qz);
+            BT_STAT(6);
             if (COUNT) ns += 1;
         }
         if (phi_new < phi) {
+            BT_STAT(bt);
             moved = sqrt((qx - px) * (qx - px) + (qy - py) * (qy - py) + (qz - pz) * (qz - pz));
             px = qx; py = qy; pz = qz;
             phi = phi_new;
@@ -442,6 +452,7 @@ __device__ __forceinline__ bool backtrack(const G &g, const FaceGeom &f, const d
         }
         alpha *= 0.5;
     }
+    BT_STAT(4);
     moved = 0.0;
     return false;
 }
@@ -492,9 +503,12 @@ __global__ void __launch_bounds__(256, UNIFORM ? FIRST_MINB : FIRST_MINB - 1) k_
         const double vphi[3] = {w->phi[0], w->phi[1], w->phi[2]};
         double alpha = g.voxel, moved;
         if (!backtrack<COUNT>(g, f, vphi, gx, gy, gz, px, py, pz, phi, alpha, moved, ns)) {
+            BT_STAT(((unsigned)hd.z >> 30) == 0 ? 8 : 9);  // no move: centroid / vertex start
+            if (((unsigned)hd.z >> 30) != 0) BT_STAT(12 + ((unsigned)hd.z >> 30));  // [13..15]: at vertex a / b / c
             done_here();  // no move: this gradient is the final one
             continue;
         }
+        BT_STAT(((unsigned)hd.z >> 30) == 0 ? 10 : 11);  // moved: centroid / vertex start
         st.point[3 * row] = px; st.point[3 * row + 1] = py; st.point[3 * row + 2] = pz;
         st.phi[row] = phi;
         st.alpha[row] = alpha;
