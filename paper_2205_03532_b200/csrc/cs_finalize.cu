@@ -282,7 +282,7 @@ __device__ __forceinline__ bool needs_touch_hull(int m, int nt, int K) { return 
 
 // Patch w = (e, q), by a team (warp or CTA). A/B: the team's sort buffers (shared
 // memory, or the patch's global rows when it is very large); B holds the member
-// weights until the sort. tile: 9 x T doubles of shared memory.
+// weights until the sort. tile: 9 x (T + 1) doubles of shared memory (padded rows).
 //   * one pass over the members: deepest (first argmax), max depth, touching count,
 //     weights, the nine weighted products (np.cross(pts, norms) * w etc.) through
 //     the tile, folded by ranks 0..8 in member order (numpy's axis-0 sums add row
@@ -335,11 +335,12 @@ __device__ void sort_patch(const Team &t, const ReduceIO &io, const ReduceParams
             if (FOLD) {
                 const double wk = weight_of(d);
                 wb[k] = wk;
-                tile[0 * T + r] = px * wk; tile[1 * T + r] = py * wk; tile[2 * T + r] = pz * wk;
-                tile[3 * T + r] = nx * wk; tile[4 * T + r] = ny * wk; tile[5 * T + r] = nz * wk;
-                tile[6 * T + r] = (py * nz - pz * ny) * wk;
-                tile[7 * T + r] = (pz * nx - px * nz) * wk;
-                tile[8 * T + r] = (px * ny - py * nx) * wk;
+                const int TP = T + 1;  // padded tile rows: the folding ranks read distinct banks
+                tile[0 * TP + r] = px * wk; tile[1 * TP + r] = py * wk; tile[2 * TP + r] = pz * wk;
+                tile[3 * TP + r] = nx * wk; tile[4 * TP + r] = ny * wk; tile[5 * TP + r] = nz * wk;
+                tile[6 * TP + r] = (py * nz - pz * ny) * wk;
+                tile[7 * TP + r] = (pz * nx - px * nz) * wk;
+                tile[8 * TP + r] = (px * ny - py * nx) * wk;
             }
             if (hull) {
                 A.u[k] = V3(px, py, pz, t1[0], t1[1], t1[2]);  // _project_2d: (n,3) @ (3,), n >= 2
@@ -354,8 +355,11 @@ __device__ void sort_patch(const Team &t, const ReduceIO &io, const ReduceParams
             t.sync();
             if (r < 9) {
                 const int cnt = min(T, m - c0);
-                const double *row = tile + r * T;
-                for (int j = 0; j < cnt; ++j) s = (c0 + j == 0) ? row[j] : s + row[j];
+                const double *row = tile + r * (T + 1);
+                int j = 0;
+                if (c0 == 0) { s = row[0]; j = 1; }
+#pragma unroll 8
+                for (; j < cnt; ++j) s = s + row[j];
             }
             t.sync();
         }
@@ -422,7 +426,7 @@ __device__ __forceinline__ void carve(unsigned char *p, int cap, Keys &A, Keys &
     B = Keys{d + 2 * cap, d + 3 * cap, k + cap};
 }
 
-constexpr size_t FW_BYTES_PER_WARP = (size_t)FW_SMEM * 2 * (8 + 8 + 4) + 9 * 32 * 8;
+constexpr size_t FW_BYTES_PER_WARP = (size_t)FW_SMEM * 2 * (8 + 8 + 4) + 9 * 33 * 8;
 #ifndef FB_SMEM_DEF
 #define FB_SMEM_DEF 1024
 #endif
@@ -484,10 +488,14 @@ __global__ void __launch_bounds__(FB_THREADS) k_fin_sort_block(ReduceIO io, Redu
 // the tile in member order (numpy's axis-0 sums add row after row); the weights
 // are kept for lane 9's pairwise sum.
 constexpr int FL_WARPS = 4;
+#ifndef FOLD_TILE_STRIDE
+#define FOLD_TILE_STRIDE 33
+#endif
+constexpr int FT = FOLD_TILE_STRIDE;  // tile row stride (doubles)
 constexpr int FL_W = 1024;  // weights per warp in shared memory (larger patches: global scratch)
 
 __global__ void __launch_bounds__(FL_WARPS * 32) k_fin_fold_large(ReduceIO io, ReduceParams p) {
-    __shared__ double s_tile[FL_WARPS][9 * 32];
+    __shared__ double s_tile[FL_WARPS][9 * FT];
     __shared__ double s_w[FL_WARPS][FL_W];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     double *tile = s_tile[wib];
@@ -522,17 +530,20 @@ __global__ void __launch_bounds__(FL_WARPS * 32) k_fin_fold_large(ReduceIO io, R
                 const double wk = weight_of(fd);
                 fetch(k + 32);
                 wb[k] = wk;
-                tile[0 * 32 + lane] = px * wk; tile[1 * 32 + lane] = py * wk; tile[2 * 32 + lane] = pz * wk;
-                tile[3 * 32 + lane] = nx * wk; tile[4 * 32 + lane] = ny * wk; tile[5 * 32 + lane] = nz * wk;
-                tile[6 * 32 + lane] = (py * nz - pz * ny) * wk;
-                tile[7 * 32 + lane] = (pz * nx - px * nz) * wk;
-                tile[8 * 32 + lane] = (px * ny - py * nx) * wk;
+                tile[0 * FT + lane] = px * wk; tile[1 * FT + lane] = py * wk; tile[2 * FT + lane] = pz * wk;
+                tile[3 * FT + lane] = nx * wk; tile[4 * FT + lane] = ny * wk; tile[5 * FT + lane] = nz * wk;
+                tile[6 * FT + lane] = (py * nz - pz * ny) * wk;
+                tile[7 * FT + lane] = (pz * nx - px * nz) * wk;
+                tile[8 * FT + lane] = (px * ny - py * nx) * wk;
             }
             __syncwarp();
-            if (lane < 9) {
+            if (lane < 9) {  // lane l folds tile row l (rows FT doubles apart: distinct banks)
                 const int cnt = min(32, m - c0);
-                const double *row = tile + lane * 32;
-                for (int j = 0; j < cnt; ++j) s = (c0 + j == 0) ? row[j] : s + row[j];
+                const double *row = tile + lane * FT;
+                int j = 0;
+                if (c0 == 0) { s = row[0]; j = 1; }
+#pragma unroll 8
+                for (; j < cnt; ++j) s = s + row[j];
             }
             __syncwarp();
         }
