@@ -97,6 +97,10 @@ extern "C" int cs_debug_bound_stat(unsigned long long *out) { return (int)cudaMe
 #else
 #define PREP_MARK(i) do {} while (0)
 #endif
+#ifdef BOX_STATS
+__device__ unsigned long long g_box_stat[8];  // chunks, sum of box cells, boxes <= 4k / 8k / 16k cells, samples
+extern "C" int cs_debug_box_stat(unsigned long long *out) { return (int)cudaMemcpyFromSymbol(out, g_box_stat, sizeof(g_box_stat)); }
+#endif
 constexpr int FACE_ITEM = 1 << 30;  // sample-list code of a face centre (else a vertex slot)
 
 // k_face_prep: one CTA per (env, chunk of FACE_CHUNK faces). The chunk's distinct
@@ -219,6 +223,37 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int4 
     // generation.py:92) and the centre of every near face (the centroid start point;
     // only used when the face survives the Lipschitz prune below).
     const int nl = s_nl;
+#ifdef BOX_STATS
+    {   // the chunk's sample box (cells of every queued sample): could it be staged in shared memory?
+        __shared__ int bb[6];
+        if (threadIdx.x < 3) { bb[threadIdx.x] = INT_MAX; bb[3 + threadIdx.x] = INT_MIN; }
+        __syncthreads();
+        for (int i = threadIdx.x; i < nl; i += FACE_CHUNK) {
+            const int code = list[i];
+            double px, py, pz;
+            if (code & FACE_ITEM) {
+                const uint2 loc = sloc[code & 0xffff];
+                const int a = (int)(loc.x & 0xffffu), b = (int)(loc.x >> 16), c = (int)loc.y;
+                px = div3(vx[a] + vx[b] + vx[c]); py = div3(vy[a] + vy[b] + vy[c]); pz = div3(vz[a] + vz[b] + vz[c]);
+            } else {
+                px = vx[code]; py = vy[code]; pz = vz[code];
+            }
+            const GPoint q = gpoint(grid, px, py, pz);
+            atomicMin(bb + 0, q.ax.i); atomicMin(bb + 1, q.ay.i); atomicMin(bb + 2, q.az.i);
+            atomicMax(bb + 3, q.ax.i); atomicMax(bb + 4, q.ay.i); atomicMax(bb + 5, q.az.i);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && nl > 0) {
+            const long long V = (long long)(bb[3] - bb[0] + 2) * (bb[4] - bb[1] + 2) * (bb[5] - bb[2] + 2);
+            atomicAdd(&g_box_stat[0], 1ull);
+            atomicAdd(&g_box_stat[1], (unsigned long long)V);
+            if (V <= 4096) atomicAdd(&g_box_stat[2], 1ull);
+            if (V <= 8192) atomicAdd(&g_box_stat[3], 1ull);
+            if (V <= 16384) atomicAdd(&g_box_stat[4], 1ull);
+            atomicAdd(&g_box_stat[5], (unsigned long long)nl);
+        }
+    }
+#endif
     for (int i = threadIdx.x; i < nl; i += FACE_CHUNK) {
         const int code = list[i];
         double px, py, pz;
