@@ -165,6 +165,12 @@ struct cs_plan {
     cs_outputs out{};
     // host e2e staging
     double *in_sdf = nullptr, *in_mesh = nullptr, *in_cd = nullptr;
+    // cs_collide_host replays the collide from a CUDA graph captured on its second call
+    // (the first, eager, does the lazy setup); none while phase timing is on
+    cudaGraphExec_t host_exec = nullptr;
+    cudaStream_t host_cap = nullptr;
+    int32_t host_fmt = -1, host_calls = 0;
+    bool host_graph_failed = false;
     int32_t *status = nullptr;
     double *env_min_depth = nullptr;  // scene semantics: min_depth None -> -cd per env
     unsigned long long *sample_counter = nullptr;  // non-null: counting builds ([0] prep, [1] pgd)
@@ -205,6 +211,8 @@ struct cs_plan {
         return &fork;
     }
     ~cs_plan() {
+        if (host_exec) cudaGraphExecDestroy(host_exec);
+        if (host_cap) cudaStreamDestroy(host_cap);
         if (fork_ready) {
             cudaStreamDestroy(fork.s_block); cudaStreamDestroy(fork.s_fold);
             cudaEventDestroy(fork.ev_fork); cudaEventDestroy(fork.ev_block); cudaEventDestroy(fork.ev_fold);
@@ -1004,8 +1012,40 @@ int cs_collide_host(cs_plan *P, const double *sdf_pose_host, const double *mesh_
     CS_CUDA(cudaMemcpyAsync(P->in_sdf, sdf_pose_host, sizeof(double) * w * (size_t)P->E, cudaMemcpyHostToDevice, s));
     CS_CUDA(cudaMemcpyAsync(P->in_mesh, mesh_pose_host, sizeof(double) * w * (size_t)P->E, cudaMemcpyHostToDevice, s));
     CS_CUDA(cudaMemcpyAsync(P->in_cd, contact_distance_host, sizeof(double) * (size_t)P->E, cudaMemcpyHostToDevice, s));
-    int r = cs_collide(P, P->in_sdf, P->in_mesh, pose_format, P->in_cd, stream);
-    if (r) return r;
+    // The step from a CUDA graph (the kernels' launch gaps removed): captured on a plan
+    // stream from the second call on, per pose format; eager while phase timing is on or
+    // if the capture failed.
+    bool replayed = false;
+    if (P->events.empty() && !P->host_graph_failed) {
+        if ((!P->host_exec || P->host_fmt != pose_format) && P->host_calls >= 1) {
+            if (P->host_exec) { cudaGraphExecDestroy(P->host_exec); P->host_exec = nullptr; }
+            cudaGraph_t graph = nullptr;
+            bool ok = P->host_cap || cudaStreamCreateWithFlags(&P->host_cap, cudaStreamNonBlocking) == cudaSuccess;
+            ok = ok && cudaStreamBeginCapture(P->host_cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+            if (ok) {
+                const int rc = cs_collide(P, P->in_sdf, P->in_mesh, pose_format, P->in_cd, P->host_cap);
+                ok = cudaStreamEndCapture(P->host_cap, &graph) == cudaSuccess && rc == CS_OK && graph;
+            }
+            ok = ok && cudaGraphInstantiate(&P->host_exec, graph, 0) == cudaSuccess;
+            if (graph) cudaGraphDestroy(graph);
+            if (!ok) {
+                if (P->host_exec) cudaGraphExecDestroy(P->host_exec);
+                P->host_exec = nullptr;
+                P->host_graph_failed = true;
+                cudaGetLastError();  // the failed capture's error is not the caller's
+            }
+            P->host_fmt = pose_format;
+        }
+        if (P->host_exec && P->host_fmt == pose_format) {
+            CS_CUDA(cudaGraphLaunch(P->host_exec, s));
+            replayed = true;
+        }
+    }
+    ++P->host_calls;
+    if (!replayed) {
+        const int r = cs_collide(P, P->in_sdf, P->in_mesh, pose_format, P->in_cd, stream);
+        if (r) return r;
+    }
     if (stats_host && (P->stages & CS_STAGE_REDUCE))
         CS_CUDA(cudaMemcpyAsync(stats_host, P->io.stats, sizeof(float) * 4 * (size_t)P->E, cudaMemcpyDeviceToHost, s));
     CS_CUDA(cudaStreamSynchronize(s));

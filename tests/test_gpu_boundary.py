@@ -233,3 +233,42 @@ def test_collide_on_a_side_stream(P, grid64, nut, gen64):
 
     with pytest.raises(NonFiniteStateError):
         P.collide(hs, hm, sp, bad, cd, stream=s)
+
+
+def test_collide_host_graph_replay(P, grid64, nut, gen64):
+    """cs_collide_host replays the step from a CUDA graph after its first call: every call
+    (eager, capture, replays, a pose-format switch) gives the device path's results."""
+    from paper_2205_03532_b200 import _native
+    from paper_2205_03532_b200.collide import Plan
+
+    envs = list(gen64["envs"])
+    E = len(envs)
+    cd = np.full(E, float(gen64["cd"]))
+    sp = np.ascontiguousarray(np.stack([gen64[f"e{e}_sdf_pose"] for e in envs]))
+    mp = np.ascontiguousarray(np.stack([gen64[f"e{e}_mesh_pose"] for e in envs]))
+    host = Plan([P.register_sdf(grid64)] * E, [P.register_mesh(nut)] * E, P.ReductionParams())
+    dev = Plan([P.register_sdf(grid64)] * E, [P.register_mesh(nut)] * E, P.ReductionParams())
+    rng = np.random.default_rng(7)
+    fields = ("n_cand", "n_patch", "n_kept", "stats", "cand_point", "cand_normal", "kept_cand", "area", "w_sum")
+    for k in range(5):
+        mpk = mp.copy()
+        mpk[:, :3] += rng.uniform(-2e-4, 2e-4, size=(E, 3))  # a different step each call
+        stats = host.collide_host(sp, mpk, cd)
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+        dev.collide(t(sp), t(mpk), t(cd))
+        torch.cuda.synchronize()
+        assert np.array_equal(stats, dev.stats.cpu().numpy())
+        for f in fields:
+            a, b = getattr(host, f).cpu().numpy(), getattr(dev, f).cpu().numpy()
+            assert np.array_equal(a, b, equal_nan=True), (k, f)
+    # the 12-value pose format: a new capture
+    def pose12(p7):
+        return np.stack([P.Transform.from_pose(p[:3], p[3:]).pose12() for p in p7])
+    for _ in range(2):
+        stats = host.collide_host(np.ascontiguousarray(pose12(sp)), np.ascontiguousarray(pose12(mp)), cd,
+                                  pose_format=_native.CS_POSE12)
+        dev.collide(torch.from_numpy(pose12(sp)).cuda(), torch.from_numpy(pose12(mp)).cuda(),
+                    torch.from_numpy(cd).cuda(), pose_format=_native.CS_POSE12)
+        torch.cuda.synchronize()
+        assert np.array_equal(stats, dev.stats.cpu().numpy())
+        assert np.array_equal(host.cand_point.cpu().numpy(), dev.cand_point.cpu().numpy())
