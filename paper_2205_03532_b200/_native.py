@@ -191,6 +191,17 @@ def hand_to_stream(stream, *tensors) -> None:
             t.record_stream(stream)
 
 
+def fetch(*tensors) -> list:
+    """Device tensors to numpy with ONE synchronisation: every copy is queued
+    asynchronously (into pinned host memory) on the current stream, then the stream is
+    waited for once (instead of a blocking .cpu() per tensor)."""
+    import torch
+
+    host = [t.to("cpu", non_blocking=True) for t in tensors]
+    torch.cuda.current_stream().synchronize()
+    return [h.numpy() for h in host]
+
+
 def sync_stream(stream=None) -> None:
     """Block until `stream` (default: the current stream) has finished."""
     import torch

@@ -356,24 +356,26 @@ class ReducedContacts:
 
     def contact_set(self, e: int, body_a: int = -1, body_b: int = -1) -> ContactSet:
         p = self.plan
-        base = int(p.cand_base[e].item())
-        n = int(p.n_cand[e].item())
+        base_n = _native.fetch(p.cand_base[e: e + 1], p.n_cand[e: e + 1])
+        base, n = int(base_n[0][0]), int(base_n[1][0])
         sl = slice(base, base + n)
-        return ContactSet(p.cand_point[sl].cpu().numpy(), p.cand_normal[sl].cpu().numpy(),
-                          p.cand_depth[sl].cpu().numpy(), p.cand_face[sl].cpu().numpy().astype(np.int64), body_a, body_b)
+        pt, nr, dp, fc = _native.fetch(p.cand_point[sl], p.cand_normal[sl], p.cand_depth[sl], p.cand_face[sl])
+        return ContactSet(pt, nr, dp, fc.astype(np.int64), body_a, body_b)
 
     def patches(self, e: int, face_indices: np.ndarray | None = None) -> list[ContactPatch]:
         """list[ContactPatch] of env e in slot order (reduction.py:75)."""
         p = self.plan
-        P = int(p.n_patch[e].item())
+        # two synchronisations: the env's counts and offsets, then every field at once
+        np_, base, moff = _native.fetch(p.n_patch[e: e + 1], p.cand_base[e: e + 1], p.member_offsets[e])
+        P, base = int(np_[0]), int(base[0])
         if P == 0:
             return []
-        base = int(p.cand_base[e].item())
-        moff = p.member_offsets[e, : P + 1].cpu().numpy().astype(np.int64)
-        members = p.members[base: base + int(moff[-1])].cpu().numpy().astype(np.int64)
-        host = {k: getattr(p, k)[e, :P].cpu().numpy() for k in (
-            "patch_normal", "patch_nkept", "kept_cand", "kept_point", "kept_normal", "kept_depth", "kept_face",
-            "w_sum", "wp_sum", "wn_sum", "wt_sum", "area", "max_depth")}
+        moff = moff[: P + 1].astype(np.int64)
+        keys = ("patch_normal", "patch_nkept", "kept_cand", "kept_point", "kept_normal", "kept_depth", "kept_face",
+                "w_sum", "wp_sum", "wn_sum", "wt_sum", "area", "max_depth")
+        got = _native.fetch(p.members[base: base + int(moff[-1])], *(getattr(p, k)[e, :P] for k in keys))
+        members = got[0].astype(np.int64)
+        host = dict(zip(keys, got[1:]))
         out = []
         for q in range(P):
             k = int(host["patch_nkept"][q])

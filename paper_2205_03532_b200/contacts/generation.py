@@ -87,12 +87,11 @@ def generate_contacts(pairing: CollisionPairing, grid: SignedDistanceGrid, mesh:
     poses = torch.from_numpy(np.stack([sdf_pose.pose12(), mesh_pose.pose12()])).cuda()
     cd = torch.tensor([float(contact_distance)], dtype=torch.float64, device="cuda")
     plan.collide(poses[0:1].contiguous(), poses[1:2].contiguous(), cd, _native.CS_POSE12)
-    n = int(plan.n_cand[0].item())
+    n = int(_native.fetch(plan.n_cand[0:1])[0][0])
     if n == 0:
         return ContactSet.empty(pairing.sdf_body, pairing.mesh_body)
-    return ContactSet(plan.cand_point[:n].cpu().numpy(), plan.cand_normal[:n].cpu().numpy(),
-                      plan.cand_depth[:n].cpu().numpy(), plan.cand_face[:n].cpu().numpy().astype(np.int64),
-                      pairing.sdf_body, pairing.mesh_body)
+    pt, nr, dp, fc = _native.fetch(plan.cand_point[:n], plan.cand_normal[:n], plan.cand_depth[:n], plan.cand_face[:n])
+    return ContactSet(pt, nr, dp, fc.astype(np.int64), pairing.sdf_body, pairing.mesh_body)
 
 
 def face_contacts(values, nx, ny, nz, ox, oy, oz, voxel, tri_verts, contact_distance, max_iters, tol, out_point,
