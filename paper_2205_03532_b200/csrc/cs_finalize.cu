@@ -750,13 +750,15 @@ __device__ void kept_patch(const WarpTeam &t, const ReduceIO &io, const ReducePa
     if (m >= 3) {
         const HullView h{hj, hj + m, len.x, (len.x - 1) + (len.y - 1)};
         const int H = h.H;
-        if (H >= 3 && H <= KH) {  // the hull's (u, v) staged by the warp, the sums in lane 0
+        if (H >= 3 && H <= KH) {  // the hull's (u, v) staged by the warp; lanes 0 and 1 run the two dots
             for (int k = lane; k < H; k += 32) huv[k] = suv[h.at(k)];
             __syncwarp();
-            if (lane == 0) {
-                const double d1 = ddot_x2(H, [&](int k) { return huv[k].x; }, [&](int k) { return huv[(k + 1) % H].y; });
-                const double d2 = ddot_x2(H, [&](int k) { return huv[k].y; }, [&](int k) { return huv[(k + 1) % H].x; });
-                area = 0.5 * fabs(d1 - d2);
+            if (lane < 2) {  // lane 0: d1 = x . roll(y, -1), lane 1: d2 = y . roll(x, -1) (same code, own data)
+                const double *hd = reinterpret_cast<const double *>(huv);
+                const double d = ddot_x2(H, [&](int k) { return hd[2 * k + lane]; },
+                                         [&](int k) { return hd[2 * (k + 1 == H ? 0 : k + 1) + 1 - lane]; });
+                const double d2 = __shfl_sync(0x3u, d, 1);
+                if (lane == 0) area = 0.5 * fabs(d - d2);
             }
             __syncwarp();
         } else if (H >= 3 && lane == 0) {
