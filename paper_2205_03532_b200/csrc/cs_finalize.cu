@@ -32,7 +32,7 @@
 namespace cs {
 
 #ifndef FW_WARPS
-#define FW_WARPS 8      // warp teams per k_fin_sort_warp CTA
+#define FW_WARPS 4      // warp teams per k_fin_sort_warp CTA
 #endif
 #ifndef FW_SMEM
 #define FW_SMEM 128     // members per warp-path patch (all in shared memory)
@@ -434,7 +434,10 @@ constexpr int FB_SMEM = FB_SMEM_DEF;  // members a k_fin_sort_block CTA sorts in
 constexpr size_t FB_BYTES = (size_t)FB_SMEM * 2 * (8 + 8 + 4);
 
 // Patches of <= FW_SMEM members: one warp each.
-__global__ void __launch_bounds__(FW_WARPS * 32) k_fin_sort_warp(ReduceIO io, ReduceParams p) {
+#ifndef FW_MINB
+#define FW_MINB 6  // 4 x 6 warps per SM at <= 85 registers (measured: 8 warps x 3 CTAs at 80: +0.03 ms; 4 x 8: +0.007; 4 x 10: +0.04)
+#endif
+__global__ void __launch_bounds__(FW_WARPS * 32, FW_MINB) k_fin_sort_warp(ReduceIO io, ReduceParams p) {
     extern __shared__ __align__(16) unsigned char dyn[];
     const int wib = threadIdx.x >> 5;
     unsigned char *mine = dyn + wib * FW_BYTES_PER_WARP;
