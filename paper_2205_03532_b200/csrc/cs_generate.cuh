@@ -6,13 +6,13 @@ namespace cs {
 // register budgets / grids of the descent wavefront (measured best, round 1); plans with
 // per-env grids (UNIFORM false) take one CTA per SM less: no spills (config 3: 1% faster)
 #ifndef FIRST_MINB
-#define FIRST_MINB 3
+#define FIRST_MINB 4  // 64 registers (spills 128 B; measured: 3 -> descent 1.033 ms, 4 -> 1.008, 2 -> 1.151, 5 -> 1.125)
 #endif
 #ifndef GRAD_MINB
 #define GRAD_MINB 4
 #endif
 #ifndef REST_MINB
-#define REST_MINB 4
+#define REST_MINB 6  // measured: 4 -> 1.033 ms (with FIRST_MINB 3), 6 -> 1.020, 3 -> 1.038, 8 -> worse than 6
 #endif
 #ifndef WAVE_GRID
 #define WAVE_GRID 32  // CTAs per SM of the grad / first wave kernels (grid-stride loops): measured best
