@@ -428,7 +428,7 @@ __device__ __forceinline__ void carve(unsigned char *p, int cap, Keys &A, Keys &
 
 constexpr size_t FW_BYTES_PER_WARP = (size_t)FW_SMEM * 2 * (8 + 8 + 4) + 9 * 33 * 8;
 #ifndef FB_SMEM_DEF
-#define FB_SMEM_DEF 1024
+#define FB_SMEM_DEF 768  // measured: 1024 -> 5 CTAs/SM by shared memory, 768 -> 7: step -0.05 ms (640: -0.04, 512: +0.01)
 #endif
 constexpr int FB_SMEM = FB_SMEM_DEF;  // members a k_fin_sort_block CTA sorts in shared memory
 constexpr size_t FB_BYTES = (size_t)FB_SMEM * 2 * (8 + 8 + 4);

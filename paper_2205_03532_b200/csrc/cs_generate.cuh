@@ -22,7 +22,7 @@ namespace cs {
 #define REST_GRID 8
 #endif
 #ifndef PREP_MINB
-#define PREP_MINB 5  // 48 registers (measured best; 4 and 6 are slower)
+#define PREP_MINB 6  // 40 registers (re-measured in round 2: 4 -> prep 0.979 ms, 5 -> 0.874, 6 -> 0.870)
 #endif
 constexpr int PGD_GRAB = 64;  // work items a warp claims per atomic
 #ifndef COMPACT_BLOCK_DEF
