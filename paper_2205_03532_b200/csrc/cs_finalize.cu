@@ -664,45 +664,49 @@ __global__ void __launch_bounds__(CH_WARPS * 32) k_fin_chain(ReduceIO io, Reduce
             u = uv.x; v = uv.y;
             ps = kpos ? __ldg(kpos + sidx) : sidx;
         };
-        double cu, cv, nu_, nv_;
-        int cp, np_;
+        double cu, cv, nu_ = 0.0, nv_ = 0.0;
+        int cp, np_ = 0;
         key(li, cu, cv, cp);
-        key(CG + li, nu_, nv_, np_);
         int top = 0;
         bool ovf = false;  // the stack outgrew CS: redone by half_chain_global
-        for (int t = 0; t < Lmax; ++t) {
-            const int c = t & (CG - 1);
-            if (c == 0 && t > 0) {
-                cu = nu_; cv = nv_; cp = np_;
-                key(t + CG + li, nu_, nv_, np_);
-            }
-            const double ub = __shfl_sync(FULL, cu, gb + c), vb = __shfl_sync(FULL, cv, gb + c);
-            const int pb = __shfl_sync(FULL, cp, gb + c);
-            const bool act = t < L && !ovf;
-            bool more = act;
-            while (true) {
-                // lane li: o = h[top-2-li], a = h[top-1-li];
-                // cross(o, a, b) = (a.u - o.u)(b.v - o.v) - (a.v - o.v)(b.u - o.u)
-                bool popi = false;
-                if (more && top - li >= 2) {
-                    const double2 a = st[top - 1 - li], o = st[top - 2 - li];
-                    popi = (a.x - o.x) * (vb - o.y) - (a.y - o.y) * (ub - o.x) <= 0.0;  // NaN: no pop (Python)
+        // one octet of keys per outer iteration, the inner loop unrolled: the key of step
+        // c comes from lane gb + c of the group (a constant shuffle source), and the next
+        // octet's loads go out at the octet's start
+        for (int t0 = 0; t0 < Lmax; t0 += CG) {
+            if (t0 + CG < Lmax) key(t0 + CG + li, nu_, nv_, np_);
+#pragma unroll
+            for (int c = 0; c < CG; ++c) {
+                const int t = t0 + c;
+                if (t >= Lmax) break;
+                const double ub = __shfl_sync(FULL, cu, gb + c), vb = __shfl_sync(FULL, cv, gb + c);
+                const int pb = __shfl_sync(FULL, cp, gb + c);
+                const bool act = t < L && !ovf;
+                bool more = act;
+                while (true) {
+                    // lane li: o = h[top-2-li], a = h[top-1-li];
+                    // cross(o, a, b) = (a.u - o.u)(b.v - o.v) - (a.v - o.v)(b.u - o.u)
+                    bool popi = false;
+                    if (more && top - li >= 2) {
+                        const double2 a = st[top - 1 - li], o = st[top - 2 - li];
+                        popi = (a.x - o.x) * (vb - o.y) - (a.y - o.y) * (ub - o.x) <= 0.0;  // NaN: no pop (Python)
+                    }
+                    const unsigned stop = (__ballot_sync(FULL, !popi) >> gb) & ((1u << CG) - 1u);
+                    const int npop = more ? (stop ? __ffs(stop) - 1 : CG) : 0;
+                    top -= npop;
+                    more = npop == CG;
+                    if (!__any_sync(FULL, more)) break;
                 }
-                const unsigned stop = (__ballot_sync(FULL, !popi) >> gb) & ((1u << CG) - 1u);
-                const int npop = more ? (stop ? __ffs(stop) - 1 : CG) : 0;
-                top -= npop;
-                more = npop == CG;
-                if (!__any_sync(FULL, more)) break;
-            }
-            if (act) {  // push b
-                if (top < CS) {
-                    if (li == 0) { st[top] = make_double2(ub, vb); stp[top] = pb; }
-                    ++top;
-                } else {
-                    ovf = true;
+                if (act) {  // push b
+                    if (top < CS) {
+                        if (li == 0) { st[top] = make_double2(ub, vb); stp[top] = pb; }
+                        ++top;
+                    } else {
+                        ovf = true;
+                    }
                 }
+                __syncwarp();
             }
-            __syncwarp();
+            cu = nu_; cv = nv_; cp = np_;
         }
         if (run) {  // the stack is the half hull (sorted positions)
             const int64_t h0 = 4 * row0 + (int64_t)kind * m;
