@@ -249,7 +249,19 @@ def test_collide_host_graph_replay(P, grid64, nut, gen64):
     host = Plan([P.register_sdf(grid64)] * E, [P.register_mesh(nut)] * E, P.ReductionParams())
     dev = Plan([P.register_sdf(grid64)] * E, [P.register_mesh(nut)] * E, P.ReductionParams())
     rng = np.random.default_rng(7)
-    fields = ("n_cand", "n_patch", "n_kept", "stats", "cand_point", "cand_normal", "kept_cand", "area", "w_sum")
+    def same(k):  # the valid outputs (padding past n_cand / n_patch is never written)
+        assert np.array_equal(host.n_cand.cpu().numpy(), dev.n_cand.cpu().numpy()), k
+        rh, rd = P.ReducedContacts(host), P.ReducedContacts(dev)
+        for e in range(E):
+            a, b = rh.contact_set(e), rd.contact_set(e)
+            assert np.array_equal(a.points, b.points) and np.array_equal(a.normals, b.normals), (k, e)
+            assert np.array_equal(a.depths, b.depths) and np.array_equal(a.face_indices, b.face_indices), (k, e)
+            pa, pb = rh.patches(e), rd.patches(e)
+            assert len(pa) == len(pb), (k, e)
+            for x, y in zip(pa, pb):
+                assert np.array_equal(x.member_indices, y.member_indices) and np.array_equal(x.points, y.points)
+                assert x.area_metric == y.area_metric and x.weight_sum == y.weight_sum, (k, e)
+
     for k in range(5):
         mpk = mp.copy()
         mpk[:, :3] += rng.uniform(-2e-4, 2e-4, size=(E, 3))  # a different step each call
@@ -258,9 +270,7 @@ def test_collide_host_graph_replay(P, grid64, nut, gen64):
         dev.collide(t(sp), t(mpk), t(cd))
         torch.cuda.synchronize()
         assert np.array_equal(stats, dev.stats.cpu().numpy())
-        for f in fields:
-            a, b = getattr(host, f).cpu().numpy(), getattr(dev, f).cpu().numpy()
-            assert np.array_equal(a, b, equal_nan=True), (k, f)
+        same(k)
     # the 12-value pose format: a new capture
     def pose12(p7):
         return np.stack([P.Transform.from_pose(p[:3], p[3:]).pose12() for p in p7])
@@ -271,4 +281,4 @@ def test_collide_host_graph_replay(P, grid64, nut, gen64):
                     torch.from_numpy(cd).cuda(), pose_format=_native.CS_POSE12)
         torch.cuda.synchronize()
         assert np.array_equal(stats, dev.stats.cpu().numpy())
-        assert np.array_equal(host.cand_point.cpu().numpy(), dev.cand_point.cpu().numpy())
+        same("pose12")
