@@ -258,13 +258,18 @@ __device__ int team_merge_sort(const Team &t, Keys a, Keys b, int m) {
             int ka = 0, kb = 0;
             if (i < a1) { ua = S.u[i]; va = S.v[i]; ka = S.k[i]; }
             if (j < b1) { ub = S.u[j]; vb = S.v[j]; kb = S.k[j]; }
+            // branch-free: the lanes of a warp take A or B in any mix, so both sides are
+            // written as selects (one store set, one load set per output)
             for (int o = s0; o < s1; ++o) {
-                if (j >= b1 || (i < a1 && key_less<NANS>(ua, va, ka, ub, vb, kb))) {
-                    D.u[o] = ua; D.v[o] = va; D.k[o] = ka;
-                    if (++i < a1) { ua = S.u[i]; va = S.v[i]; ka = S.k[i]; }
-                } else {
-                    D.u[o] = ub; D.v[o] = vb; D.k[o] = kb;
-                    if (++j < b1) { ub = S.u[j]; vb = S.v[j]; kb = S.k[j]; }
+                const bool ta = j >= b1 || (i < a1 && key_less<NANS>(ua, va, ka, ub, vb, kb));
+                D.u[o] = ta ? ua : ub; D.v[o] = ta ? va : vb; D.k[o] = ta ? ka : kb;
+                i += ta ? 1 : 0;
+                j += ta ? 0 : 1;
+                const int x = ta ? i : j;  // the consumed side's next key
+                if (x < (ta ? a1 : b1)) {
+                    const double nu = S.u[x], nv = S.v[x];
+                    const int nk = S.k[x];
+                    if (ta) { ua = nu; va = nv; ka = nk; } else { ub = nu; vb = nv; kb = nk; }
                 }
             }
         }
