@@ -241,10 +241,10 @@ __device__ int team_merge_sort(const Team &t, Keys a, Keys b, int m) {
     }
     t.sync();
     int src = 0;
-    for (int run = c; run < m; run <<= 1) {
+    for (int run = c, pm = 1; run < m; run <<= 1, pm = 2 * pm + 1) {
         const Keys S = src ? b : a, D = src ? a : b;
         if (s0 < m) {
-            const int ps = (s0 / (2 * run)) * (2 * run);
+            const int ps = (r & ~pm) * c;  // (s0 / (2 run)) (2 run): run = c 2^k, s0 = r c, pm = 2^(k+1) - 1
             const int a0 = ps, a1 = min(ps + run, m), b1 = min(ps + 2 * run, m);
             const int d = s0 - ps;
             int lo = max(0, d - (b1 - a1)), hi = min(d, a1 - a0);
