@@ -121,6 +121,9 @@ static __device__ unsigned long long g_bound_stat[4];  // brick passes, brick se
 #define CWIN_MAX_LOOKUPS 12  // face boxes needing more window lookups skip the bound (measured: 8, 12, 16 -> prep 0.86, 0.87, 0.92 ms; descent 1.10, 1.03, 1.03 ms)
 #endif
 constexpr int CWIN_LEVELS = 4;  // window widths 1, 2, 4, 8 cells
+#ifndef CWIN_GROUP
+#define CWIN_GROUP 12  // window lookups in flight together (>= CWIN_MAX_LOOKUPS: all at once)
+#endif
 
 template <class T>
 __host__ __device__ inline GridT<T> make_grid(const T *v, int nx, int ny, int nz, double ox, double oy, double oz,
@@ -400,17 +403,32 @@ __device__ __forceinline__ double sample_lower_bound(const GridT<T> &g, const do
     float m = INFINITY;
     const int nxw = (last[0] - c0[0] + w - 1) / w + 1;  // windows per row
     const int nyw = (last[1] - c0[1] + w - 1) / w + 1;
-    // all lookups issued together: (ix, iy, iz) walks the windows, loads are predicated
+    // lookups issued CWIN_GROUP at a time: (ix, iy, iz) walks the windows, loads are
+    // predicated (the cell tables hold < 2^31 entries: 32-bit offsets)
     int ix = 0, iy = 0, iz = 0;
+#if CWIN_GROUP >= CWIN_MAX_LOOKUPS
     float r[CWIN_MAX_LOOKUPS];
 #pragma unroll
     for (int i = 0; i < CWIN_MAX_LOOKUPS; ++i) {
         const int x = min(c0[0] + ix * w, last[0]), y = min(c0[1] + iy * w, last[1]), z = min(c0[2] + iz * w, last[2]);
-        r[i] = i < n ? __ldg(tab + x + (size_t)cnx * (y + (size_t)cny * z)) : INFINITY;
+        r[i] = i < n ? __ldg(tab + (x + cnx * (y + cny * z))) : INFINITY;
         if (++ix == nxw) { ix = 0; if (++iy == nyw) { iy = 0; ++iz; } }
     }
 #pragma unroll
     for (int i = 0; i < CWIN_MAX_LOOKUPS; ++i) m = fminf(m, r[i]);
+#else
+    for (int i0 = 0; i0 < n; i0 += CWIN_GROUP) {
+        float r[CWIN_GROUP];
+#pragma unroll
+        for (int j = 0; j < CWIN_GROUP; ++j) {
+            const int x = min(c0[0] + ix * w, last[0]), y = min(c0[1] + iy * w, last[1]), z = min(c0[2] + iz * w, last[2]);
+            r[j] = i0 + j < n ? __ldg(tab + (x + cnx * (y + cny * z))) : INFINITY;
+            if (++ix == nxw) { ix = 0; if (++iy == nyw) { iy = 0; ++iz; } }
+        }
+#pragma unroll
+        for (int j = 0; j < CWIN_GROUP; ++j) m = fminf(m, r[j]);
+    }
+#endif
     const double md = (double)m;
     return md - fabs(md) * 0x1p-40 - g.lbm - 1e-300;
 }
