@@ -121,9 +121,7 @@ static __device__ unsigned long long g_bound_stat[4];  // brick passes, brick se
 #define CWIN_MAX_LOOKUPS 12  // face boxes needing more window lookups skip the bound (measured: 8, 12, 16 -> prep 0.86, 0.87, 0.92 ms; descent 1.10, 1.03, 1.03 ms)
 #endif
 constexpr int CWIN_LEVELS = 4;  // window widths 1, 2, 4, 8 cells
-#ifndef CWIN_GROUP
-#define CWIN_GROUP 12  // window lookups in flight together (>= CWIN_MAX_LOOKUPS: all at once)
-#endif
+
 
 template <class T>
 __host__ __device__ inline GridT<T> make_grid(const T *v, int nx, int ny, int nz, double ox, double oy, double oz,
@@ -391,44 +389,39 @@ __device__ __forceinline__ double sample_lower_bound(const GridT<T> &g, const do
 #endif
     const int rmin = min(c1[0] - c0[0], min(c1[1] - c0[1], c1[2] - c0[2])) + 1;
     const int lvl = rmin >= 8 ? 3 : rmin >= 4 ? 2 : rmin >= 2 ? 1 : 0, w = 1 << lvl;
-    int n = 1, last[3];
+    int n = 1, last[3], nw[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        last[k] = c1[k] - w + 1;  // start of the last window
-        n *= (last[k] - c0[k] + w - 1) / w + 1;
+        last[k] = c1[k] - w + 1;                     // start of the last window (>= c0[k])
+        nw[k] = ((last[k] - c0[k] + w - 1) >> lvl) + 1;  // windows along the axis
+        n *= nw[k];
     }
     if (n > CWIN_MAX_LOOKUPS) { BOUND_STAT(3); return -INFINITY; }
     BOUND_STAT(2);
-    const float *tab = g.cwin + (size_t)lvl * ntab;
+    const float *tab = g.cwin + (size_t)lvl * ntab;  // < 2^31 entries per table: 32-bit offsets
     float m = INFINITY;
-    const int nxw = (last[0] - c0[0] + w - 1) / w + 1;  // windows per row
-    const int nyw = (last[1] - c0[1] + w - 1) / w + 1;
-    // lookups issued CWIN_GROUP at a time: (ix, iy, iz) walks the windows, loads are
-    // predicated (the cell tables hold < 2^31 entries: 32-bit offsets)
-    int ix = 0, iy = 0, iz = 0;
-#if CWIN_GROUP >= CWIN_MAX_LOOKUPS
-    float r[CWIN_MAX_LOOKUPS];
+    if (nw[0] <= 2 && nw[1] <= 2 && nw[2] <= 2) {
+        // the usual case: per axis the windows start at c0 and at last (one window: the
+        // same start twice; min is idempotent), eight independent loads
+        const int x0 = c0[0], x1 = last[0], sy = cnx, sz = cnx * cny;
+        const int y0 = sy * c0[1], y1 = sy * last[1], z0 = sz * c0[2], z1 = sz * last[2];
+        m = fminf(fminf(fminf(__ldg(tab + (x0 + y0 + z0)), __ldg(tab + (x1 + y0 + z0))),
+                        fminf(__ldg(tab + (x0 + y1 + z0)), __ldg(tab + (x1 + y1 + z0)))),
+                  fminf(fminf(__ldg(tab + (x0 + y0 + z1)), __ldg(tab + (x1 + y0 + z1))),
+                        fminf(__ldg(tab + (x0 + y1 + z1)), __ldg(tab + (x1 + y1 + z1)))));
+    } else {
+        // up to CWIN_MAX_LOOKUPS windows: (ix, iy, iz) walks them, loads predicated
+        int ix = 0, iy = 0, iz = 0;
+        float r[CWIN_MAX_LOOKUPS];
 #pragma unroll
-    for (int i = 0; i < CWIN_MAX_LOOKUPS; ++i) {
-        const int x = min(c0[0] + ix * w, last[0]), y = min(c0[1] + iy * w, last[1]), z = min(c0[2] + iz * w, last[2]);
-        r[i] = i < n ? __ldg(tab + (x + cnx * (y + cny * z))) : INFINITY;
-        if (++ix == nxw) { ix = 0; if (++iy == nyw) { iy = 0; ++iz; } }
-    }
-#pragma unroll
-    for (int i = 0; i < CWIN_MAX_LOOKUPS; ++i) m = fminf(m, r[i]);
-#else
-    for (int i0 = 0; i0 < n; i0 += CWIN_GROUP) {
-        float r[CWIN_GROUP];
-#pragma unroll
-        for (int j = 0; j < CWIN_GROUP; ++j) {
+        for (int i = 0; i < CWIN_MAX_LOOKUPS; ++i) {
             const int x = min(c0[0] + ix * w, last[0]), y = min(c0[1] + iy * w, last[1]), z = min(c0[2] + iz * w, last[2]);
-            r[j] = i0 + j < n ? __ldg(tab + (x + cnx * (y + cny * z))) : INFINITY;
-            if (++ix == nxw) { ix = 0; if (++iy == nyw) { iy = 0; ++iz; } }
+            r[i] = i < n ? __ldg(tab + (x + cnx * (y + cny * z))) : INFINITY;
+            if (++ix == nw[0]) { ix = 0; if (++iy == nw[1]) { iy = 0; ++iz; } }
         }
 #pragma unroll
-        for (int j = 0; j < CWIN_GROUP; ++j) m = fminf(m, r[j]);
+        for (int i = 0; i < CWIN_MAX_LOOKUPS; ++i) m = fminf(m, r[i]);
     }
-#endif
     const double md = (double)m;
     return md - fabs(md) * 0x1p-40 - g.lbm - 1e-300;
 }
