@@ -487,10 +487,12 @@ __device__ __forceinline__ bool face_body(const GridT<T> &g, double ax, double a
                                           double tol, FaceResult &r) {
     if (COUNT) r.nsamp = 3;
     double phi_a = sample(g, ax, ay, az), phi_b = sample(g, bx, by, bz), phi_c = sample(g, cx, cy, cz);
-    double e0 = sqrt((bx - ax) * (bx - ax) + (by - ay) * (by - ay) + (bz - az) * (bz - az));
-    double e1 = sqrt((cx - bx) * (cx - bx) + (cy - by) * (cy - by) + (cz - bz) * (cz - bz));
-    double e2 = sqrt((ax - cx) * (ax - cx) + (ay - cy) * (ay - cy) + (az - cz) * (az - cz));
-    double diam = dmax(e0, dmax(e1, e2));
+    // max of the three edge lengths (contacts/_kernels.py:30-33): sqrt is correctly rounded and
+    // monotone, so the max of the roots is the root of the max (one sqrt instead of three)
+    const double s0 = (bx - ax) * (bx - ax) + (by - ay) * (by - ay) + (bz - az) * (bz - az);
+    const double s1 = (cx - bx) * (cx - bx) + (cy - by) * (cy - by) + (cz - bz) * (cz - bz);
+    const double s2 = (ax - cx) * (ax - cx) + (ay - cy) * (ay - cy) + (az - cz) * (az - cz);
+    double diam = sqrt(dmax(s0, dmax(s1, s2)));
     double phi_min = dmin(phi_a, dmin(phi_b, phi_c));
     if (phi_min - diam > cd) return false;
     double sx = div3(ax + bx + cx), sy = div3(ay + by + cy), sz = div3(az + bz + cz);

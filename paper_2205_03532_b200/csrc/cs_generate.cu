@@ -283,10 +283,12 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int4 
         const double bx = vx[lb], by = vy[lb], bz = vz[lb];
         const double cx = vx[lc], cy = vy[lc], cz = vz[lc];
         pa = vphi[la]; pb = vphi[lb]; pc = vphi[lc];
-        const double e0 = sqrt((bx - ax) * (bx - ax) + (by - ay) * (by - ay) + (bz - az) * (bz - az));
-        const double e1 = sqrt((cx - bx) * (cx - bx) + (cy - by) * (cy - by) + (cz - bz) * (cz - bz));
-        const double e2 = sqrt((ax - cx) * (ax - cx) + (ay - cy) * (ay - cy) + (az - cz) * (az - cz));
-        const double diam = dmax(e0, dmax(e1, e2));
+        // max of the three edge lengths (contacts/_kernels.py:30-33): sqrt is correctly rounded and
+        // monotone, so the max of the roots is the root of the max (one sqrt instead of three)
+        const double s0 = (bx - ax) * (bx - ax) + (by - ay) * (by - ay) + (bz - az) * (bz - az);
+        const double s1 = (cx - bx) * (cx - bx) + (cy - by) * (cy - by) + (cz - bz) * (cz - bz);
+        const double s2 = (ax - cx) * (ax - cx) + (ay - cy) * (ay - cy) + (az - cz) * (az - cz);
+        const double diam = sqrt(dmax(s0, dmax(s1, s2)));
         PREP_CONST double phi_min = dmin(pa, dmin(pb, pc));
 #ifdef PREP_STATS
         const bool pcull = phi_min - diam > sx.cd;
