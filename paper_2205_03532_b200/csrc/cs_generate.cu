@@ -456,9 +456,9 @@ extern "C" int cs_debug_bt_stat(unsigned long long *out) { return (int)cudaMemcp
 
 template <bool COUNT, class G>
 __device__ __forceinline__ bool backtrack(const G &g, const FaceGeom &f, const double *vphi, double gx, double gy,
-                                          double gz, double &px, double &py, double &pz, double &phi, double &alpha,
-                                          double &moved, unsigned long long &ns) {
-    const double gnorm = sqrt(gx * gx + gy * gy + gz * gz);
+                                          double gz, double gnorm, double &px, double &py, double &pz, double &phi,
+                                          double &alpha, double &moved, unsigned long long &ns) {
+    // gnorm = sqrt(gx gx + gy gy + gz gz): the caller's (it tested it against 1e-12)
     // g / gnorm, correctly rounded: one reciprocal for the three (div_rn proves each
     // quotient or falls back to the IEEE division)
     const double rg = 1.0 / gnorm;
@@ -532,14 +532,15 @@ __global__ void __launch_bounds__(256, UNIFORM ? FIRST_MINB : FIRST_MINB - 1) k_
             }
             finish_face(st, row, blk, face, phi, X.cd);
         };
-        if (sqrt(gx * gx + gy * gy + gz * gz) < 1e-12) {  // contacts/_kernels.py:61-62: break
+        const double gnorm = sqrt(gx * gx + gy * gy + gz * gz);
+        if (gnorm < 1e-12) {  // contacts/_kernels.py:61-62: break
             done_here();
             continue;
         }
         const PlanGrid &g = grid_of<UNIFORM>(gu, sdfs, xf, e);
         const double vphi[3] = {w->phi[0], w->phi[1], w->phi[2]};
         double alpha = g.voxel, moved;
-        if (!backtrack<COUNT>(g, f, vphi, gx, gy, gz, px, py, pz, phi, alpha, moved, ns)) {
+        if (!backtrack<COUNT>(g, f, vphi, gx, gy, gz, gnorm, px, py, pz, phi, alpha, moved, ns)) {
             BT_STAT(((unsigned)hd.z >> 30) == 0 ? 8 : 9);  // no move: centroid / vertex start
             if (((unsigned)hd.z >> 30) != 0) BT_STAT(12 + ((unsigned)hd.z >> 30));  // [13..15]: at vertex a / b / c
             done_here();  // no move: this gradient is the final one
@@ -567,9 +568,10 @@ __device__ __forceinline__ void descend_rest(const G &g, const EnvXf &X, const F
                                              double &px, double &py, double &pz, double &phi, double alpha,
                                              double &gx, double &gy, double &gz, unsigned long long &ns) {
     for (int it = 1; it < MAX_MINIMIZE_ITERS; ++it) {
-        if (sqrt(gx * gx + gy * gy + gz * gz) < 1e-12) break;
+        const double gnorm = sqrt(gx * gx + gy * gy + gz * gz);
+        if (gnorm < 1e-12) break;
         double moved;
-        const bool acc = backtrack<COUNT>(g, f, vphi, gx, gy, gz, px, py, pz, phi, alpha, moved, ns);
+        const bool acc = backtrack<COUNT>(g, f, vphi, gx, gy, gz, gnorm, px, py, pz, phi, alpha, moved, ns);
         if (acc) {  // the gradient at the new point: the next iteration's, or the final one
             gradient(g, px, py, pz, gx, gy, gz);
             if (COUNT) ns += 6;
