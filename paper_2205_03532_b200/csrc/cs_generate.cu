@@ -471,9 +471,9 @@ __device__ __forceinline__ bool backtrack(const G &g, const FaceGeom &f, const d
         // inputs, so the sample's value is already known
         double phi_new;
         if (same3(qx, qy, qz, px, py, pz)) { phi_new = phi; BT_STAT(5); BT_STAT(12); }
-        else if (same3(qx, qy, qz, f.ax, f.ay, f.az)) { phi_new = vphi[0]; BT_STAT(5); }
-        else if (same3(qx, qy, qz, f.bx, f.by, f.bz)) { phi_new = vphi[1]; BT_STAT(5); }
-        else if (same3(qx, qy, qz, f.cx, f.cy, f.cz)) { phi_new = vphi[2]; BT_STAT(5); }
+        else if (same3(qx, qy, qz, f.ax, f.ay, f.az)) { phi_new = __ldg(vphi); BT_STAT(5); }
+        else if (same3(qx, qy, qz, f.bx, f.by, f.bz)) { phi_new = __ldg(vphi + 1); BT_STAT(5); }
+        else if (same3(qx, qy, qz, f.cx, f.cy, f.cz)) { phi_new = __ldg(vphi + 2); BT_STAT(5); }
         else {
             phi_new = sample(g, qx, qy, qz);
             BT_STAT(6);
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(256, UNIFORM ? FIRST_MINB : FIRST_MINB - 1) k_
             continue;
         }
         const PlanGrid &g = grid_of<UNIFORM>(gu, sdfs, xf, e);
-        const double vphi[3] = {w->phi[0], w->phi[1], w->phi[2]};
+        const double *vphi = w->phi;  // the vertex phis stay in the work record (read when a projection hits a corner)
         double alpha = g.voxel, moved;
         if (!backtrack<COUNT>(g, f, vphi, gx, gy, gz, gnorm, px, py, pz, phi, alpha, moved, ns)) {
             BT_STAT(((unsigned)hd.z >> 30) == 0 ? 8 : 9);  // no move: centroid / vertex start
@@ -606,8 +606,7 @@ __global__ void __launch_bounds__(256, UNIFORM ? FIRST_MINB : FIRST_MINB - 1) k_
             const EnvXf &X = xf[e];
             const FaceWork *w = st.work + idx;
             const FaceGeom f = face_geom(X, meshes, mu, um, face);
-            const double vphi[3] = {w->phi[0], w->phi[1], w->phi[2]};
-            descend_rest<COUNT>(g, X, f, vphi, px, py, pz, phi, st.alpha[row], gx, gy, gz, ns);
+            descend_rest<COUNT>(g, X, f, w->phi, px, py, pz, phi, st.alpha[row], gx, gy, gz, ns);
             st.point[3 * row] = px; st.point[3 * row + 1] = py; st.point[3 * row + 2] = pz;
             st.phi[row] = phi;
         }
@@ -639,7 +638,7 @@ __global__ void __launch_bounds__(128, UNIFORM ? REST_MINB : REST_MINB - 1) k_pg
         const EnvXf &X = xf[e];
         const PlanGrid &g = grid_of<UNIFORM>(gu, sdfs, xf, e);
         const FaceGeom f = face_geom(X, meshes, mu, um, face);
-        const double vphi[3] = {w->phi[0], w->phi[1], w->phi[2]};
+        const double *vphi = w->phi;
         double px = st.point[3 * row], py = st.point[3 * row + 1], pz = st.point[3 * row + 2];
         double phi = st.phi[row];
         double gx = st.grad[3 * row], gy = st.grad[3 * row + 1], gz = st.grad[3 * row + 2];
