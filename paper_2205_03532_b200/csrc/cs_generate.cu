@@ -503,27 +503,37 @@ __global__ void __launch_bounds__(256, UNIFORM ? FIRST_MINB : FIRST_MINB - 1) k_
     unsigned long long ns = 0;
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const FaceWork *w = st.work + i;
-        const int4 hd = __ldg(reinterpret_cast<const int4 *>(w));  // row, blk, face, env in one load
-        const int64_t row = hd.x;
-        const int blk = hd.y;
-        const int face = hd.z & 0x3fffffff;
-        const int e = hd.w;
-        const EnvXf &X = xf[e];
-        double phi = w->phi[3];
-        const FaceGeom f = face_geom(X, meshes, mu, um, face);
-        double px, py, pz;
-        face_start(f, (int)((unsigned)hd.z >> 30), px, py, pz);
+        double px, py, pz, gx, gy, gz, phi = w->phi[3];
+        FaceGeom f;
+        const PlanGrid *gp;
+        {   // the header's fields die here: the tail reads them again (registers are this kernel's limit)
+            const int4 hd = __ldg(reinterpret_cast<const int4 *>(w));  // row, blk, face, env in one load
+            const int64_t row = hd.x;
+            f = face_geom(xf[hd.w], meshes, mu, um, hd.z & 0x3fffffff);
+            face_start(f, (int)((unsigned)hd.z >> 30), px, py, pz);
+            gp = &grid_of<UNIFORM>(gu, sdfs, xf, hd.w);
 #if PGD_FUSE0
-        // iteration 0's gradient at the start point, here (no k_pgd_grad stage 0)
-        double gx, gy, gz;
-        gradient(grid_of<UNIFORM>(gu, sdfs, xf, e), px, py, pz, gx, gy, gz);
-        if (COUNT) ns += 6;
+            // iteration 0's gradient at the start point, here (no k_pgd_grad stage 0)
+            gradient(*gp, px, py, pz, gx, gy, gz);
+            if (COUNT) ns += 6;
 #else
-        const double gx = st.grad[3 * row], gy = st.grad[3 * row + 1], gz = st.grad[3 * row + 2];
+            gx = st.grad[3 * row]; gy = st.grad[3 * row + 1]; gz = st.grad[3 * row + 2];
 #endif
-        // a face that does not move ends here with this gradient: its point, phi (and
-        // gradient) go to the staging row only when it is found (the only rows k_compact reads)
-        auto done_here = [&]() {
+        }
+        const double gnorm = sqrt(gx * gx + gy * gy + gz * gz);
+        double alpha = gp->voxel, moved = 0.0;
+        // contacts/_kernels.py:61-62: a vanishing gradient ends the descent here
+        const bool mv = !(gnorm < 1e-12) &&
+                        backtrack<COUNT>(*gp, f, w->phi, gx, gy, gz, gnorm, px, py, pz, phi, alpha, moved, ns);
+        const int4 hd = __ldg(reinterpret_cast<const int4 *>(w));
+        const int64_t row = hd.x;
+        const int blk = hd.y, face = hd.z & 0x3fffffff;
+        const EnvXf &X = xf[hd.w];
+        BT_STAT(mv ? (((unsigned)hd.z >> 30) == 0 ? 10 : 11) : (((unsigned)hd.z >> 30) == 0 ? 8 : 9));
+        if (!mv && ((unsigned)hd.z >> 30) != 0) BT_STAT(12 + ((unsigned)hd.z >> 30));  // [13..15]: stuck at a / b / c
+        if (!mv) {
+            // no move: this gradient is the final one; the point and phi go to the staging row
+            // only when the face is found (the only rows k_compact reads)
             if (phi <= X.cd) {
                 st.point[3 * row] = px; st.point[3 * row + 1] = py; st.point[3 * row + 2] = pz; st.phi[row] = phi;
 #if PGD_FUSE0
@@ -531,22 +541,8 @@ __global__ void __launch_bounds__(256, UNIFORM ? FIRST_MINB : FIRST_MINB - 1) k_
 #endif
             }
             finish_face(st, row, blk, face, phi, X.cd);
-        };
-        const double gnorm = sqrt(gx * gx + gy * gy + gz * gz);
-        if (gnorm < 1e-12) {  // contacts/_kernels.py:61-62: break
-            done_here();
             continue;
         }
-        const PlanGrid &g = grid_of<UNIFORM>(gu, sdfs, xf, e);
-        const double *vphi = w->phi;  // the vertex phis stay in the work record (read when a projection hits a corner)
-        double alpha = g.voxel, moved;
-        if (!backtrack<COUNT>(g, f, vphi, gx, gy, gz, gnorm, px, py, pz, phi, alpha, moved, ns)) {
-            BT_STAT(((unsigned)hd.z >> 30) == 0 ? 8 : 9);  // no move: centroid / vertex start
-            if (((unsigned)hd.z >> 30) != 0) BT_STAT(12 + ((unsigned)hd.z >> 30));  // [13..15]: at vertex a / b / c
-            done_here();  // no move: this gradient is the final one
-            continue;
-        }
-        BT_STAT(((unsigned)hd.z >> 30) == 0 ? 10 : 11);  // moved: centroid / vertex start
         st.point[3 * row] = px; st.point[3 * row + 1] = py; st.point[3 * row + 2] = pz;
         st.phi[row] = phi;
         st.alpha[row] = alpha;
