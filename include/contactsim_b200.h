@@ -224,7 +224,9 @@ int cs_collide_host(cs_plan *plan, const double *sdf_pose_host, const double *me
  * [row_off[s], row_off[s+1]) (sweep order; row_off [dev] (n_sys+1) int64) and
  * bodies [s*n_bodies, (s+1)*n_bodies) of the state arrays (ref (.,3),
  * w_mat (.,6,6), vel/imp (.,6)); body_a/body_b hold system-local ids
- * (0 <= id < n_bodies <= 8). All arrays [dev], float64 / int64, C order.
+ * (0 <= id < n_bodies <= 2^20: no limit in the reference; systems above 8
+ * bodies keep their state in global memory). All arrays [dev], float64 /
+ * int64, C order.
  * With n_sys = 1 and row_off = {0, m} these are the reference's per-scene calls.
  * ---------------------------------------------------------------------- */
 

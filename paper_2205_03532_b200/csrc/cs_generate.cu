@@ -347,6 +347,9 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int4 
 // Same operations in the same order as the sequential loop; only the schedule
 // differs (uniform work per kernel instead of one divergent state machine).
 
+#ifndef GRAD_ONE_VERT
+#define GRAD_ONE_VERT 1  // stage 0: a corner start transforms only its own vertex
+#endif
 #ifndef PGD_FUSE_REST
 #define PGD_FUSE_REST 0  // stage 1 and the rest of the descent in one kernel (k_pgd_grad1_rest)
 #endif
@@ -425,7 +428,17 @@ __global__ void __launch_bounds__(256, UNIFORM ? GRAD_MINB : GRAD_MINB - 1) k_pg
         const PlanGrid &g = grid_of<UNIFORM>(gu, sdfs, xf, e);
         double px, py, pz;
         if (stage == 0) {  // the start point, from the corners (not staged: recomputing is cheaper than the traffic)
-            face_start(face_geom(xf[e], meshes, mu, um, hd.z & 0x3fffffff), (int)((unsigned)hd.z >> 30), px, py, pz);
+            const int which = (int)((unsigned)hd.z >> 30), face = hd.z & 0x3fffffff;
+#if GRAD_ONE_VERT
+            if (which != 0) {  // a corner start (91% of the faces): only that vertex, same to_grid rounding
+                const EnvXf &X = xf[e];
+                const int4 tri = __ldg((um ? mu.tris : meshes[X.mesh].tris) + face);
+                const int vi = which == 1 ? tri.x : (which == 2 ? tri.y : tri.z);
+                const double3 q = to_grid(X, ld_vert((um ? mu.verts : meshes[X.mesh].verts) + vi));
+                px = q.x; py = q.y; pz = q.z;
+            } else
+#endif
+                face_start(face_geom(xf[e], meshes, mu, um, face), which, px, py, pz);
         } else {
             px = st.point[3 * row]; py = st.point[3 * row + 1]; pz = st.point[3 * row + 2];
         }

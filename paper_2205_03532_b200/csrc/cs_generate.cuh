@@ -9,7 +9,7 @@ namespace cs {
 #define FIRST_MINB 4  // 64 registers (spills 128 B; measured: 3 -> descent 1.033 ms, 4 -> 1.008, 2 -> 1.151, 5 -> 1.125)
 #endif
 #ifndef GRAD_MINB
-#define GRAD_MINB 4
+#define GRAD_MINB 5  // 48 registers, spills 56 B (measured: 4 -> descent 0.964 ms, 5 -> 0.952, 6 -> 1.012)
 #endif
 #ifndef REST_MINB
 #define REST_MINB 6  // measured: 4 -> 1.033 ms (with FIRST_MINB 3), 6 -> 1.020, 3 -> 1.038, 8 -> worse than 6

@@ -271,6 +271,7 @@ constexpr int ROW_F = 22;  // a[3] b[3] n[3] t1[3] t2[3] kn kt1 kt2 target mu bo
 constexpr int LAM_CAP = 1024;
 
 __host__ __device__ inline size_t sweep_smem_doubles(int nb, bool two) {
+    if (nb > SOLVER_SMEM_BODIES) return (size_t)RING * ROW_F + 3 * (size_t)LAM_CAP;  // MODE 1: state in global
     return (size_t)36 * nb + (two ? 0 : (size_t)12 * nb) + (size_t)RING * ROW_F + 3 * (size_t)LAM_CAP;
 }
 
@@ -426,10 +427,13 @@ __global__ void __launch_bounds__(SW_T) k_sweeps(int64_t S, int nb, SysRows rows
     const int64_t s = blockIdx.x * (int64_t)SW_T + threadIdx.x;
     if (s >= S) return;
     const int nv = 6 * nb;
-    double *Ws = sm + threadIdx.x;  // [36 nb][SW_T]
-    for (int j = 0; j < 36 * nb; ++j) Ws[j * SW_T] = __ldg(io.w_mat + s * 36 * nb + j);
+    constexpr bool GLOBAL = MODE == 1;  // systems above SOLVER_SMEM_BODIES: the state stays in global memory
+    static_assert(!GLOBAL || SW_T == 1, "global body state is addressed with the shared columns' stride");
+    const double *Ws = GLOBAL ? io.w_mat + s * 36 * nb : sm + threadIdx.x;  // [36 nb][SW_T]
+    if (!GLOBAL)
+        for (int j = 0; j < 36 * nb; ++j) sm[threadIdx.x + j * SW_T] = __ldg(io.w_mat + s * 36 * nb + j);
     constexpr bool TWO = MODE == 2;
-    double *after_w = sm + (size_t)36 * nb * SW_T + (MODE ? 0 : (size_t)12 * nb * SW_T);
+    double *after_w = GLOBAL ? sm : sm + (size_t)36 * nb * SW_T + (MODE ? 0 : (size_t)12 * nb * SW_T);
     double *ring = after_w + threadIdx.x;
     double *lam = after_w + (size_t)RING * ROW_F * SW_T + threadIdx.x;
     const SweepPhase phs[2] = {p0, p1};
@@ -470,6 +474,12 @@ __global__ void __launch_bounds__(SW_T) k_sweeps(int64_t S, int nb, SysRows rows
                     io.vel[s * nv + 6 * b + k] = st.v_[b][k];
                     io.imp[s * nv + 6 * b + k] = st.i_[b][k];
                 }
+    } else if (GLOBAL) {  // velocities and impulses updated in place (one thread owns the system)
+        SmemState st;
+        st.W = Ws;
+        st.V = io.vel + s * nv;
+        st.I = io.imp + s * nv;
+        sweep_system<false>(st, io, phs, n_phases, rows, s, ring, lam);
     } else {
         SmemState st;
         st.W = Ws;
@@ -605,6 +615,7 @@ __device__ __forceinline__ void sweep_packed(St &st, const SweepIO &io, const Sw
 }
 
 __host__ __device__ inline size_t packed_smem_doubles(int nb, bool regs) {
+    if (nb > SOLVER_SMEM_BODIES) return (size_t)2 * PK_CH * PK_F + 3 * (size_t)LAM_CAP;
     return (size_t)36 * nb + (regs ? 0 : (size_t)12 * nb) + (size_t)2 * PK_CH * PK_F + 3 * (size_t)LAM_CAP;
 }
 
@@ -623,9 +634,11 @@ __global__ void __launch_bounds__(SW_T) k_sweeps_packed(int64_t S, int nb, SysRo
     mbar_init(bar + 1, 1);
     fence_proxy_async();
     const int nv = 6 * nb;
-    double *Ws = sm;
-    for (int j = 0; j < 36 * nb; ++j) Ws[j] = __ldg(io.w_mat + s * 36 * nb + j);
-    double *after_w = sm + (size_t)36 * nb + (MODE ? 0 : (size_t)12 * nb);
+    constexpr bool GLOBAL = MODE == 1;  // as k_sweeps
+    const double *Ws = GLOBAL ? io.w_mat + s * 36 * nb : sm;
+    if (!GLOBAL)
+        for (int j = 0; j < 36 * nb; ++j) sm[j] = __ldg(io.w_mat + s * 36 * nb + j);
+    double *after_w = GLOBAL ? sm : sm + (size_t)36 * nb + (MODE ? 0 : (size_t)12 * nb);
     double *buf = after_w;  // 16-byte aligned: 36 nb (+ 12 nb) doubles are a multiple of 2
     double *lam = after_w + 2 * PK_CH * PK_F;
     const SweepPhase phs[2] = {p0, p1};
@@ -666,6 +679,12 @@ __global__ void __launch_bounds__(SW_T) k_sweeps_packed(int64_t S, int nb, SysRo
                     io.vel[s * nv + 6 * b + k] = st.v_[b][k];
                     io.imp[s * nv + 6 * b + k] = st.i_[b][k];
                 }
+    } else if (GLOBAL) {
+        SmemState st;
+        st.W = Ws;
+        st.V = io.vel + s * nv;
+        st.I = io.imp + s * nv;
+        sweep_packed<FIX>(st, io, phs, n_phases, rows, s, packed, buf, bar, lam);
     } else {
         SmemState st;
         st.W = Ws;
@@ -695,10 +714,11 @@ __global__ void __launch_bounds__(WR_WARPS * 32) k_body_wrenches(int64_t S, int 
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t s = blockIdx.x * (int64_t)WR_WARPS + w;
     if (s >= S) return;
-    const int nv = 6 * nb;  // <= 48: lanes 0..nv-1 own an element, lanes >= 32 folded below
+    const int nv = 6 * nb;  // elements in groups of 64: lane owns e0 + lane and e0 + lane + 32
     const int64_t m = rows.n(s);
     const double h = io.h;
-    double acc0 = 0.0, acc1 = 0.0;  // elements lane and lane + 32
+    for (int e0 = 0; e0 < nv; e0 += 64) {  // one group up to 10 bodies; larger systems recompute the row terms
+    double acc0 = 0.0, acc1 = 0.0;
     for (int64_t t0 = 0; t0 < m; t0 += WR_TILE) {
         if (t0 + lane < m) {
             const int64_t c = rows.row(s, t0 + lane);
@@ -726,7 +746,7 @@ __global__ void __launch_bounds__(WR_WARPS * 32) k_body_wrenches(int64_t S, int 
         __syncwarp();
         const int n = m - t0 < WR_TILE ? (int)(m - t0) : WR_TILE;
         for (int q = 0; q < 2; ++q) {
-            const int el = lane + 32 * q;
+            const int el = e0 + lane + 32 * q;
             if (el >= nv) break;
             const int body = el / 6, k = el - 6 * body;
             double acc = q ? acc1 : acc0;
@@ -738,8 +758,9 @@ __global__ void __launch_bounds__(WR_WARPS * 32) k_body_wrenches(int64_t S, int 
         }
         __syncwarp();
     }
-    if (lane < nv) io.out[s * nv + lane] = acc0;
-    if (lane + 32 < nv) io.out[s * nv + lane + 32] = acc1;
+    if (e0 + lane < nv) io.out[s * nv + e0 + lane] = acc0;
+    if (e0 + lane + 32 < nv) io.out[s * nv + e0 + lane + 32] = acc1;
+    }
 }
 
 // Scene rows of a plan's reduced contacts: warp per system; its pair slots in
@@ -805,6 +826,7 @@ void launch_sweeps(int64_t n_sys, int nb, const SysRows &rows, const SweepIO &io
     if (two && fixed_bodies) go(k_sweeps<2, true>);
     else if (two) go(k_sweeps<2, false>);
     else if (regs) go(k_sweeps<4, false>);
+    else if (nb > SOLVER_SMEM_BODIES) go(k_sweeps<1, false>);
     else go(k_sweeps<0, false>);
 }
 
@@ -826,6 +848,7 @@ void launch_sweeps_packed(int64_t n_sys, int nb, const SysRows &rows, const Swee
     if (two && fixed_bodies) go(k_sweeps_packed<2, true>);
     else if (two) go(k_sweeps_packed<2, false>);
     else if (regs) go(k_sweeps_packed<4, false>);
+    else if (nb > SOLVER_SMEM_BODIES) go(k_sweeps_packed<1, false>);
     else go(k_sweeps_packed<0, false>);
 }
 

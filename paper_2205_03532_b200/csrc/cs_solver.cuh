@@ -10,7 +10,12 @@
 
 namespace cs {
 
-constexpr int SOLVER_MAX_BODIES = 8;
+// Systems up to SOLVER_SMEM_BODIES bodies keep the 6x6 mobility blocks and the body
+// state on chip (registers / shared memory); larger ones (MODE 1 of the sweeps) read
+// and update them in global memory. The reference has no limit; the bound below
+// only keeps the element indices in 32 bits.
+constexpr int SOLVER_SMEM_BODIES = 8;
+constexpr int SOLVER_MAX_BODIES = 1 << 20;
 
 struct SysRows {
     const int64_t *off;    // [S + 1] CSR offsets (the reference's layout: rows of a system

@@ -47,16 +47,16 @@ class SolverParams:
                                      self.vel_iterations)
 
 
-SOLVER_MAX_BODIES = 8  # cs_solver.cuh SOLVER_MAX_BODIES
+SOLVER_MAX_BODIES = 1 << 20  # cs_solver.cuh SOLVER_MAX_BODIES
 
 
 def check_solver_bodies(nb: int) -> None:
-    """The device solver keeps a system's bodies (velocities, impulses, 6x6 mobility
-    blocks) on chip, which bounds a system to SOLVER_MAX_BODIES bodies. The reference
-    has no limit; scenes above it must be split into independent systems."""
+    """Systems up to 8 bodies keep their state on chip; larger ones (any size the
+    reference takes) run the sweeps with the state in global memory. The bound only
+    keeps the device's element indices in 32 bits."""
     if not 1 <= int(nb) <= SOLVER_MAX_BODIES:
         raise ValueError(f"the device contact solver handles systems of 1..{SOLVER_MAX_BODIES} bodies per call "
-                         f"(got {int(nb)}); split larger scenes into independent systems")
+                         f"(got {int(nb)})")
 
 
 class SolverState:

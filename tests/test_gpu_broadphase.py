@@ -186,6 +186,17 @@ def test_multipair_scenes_match_oracle(P, grid64_npz, meshes):
         assert np.array_equal(gv[i], v), i
         assert np.array_equal(wrench[i], wr), i
 
+    # the same solve on the scene state padded to 10 bodies (bodies 4..9 idle): the
+    # packed sweeps' global-memory state path (systems above 8 bodies) gives the same bits
+    idle = rng.standard_normal((S, 6, 6))
+    st10 = BatchedSolverState.from_numpy(np.concatenate([ref_pt, np.zeros((S, 6, 3))], 1),
+                                         np.concatenate([W, np.zeros((S, 6, 6, 6))], 1),
+                                         np.concatenate([vel, idle], 1))
+    wrench10 = mps.solve(st10, prm).cpu().numpy()
+    gv10 = st10.vel.cpu().numpy()
+    assert np.array_equal(gv10[:, :4], gv) and np.array_equal(gv10[:, 4:], idle)
+    assert np.array_equal(wrench10[:, :4], wrench) and not wrench10[:, 4:].any()
+
 
 def test_broadphase_max_scene_and_status_codes(P):
     """The per-scene cap (2048 bodies, sweep semantics, inverted boxes included)

@@ -214,16 +214,18 @@ def test_solver_errors(P):
         SolverParams(vel_iterations=-1)
 
 
-def test_solver_six_body_system_vs_oracle(P):
-    """Systems above four bodies take the shared-memory state path: a 6-body system
-    (three dynamic bodies, random rows between all of them) against the oracle."""
+@pytest.mark.parametrize("nb", [6, 13, 40])
+def test_solver_many_body_system_vs_oracle(P, nb):
+    """Systems above four bodies take the shared-memory state path (6), above eight the
+    global-memory one (13, 40: the reference has no body limit): random rows between
+    dynamic and static bodies against the oracle."""
     from oracle import oracle as O
     from paper_2205_03532_b200.dynamics import ContactConstraints, SolverState
 
-    rng = np.random.default_rng(21)
-    nb, m = 6, 90
+    rng = np.random.default_rng(21 + nb)
+    m = 15 * nb
     st = SolverState(nb)
-    for b in (0, 2, 5):  # bodies 0, 2: the rigid-body mobility layout; 5: a full 6x6
+    for b in sorted({0, 2, nb - 1} | set(range(3, nb, 3))):  # the rigid-body mobility layout; the last a full 6x6
         mass = rng.uniform(0.01, 0.05)
         st.ref[b] = rng.standard_normal(3) * 0.01
         st.w_mat[b, :3, :3] = np.eye(3) / mass
@@ -231,7 +233,7 @@ def test_solver_six_body_system_vs_oracle(P):
         st.w_mat[b, 3:, 3:] = np.linalg.inv(A @ A.T * 1e-6 + np.eye(3) * 1e-7)
         st.vel[b] = rng.standard_normal(6) * 0.1
     B = rng.standard_normal((6, 6))
-    st.w_mat[5] = B @ B.T * 10.0
+    st.w_mat[nb - 1] = B @ B.T * 10.0
     rows = []
     for c in range(m):
         a, b = rng.choice(nb, size=2, replace=False)
