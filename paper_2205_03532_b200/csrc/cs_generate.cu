@@ -347,6 +347,9 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int4 
 // Same operations in the same order as the sequential loop; only the schedule
 // differs (uniform work per kernel instead of one divergent state machine).
 
+#ifndef STUCK0
+#define STUCK0 1  // stage 0 finishes the faces whose iteration 0 provably does not move (see k_pgd_grad)
+#endif
 #ifndef GRAD_ONE_VERT
 #define GRAD_ONE_VERT 1  // stage 0: a corner start transforms only its own vertex
 #endif
@@ -403,6 +406,43 @@ __device__ __forceinline__ void face_start(const FaceGeom &f, int which, double 
     }
 }
 
+// True when all four backtracking projections of iteration 0 (alpha = voxel, /2, /4, /8)
+// return the corner p itself. closest_point's first three region tests (corner a,
+// corner b, edge ab, then corner c) with every dot product evaluated for every lane,
+// each with closest_point's own expression (so the same bits), and the outcome
+// selected without branches: the four tries cost the same on every lane of a warp.
+__device__ __forceinline__ bool corner_stays(const FaceGeom &f, double px, double py, double pz, double ux,
+                                             double uy, double uz, double alpha) {
+    const double abx = f.bx - f.ax, aby = f.by - f.ay, abz = f.bz - f.az;
+    const double acx = f.cx - f.ax, acy = f.cy - f.ay, acz = f.cz - f.az;
+    bool stays = true;
+    for (int bt = 0; bt < 4 && stays; ++bt) {
+        const double qx = px - alpha * ux, qy = py - alpha * uy, qz = pz - alpha * uz;
+        const double apx = qx - f.ax, apy = qy - f.ay, apz = qz - f.az;
+        const double d1 = abx * apx + aby * apy + abz * apz;
+        const double d2 = acx * apx + acy * apy + acz * apz;
+        const double bpx = qx - f.bx, bpy = qy - f.by, bpz = qz - f.bz;
+        const double d3 = abx * bpx + aby * bpy + abz * bpz;
+        const double d4 = acx * bpx + acy * bpy + acz * bpz;
+        const double vc = d1 * d4 - d3 * d2;
+        const double cpx = qx - f.cx, cpy = qy - f.cy, cpz = qz - f.cz;
+        const double d5 = abx * cpx + aby * cpy + abz * cpz;
+        const double d6 = acx * cpx + acy * cpy + acz * cpz;
+        const bool ra = d1 <= 0.0 && d2 <= 0.0;
+        const bool rb = d3 >= 0.0 && d4 <= d3;
+        const bool eab = vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0;
+        const bool rc = d6 >= 0.0 && d5 <= d6;
+        // the corner closest_point returns (a, b, c in test order), if any
+        const int r = ra ? 1 : (rb ? 2 : (eab ? 0 : (rc ? 3 : 0)));
+        const double vx = r == 1 ? f.ax : (r == 2 ? f.bx : f.cx);
+        const double vy = r == 1 ? f.ay : (r == 2 ? f.by : f.cy);
+        const double vz = r == 1 ? f.az : (r == 2 ? f.bz : f.cz);
+        stays = r != 0 && same3(vx, vy, vz, px, py, pz);
+        alpha *= 0.5;
+    }
+    return stays;
+}
+
 template <bool COUNT, bool UNIFORM>
 __global__ void __launch_bounds__(256, UNIFORM ? GRAD_MINB : GRAD_MINB - 1) k_pgd_grad(const int2 *__restrict__ block_map, const EnvXf *__restrict__ xf,
                                                   const SdfDesc *__restrict__ sdfs, const MeshDesc *__restrict__ meshes,
@@ -446,6 +486,39 @@ __global__ void __launch_bounds__(256, UNIFORM ? GRAD_MINB : GRAD_MINB - 1) k_pg
         gradient(g, px, py, pz, gx, gy, gz);
         if (COUNT) ns += 6;
         st.grad[3 * row] = gx; st.grad[3 * row + 1] = gy; st.grad[3 * row + 2] = gz;
+#if STUCK0 && !PGD_FUSE0
+        if (stage == 0) {
+            // Iteration 0 without k_pgd_first when it provably leaves the face where it is:
+            // a vanishing gradient, or a corner start whose four backtracking projections
+            // (contacts/_kernels.py:64-75, the same operations as backtrack()) all return the
+            // corner itself -- then every try's phi equals the current phi (no sample) and
+            // none is accepted. 78% of the descended faces; the rest go to k_pgd_first's list.
+            const int which = (int)((unsigned)hd.z >> 30);
+            const double gnorm = sqrt(gx * gx + gy * gy + gz * gz);
+            bool stuck = gnorm < 1e-12;
+            if (!stuck && which != 0) {
+                const double rg = 1.0 / gnorm;
+                const double ux = div_rn(gx, gnorm, rg), uy = div_rn(gy, gnorm, rg), uz = div_rn(gz, gnorm, rg);
+                const FaceGeom f = face_geom(xf[e], meshes, mu, um, hd.z & 0x3fffffff);
+                stuck = corner_stays(f, px, py, pz, ux, uy, uz, g.voxel);
+            }
+            const unsigned bal = __ballot_sync(__activemask(), !stuck);
+            if (stuck) {  // k_pgd_first's no-move branch
+                const double phi = __ldg(st.work[idx].phi + 3);
+                const double cd = xf[e].cd;
+                if (phi <= cd) {
+                    st.point[3 * row] = px; st.point[3 * row + 1] = py; st.point[3 * row + 2] = pz; st.phi[row] = phi;
+                }
+                finish_face(st, row, blk, hd.z & 0x3fffffff, phi, cd);
+            } else {  // k_pgd_first's list (warp-aggregated append)
+                const unsigned lane = threadIdx.x & 31, lead = __ffs(bal) - 1;
+                unsigned b0 = 0;
+                if (lane == lead) b0 = atomicAdd(st.work_count + 1, (unsigned)__popc(bal));
+                b0 = __shfl_sync(bal, b0, lead);
+                st.slow[b0 + __popc(bal & ((1u << lane) - 1u))] = idx;
+            }
+        }
+#endif
         if (stage == 1) {
             if (flag) finish_face(st, row, blk, hd.z & 0x3fffffff, st.phi[row], xf[e].cd);
             else st.slow[atomicAdd(st.work_count + 3, 1u)] = idx;
@@ -512,10 +585,19 @@ __global__ void __launch_bounds__(256, UNIFORM ? FIRST_MINB : FIRST_MINB - 1) k_
                                                    const SdfDesc *__restrict__ sdfs, const MeshDesc *__restrict__ meshes,
                                                    Staging st, unsigned long long *__restrict__ counter, const PlanGrid gu,
                                                   const MeshDesc mu, int um) {
+#if STUCK0 && !PGD_FUSE0
+    const unsigned n = st.work_count[1];  // the faces stage 0 could not finish, listed in st.slow
+#else
     const unsigned n = st.work_count[0];
+#endif
     unsigned long long ns = 0;
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const FaceWork *w = st.work + i;
+#if STUCK0 && !PGD_FUSE0
+        const unsigned idx = st.slow[i];
+#else
+        const unsigned idx = i;
+#endif
+        const FaceWork *w = st.work + idx;
         double px, py, pz, gx, gy, gz, phi = w->phi[3];
         FaceGeom f;
         const PlanGrid *gp;
@@ -561,7 +643,7 @@ __global__ void __launch_bounds__(256, UNIFORM ? FIRST_MINB : FIRST_MINB - 1) k_
         st.alpha[row] = alpha;
         // moved < tol ends the descent (its final gradient is at the new point); 1 < max_iters
         const unsigned slot = atomicAdd(st.work_count + 2, 1u);
-        st.acc[slot] = i | (moved < X.tol ? ACC_FINAL : 0u);
+        st.acc[slot] = idx | (moved < X.tol ? ACC_FINAL : 0u);
         st.acc_hd[slot] = hd;
     }
     if (COUNT) {

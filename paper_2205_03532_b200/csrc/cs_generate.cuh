@@ -9,7 +9,7 @@ namespace cs {
 #define FIRST_MINB 4  // 64 registers (spills 128 B; measured: 3 -> descent 1.033 ms, 4 -> 1.008, 2 -> 1.151, 5 -> 1.125)
 #endif
 #ifndef GRAD_MINB
-#define GRAD_MINB 5  // 48 registers, spills 56 B (measured: 4 -> descent 0.964 ms, 5 -> 0.952, 6 -> 1.012)
+#define GRAD_MINB 4  // 64 registers (with the stage-0 corner test: 4 -> descent 0.941 ms, 5 -> 1.008; without it 5 was best)
 #endif
 #ifndef REST_MINB
 #define REST_MINB 6  // measured: 4 -> 1.033 ms (with FIRST_MINB 3), 6 -> 1.020, 3 -> 1.038, 8 -> worse than 6
@@ -60,7 +60,7 @@ struct Staging {
     uint32_t *acc;         // [capacity] work indices moved by k_pgd_first (| ACC_FINAL)
     int4 *acc_hd;          // [capacity] ... and their work-record headers (row, blk, face, env)
     uint32_t *slow;        // [capacity] work indices still moving after iteration 0
-    unsigned *work_count;  // [0] survivors, [1] (unused), [2] accepted, [3] slow
+    unsigned *work_count;  // [0] survivors, [1] left to k_pgd_first by stage 0 (listed in slow), [2] accepted, [3] slow
 };
 
 // Candidate arrays (row = cand_base[e] + candidate index).
