@@ -444,7 +444,7 @@ __device__ __forceinline__ bool corner_stays(const FaceGeom &f, double px, doubl
 }
 
 template <bool COUNT, bool UNIFORM>
-__global__ void __launch_bounds__(256, UNIFORM ? GRAD_MINB : GRAD_MINB - 1) k_pgd_grad(const int2 *__restrict__ block_map, const EnvXf *__restrict__ xf,
+__global__ void __launch_bounds__(256, UNIFORM ? GRAD_MINB : GRAD_MINB_NU) k_pgd_grad(const int2 *__restrict__ block_map, const EnvXf *__restrict__ xf,
                                                   const SdfDesc *__restrict__ sdfs, const MeshDesc *__restrict__ meshes,
                                                   Staging st, int stage,
                                                   unsigned long long *__restrict__ counter, const PlanGrid gu,

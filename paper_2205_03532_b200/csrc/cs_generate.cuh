@@ -11,6 +11,9 @@ namespace cs {
 #ifndef GRAD_MINB
 #define GRAD_MINB 4  // 64 registers (with the stage-0 corner test: 4 -> descent 0.941 ms, 5 -> 1.008; without it 5 was best)
 #endif
+#ifndef GRAD_MINB_NU
+#define GRAD_MINB_NU (GRAD_MINB - 1)  // plans with per-env grids (config 3: 2 -> 7.81 ms, 3 -> 7.42, 4 -> 7.59)
+#endif
 #ifndef REST_MINB
 #define REST_MINB 6  // measured: 4 -> 1.033 ms (with FIRST_MINB 3), 6 -> 1.020, 3 -> 1.038, 8 -> worse than 6
 #endif
