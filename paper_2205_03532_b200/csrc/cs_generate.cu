@@ -310,8 +310,44 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int4 
         for (int o = 16; o; o >>= 1) ns += __shfl_xor_sync(0xffffffffu, ns, o);
         if ((threadIdx.x & 31) == 0 && ns) atomicAdd(counter, (unsigned long long)ns);
     }
+#if GROUP_STARTS
+    // Survivors' staging rows follow face order (rank among the chunk's survivors: the
+    // compaction reads them in order); their work-list slots are grouped by start
+    // (centroid, corner a, b, c) so the descent's warps mostly see one kind of start.
+    int total, pos, slot;
+    {
+        __shared__ int wc[FACE_CHUNK / 32][4];
+        const unsigned lt = (1u << lane) - 1u;
+        const unsigned m0 = __ballot_sync(0xffffffffu, survive && which == 0);
+        const unsigned m1 = __ballot_sync(0xffffffffu, survive && which == 1);
+        const unsigned m2 = __ballot_sync(0xffffffffu, survive && which == 2);
+        const unsigned m3 = __ballot_sync(0xffffffffu, survive && which == 3);
+        const int wid = threadIdx.x >> 5;
+        if (lane < 4) wc[wid][lane] = __popc(lane == 0 ? m0 : (lane == 1 ? m1 : (lane == 2 ? m2 : m3)));
+        __syncthreads();
+        int before = 0, before_w = 0, tot_w = 0, cat_off = 0;
+        total = 0;
+#pragma unroll
+        for (int w = 0; w < FACE_CHUNK / 32; ++w) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int v = wc[w][c];
+                total += v;
+                if (w < wid) before += v;
+                if (c == which) { tot_w += v; if (w < wid) before_w += v; }
+                else if (c < which) cat_off += v;
+            }
+        }
+        const unsigned mw = which == 0 ? m0 : (which == 1 ? m1 : (which == 2 ? m2 : m3));
+        pos = before + __popc((m0 | m1 | m2 | m3) & lt);
+        slot = cat_off + before_w + __popc(mw & lt);
+        (void)tot_w;
+    }
+#else
     int total;
     const int pos = block_excl_scan(survive ? 1 : 0, ws, &total);
+    const int slot = pos;
+#endif
     if (threadIdx.x == 0) {
         sbase = total ? atomicAdd(st.work_count, (unsigned)total) : 0u;
         st.chunk_count[blockIdx.x] = total;
@@ -319,7 +355,7 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int4 
     }
     __syncthreads();
     if (survive) {
-        FaceWork *w = st.work + sbase + pos;
+        FaceWork *w = st.work + sbase + slot;
         // the record as three 16-byte stores
         reinterpret_cast<int4 *>(w)[0] =
             make_int4((int32_t)(cand_base[e] + f0 + pos), (int32_t)blockIdx.x, (int32_t)f | (which << 30), e);
@@ -347,6 +383,9 @@ __global__ void __launch_bounds__(FACE_CHUNK, PREP_MINB) k_face_prep(const int4 
 // Same operations in the same order as the sequential loop; only the schedule
 // differs (uniform work per kernel instead of one divergent state machine).
 
+#ifndef GROUP_STARTS
+#define GROUP_STARTS 1  // k_face_prep groups each chunk's work-list slots by start kind
+#endif
 #ifndef STUCK0
 #define STUCK0 1  // stage 0 finishes the faces whose iteration 0 provably does not move (see k_pgd_grad)
 #endif
@@ -411,6 +450,47 @@ __device__ __forceinline__ void face_start(const FaceGeom &f, int which, double 
 // corner b, edge ab, then corner c) with every dot product evaluated for every lane,
 // each with closest_point's own expression (so the same bits), and the outcome
 // selected without branches: the four tries cost the same on every lane of a warp.
+//
+// With the starts grouped (GROUP_STARTS) a warp mostly holds one start corner, and
+// only the tests that decide it are evaluated: corner a stays iff closest_point takes
+// its first branch (it returns a == p); corner b iff the first fails and the second
+// holds; corner c needs all four. (A later branch returning a corner bitwise equal
+// to p -- a degenerate triangle -- is left to k_pgd_first: conservative.)
+__device__ __forceinline__ bool corner_stays_which(const FaceGeom &f, int which, double px, double py, double pz,
+                                                   double ux, double uy, double uz, double alpha) {
+    const double abx = f.bx - f.ax, aby = f.by - f.ay, abz = f.bz - f.az;
+    const double acx = f.cx - f.ax, acy = f.cy - f.ay, acz = f.cz - f.az;
+    bool stays = true;
+    for (int bt = 0; bt < 4 && stays; ++bt) {
+        const double qx = px - alpha * ux, qy = py - alpha * uy, qz = pz - alpha * uz;
+        const double apx = qx - f.ax, apy = qy - f.ay, apz = qz - f.az;
+        const double d1 = abx * apx + aby * apy + abz * apz;
+        const double d2 = acx * apx + acy * apy + acz * apz;
+        const bool ra = d1 <= 0.0 && d2 <= 0.0;
+        if (which == 1) {
+            stays = ra;
+        } else {
+            const double bpx = qx - f.bx, bpy = qy - f.by, bpz = qz - f.bz;
+            const double d3 = abx * bpx + aby * bpy + abz * bpz;
+            const double d4 = acx * bpx + acy * bpy + acz * bpz;
+            const bool rb = d3 >= 0.0 && d4 <= d3;
+            if (which == 2) {
+                stays = !ra && rb;
+            } else {
+                const double vc = d1 * d4 - d3 * d2;
+                const double cpx = qx - f.cx, cpy = qy - f.cy, cpz = qz - f.cz;
+                const double d5 = abx * cpx + aby * cpy + abz * cpz;
+                const double d6 = acx * cpx + acy * cpy + acz * cpz;
+                const bool eab = vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0;
+                const bool rc = d6 >= 0.0 && d5 <= d6;
+                stays = !ra && !rb && !eab && rc;
+            }
+        }
+        alpha *= 0.5;
+    }
+    return stays;
+}
+
 __device__ __forceinline__ bool corner_stays(const FaceGeom &f, double px, double py, double pz, double ux,
                                              double uy, double uz, double alpha) {
     const double abx = f.bx - f.ax, aby = f.by - f.ay, abz = f.bz - f.az;
@@ -500,7 +580,8 @@ __global__ void __launch_bounds__(256, UNIFORM ? GRAD_MINB : GRAD_MINB_NU) k_pgd
                 const double rg = 1.0 / gnorm;
                 const double ux = div_rn(gx, gnorm, rg), uy = div_rn(gy, gnorm, rg), uz = div_rn(gz, gnorm, rg);
                 const FaceGeom f = face_geom(xf[e], meshes, mu, um, hd.z & 0x3fffffff);
-                stuck = corner_stays(f, px, py, pz, ux, uy, uz, g.voxel);
+                stuck = GROUP_STARTS ? corner_stays_which(f, which, px, py, pz, ux, uy, uz, g.voxel)
+                                     : corner_stays(f, px, py, pz, ux, uy, uz, g.voxel);
             }
             const unsigned bal = __ballot_sync(__activemask(), !stuck);
             if (stuck) {  // k_pgd_first's no-move branch
