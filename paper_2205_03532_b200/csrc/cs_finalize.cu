@@ -695,8 +695,9 @@ __global__ void __launch_bounds__(CH_WARPS * 32) k_fin_chain(ReduceIO io, Reduce
                         const double2 a = st[top - 1 - li], o = st[top - 2 - li];
                         popi = (a.x - o.x) * (vb - o.y) - (a.y - o.y) * (ub - o.x) <= 0.0;  // NaN: no pop (Python)
                     }
-                    const unsigned stop = (__ballot_sync(FULL, !popi) >> gb) & ((1u << CG) - 1u);
-                    const int npop = more ? (stop ? __ffs(stop) - 1 : CG) : 0;
+                    // pops = the group's first non-popping lane (a sentinel above the group's
+                    // bits: CG when all pop; 0 when the group is done, its lanes do not pop)
+                    const int npop = __ffs((__ballot_sync(FULL, !popi) >> gb) | (1u << CG)) - 1;
                     top -= npop;
                     more = npop == CG;
                     if (!__any_sync(FULL, more)) break;
