@@ -164,8 +164,10 @@ typedef struct cs_outputs {
     double *max_depth;          /* [E,N] */
     int32_t *member_offsets;    /* [E,N+1] CSR into members (relative to cand_base[e]) */
     int32_t *members;           /* [cap] candidate indices, patch-major, ascending within a patch */
-    uint32_t *face_work;        /* [4] last step's face-descent workload: faces descended, -, faces moved
-                                 * by the first iteration, faces still moving after it (diagnostics) */
+    uint32_t *face_work;        /* [4] last step's face-descent workload: faces descended, faces whose
+                                 * first iteration was not settled by the stage-0 corner test, faces
+                                 * moved by the first iteration, faces still moving after it
+                                 * (diagnostics) */
 } cs_outputs;
 
 typedef struct cs_plan cs_plan;
