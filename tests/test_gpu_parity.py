@@ -256,6 +256,11 @@ def test_full_size_1024_envs_vs_oracle(P):
         # the deepest candidate of every patch is kept
         assert len(got["nkept"]) <= 128 and (got["nkept"] <= 6).all()
         assert np.array_equal(np.sort(got["members"]), np.arange(len(cs)))
+    # descent workload counters: survivors >= faces left to k_pgd_first by the stage-0
+    # corner test >= faces moved by iteration 0 >= faces still moving after it; the corner
+    # test settles most faces on this workload (78% of them stay at their start corner)
+    fw = res.plan.face_work.cpu().numpy().astype(np.int64)
+    assert fw[0] >= fw[1] >= fw[2] >= fw[3] >= 0 and fw[1] < 0.5 * fw[0], fw.tolist()
     # bitwise determinism across launches
     snap = {k: getattr(res, k).clone() for k in ("cand_point", "patch_normal", "kept_point", "w_sum", "area")}
     res2 = P.collide([P.register_sdf(grid)] * E, [P.register_mesh(nut)] * E, w["sdf_pose"], w["mesh_pose"], w["cd"])
