@@ -702,6 +702,7 @@ __global__ void __launch_bounds__(CH_WARPS * 32) k_fin_chain(ReduceIO io, Reduce
                     more = npop == CG;
                     if (!__any_sync(FULL, more)) break;
                 }
+                __syncwarp();  // the pop rounds' stack reads are ordered before the push (memory model)
                 if (act) {  // push b
                     if (top < CS) {
                         if (li == 0) { st[top] = make_double2(ub, vb); stp[top] = pb; }
